@@ -1,0 +1,280 @@
+"""V3DB fixed-shape IVF-PQ oracle -- TEST INFRASTRUCTURE ONLY.
+
+Plain numpy, int64 arithmetic, following the paper step by step:
+  * build:  PAPER.md:93-100 (IVF + PQ of residuals), :288-294 (capacity bound n,
+    padding with validity flag), :331-340 (snapshot contents), with BASELINE.json's
+    shaping rule (nearest centroid, lowest index on ties, overflow to the
+    next-nearest list with room) in place of Alg. 1 -- SURVEY.md §8(c) B1-B6, R1-R8.
+  * query:  PAPER.md:351-428, §4.2 Steps 1-5.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this module.  It shares no code with the CUDA path and imports
+nothing from it.  Every function below is pinned by tests in tests/test_oracle_*.py
+(see DESIGN.md "Oracle pins"); none is "parity unpinned".
+
+Readings where the paper is silent (binding on oracle and library alike; DESIGN.md
+lists them): R2 ranking key (e, i); R4 residual w.r.t. the final list; R5 codewords
+saturated to [-127,127], residuals not clamped; R6 encode ties -> lowest codeword;
+R7 valid slots first in ascending id, padding id -1 / code 0; R8 d_max = 2^31-1;
+R9/R10 total orders (d_i, i) and (D, id); R11 < k valid -> (-1, d_max) fill;
+R12 flatten S^orig in probe-rank order then slot order.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+# R8: "a public constant d_max that exceeds any attainable d~".
+D_MAX = 2**31 - 1
+
+
+def dist(x, y) -> int:
+    """dist(x, y) := sum_t (x_t - y_t)^2  (§4.2), exact over the integers."""
+    x = np.asarray(x, dtype=np.int64)
+    y = np.asarray(y, dtype=np.int64)
+    return int(((x - y) ** 2).sum())
+
+
+@dataclass
+class Snapshot:
+    """Fixed-shape snapshot: centroids mu, PQ codebooks C_{m,c},
+    and per (list i, slot j) the record (f_ij, item_ij, v^PQ_ij) with f = (id != -1)."""
+    centroids: np.ndarray   # int8  [nlist][D]          mu_i
+    codebooks: np.ndarray   # int8  [M][Ks][d]          C_{m,c}
+    ids: np.ndarray         # int32 [nlist][L]          item_{i,j}; -1 = padding (f_{i,j} = 0)
+    codes: np.ndarray       # uint8 [nlist][L][M]       v^{(m)}_{i,j}
+    counts: np.ndarray      # int32 [nlist]             number of valid slots
+    list_of: np.ndarray     # int32 [N]                 final list of each vector
+
+    @property
+    def nlist(self): return self.ids.shape[0]
+    @property
+    def L(self): return self.ids.shape[1]
+    @property
+    def M(self): return self.codebooks.shape[0]
+    @property
+    def Ks(self): return self.codebooks.shape[1]
+    @property
+    def D(self): return self.centroids.shape[1]
+
+
+# ----------------------------------------------------------------------------------------
+# Build (offline index shaping)
+# ----------------------------------------------------------------------------------------
+
+def _rank_keys(x: np.ndarray, mu: np.ndarray) -> np.ndarray:
+    """key_{t,i} = ||mu_i||^2 - 2 <x_t, mu_i> = e_{t,i} - ||x_t||^2, exact.
+
+    For a fixed vector t, ordering the lists by e_{t,i} is the same as ordering them by
+    key_{t,i} (they differ by the per-t constant ||x_t||^2), so the ranking of B2 can
+    use key.  Computed in float32 when every value is an integer below 2^24 (exact),
+    else in float64 (exact below 2^53)."""
+    mun = (mu.astype(np.int64) ** 2).sum(1)
+    bound = int(mun.max(initial=0)) + 2 * 128 * 128 * x.shape[1]
+    ft = np.float32 if bound < 2**24 else np.float64
+    return mun.astype(ft)[None, :] - ft(2) * (x.astype(ft) @ mu.astype(ft).T)
+
+
+def assign_greedy(db: np.ndarray, mu: np.ndarray, L: int, chunk: int = 4096) -> np.ndarray:
+    """B2: streaming greedy assignment with capacity L (BASELINE.json shaping rule, R1/R2).
+
+    For t = 0, 1, ..., N-1 in order: rank the lists by (e_{t,i} = dist(db[t], mu_i), i)
+    ascending and append t to the FIRST list in that ranking whose current count is < L.
+    The first list in the (e, i) ranking that has room is exactly the lowest-index
+    minimiser of e over the lists that have room, which is what is computed below
+    (np.argmin returns the first, i.e. lowest-index, minimum).
+    """
+    N = db.shape[0]
+    nlist = mu.shape[0]
+    list_of = np.empty(N, dtype=np.int32)
+    counts = [0] * nlist
+    full = np.zeros(nlist, dtype=bool)
+    for lo in range(0, N, chunk):
+        hi = min(N, lo + chunk)
+        e = _rank_keys(db[lo:hi], mu)                    # [chunk, nlist] e_{t,i} - ||x_t||^2
+        first = np.argmin(e, axis=1).tolist()            # nearest list, lowest index on ties
+        for r in range(hi - lo):
+            i = first[r]
+            if counts[i] >= L:                           # overflow: next-nearest list with room
+                i = int(np.argmin(np.where(full, np.inf, e[r])))
+                assert not full[i], "N > nlist * L (infeasible)"
+            list_of[lo + r] = i
+            counts[i] += 1
+            if counts[i] == L:
+                full[i] = True
+    return list_of
+
+
+def encode(residuals: np.ndarray, codebooks: np.ndarray, chunk: int = 65536) -> np.ndarray:
+    """B5: code_t[m] = argmin_c sum_u (r_t[m d + u] - C_{m,c,u})^2, lowest c on ties (R6).
+
+    PQ encoding of residuals.  For a fixed t the ranking of
+    sum_u (r_u - C_u)^2 over c equals the ranking of ||C_c||^2 - 2 <r, C_c> (they differ by
+    the per-t constant ||r||^2); those keys are integers below 2^24 (d <= 16, |r| <= 255,
+    |C| <= 127), so the float32 matmul computing them is exact.  Subspaces are independent
+    and run on a thread pool (numpy releases the GIL in matmul/argmin).
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
+    N, D = residuals.shape
+    M, Ks, d = codebooks.shape
+    assert d * (127 * 127 + 2 * 255 * 127) < 2**24
+    codes = np.empty((N, M), dtype=np.uint8)
+
+    def one(m):
+        C = codebooks[m].astype(np.float32)                # [Ks, d]
+        cn = (C * C).sum(1)
+        for lo in range(0, N, chunk):
+            hi = min(N, lo + chunk)
+            key = cn[None, :] - np.float32(2) * (residuals[lo:hi, m * d:(m + 1) * d].astype(np.float32) @ C.T)
+            codes[lo:hi, m] = np.argmin(key, axis=1)       # lowest c on ties (R6)
+
+    with ThreadPoolExecutor(max_workers=min(M, os.cpu_count() or 1)) as ex:
+        list(ex.map(one, range(M)))
+    return codes
+
+
+def build_snapshot(db, nlist: int, L: int, M: int, Ks: int, centroid_rows, codeword_rows) -> Snapshot:
+    """Index shaping B1-B6."""
+    db = np.ascontiguousarray(db, dtype=np.int8)
+    N, D = db.shape
+    centroid_rows = np.asarray(centroid_rows, dtype=np.int64)
+    codeword_rows = np.asarray(codeword_rows, dtype=np.int64).reshape(M, Ks)
+    if D % M:
+        raise ValueError("D must be a multiple of M (PAPER.md:331, D = Md)")
+    if not 1 <= Ks <= 256:
+        raise ValueError("Ks must be in [1, 256] (1-byte codes)")
+    if N > nlist * L:
+        raise ValueError("infeasible: N > nlist * L (PAPER.md:290 needs |X_i| <= n)")
+    if len(set(centroid_rows.tolist())) != nlist or centroid_rows.min() < 0 or centroid_rows.max() >= N:
+        raise ValueError("centroid_rows must be nlist distinct rows in [0, N)")
+    for m in range(M):
+        if len(set(codeword_rows[m].tolist())) != Ks or codeword_rows[m].min() < 0 or codeword_rows[m].max() >= N:
+            raise ValueError("codeword_rows[m] must be Ks distinct rows in [0, N)")
+    d = D // M
+
+    # B1: mu_i = db[centroid_rows[i]]  (BASELINE.json: "nlist coarse centroids = seeded-sampled database vectors")
+    mu = db[centroid_rows].copy()
+
+    # B2: nearest list, lowest index on ties, overflow to the next-nearest list with room (R1, R2)
+    list_of = assign_greedy(db, mu, L)
+
+    # B3: residual r_t = db[t] - mu_{list_of[t]} as int16 in [-255, 255], not clamped (R4, R5)
+    resid = db.astype(np.int16) - mu[list_of].astype(np.int16)
+
+    # B4: C_{m,c} = sat_[-127,127]( r_{codeword_rows[m][c]}^{(m)} )  (R5)
+    cb = np.empty((M, Ks, d), dtype=np.int8)
+    for m in range(M):
+        cb[m] = np.clip(resid[codeword_rows[m], m * d:(m + 1) * d], -127, 127).astype(np.int8)
+
+    # B5: PQ codes of the residuals
+    code = encode(resid, cb)
+
+    # B6: list i holds its members in ascending t in slots 0..count_i-1; padding (id -1, code 0) after (R7)
+    ids = np.full((nlist, L), -1, dtype=np.int32)
+    codes = np.zeros((nlist, L, M), dtype=np.uint8)
+    counts = np.bincount(list_of, minlength=nlist).astype(np.int32)
+    order = np.argsort(list_of, kind="stable")             # ascending t within each list
+    start = 0
+    for i in range(nlist):
+        members = order[start:start + counts[i]]
+        start += counts[i]
+        ids[i, :counts[i]] = members
+        codes[i, :counts[i]] = code[members]
+    return Snapshot(mu, cb, ids, codes, counts, list_of)
+
+
+# ----------------------------------------------------------------------------------------
+# Query: the five-step fixed-shape semantics (§4.2)
+# ----------------------------------------------------------------------------------------
+
+def step1_centroid_distances(q, s: Snapshot) -> np.ndarray:
+    """Step 1: d_i := dist(q, mu_i) for i in [n_list]."""
+    q = np.asarray(q, dtype=np.int64)
+    d = ((q[None, :] - s.centroids.astype(np.int64)) ** 2).sum(axis=1)
+    assert d.max(initial=0) < 2**31
+    return d
+
+
+def step2_probe_select(d: np.ndarray, nprobe: int) -> np.ndarray:
+    """Step 2: sort S^orig_{idx,dist} by distance; P(q) = first n_probe
+    indices.  Ties are totalised by the list index (R9), i.e. the key is (d_i, i)."""
+    nlist = d.shape[0]
+    assert 1 <= nprobe <= nlist
+    order = np.lexsort((np.arange(nlist), d))              # primary key d, secondary i
+    return order[:nprobe]
+
+
+def step3_adc_tables(q, s: Snapshot, probes: np.ndarray) -> np.ndarray:
+    """Step 3: for each probed i, LUT_{i,m,c} := dist(C_{m,c}, (q - mu_i)^{(m)}).
+
+    Returns int64 [nprobe][M][Ks] in probe-rank order."""
+    q = np.asarray(q, dtype=np.int64)
+    M, Ks, d = s.codebooks.shape
+    C = s.codebooks.astype(np.int64)                       # [M, Ks, d]
+    lut = np.empty((len(probes), M, Ks), dtype=np.int64)
+    for rho, i in enumerate(probes):
+        res = q - s.centroids[i].astype(np.int64)          # residual query q - mu_i
+        blocks = res.reshape(M, 1, d)                      # (q - mu_i)^{(m)}
+        lut[rho] = ((C - blocks) ** 2).sum(axis=2)
+    return lut
+
+
+def step4_candidate_distances(s: Snapshot, probes: np.ndarray, lut: np.ndarray) -> np.ndarray:
+    """Step 4: d~_{i,j} := sum_m LUT_{i,m,v^{(m)}_{i,j}} and the masked
+    D_{i,j} := f_ij * d~_ij + (1 - f_ij) * d_max.  Returns int64 [nprobe][L] (R12 order)."""
+    M = s.M
+    m_idx = np.arange(M)[None, :]
+    out = np.empty((len(probes), s.L), dtype=np.int64)
+    for rho, i in enumerate(probes):
+        f = (s.ids[i] != -1).astype(np.int64)              # validity flag f_{i,j}
+        dtil = lut[rho][m_idx, s.codes[i].astype(np.int64)].sum(axis=1)
+        assert (dtil[f == 1] < D_MAX).all(), "d_max must exceed every valid d~ (PAPER.md:398-401)"
+        out[rho] = f * dtil + (1 - f) * D_MAX
+    return out
+
+
+def step5_topk(items: np.ndarray, dists: np.ndarray, k: int):
+    """Step 5: sort S^orig_{item,dist} by distance and output the first k.
+    Ties are totalised by the item id as a signed integer (R10)."""
+    assert 1 <= k <= len(items)
+    order = np.lexsort((items, dists))                     # primary key D, secondary item
+    top = order[:k]
+    return items[top], dists[top]
+
+
+def query(q, s: Snapshot, nprobe: int, k: int):
+    """Steps 1-5 for one query.  Returns (ids[k], dist[k], P[nprobe], d_P[nprobe], Dc[nprobe][L])."""
+    d = step1_centroid_distances(q, s)
+    probes = step2_probe_select(d, nprobe)
+    lut = step3_adc_tables(q, s, probes)
+    cand = step4_candidate_distances(s, probes, lut)
+    items = s.ids[probes].reshape(-1).astype(np.int64)     # flattened S^orig: rank rho, then slot j
+    out_ids, out_d = step5_topk(items, cand.reshape(-1), k)
+    return out_ids, out_d, probes, d[probes], cand
+
+
+def query_batch(s: Snapshot, queries, nprobe: int, k: int, rows=None) -> dict:
+    """Run `query` for every row (or the given subset `rows`) of `queries`; int32 outputs in
+    the C-ABI's layouts: out_ids/out_dist [Q][k], trace_lists/trace_list_dist [Q][nprobe],
+    trace_cand_dist [Q][nprobe][L]."""
+    queries = np.asarray(queries, dtype=np.int8)
+    rows = np.arange(queries.shape[0]) if rows is None else np.asarray(rows)
+    nq = len(rows)
+    out = {
+        "out_ids": np.empty((nq, k), np.int32),
+        "out_dist": np.empty((nq, k), np.int32),
+        "trace_lists": np.empty((nq, nprobe), np.int32),
+        "trace_list_dist": np.empty((nq, nprobe), np.int32),
+        "trace_cand_dist": np.empty((nq, nprobe, s.L), np.int32),
+    }
+    for a, r in enumerate(rows):
+        ids, dd, p, dp, cand = query(queries[r], s, nprobe, k)
+        out["out_ids"][a] = ids
+        out["out_dist"][a] = dd
+        out["trace_lists"][a] = p
+        out["trace_list_dist"][a] = dp
+        out["trace_cand_dist"][a] = cand
+    return out
