@@ -1,0 +1,165 @@
+/*
+ * v3db.h -- C ABI of the B200-native fixed-shape IVF-PQ query path of V3DB
+ * (arxiv 2603.03065).  Implemented by libv3db.so (paper_2603_03065_b200/csrc/).
+ *
+ * Scope: build a fixed-shape IVF-PQ snapshot from a database
+ * ("Index shaping", §4.1, snapshot contents
+ * PAPER.md:331-340), then run the five-step query semantics (§4.2)
+ * on a batch of queries, returning the top-k items plus the witness trace that the
+ * multiset-based prover consumes (§4.7).  The commitment `com`
+ * is out of scope: the opaque snapshot handle stands in for it.
+ *
+ * Arithmetic: int8 inputs, exact integer distances (int32 results).  Every distance of
+ * every config fits in int32 (bounds in DESIGN.md), so results are bit-identical to the
+ * paper's field arithmetic with range bounds.
+ *
+ * Conventions for every entry point:
+ *   - Return value: v3db_status (0 == V3DB_OK).  On a non-OK status nothing is written
+ *     to any output and v3db_last_error() returns a thread-local message.
+ *   - "DEVICE" pointers are CUDA device pointers on the current device (e.g. torch CUDA
+ *     tensors' data_ptr()); "HOST" pointers are CPU memory.  The caller owns every
+ *     input/output buffer; the library never frees them.  The library owns a snapshot
+ *     until v3db_free().
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Query work is enqueued on it asynchronously; outputs are valid after the stream
+ *     synchronizes.  The library never aborts or exits; CUDA errors map to V3DB_ECUDA.
+ *   - A snapshot is immutable after build, so concurrent v3db_query_batch calls on the
+ *     same snapshot from different streams/threads are safe.
+ *   - No CPU fallback: every query step runs in this library's CUDA kernels.
+ */
+#ifndef V3DB_H
+#define V3DB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct v3db_snapshot* v3db_snapshot_t; /* opaque; library-owned device memory */
+
+typedef enum v3db_status {
+  V3DB_OK = 0,
+  V3DB_EINVAL = 1,      /* NULL required pointer, shape/range violation, bad handle */
+  V3DB_EINFEASIBLE = 2, /* n > nlist * list_cap: the capacity bound |X_i| <= n cannot hold */
+  V3DB_ENOMEM = 3,      /* device or host allocation failed */
+  V3DB_ECUDA = 4        /* any other CUDA error (message from cudaGetErrorString) */
+} v3db_status;
+
+/* Library limits (argument validation returns V3DB_EINVAL beyond them). */
+#define V3DB_MAX_DIM 2048
+#define V3DB_MAX_NPROBE 1024
+#define V3DB_MAX_K 1024
+
+/*
+ * v3db_build_snapshot -- offline index shaping
+ * with BASELINE.json's rules (readings R1-R8):
+ *   B1 mu_i = db[centroid_rows[i]]                        ("seeded-sampled database vectors")
+ *   B2 for t = 0..n-1 in order: append t to the first list, in the ranking by
+ *      (dist(db[t], mu_i), i), whose count is < list_cap  (nearest list, lowest index on
+ *      ties, overflow to the next-nearest list with room)
+ *   B3 residual r_t = db[t] - mu_{list(t)}  (int16, not clamped)
+ *   B4 C_{m,c} = saturate_[-127,127]( r_{codeword_rows[m*ks+c]}[m*d .. m*d+d) )
+ *   B5 code_t[m] = argmin_c dist(r_t^{(m)}, C_{m,c}), lowest c on ties
+ *   B6 list i: members in ascending t in slots 0..count_i-1, then padding slots with
+ *      item -1 (validity flag f = 0) and code 0
+ *
+ *   db            DEVICE int8 [n][dim], row-major.  Read only during the call.
+ *   n             number of vectors N_0; nlist <= n < 2^31.
+ *   dim           D, 1..V3DB_MAX_DIM, multiple of m.
+ *   nlist         n_list >= 1;  list_cap = n (per-list capacity) >= 1;
+ *                 nlist * list_cap < 2^31.
+ *   m, ks         M sub-quantizers (d = dim/m), K codewords per sub-quantizer, 1..256.
+ *   centroid_rows HOST int32 [nlist], distinct, each in [0, n).
+ *   codeword_rows HOST int32 [m][ks]; row m distinct, each in [0, n).
+ *   stream        work is enqueued on it; the call synchronizes it before returning.
+ *   out           set to the new handle only on V3DB_OK.
+ * Errors: EINVAL (NULL pointer, bad shape, duplicate/out-of-range rows), EINFEASIBLE
+ * (n > nlist*list_cap), ENOMEM, ECUDA.
+ */
+int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap,
+                        int32_t m, int32_t ks, const int32_t* centroid_rows,
+                        const int32_t* codeword_rows, void* stream, v3db_snapshot_t* out);
+
+/*
+ * v3db_query_batch -- Steps 1-5 of PAPER.md:351-428 for nq queries, all on the GPU.
+ *   Step 1 d_i = dist(q, mu_i) for every list
+ *   Step 2 P(q) = the nprobe smallest (d_i, i), in that order (ties -> lower i, R9) (:362-381)
+ *   Step 3 LUT_{i,m,c} = dist(C_{m,c}, (q - mu_i)^{(m)})                     (:383-390)
+ *   Step 4 D_{i,j} = f_ij * sum_m LUT_{i,m,code_ij[m]} + (1 - f_ij) * d_max, d_max = 2^31-1
+ *                                                                           (:392-408)
+ *   Step 5 the k smallest (D, item) pairs of the N_sel = nprobe*L candidates, ascending,
+ *          ties -> lower item as signed int32 (R10)                          (:410-428)
+ *
+ *   s               snapshot from v3db_build_snapshot.
+ *   queries         DEVICE int8 [nq][dim].
+ *   nq              >= 0 (0 is a no-op).
+ *   nprobe          1..min(nlist, V3DB_MAX_NPROBE).
+ *   k               1..min(nprobe*L, V3DB_MAX_K).
+ *   out_ids         DEVICE int32 [nq][k]: items, ascending (D, item).  If fewer than k valid
+ *                   candidates exist, the tail is -1 (R11).
+ *   out_dist        DEVICE int32 [nq][k]: D of each returned item (d_max with item -1).
+ *   trace_lists     DEVICE int32 [nq][nprobe] or NULL: P(q) in probe order.
+ *   trace_list_dist DEVICE int32 [nq][nprobe] or NULL: d_i of those lists.
+ *   trace_cand_dist DEVICE int32 [nq][nprobe][L] or NULL: masked D_{i,j} of every slot
+ *                   of every probed list, in probe-rank then slot order (S^orig_{item,dist},
+ *                   R12); items are ids[trace_lists[q][r]][j] of the snapshot.
+ *   stream          asynchronous; outputs valid after the stream synchronizes.
+ * Errors: EINVAL (NULL handle/required pointer, nprobe/k out of range), ENOMEM, ECUDA.
+ */
+int v3db_query_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe,
+                     int32_t k, int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists,
+                     int32_t* trace_list_dist, int32_t* trace_cand_dist, void* stream);
+
+/* Scan-kernel selection for v3db_query_batch_ex (results are identical for all). */
+#define V3DB_SCAN_AUTO 0
+#define V3DB_SCAN_QUERY_MAJOR 1 /* per-query LUT in shared memory, stream each probed list */
+#define V3DB_SCAN_LIST_MAJOR 2  /* group (query, list) pairs by list; read each list once  */
+
+/* v3db_query_batch_ex -- v3db_query_batch with an explicit scan kernel (`algo`, one of
+ * V3DB_SCAN_*).  EINVAL for an unknown or unsupported algo. */
+int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe,
+                        int32_t k, int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists,
+                        int32_t* trace_list_dist, int32_t* trace_cand_dist, int32_t algo,
+                        void* stream);
+
+/*
+ * v3db_query_batch_host -- the same computation with HOST buffers (end-to-end entry):
+ * copies queries host->device, runs v3db_query_batch on `stream` with library-owned
+ * device buffers, copies the requested outputs device->host, and synchronizes the stream
+ * before returning.  Pointers have the layouts of v3db_query_batch but are HOST memory
+ * (pinned memory makes the copies asynchronous DMA).  trace pointers may be NULL.
+ */
+int v3db_query_batch_host(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe,
+                          int32_t k, int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists,
+                          int32_t* trace_list_dist, int32_t* trace_cand_dist, void* stream);
+
+/* v3db_free -- release a snapshot.  NULL-safe.  The caller must not free a snapshot with
+ * query work still in flight on any stream. */
+void v3db_free(v3db_snapshot_t s);
+
+/* v3db_snapshot_info -- HOST int64 [8] <- {n, dim, nlist, list_cap, m, ks, d, total_valid}. */
+int v3db_snapshot_info(v3db_snapshot_t s, int64_t* out8);
+
+/* Field ids for v3db_snapshot_export. */
+#define V3DB_FIELD_CENTROIDS 0 /* int8  [nlist][dim]        mu                          */
+#define V3DB_FIELD_CODEBOOKS 1 /* int8  [m][ks][d]          C_{m,c}                     */
+#define V3DB_FIELD_IDS 2       /* int32 [nlist][list_cap]   item_{i,j}, -1 = padding     */
+#define V3DB_FIELD_CODES 3     /* uint8 [nlist][list_cap][m] v^PQ_{i,j}                  */
+#define V3DB_FIELD_COUNTS 4    /* int32 [nlist]             valid slots per list         */
+#define V3DB_FIELD_LIST_OF 5   /* int32 [n]                 final list of every vector   */
+
+/* v3db_snapshot_export -- test-only introspection (never on the timed path): copy one
+ * canonical snapshot array into HOST memory.  `bytes` must equal the field's exact size.
+ * Synchronous.  EINVAL for an unknown field or a size mismatch. */
+int v3db_snapshot_export(v3db_snapshot_t s, int32_t field, void* host_dst, size_t bytes);
+
+/* v3db_last_error -- thread-local message for the last non-OK status on this thread
+ * ("" if none).  The pointer stays valid until the next call on the same thread. */
+const char* v3db_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* V3DB_H */

@@ -1,0 +1,169 @@
+// build_kernels.cu -- offline index shaping kernels (BUILD rows of SURVEY.md §8(a)).
+//
+//   B1 gather_rows      mu_i = db[centroid_rows[i]], ||mu_i||^2          (BASELINE.json rule)
+//   B4 make_codebooks   C_{m,c} = sat_[-127,127](db[row] - mu_{list(row)})^{(m)}   (R5)
+//   B3+B5 encode_and_place  residual r_t = db[t] - mu_{list(t)} (int16, unclamped),
+//                       code_t[m] = argmin_c dist(r_t^{(m)}, C_{m,c}), lowest c (R6),
+//                       written to the slot chosen by the host greedy (B2/B6)
+//   slot_terms          P_{i,j} = ||xhat_ij||^2 + 2 <mu_i, xhat_ij>, the per-slot term of the
+//                       exact identity d~_ij = d_i + P_ij + sum_m A_q[m][c_m] used by the scan
+//                       (DESIGN.md "LUT factorisation"); 0 for padding slots.
+// PQ of residuals: PAPER.md:97-100; fixed-shape lists: PAPER.md:292-294, 331-340.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "v3db_internal.cuh"
+
+namespace v3db {
+namespace {
+
+__global__ void gather_rows_kernel(const int8_t* __restrict__ db, int dim, const int32_t* __restrict__ rows,
+                                   int nrows, int8_t* __restrict__ out, int32_t* __restrict__ norms) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= nrows) return;
+  const int8_t* src = db + static_cast<int64_t>(rows[warp]) * dim;
+  int acc = 0;
+  for (int u = lane; u < dim; u += 32) {
+    const int v = src[u];
+    out[static_cast<int64_t>(warp) * dim + u] = static_cast<int8_t>(v);
+    acc += v * v;
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  if (norms && lane == 0) norms[warp] = acc;
+}
+
+__global__ void codebook_kernel(const int8_t* __restrict__ db, const int8_t* __restrict__ mu,
+                                const int32_t* __restrict__ list_of, int dim, int M, int Ks,
+                                const int32_t* __restrict__ codeword_rows, int8_t* __restrict__ cb) {
+  const int d = dim / M;
+  const int64_t total = static_cast<int64_t>(M) * Ks * d;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int u = static_cast<int>(e % d);
+    const int64_t mc = e / d;                    // m * Ks + c
+    const int m = static_cast<int>(mc / Ks);
+    const int row = codeword_rows[mc];
+    const int col = m * d + u;
+    int v = static_cast<int>(db[static_cast<int64_t>(row) * dim + col]) -
+            static_cast<int>(mu[static_cast<int64_t>(list_of[row]) * dim + col]);
+    v = v < -127 ? -127 : (v > 127 ? 127 : v);
+    cb[e] = static_cast<int8_t>(v);
+  }
+}
+
+// One block = 256 consecutive vectors x one subspace m (blockIdx.y).  The subspace's
+// codebook (Ks x d int8) is staged in shared memory; every lane reads the same codeword
+// at the same time (broadcast).
+template <int DS>
+__global__ void __launch_bounds__(256) encode_kernel(const int8_t* __restrict__ db, int64_t n, int dim,
+                                                     const int8_t* __restrict__ mu,
+                                                     const int32_t* __restrict__ list_of,
+                                                     const int32_t* __restrict__ flat_pos,
+                                                     const int8_t* __restrict__ cb, int M, int Ks,
+                                                     uint8_t* __restrict__ codes, int32_t* __restrict__ ids) {
+  extern __shared__ int8_t sC[];  // [Ks][d]
+  const int d = dim / M;
+  const int m = blockIdx.y;
+  for (int e = threadIdx.x; e < Ks * d; e += blockDim.x) sC[e] = cb[static_cast<int64_t>(m) * Ks * d + e];
+  __syncthreads();
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int li = list_of[t];
+  int r[DS];
+#pragma unroll
+  for (int u = 0; u < DS; ++u) {
+    r[u] = 0;
+    if (u < d) {
+      const int col = m * d + u;
+      r[u] = static_cast<int>(db[t * dim + col]) - static_cast<int>(mu[static_cast<int64_t>(li) * dim + col]);
+    }
+  }
+  int best = 0x7fffffff, bestc = 0;
+  for (int c = 0; c < Ks; ++c) {
+    int acc = 0;
+#pragma unroll
+    for (int u = 0; u < DS; ++u) {
+      if (u < d) {
+        const int diff = r[u] - static_cast<int>(sC[c * d + u]);
+        acc += diff * diff;
+      }
+    }
+    if (acc < best) {  // strict: the lowest c wins ties (R6)
+      best = acc;
+      bestc = c;
+    }
+  }
+  const int64_t pos = flat_pos[t];
+  codes[pos * M + m] = static_cast<uint8_t>(bestc);
+  if (m == 0) ids[pos] = static_cast<int32_t>(t);
+}
+
+__global__ void slot_terms_kernel(const int8_t* __restrict__ mu, const int8_t* __restrict__ cb,
+                                  const uint8_t* __restrict__ codes, const int32_t* __restrict__ ids, int nlist,
+                                  int L, int dim, int M, int Ks, int32_t* __restrict__ pterm) {
+  const int d = dim / M;
+  const int64_t total = static_cast<int64_t>(nlist) * L;
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < total;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int acc = 0;
+    if (ids[s] != -1) {
+      const int8_t* mui = mu + (s / L) * dim;
+      for (int m = 0; m < M; ++m) {
+        const int8_t* cw = cb + (static_cast<int64_t>(m) * Ks + codes[s * M + m]) * d;
+        for (int u = 0; u < d; ++u) {
+          const int x = cw[u];
+          acc += x * x + 2 * static_cast<int>(mui[m * d + u]) * x;
+        }
+      }
+    }
+    pterm[s] = acc;
+  }
+}
+
+}  // namespace
+
+cudaError_t gather_rows(const int8_t* db, int dim, const int32_t* rows, int nrows, int8_t* out, int32_t* norms,
+                        cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  gather_rows_kernel<<<(nrows * 32 + 255) / 256, 256, 0, st>>>(db, dim, rows, nrows, out, norms);
+  return cudaGetLastError();
+}
+
+cudaError_t make_codebooks(const int8_t* db, const int8_t* mu, const int32_t* list_of, int dim, int M, int Ks,
+                           const int32_t* codeword_rows, int8_t* codebooks, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(dim) * Ks;
+  const int blocks = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  codebook_kernel<<<blocks, 256, 0, st>>>(db, mu, list_of, dim, M, Ks, codeword_rows, codebooks);
+  return cudaGetLastError();
+}
+
+cudaError_t encode_and_place(const int8_t* db, int64_t n, int dim, const int8_t* mu, const int32_t* list_of,
+                             const int32_t* flat_pos, const int8_t* codebooks, int M, int Ks, uint8_t* codes,
+                             int32_t* ids, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int d = dim / M;
+  dim3 grid(static_cast<unsigned>((n + 255) / 256), M);
+  const size_t smem = static_cast<size_t>(Ks) * d;
+#define V3DB_ENC(DS)                                                                                         \
+  encode_kernel<DS><<<grid, 256, smem, st>>>(db, n, dim, mu, list_of, flat_pos, codebooks, M, Ks, codes, ids); \
+  break;
+  switch (d <= 4 ? 4 : d <= 8 ? 8 : d <= 16 ? 16 : d <= 32 ? 32 : 64) {
+    case 4: V3DB_ENC(4)
+    case 8: V3DB_ENC(8)
+    case 16: V3DB_ENC(16)
+    case 32: V3DB_ENC(32)
+    default: V3DB_ENC(64)
+  }
+#undef V3DB_ENC
+  return cudaGetLastError();
+}
+
+cudaError_t slot_terms(const int8_t* mu, const int8_t* codebooks, const uint8_t* codes, const int32_t* ids,
+                       int nlist, int L, int dim, int M, int Ks, int32_t* pterm, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(nlist) * L;
+  const int blocks = static_cast<int>((total + 255) / 256 < 8192 ? (total + 255) / 256 : 8192);
+  slot_terms_kernel<<<blocks, 256, 0, st>>>(mu, codebooks, codes, ids, nlist, L, dim, M, Ks, pterm);
+  return cudaGetLastError();
+}
+
+}  // namespace v3db

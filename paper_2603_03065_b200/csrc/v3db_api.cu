@@ -1,0 +1,347 @@
+// v3db_api.cu -- the C ABI declared in include/v3db.h: argument validation, snapshot
+// ownership, the host side of the build (the ordered greedy placement B2), and the
+// stream-ordered launch sequence of the query path.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "v3db_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? V3DB_ENOMEM : V3DB_ECUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define V3DB_CUDA(call)                               \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+// Device buffer owned by the host code of one call.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t count) { return cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * (count ? count : 1)); }
+};
+
+template <typename T>
+struct HostPinned {
+  T* p = nullptr;
+  ~HostPinned() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t alloc(size_t count) { return cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(T) * (count ? count : 1)); }
+};
+
+void free_snapshot(v3db_snapshot* s) {
+  if (!s) return;
+  cudaFree(s->centroids);
+  cudaFree(s->cnorm);
+  cudaFree(s->codebooks);
+  cudaFree(s->ids);
+  cudaFree(s->codes);
+  cudaFree(s->counts);
+  cudaFree(s->pterm);
+  cudaFree(s->list_of);
+  delete s;
+}
+
+int check_device(const v3db_snapshot* s) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != s->device)
+    return fail(V3DB_EINVAL, "snapshot belongs to CUDA device " + std::to_string(s->device) +
+                                 " but the current device is " + std::to_string(dev));
+  return V3DB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* v3db_last_error(void) { return g_err.c_str(); }
+
+void v3db_free(v3db_snapshot_t s) { free_snapshot(s); }
+
+int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
+                        int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, void* stream,
+                        v3db_snapshot_t* out) {
+  g_err.clear();
+  if (!db || !centroid_rows || !codeword_rows || !out) return fail(V3DB_EINVAL, "NULL required pointer");
+  if (dim < 1 || dim > V3DB_MAX_DIM) return fail(V3DB_EINVAL, "dim out of range [1, V3DB_MAX_DIM]");
+  if (m < 1 || dim % m) return fail(V3DB_EINVAL, "dim must be a positive multiple of m (D = Md, PAPER.md:331)");
+  if (dim / m > 64) return fail(V3DB_EINVAL, "sub-block dimension d = dim/m > 64 is not supported");
+  if (ks < 1 || ks > 256) return fail(V3DB_EINVAL, "ks out of range [1, 256]");
+  if (static_cast<int64_t>(m) * ks > 32768) return fail(V3DB_EINVAL, "m * ks > 32768 (per-query LUT > 128 KiB)");
+  if (nlist < 1 || list_cap < 1) return fail(V3DB_EINVAL, "nlist and list_cap must be >= 1");
+  if (static_cast<int64_t>(nlist) * list_cap >= (int64_t(1) << 31)) return fail(V3DB_EINVAL, "nlist * list_cap >= 2^31");
+  if (n < nlist || n >= (int64_t(1) << 31)) return fail(V3DB_EINVAL, "n must satisfy nlist <= n < 2^31");
+  if (n > static_cast<int64_t>(nlist) * list_cap)
+    return fail(V3DB_EINFEASIBLE, "n > nlist * list_cap: capacity bound |X_i| <= n cannot hold (PAPER.md:290)");
+  {
+    std::unordered_set<int32_t> seen;
+    for (int i = 0; i < nlist; ++i) {
+      if (centroid_rows[i] < 0 || centroid_rows[i] >= n || !seen.insert(centroid_rows[i]).second)
+        return fail(V3DB_EINVAL, "centroid_rows must be nlist distinct rows in [0, n)");
+    }
+    for (int mm = 0; mm < m; ++mm) {
+      seen.clear();
+      for (int c = 0; c < ks; ++c) {
+        const int32_t r = codeword_rows[mm * ks + c];
+        if (r < 0 || r >= n || !seen.insert(r).second)
+          return fail(V3DB_EINVAL, "codeword_rows[m] must be ks distinct rows in [0, n)");
+      }
+    }
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int d = dim / m;
+  const int L = list_cap;
+
+  v3db_snapshot* s = new (std::nothrow) v3db_snapshot();
+  if (!s) return fail(V3DB_ENOMEM, "host allocation failed");
+  struct Guard {
+    v3db_snapshot* s;
+    ~Guard() { free_snapshot(s); }
+  } guard{s};
+  s->n = n;
+  s->dim = dim;
+  s->nlist = nlist;
+  s->L = L;
+  s->M = m;
+  s->Ks = ks;
+  s->d = d;
+  V3DB_CUDA(cudaGetDevice(&s->device));
+  const int64_t slots = static_cast<int64_t>(nlist) * L;
+  V3DB_CUDA(cudaMalloc(&s->centroids, static_cast<size_t>(nlist) * dim));
+  V3DB_CUDA(cudaMalloc(&s->cnorm, sizeof(int32_t) * nlist));
+  V3DB_CUDA(cudaMalloc(&s->codebooks, static_cast<size_t>(m) * ks * d));
+  V3DB_CUDA(cudaMalloc(&s->ids, sizeof(int32_t) * slots));
+  V3DB_CUDA(cudaMalloc(&s->codes, static_cast<size_t>(slots) * m));
+  V3DB_CUDA(cudaMalloc(&s->counts, sizeof(int32_t) * nlist));
+  V3DB_CUDA(cudaMalloc(&s->pterm, sizeof(int32_t) * slots));
+  V3DB_CUDA(cudaMalloc(&s->list_of, sizeof(int32_t) * n));
+
+  // B1: centroids and their squared norms.
+  DevBuf<int32_t> d_rows;
+  V3DB_CUDA(d_rows.alloc(nlist));
+  V3DB_CUDA(cudaMemcpyAsync(d_rows.p, centroid_rows, sizeof(int32_t) * nlist, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(v3db::gather_rows(db, dim, d_rows.p, nlist, s->centroids, s->cnorm, st));
+
+  // B2: GPU ranks each vector's R nearest lists by (e, i); host places in ascending t.
+  const int R = std::min(nlist, 64);
+  const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 20);
+  DevBuf<int32_t> d_rank, d_rdist;
+  HostPinned<int32_t> h_rank;
+  V3DB_CUDA(d_rank.alloc(static_cast<size_t>(chunk) * R));
+  V3DB_CUDA(d_rdist.alloc(static_cast<size_t>(chunk) * R));
+  V3DB_CUDA(h_rank.alloc(static_cast<size_t>(chunk) * R));
+  std::vector<int32_t> list_of(n), flat_pos(n), counts(nlist, 0);
+  std::vector<int8_t> mu_host;
+  std::vector<int8_t> row(dim);
+  int64_t fallbacks = 0;
+  for (int64_t lo = 0; lo < n; lo += chunk) {
+    const int64_t rows = std::min(chunk, n - lo);
+    V3DB_CUDA(v3db::coarse_topk(db + lo * dim, rows, dim, s->centroids, s->cnorm, nlist, R, d_rank.p, d_rdist.p, st));
+    V3DB_CUDA(cudaMemcpyAsync(h_rank.p, d_rank.p, sizeof(int32_t) * rows * R, cudaMemcpyDeviceToHost, st));
+    V3DB_CUDA(cudaStreamSynchronize(st));
+    for (int64_t r = 0; r < rows; ++r) {
+      const int64_t t = lo + r;
+      int chosen = -1;
+      const int32_t* rk = h_rank.p + r * R;
+      for (int a = 0; a < R; ++a) {
+        if (counts[rk[a]] < L) {
+          chosen = rk[a];
+          break;
+        }
+      }
+      if (chosen < 0) {  // all R nearest lists are full: exact full ranking on the host
+        ++fallbacks;
+        if (mu_host.empty()) {
+          mu_host.resize(static_cast<size_t>(nlist) * dim);
+          V3DB_CUDA(cudaMemcpy(mu_host.data(), s->centroids, mu_host.size(), cudaMemcpyDeviceToHost));
+        }
+        V3DB_CUDA(cudaMemcpy(row.data(), db + t * dim, dim, cudaMemcpyDeviceToHost));
+        int64_t best = INT64_MAX;
+        for (int i = 0; i < nlist; ++i) {
+          if (counts[i] >= L) continue;
+          int64_t e = 0;
+          for (int u = 0; u < dim; ++u) {
+            const int64_t df = int64_t(row[u]) - int64_t(mu_host[static_cast<size_t>(i) * dim + u]);
+            e += df * df;
+          }
+          if (e < best) {  // strict: lowest index on ties
+            best = e;
+            chosen = i;
+          }
+        }
+        if (chosen < 0) return fail(V3DB_EINFEASIBLE, "no list with room (internal)");
+      }
+      list_of[t] = chosen;
+      flat_pos[t] = chosen * L + counts[chosen];  // B6: members in ascending t
+      ++counts[chosen];
+    }
+  }
+  (void)fallbacks;
+
+  // B3-B6 on the GPU.
+  DevBuf<int32_t> d_pos, d_cwrows;
+  V3DB_CUDA(d_pos.alloc(n));
+  V3DB_CUDA(d_cwrows.alloc(static_cast<size_t>(m) * ks));
+  V3DB_CUDA(cudaMemcpyAsync(s->list_of, list_of.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemcpyAsync(d_pos.p, flat_pos.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemcpyAsync(d_cwrows.p, codeword_rows, sizeof(int32_t) * m * ks, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemcpyAsync(s->counts, counts.data(), sizeof(int32_t) * nlist, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemsetAsync(s->ids, 0xff, sizeof(int32_t) * slots, st));  // padding item -1 (R7)
+  V3DB_CUDA(cudaMemsetAsync(s->codes, 0, static_cast<size_t>(slots) * m, st));  // padding code 0
+  V3DB_CUDA(v3db::make_codebooks(db, s->centroids, s->list_of, dim, m, ks, d_cwrows.p, s->codebooks, st));
+  V3DB_CUDA(v3db::encode_and_place(db, n, dim, s->centroids, s->list_of, d_pos.p, s->codebooks, m, ks, s->codes,
+                                   s->ids, st));
+  V3DB_CUDA(v3db::slot_terms(s->centroids, s->codebooks, s->codes, s->ids, nlist, L, dim, m, ks, s->pterm, st));
+  V3DB_CUDA(cudaStreamSynchronize(st));
+  s->total_valid = n;
+  guard.s = nullptr;
+  *out = s;
+  return V3DB_OK;
+}
+
+static int validate_query(v3db_snapshot_t s, const void* queries, int64_t nq, int32_t nprobe, int32_t k,
+                          const void* out_ids, const void* out_dist) {
+  if (!s) return fail(V3DB_EINVAL, "NULL snapshot");
+  if (nq < 0 || nq >= (int64_t(1) << 31)) return fail(V3DB_EINVAL, "nq out of range");
+  if (nq > 0 && (!queries || !out_ids || !out_dist)) return fail(V3DB_EINVAL, "NULL required pointer");
+  if (nprobe < 1 || nprobe > s->nlist || nprobe > V3DB_MAX_NPROBE)
+    return fail(V3DB_EINVAL, "nprobe out of range [1, min(nlist, V3DB_MAX_NPROBE)]");
+  const int64_t nsel = static_cast<int64_t>(nprobe) * s->L;
+  if (k < 1 || k > nsel || k > V3DB_MAX_K) return fail(V3DB_EINVAL, "k out of range [1, min(nprobe*L, V3DB_MAX_K)]");
+  return V3DB_OK;
+}
+
+int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe, int32_t k,
+                        int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists, int32_t* trace_list_dist,
+                        int32_t* trace_cand_dist, int32_t algo, void* stream) {
+  g_err.clear();
+  int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
+  if (rc != V3DB_OK) return rc;
+  if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_QUERY_MAJOR)
+    return fail(V3DB_EINVAL, "unsupported scan algo");
+  if ((rc = check_device(s)) != V3DB_OK) return rc;
+  if (nq == 0) return V3DB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t* lists = trace_lists;
+  int32_t* ldist = trace_list_dist;
+  void* scratch = nullptr;
+  if (!lists || !ldist) {
+    V3DB_CUDA(cudaMallocAsync(&scratch, sizeof(int32_t) * 2 * nq * nprobe, st));
+    if (!lists) lists = static_cast<int32_t*>(scratch);
+    if (!ldist) ldist = static_cast<int32_t*>(scratch) + nq * nprobe;
+  }
+  cudaError_t e = v3db::coarse_topk(queries, nq, s->dim, s->centroids, s->cnorm, s->nlist, nprobe, lists, ldist, st);
+  if (e == cudaSuccess)
+    e = v3db::scan_query_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+  if (scratch) cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "query kernels");
+  return V3DB_OK;
+}
+
+int v3db_query_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe, int32_t k,
+                     int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists, int32_t* trace_list_dist,
+                     int32_t* trace_cand_dist, void* stream) {
+  return v3db_query_batch_ex(s, queries, nq, nprobe, k, out_ids, out_dist, trace_lists, trace_list_dist,
+                             trace_cand_dist, V3DB_SCAN_AUTO, stream);
+}
+
+int v3db_query_batch_host(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe, int32_t k,
+                          int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists, int32_t* trace_list_dist,
+                          int32_t* trace_cand_dist, void* stream) {
+  g_err.clear();
+  int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
+  if (rc != V3DB_OK) return rc;
+  if ((rc = check_device(s)) != V3DB_OK) return rc;
+  if (nq == 0) return V3DB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t qb = static_cast<size_t>(nq) * s->dim;
+  const size_t ob = sizeof(int32_t) * static_cast<size_t>(nq) * k;
+  const size_t lb = sizeof(int32_t) * static_cast<size_t>(nq) * nprobe;
+  const size_t tb = trace_cand_dist ? sizeof(int32_t) * static_cast<size_t>(nq) * nprobe * s->L : 0;
+  const size_t total = ((qb + 255) & ~size_t(255)) + 2 * ob + 2 * lb + tb + 1024;
+  uint8_t* buf = nullptr;
+  V3DB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), total, st));
+  uint8_t* p = buf;
+  auto take = [&](size_t bytes) {
+    uint8_t* r = p;
+    p += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  int8_t* dq = reinterpret_cast<int8_t*>(take(qb));
+  int32_t* dids = reinterpret_cast<int32_t*>(take(ob));
+  int32_t* ddist = reinterpret_cast<int32_t*>(take(ob));
+  int32_t* dl = reinterpret_cast<int32_t*>(take(lb));
+  int32_t* dld = reinterpret_cast<int32_t*>(take(lb));
+  int32_t* dtr = tb ? reinterpret_cast<int32_t*>(take(tb)) : nullptr;
+  cudaError_t e = cudaMemcpyAsync(dq, queries, qb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    rc = v3db_query_batch_ex(s, dq, nq, nprobe, k, dids, ddist, dl, dld, dtr, V3DB_SCAN_AUTO, stream);
+    if (rc != V3DB_OK) {
+      cudaFreeAsync(buf, st);
+      return rc;
+    }
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_ids, dids, ob, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_dist, ddist, ob, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && trace_lists) e = cudaMemcpyAsync(trace_lists, dl, lb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && trace_list_dist) e = cudaMemcpyAsync(trace_list_dist, dld, lb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && dtr) e = cudaMemcpyAsync(trace_cand_dist, dtr, tb, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(buf, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_host");
+  return V3DB_OK;
+}
+
+int v3db_snapshot_info(v3db_snapshot_t s, int64_t* out8) {
+  g_err.clear();
+  if (!s || !out8) return fail(V3DB_EINVAL, "NULL pointer");
+  const int64_t v[8] = {s->n, s->dim, s->nlist, s->L, s->M, s->Ks, s->d, s->total_valid};
+  std::memcpy(out8, v, sizeof(v));
+  return V3DB_OK;
+}
+
+int v3db_snapshot_export(v3db_snapshot_t s, int32_t field, void* host_dst, size_t bytes) {
+  g_err.clear();
+  if (!s || !host_dst) return fail(V3DB_EINVAL, "NULL pointer");
+  const int64_t slots = static_cast<int64_t>(s->nlist) * s->L;
+  const void* src = nullptr;
+  size_t need = 0;
+  switch (field) {
+    case V3DB_FIELD_CENTROIDS: src = s->centroids; need = static_cast<size_t>(s->nlist) * s->dim; break;
+    case V3DB_FIELD_CODEBOOKS: src = s->codebooks; need = static_cast<size_t>(s->M) * s->Ks * s->d; break;
+    case V3DB_FIELD_IDS: src = s->ids; need = sizeof(int32_t) * slots; break;
+    case V3DB_FIELD_CODES: src = s->codes; need = static_cast<size_t>(slots) * s->M; break;
+    case V3DB_FIELD_COUNTS: src = s->counts; need = sizeof(int32_t) * s->nlist; break;
+    case V3DB_FIELD_LIST_OF: src = s->list_of; need = sizeof(int32_t) * s->n; break;
+    default: return fail(V3DB_EINVAL, "unknown field");
+  }
+  if (bytes != need) return fail(V3DB_EINVAL, "size mismatch: field needs " + std::to_string(need) + " bytes");
+  int rc = check_device(s);
+  if (rc != V3DB_OK) return rc;
+  V3DB_CUDA(cudaMemcpy(host_dst, src, need, cudaMemcpyDeviceToHost));
+  return V3DB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+"""Thin Python binding of the C ABI (include/v3db.h) -- same entry points, argument
+marshalling only.  Every query step runs in libv3db.so's CUDA kernels; torch is used for
+device memory and streams only.  Functions mirror the C names without the ``v3db_`` prefix:
+
+  build_snapshot(db, nlist, list_cap, m, ks, centroid_rows, codeword_rows, stream=None) -> Snapshot
+  query_batch(s, queries, nprobe, k, trace=True, algo=SCAN_AUTO, out=None, stream=None) -> dict
+  query_batch_host(s, queries_host, nprobe, k, out) -> None          (end-to-end, host buffers)
+  snapshot_info(s) -> dict;  snapshot_export(s, field) -> numpy array;  free(s)
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_CODES, FIELD_COUNTS, FIELD_IDS,  # noqa: F401
+                   FIELD_LIST_OF, SCAN_AUTO, SCAN_LIST_MAJOR, SCAN_QUERY_MAJOR, V3DBError)
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _need(t: torch.Tensor, dtype, device_type: str, shape, name: str) -> None:
+    if t.dtype != dtype or t.device.type != device_type or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise ValueError(f"{name}: expected contiguous {dtype} {device_type} tensor of shape {tuple(shape)}, got "
+                         f"{t.dtype} {t.device} {tuple(t.shape)}")
+
+
+class Snapshot:
+    """Owner of a v3db_snapshot_t handle (library-owned device memory)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        self.info = snapshot_info(self)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if not self._h:
+            raise ValueError("snapshot has been freed")
+        return self._h
+
+    def __getattr__(self, name):
+        info = self.__dict__.get("info")
+        if info is not None and name in info:
+            return info[name]
+        raise AttributeError(name)
+
+    def free(self) -> None:
+        if self._h:
+            _lib.load().v3db_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def build_snapshot(db: torch.Tensor, nlist: int, list_cap: int, m: int, ks: int, centroid_rows, codeword_rows,
+                   stream=None) -> Snapshot:
+    """v3db_build_snapshot: db is a CUDA int8 [n][dim] tensor; the row samples are host arrays."""
+    lib = _lib.load()
+    if db.dtype != torch.int8 or db.device.type != "cuda" or db.dim() != 2 or not db.is_contiguous():
+        raise ValueError("db must be a contiguous CUDA int8 [n][dim] tensor")
+    cent = np.ascontiguousarray(np.asarray(centroid_rows, dtype=np.int32).reshape(-1))
+    code = np.ascontiguousarray(np.asarray(codeword_rows, dtype=np.int32).reshape(-1))
+    if cent.size != nlist or code.size != m * ks:
+        raise ValueError("centroid_rows must have nlist entries and codeword_rows m*ks entries")
+    h = ctypes.c_void_p()
+    _lib.check(lib.v3db_build_snapshot(_ptr(db), db.shape[0], db.shape[1], nlist, list_cap, m, ks,
+                                       cent.ctypes.data_as(ctypes.c_void_p), code.ctypes.data_as(ctypes.c_void_p),
+                                       _stream_ptr(stream), ctypes.byref(h)))
+    return Snapshot(h)
+
+
+def alloc_outputs(s: Snapshot, nq: int, nprobe: int, k: int, trace: bool = True, device="cuda", pin=False) -> dict:
+    kw = dict(dtype=torch.int32, device=device)
+    if device == "cpu" and pin:
+        kw["pin_memory"] = True
+    out = {"out_ids": torch.empty((nq, k), **kw), "out_dist": torch.empty((nq, k), **kw)}
+    if trace:
+        out["trace_lists"] = torch.empty((nq, nprobe), **kw)
+        out["trace_list_dist"] = torch.empty((nq, nprobe), **kw)
+        out["trace_cand_dist"] = torch.empty((nq, nprobe, s.list_cap), **kw)
+    return out
+
+
+def query_batch(s: Snapshot, queries: torch.Tensor, nprobe: int, k: int, trace: bool = True,
+                algo: int = SCAN_AUTO, out: dict | None = None, stream=None) -> dict:
+    """v3db_query_batch(_ex): Steps 1-5 on the GPU.  Returns (or fills) a dict of CUDA int32
+    tensors out_ids/out_dist [nq][k] and, with trace, trace_lists/trace_list_dist [nq][nprobe],
+    trace_cand_dist [nq][nprobe][L]."""
+    lib = _lib.load()
+    nq = queries.shape[0]
+    _need(queries, torch.int8, "cuda", (nq, s.dim), "queries")
+    if out is None:
+        out = alloc_outputs(s, nq, nprobe, k, trace, device=queries.device)
+    _need(out["out_ids"], torch.int32, "cuda", (nq, k), "out_ids")
+    _need(out["out_dist"], torch.int32, "cuda", (nq, k), "out_dist")
+    tl, tld, tcd = out.get("trace_lists"), out.get("trace_list_dist"), out.get("trace_cand_dist")
+    if tl is not None:
+        _need(tl, torch.int32, "cuda", (nq, nprobe), "trace_lists")
+    if tld is not None:
+        _need(tld, torch.int32, "cuda", (nq, nprobe), "trace_list_dist")
+    if tcd is not None:
+        _need(tcd, torch.int32, "cuda", (nq, nprobe, s.list_cap), "trace_cand_dist")
+    _lib.check(lib.v3db_query_batch_ex(s.handle, _ptr(queries), nq, nprobe, k, _ptr(out["out_ids"]),
+                                       _ptr(out["out_dist"]), _ptr(tl), _ptr(tld), _ptr(tcd), algo,
+                                       _stream_ptr(stream)))
+    return out
+
+
+def query_batch_host(s: Snapshot, queries: torch.Tensor, nprobe: int, k: int, out: dict, stream=None) -> dict:
+    """v3db_query_batch_host: HOST buffers (pin them for asynchronous DMA); the call copies
+    queries in, runs Steps 1-5 on the GPU, copies the outputs back and synchronizes."""
+    lib = _lib.load()
+    nq = queries.shape[0]
+    _need(queries, torch.int8, "cpu", (nq, s.dim), "queries")
+    for name in ("out_ids", "out_dist"):
+        _need(out[name], torch.int32, "cpu", (nq, k), name)
+    tl, tld, tcd = out.get("trace_lists"), out.get("trace_list_dist"), out.get("trace_cand_dist")
+    _lib.check(lib.v3db_query_batch_host(s.handle, _ptr(queries), nq, nprobe, k, _ptr(out["out_ids"]),
+                                         _ptr(out["out_dist"]), _ptr(tl), _ptr(tld), _ptr(tcd),
+                                         _stream_ptr(stream)))
+    return out
+
+
+_INFO_KEYS = ("n", "dim", "nlist", "list_cap", "m", "ks", "d", "total_valid")
+
+
+def snapshot_info(s: Snapshot) -> dict:
+    buf = (ctypes.c_int64 * 8)()
+    _lib.check(_lib.load().v3db_snapshot_info(s.handle, buf))
+    return dict(zip(_INFO_KEYS, list(buf)))
+
+
+def snapshot_export(s: Snapshot, field: int) -> np.ndarray:
+    """v3db_snapshot_export: canonical snapshot arrays as numpy (test-only introspection)."""
+    i = s.info
+    shapes = {
+        FIELD_CENTROIDS: ((i["nlist"], i["dim"]), np.int8),
+        FIELD_CODEBOOKS: ((i["m"], i["ks"], i["d"]), np.int8),
+        FIELD_IDS: ((i["nlist"], i["list_cap"]), np.int32),
+        FIELD_CODES: ((i["nlist"], i["list_cap"], i["m"]), np.uint8),
+        FIELD_COUNTS: ((i["nlist"],), np.int32),
+        FIELD_LIST_OF: ((i["n"],), np.int32),
+    }
+    shape, dt = shapes[field]
+    arr = np.empty(shape, dtype=dt)
+    _lib.check(_lib.load().v3db_snapshot_export(s.handle, field, arr.ctypes.data_as(ctypes.c_void_p), arr.nbytes))
+    return arr
+
+
+def free(s: Snapshot) -> None:
+    s.free()
