@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""bench.py -- batched fixed-shape IVF-PQ query path (V3DB, arxiv 2603.03065) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--trace on|off]
+  python bench.py --impl reference ...      (the CPU oracle on the host cores)
+
+One step = one v3db_query_batch over the config's whole query batch (Steps 1-5 of
+PAPER.md §4.2, all on the GPU, witness trace on by default), inputs resident in HBM.
+Multi-GPU (torchrun): every rank runs its own independent batch against its own snapshot
+replica -- weak scaling, no data-path collective.
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import generate, get_config  # noqa: E402
+
+METRIC = "queries/sec and scan HBM GB/s (fraction of roofline) at nprobe, k, 1 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c4")
+    p.add_argument("--trace", default="on", choices=["on", "off"])
+    p.add_argument("--algo", type=int, default=0, help="V3DB_SCAN_* (0 = auto)")
+    p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------- helpers
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def code_bytes_per_slot(M: int, Ks: int) -> int:
+    """ceil(M * log2(Ks) / 8): the information content of one PQ code."""
+    return math.ceil(M * max(1, math.ceil(math.log2(Ks))) / 8) if Ks > 1 else 0
+
+
+def algorithmic_scan_bytes(cfg, lists: np.ndarray, counts: np.ndarray, trace: bool) -> dict:
+    """Bytes the scan (Steps 3-5) must move per batch: per query the query
+    vector, the codes of the VALID slots of its probed lists, the probed lists' counts, the
+    top-k output, and with the trace the masked distance of every probed slot plus the probe
+    list/distance -- no credit for cross-query reuse."""
+    valid = int(counts[lists].sum())
+    Q = lists.shape[0]
+    cb = code_bytes_per_slot(cfg.M, cfg.Ks)
+    per_batch = Q * cfg.D + valid * cb + Q * 4 * cfg.nprobe + Q * 8 * cfg.k
+    padded = Q * cfg.D + Q * cfg.nprobe * cfg.L * cb + Q * 4 * cfg.nprobe + Q * 8 * cfg.k
+    if trace:
+        tr = Q * (4 * cfg.nprobe * cfg.L + 8 * cfg.nprobe)
+        per_batch += tr
+        padded += tr
+    return {"valid": per_batch, "padded": padded, "valid_slots": valid}
+
+
+def load_traffic(cfg_name: str):
+    """DRAM bytes per scan launch from the committed ncu --set full capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(cfg_name)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------- CPU oracle
+
+_OS = None
+_OQ = None
+
+
+def _oracle_init(snap, queries):
+    global _OS, _OQ
+    _OS, _OQ = snap, queries
+
+
+def _oracle_work(args):
+    import oracle
+    rows, nprobe, k = args
+    oracle.query_batch(_OS, _OQ, nprobe, k, rows=rows)
+    return len(rows)
+
+
+def time_oracle(snap, queries, cfg, seconds: float, workers: int):
+    """Time the oracle's query (Steps 1-5, as it stands) on a bounded sample of the batch
+    over `workers` processes.  Returns (qps, n_sampled, wall_s)."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    import oracle
+    t0 = time.perf_counter()
+    oracle.query_batch(snap, queries, cfg.nprobe, cfg.k, rows=np.arange(2))
+    per_q = (time.perf_counter() - t0) / 2
+    n = int(min(cfg.Q, max(workers, round(seconds / max(per_q, 1e-6)))))
+    rows = np.arange(n)
+    shards = [s for s in np.array_split(rows, workers) if len(s)]
+    with ProcessPoolExecutor(len(shards), mp_context=mp.get_context("fork"), initializer=_oracle_init,
+                             initargs=(snap, queries)) as ex:
+        list(ex.map(_oracle_work, [(shards[0][:1], cfg.nprobe, cfg.k)] * len(shards)))  # warm workers
+        t0 = time.perf_counter()
+        done = sum(ex.map(_oracle_work, [(s, cfg.nprobe, cfg.k) for s in shards]))
+        wall = time.perf_counter() - t0
+    return done / wall, done, wall
+
+
+def oracle_snapshot_from_arrays(arr: dict):
+    import oracle
+    return oracle.Snapshot(arr["centroids"], arr["codebooks"], arr["ids"], arr["codes"], arr["counts"],
+                           arr.get("list_of", np.zeros(0, np.int32)))
+
+
+# ------------------------------------------------------------------------------- reference arm
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the oracle (plain numpy, CPU) builds the snapshot and answers a
+    bounded sample of the batch per step, on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    cfg = get_config(args.config)
+    inp = generate(cfg)
+    workers = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    snap = oracle.build_snapshot(inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    build_s = time.perf_counter() - t0
+    per_step = max(2.0, args.cpu_sample_seconds / max(1, args.steps + args.warmup) * workers)
+    for _ in range(args.warmup):
+        time_oracle(snap, inp.queries, cfg, per_step, workers)
+    tot_q, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        _, n, wall = time_oracle(snap, inp.queries, cfg, per_step, workers)
+        tot_q += n
+        tot_t += wall
+    qps = tot_q / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "D": cfg.D, "nlist": cfg.nlist, "L": cfg.L,
+                   "M": cfg.M, "Ks": cfg.Ks, "nprobe": cfg.nprobe, "k": cfg.k, "trace": args.trace},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": workers, "kind": "oracle",
+                         "sample": f"{tot_q} queries of the {cfg.name} batch over {args.steps} steps "
+                                   f"(oracle snapshot build {build_s:.1f} s, not timed)"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2603_03065_b200 import v3db
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = get_config(args.config)
+    trace = args.trace == "on"
+    inp = generate(cfg)
+
+    # Snapshot build (offline index shaping; timed separately, not part of a step).
+    db = torch.from_numpy(inp.db).to(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    snap = v3db.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    build_s = time.perf_counter() - t0
+    del db
+    counts = v3db.snapshot_export(snap, v3db.FIELD_COUNTS)
+
+    q = torch.from_numpy(inp.queries).to(dev)
+    out = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=True, device=dev)
+    if not trace:
+        for key in ("trace_cand_dist",):
+            out.pop(key)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    v3db.profile_enable(True)
+    for _ in range(args.warmup):
+        v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out, algo=args.algo)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kt = []
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        l0 = v3db.kernel_launches()
+        for i in range(args.steps):
+            flush.zero_()                                   # L2 flush between timed steps (not timed)
+            starts[i].record(stream)
+            v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out, algo=args.algo)
+            ends[i].record(stream)
+            kt.append(v3db.profile_read())                  # per-kernel CUDA-event times of this step
+        launches = v3db.kernel_launches() - l0
+        torch.cuda.synchronize()
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    qps = cfg.Q * world / (ms_per_step / 1e3)
+    coarse_ms = float(np.mean([a for a, _ in kt]))
+    scan_ms = float(np.mean([b for _, b in kt]))
+
+    lists = out["trace_lists"].cpu().numpy()
+    ab = algorithmic_scan_bytes(cfg, lists, counts, trace)
+    hbm, peak_src = peaks()
+    achieved = ab["valid"] / (scan_ms / 1e3) / 1e9
+    traffic = load_traffic(cfg.name)
+
+    result = {
+        "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "D": cfg.D, "nlist": cfg.nlist, "L": cfg.L,
+                   "M": cfg.M, "Ks": cfg.Ks, "nprobe": cfg.nprobe, "k": cfg.k, "trace": args.trace,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MiB write); snapshot codes exceed L2",
+                   "algo": args.algo, "snapshot_build_s": round(build_s, 3)},
+        "scan_gbs": achieved,
+        "scan_gbs_padded": ab["padded"] / (scan_ms / 1e3) / 1e9,
+        "kernel_ms": {"coarse_steps12": coarse_ms, "scan_steps345": scan_ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "kernel": "scan (Steps 3-5)", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": ab["valid"]},
+        "gpu_launches": int(launches),
+    }
+
+    # End-to-end through the C ABI with HOST buffers (H2D queries, D2H outputs inside).
+    if not args.no_e2e:
+        qh = torch.from_numpy(inp.queries).pin_memory()
+        oh = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=trace, device="cpu", pin=True)
+        v3db.query_batch_host(snap, qh, cfg.nprobe, cfg.k, oh)
+        n_e2e = max(1, min(args.steps, 5))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            v3db.query_batch_host(snap, qh, cfg.nprobe, cfg.k, oh)
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        d2h = sum(v.numel() * 4 for v in oh.values())
+        result["e2e"] = {"value": cfg.Q * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": qh.numel(),
+                         "d2h_bytes_per_step": d2h, "steps": n_e2e}
+
+    result["clocks"] = clk.summary()
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        arr = {"centroids": v3db.snapshot_export(snap, v3db.FIELD_CENTROIDS),
+               "codebooks": v3db.snapshot_export(snap, v3db.FIELD_CODEBOOKS),
+               "ids": v3db.snapshot_export(snap, v3db.FIELD_IDS),
+               "codes": v3db.snapshot_export(snap, v3db.FIELD_CODES), "counts": counts}
+        workers = len(os.sched_getaffinity(0))
+        cq, n, wall = time_oracle(oracle_snapshot_from_arrays(arr), inp.queries, cfg, args.cpu_sample_seconds,
+                                  workers)
+        result["cpu_baseline"] = {"value": cq, "unit": "queries/s", "cores": workers, "kind": "oracle",
+                                  "sample": f"{n} of {cfg.Q} {cfg.name} queries, Steps 1-5 on this snapshot's "
+                                            f"arrays, {wall:.1f} s wall on {workers} processes"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    snap.free()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -155,6 +155,17 @@ int v3db_snapshot_info(v3db_snapshot_t s, int64_t* out8);
  * Synchronous.  EINVAL for an unknown field or a size mismatch. */
 int v3db_snapshot_export(v3db_snapshot_t s, int32_t field, void* host_dst, size_t bytes);
 
+/* Profiling hooks (used by bench.py; off by default, never change results).
+ * v3db_profile_enable(1) makes every v3db_query_batch* call record CUDA events on its
+ * stream around each kernel; v3db_profile_read waits for the most recent call's events and
+ * writes up to n elapsed times in milliseconds: [0] Steps 1-2 (coarse top-nprobe kernel),
+ * [1] Steps 3-5 (scan kernel(s) incl. any grouping pass).  Not thread-safe: profile one
+ * stream at a time.  v3db_kernel_launches returns the number of kernels this library has
+ * launched since load (all entry points). */
+int v3db_profile_enable(int32_t on);
+int v3db_profile_read(float* out_ms, int32_t n);
+int64_t v3db_kernel_launches(void);
+
 /* v3db_last_error -- thread-local message for the last non-OK status on this thread
  * ("" if none).  The pointer stays valid until the next call on the same thread. */
 const char* v3db_last_error(void);

@@ -69,12 +69,19 @@ def _rank_keys(x: np.ndarray, mu: np.ndarray) -> np.ndarray:
 
     For a fixed vector t, ordering the lists by e_{t,i} is the same as ordering them by
     key_{t,i} (they differ by the per-t constant ||x_t||^2), so the ranking of B2 can
-    use key.  Computed in float32 when every value is an integer below 2^24 (exact),
-    else in float64 (exact below 2^53)."""
+    use key.  One library matmul of the augmented rows [x_t, 1] . [-2 mu_i, ||mu_i||^2]
+    gives key directly; it runs in float32 when every partial sum is an integer below 2^24
+    (exact), else in float64 (exact below 2^53)."""
     mun = (mu.astype(np.int64) ** 2).sum(1)
     bound = int(mun.max(initial=0)) + 2 * 128 * 128 * x.shape[1]
     ft = np.float32 if bound < 2**24 else np.float64
-    return mun.astype(ft)[None, :] - ft(2) * (x.astype(ft) @ mu.astype(ft).T)
+    xa = np.empty((x.shape[0], x.shape[1] + 1), ft)
+    xa[:, :-1] = x
+    xa[:, -1] = 1
+    ma = np.empty((mu.shape[0], mu.shape[1] + 1), ft)
+    ma[:, :-1] = -2 * mu.astype(np.int64)
+    ma[:, -1] = mun
+    return xa @ ma.T
 
 
 def assign_greedy(db: np.ndarray, mu: np.ndarray, L: int, chunk: int = 4096) -> np.ndarray:
@@ -84,26 +91,39 @@ def assign_greedy(db: np.ndarray, mu: np.ndarray, L: int, chunk: int = 4096) -> 
     ascending and append t to the FIRST list in that ranking whose current count is < L.
     The first list in the (e, i) ranking that has room is exactly the lowest-index
     minimiser of e over the lists that have room, which is what is computed below
-    (np.argmin returns the first, i.e. lowest-index, minimum).
+    (np.argmin returns the first, i.e. lowest-index, minimum).  The ranking keys of a
+    chunk of vectors do not depend on the placement, so a thread pool computes them a few
+    chunks ahead; the placement itself runs strictly in ascending t.
     """
+    from concurrent.futures import ThreadPoolExecutor
+
     N = db.shape[0]
     nlist = mu.shape[0]
     list_of = np.empty(N, dtype=np.int32)
     counts = [0] * nlist
-    full = np.zeros(nlist, dtype=bool)
-    for lo in range(0, N, chunk):
-        hi = min(N, lo + chunk)
-        e = _rank_keys(db[lo:hi], mu)                    # [chunk, nlist] e_{t,i} - ||x_t||^2
-        first = np.argmin(e, axis=1).tolist()            # nearest list, lowest index on ties
-        for r in range(hi - lo):
-            i = first[r]
-            if counts[i] >= L:                           # overflow: next-nearest list with room
-                i = int(np.argmin(np.where(full, np.inf, e[r])))
-                assert not full[i], "N > nlist * L (infeasible)"
-            list_of[lo + r] = i
-            counts[i] += 1
-            if counts[i] == L:
-                full[i] = True
+    room = np.zeros(nlist, dtype=np.float64)          # 0 where the list has room, +inf when full
+
+    def rank(lo):
+        e = _rank_keys(db[lo:min(N, lo + chunk)], mu)  # [chunk, nlist] e_{t,i} - ||x_t||^2
+        return e, np.argmin(e, axis=1).tolist()        # nearest list, lowest index on ties
+
+    starts = list(range(0, N, chunk))
+    with ThreadPoolExecutor(max_workers=3) as ex:
+        futs = [ex.submit(rank, lo) for lo in starts[:3]]
+        for c, lo in enumerate(starts):
+            e, first = futs[c].result()
+            futs[c] = None
+            if c + 3 < len(starts):
+                futs.append(ex.submit(rank, starts[c + 3]))
+            for r in range(len(first)):
+                i = first[r]
+                if counts[i] >= L:                       # overflow: next-nearest list with room
+                    i = int(np.argmin(e[r] + room))
+                    assert counts[i] < L, "N > nlist * L (infeasible)"
+                list_of[lo + r] = i
+                counts[i] += 1
+                if counts[i] == L:
+                    room[i] = np.inf
     return list_of
 
 

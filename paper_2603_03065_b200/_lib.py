@@ -38,6 +38,9 @@ _SIGS = {
     "v3db_snapshot_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "v3db_snapshot_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t]),
     "v3db_last_error": (ctypes.c_char_p, []),
+    "v3db_profile_enable": (ctypes.c_int, [ctypes.c_int32]),
+    "v3db_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int32]),
+    "v3db_kernel_launches": (ctypes.c_int64, []),
 }
 
 _lib = None

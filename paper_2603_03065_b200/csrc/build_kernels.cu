@@ -126,6 +126,7 @@ cudaError_t gather_rows(const int8_t* db, int dim, const int32_t* rows, int nrow
                         cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
   gather_rows_kernel<<<(nrows * 32 + 255) / 256, 256, 0, st>>>(db, dim, rows, nrows, out, norms);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -134,6 +135,7 @@ cudaError_t make_codebooks(const int8_t* db, const int8_t* mu, const int32_t* li
   const int64_t total = static_cast<int64_t>(dim) * Ks;
   const int blocks = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
   codebook_kernel<<<blocks, 256, 0, st>>>(db, mu, list_of, dim, M, Ks, codeword_rows, codebooks);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -155,6 +157,7 @@ cudaError_t encode_and_place(const int8_t* db, int64_t n, int dim, const int8_t*
     default: V3DB_ENC(64)
   }
 #undef V3DB_ENC
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -163,6 +166,7 @@ cudaError_t slot_terms(const int8_t* mu, const int8_t* codebooks, const uint8_t*
   const int64_t total = static_cast<int64_t>(nlist) * L;
   const int blocks = static_cast<int>((total + 255) / 256 < 8192 ? (total + 255) / 256 : 8192);
   slot_terms_kernel<<<blocks, 256, 0, st>>>(mu, codebooks, codes, ids, nlist, L, dim, M, Ks, pterm);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -188,6 +188,7 @@ cudaError_t launch(const int8_t* X, int64_t n, int dim, int dp, const int8_t* mu
   const int64_t blocks = (n + BM - 1) / BM;
   coarse_topk_kernel<BM><<<static_cast<unsigned>(blocks), kThreads, smem, st>>>(X, n, dim, dp, mu, cnorm, nlist, R,
                                                                                  out_idx, out_dist, vec_ok);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -159,6 +159,7 @@ cudaError_t scan_query_major(const v3db_snapshot* s, const int8_t* queries, int6
     default: V3DB_SCAN(0)
   }
 #undef V3DB_SCAN
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -5,7 +5,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -72,9 +74,57 @@ int check_device(const v3db_snapshot* s) {
   return V3DB_OK;
 }
 
+// Profiling state (v3db_profile_*): events around each query kernel on the call's stream.
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  bool created = false;
+  bool recorded = false;
+  cudaEvent_t ev[3];
+};
+Profiler g_prof;
+std::atomic<int64_t> g_launches{0};
+
+void prof_record(int i, cudaStream_t st) {
+  if (!g_prof.on) return;
+  cudaEventRecord(g_prof.ev[i], st);
+  if (i == 2) g_prof.recorded = true;
+}
+
 }  // namespace
 
+namespace v3db {
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace v3db
+
 extern "C" {
+
+int v3db_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_err.clear();
+  if (on && !g_prof.created) {
+    for (auto& e : g_prof.ev) V3DB_CUDA(cudaEventCreate(&e));
+    g_prof.created = true;
+  }
+  g_prof.on = on != 0;
+  g_prof.recorded = false;
+  return V3DB_OK;
+}
+
+int v3db_profile_read(float* out_ms, int32_t n) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_err.clear();
+  if (!out_ms || n < 0) return fail(V3DB_EINVAL, "NULL pointer");
+  if (!g_prof.recorded) return fail(V3DB_EINVAL, "no profiled query call recorded");
+  V3DB_CUDA(cudaEventSynchronize(g_prof.ev[2]));
+  float t[2];
+  V3DB_CUDA(cudaEventElapsedTime(&t[0], g_prof.ev[0], g_prof.ev[1]));
+  V3DB_CUDA(cudaEventElapsedTime(&t[1], g_prof.ev[1], g_prof.ev[2]));
+  for (int i = 0; i < n && i < 2; ++i) out_ms[i] = t[i];
+  return V3DB_OK;
+}
+
+int64_t v3db_kernel_launches(void) { return g_launches.load(); }
 
 const char* v3db_last_error(void) { return g_err.c_str(); }
 
@@ -252,9 +302,12 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
     if (!lists) lists = static_cast<int32_t*>(scratch);
     if (!ldist) ldist = static_cast<int32_t*>(scratch) + nq * nprobe;
   }
+  prof_record(0, st);
   cudaError_t e = v3db::coarse_topk(queries, nq, s->dim, s->centroids, s->cnorm, s->nlist, nprobe, lists, ldist, st);
+  prof_record(1, st);
   if (e == cudaSuccess)
     e = v3db::scan_query_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+  prof_record(2, st);
   if (scratch) cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "query kernels");
   return V3DB_OK;

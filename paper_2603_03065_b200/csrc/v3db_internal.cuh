@@ -32,6 +32,9 @@ struct v3db_snapshot {
 
 namespace v3db {
 
+// Counts every kernel launch of the library (v3db_kernel_launches).
+void note_launch(int n = 1);
+
 constexpr int32_t kDMax = 0x7fffffff;  // d_max = 2^31 - 1 (reading R8)
 
 // Step 1 + Step 2 (and build ranking B2): for each row x of X [n][dim], the R smallest

@@ -163,3 +163,20 @@ def snapshot_export(s: Snapshot, field: int) -> np.ndarray:
 
 def free(s: Snapshot) -> None:
     s.free()
+
+
+def profile_enable(on: bool = True) -> None:
+    """v3db_profile_enable: record CUDA events around each query kernel (bench.py)."""
+    _lib.check(_lib.load().v3db_profile_enable(1 if on else 0))
+
+
+def profile_read() -> tuple[float, float]:
+    """v3db_profile_read: (coarse ms, scan ms) of the most recent profiled query call."""
+    buf = (ctypes.c_float * 2)()
+    _lib.check(_lib.load().v3db_profile_read(buf, 2))
+    return float(buf[0]), float(buf[1])
+
+
+def kernel_launches() -> int:
+    """v3db_kernel_launches: kernels launched by libv3db since load."""
+    return int(_lib.load().v3db_kernel_launches())
