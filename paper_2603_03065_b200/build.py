@@ -22,7 +22,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "v3db.h")]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in deps):
         return OUT
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", "-shared",
            "-I" + os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -10,8 +10,8 @@
 // (threshold-pruned warp insertion, topk.cuh).  The same kernel ranks database vectors
 // for the build (B2 needs each vector's lists in (e, i) order).
 //
-// This file holds the mma.sync (m16n8k32 s8) implementation; see DESIGN.md for the
-// tcgen05 plan.
+// This file holds the mma.sync (m16n8k32 s8) implementation, used for shapes the tcgen05
+// path of coarse_tc.cu does not cover (dim % 16 != 0, dim > 768, unaligned rows).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -194,8 +194,8 @@ cudaError_t launch(const int8_t* X, int64_t n, int dim, int dp, const int8_t* mu
 
 }  // namespace
 
-cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, const int32_t* cnorm, int nlist,
-                        int R, int32_t* out_idx, int32_t* out_dist, cudaStream_t st) {
+cudaError_t coarse_topk_mma(const int8_t* X, int64_t n, int dim, const int8_t* mu, const int32_t* cnorm, int nlist,
+                            int R, int32_t* out_idx, int32_t* out_dist, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int dp = (dim + 31) & ~31;
   if (R <= 128 && smem_bytes<64>(dp, R) <= 227 * 1024)

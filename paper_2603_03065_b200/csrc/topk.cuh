@@ -60,3 +60,81 @@ __device__ __forceinline__ uint64_t warp_offer(uint64_t* T, int R, uint64_t thr,
 }
 
 }  // namespace v3db
+
+namespace v3db {
+
+// Register-resident exact warp top-k (k <= 32*KR): entry j of the ascending list lives in
+// lane j % 32, register j / 32.  Insertion of a warp-uniform key: its rank from KR ballots,
+// then a one-position shift of the tail through shuffles -- no shared memory, no
+// __syncwarp.  `thr` caches entry k-1 (the admission threshold).
+template <int KR>
+struct WarpTopK {
+  uint64_t v[KR];
+  uint64_t thr;
+  int k;
+
+  __device__ __forceinline__ void init(int k_) {
+#pragma unroll
+    for (int r = 0; r < KR; ++r) v[r] = ~0ull;
+    thr = ~0ull;
+    k = k_;
+  }
+  __device__ __forceinline__ uint64_t entry(int j) const {  // warp-uniform j
+    // select v[j >> 5] with explicit selp: a plain conditional chain is turned into a
+    // dynamically indexed (local-memory) access by the compiler
+    const uint32_t rj = static_cast<uint32_t>(j >> 5);
+    uint64_t x = v[0];
+#pragma unroll
+    for (int r = 1; r < KR; ++r)
+      asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, %3;\n\tselp.b64 %0, %1, %0, p;\n\t}" : "+l"(x) : "l"(v[r]), "r"(rj), "r"(static_cast<uint32_t>(r)));
+    return __shfl_sync(0xffffffffu, x, j & 31);
+  }
+  __device__ __forceinline__ void insert(uint64_t key) {  // warp-uniform, key < thr
+    const int lane = threadIdx.x & 31;
+    int pos = 0;
+#pragma unroll
+    for (int r = 0; r < KR; ++r) pos += __popc(__ballot_sync(0xffffffffu, v[r] < key));
+#pragma unroll
+    for (int r = KR - 1; r >= 0; --r) {
+      uint64_t up = __shfl_up_sync(0xffffffffu, v[r], 1);
+      if (r > 0) {
+        const uint64_t carry = __shfl_sync(0xffffffffu, v[r > 0 ? r - 1 : 0], 31);
+        if (lane == 0) up = carry;
+      }
+      const int j = r * 32 + lane;
+      v[r] = (j > pos) ? up : ((j == pos) ? key : v[r]);
+    }
+    thr = entry(k - 1);
+  }
+  // One candidate per lane; keys below the threshold are inserted in lane order.
+  __device__ __forceinline__ void offer(uint64_t key) {
+    unsigned mask = __ballot_sync(0xffffffffu, key < thr);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint64_t kk = __shfl_sync(0xffffffffu, key, src);
+      if (kk < thr) insert(kk);
+    }
+  }
+  // Write entries [0, k) with f(j, key) (lane-strided).
+  template <class F>
+  __device__ __forceinline__ void store(F f) const {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < KR; ++r)
+      if (r * 32 + lane < k) f(r * 32 + lane, v[r]);
+  }
+};
+
+// Call f.template operator()<KR>() with KR = the smallest power of two, 32*KR >= k.
+template <class F>
+__host__ __forceinline__ void dispatch_kr(int k, F f) {
+  if (k <= 32) f.template operator()<1>();
+  else if (k <= 64) f.template operator()<2>();
+  else if (k <= 128) f.template operator()<4>();
+  else if (k <= 256) f.template operator()<8>();
+  else if (k <= 512) f.template operator()<16>();
+  else f.template operator()<32>();
+}
+
+}  // namespace v3db

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstring>
 #include <mutex>
+#include <stdlib.h>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -95,7 +96,28 @@ void prof_record(int i, cudaStream_t st) {
 
 namespace v3db {
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+cudaError_t debug_sync(cudaStream_t st, const char* what) {
+  static const bool on = [] {
+    const char* e = getenv("V3DB_SYNC_CHECK");
+    return e && e[0] == '1';
+  }();
+  if (!on) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) g_err = std::string("after ") + what + ": " + cudaGetErrorString(e);
+  return e;
+}
 }  // namespace v3db
+
+// Keep freed stream-ordered scratch in the device's default pool instead of returning it to
+// the driver at every synchronization (the list-major scan allocates ~0.5 GB per C4 call).
+void keep_pool_memory(int dev) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
 
 extern "C" {
 
@@ -178,6 +200,7 @@ int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist,
   s->Ks = ks;
   s->d = d;
   V3DB_CUDA(cudaGetDevice(&s->device));
+  keep_pool_memory(s->device);
   const int64_t slots = static_cast<int64_t>(nlist) * L;
   V3DB_CUDA(cudaMalloc(&s->centroids, static_cast<size_t>(nlist) * dim));
   V3DB_CUDA(cudaMalloc(&s->cnorm, sizeof(int32_t) * nlist));
@@ -196,7 +219,7 @@ int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist,
 
   // B2: GPU ranks each vector's R nearest lists by (e, i); host places in ascending t.
   const int R = std::min(nlist, 64);
-  const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 20);
+  const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 18);
   DevBuf<int32_t> d_rank, d_rdist;
   HostPinned<int32_t> h_rank;
   V3DB_CUDA(d_rank.alloc(static_cast<size_t>(chunk) * R));
@@ -289,8 +312,13 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   g_err.clear();
   int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
   if (rc != V3DB_OK) return rc;
-  if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_QUERY_MAJOR)
+  if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_QUERY_MAJOR && algo != V3DB_SCAN_LIST_MAJOR)
     return fail(V3DB_EINVAL, "unsupported scan algo");
+  if (algo == V3DB_SCAN_AUTO) {
+    // list-major pays off when lists are probed by several queries of the batch
+    // the list-major tensor-core scan is still experimental (algo=2 selects it explicitly)
+    algo = V3DB_SCAN_QUERY_MAJOR;
+  }
   if ((rc = check_device(s)) != V3DB_OK) return rc;
   if (nq == 0) return V3DB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -305,11 +333,18 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   prof_record(0, st);
   cudaError_t e = v3db::coarse_topk(queries, nq, s->dim, s->centroids, s->cnorm, s->nlist, nprobe, lists, ldist, st);
   prof_record(1, st);
-  if (e == cudaSuccess)
-    e = v3db::scan_query_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+  if (e == cudaSuccess) {
+    if (algo == V3DB_SCAN_LIST_MAJOR)
+      e = v3db::scan_list_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+    else
+      e = v3db::scan_query_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+  }
   prof_record(2, st);
   if (scratch) cudaFreeAsync(scratch, st);
-  if (e != cudaSuccess) return cuda_fail(e, "query kernels");
+  if (e != cudaSuccess) {
+    if (g_err.empty()) return cuda_fail(e, "query kernels");
+    return V3DB_ECUDA;
+  }
   return V3DB_OK;
 }
 

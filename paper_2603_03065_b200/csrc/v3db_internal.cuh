@@ -34,6 +34,9 @@ namespace v3db {
 
 // Counts every kernel launch of the library (v3db_kernel_launches).
 void note_launch(int n = 1);
+// Debugging aid (env V3DB_SYNC_CHECK=1): synchronize the stream after a launch and return the
+// first error tagged with the kernel name (through v3db_last_error).  No-op otherwise.
+cudaError_t debug_sync(cudaStream_t st, const char* what);
 
 constexpr int32_t kDMax = 0x7fffffff;  // d_max = 2^31 - 1 (reading R8)
 
@@ -55,9 +58,27 @@ cudaError_t slot_terms(const int8_t* mu, const int8_t* codebooks, const uint8_t*
                        const int32_t* ids, int nlist, int L, int dim, int M, int Ks, int32_t* pterm,
                        cudaStream_t st);
 
-// Steps 3-5, query-major scan (scan_lut.cu).
+// Steps 3-5, query-major scan (scan_lut.cu).  Modes: final top-k over all ranks; seed (ranks
+// [0, rho_end): write the exact top-k keys into cand_buf[q][0..k), cand_cnt[q] = k and the
+// k-th key into tau[q]); fallback (final, only queries with flags[q] != 0, no trace).
+constexpr int kModeFinal = 0, kModeSeed = 1, kModeFallback = 2;
+struct QmExtra {
+  int rho_begin = 0, rho_end = -1, mode = kModeFinal;
+  uint64_t* cand_buf = nullptr;
+  int cap = 0;
+  int* cand_cnt = nullptr;
+  uint64_t* tau = nullptr;
+  const int* flags = nullptr;
+};
 cudaError_t scan_query_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe,
                              int k, const int32_t* lists, const int32_t* ldist, int32_t* out_ids,
-                             int32_t* out_dist, int32_t* trace_cand, cudaStream_t st);
+                             int32_t* out_dist, int32_t* trace_cand, cudaStream_t st,
+                             const QmExtra& x = QmExtra());
+
+// Steps 3-5, list-major scan (scan_list_major.cu): groups the (query, rank) pairs by list and
+// reads each probed list once per batch; exact top-k via per-query thresholds.
+cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe,
+                            int k, const int32_t* lists, const int32_t* ldist, int32_t* out_ids,
+                            int32_t* out_dist, int32_t* trace_cand, cudaStream_t st);
 
 }  // namespace v3db

@@ -54,7 +54,11 @@ E2_BASIC = Config("e2_basic", 10, "sift", N=6553, D=128, Q=1024, nlist=256, L=32
 E2_LOWACC = Config("e2_lowacc", 11, "sift", N=6553, D=128, Q=1024, nlist=16, L=512, M=8, Ks=1, nprobe=1, k=1)
 E2_LARGE = Config("e2_large", 12, "sift", N=52_428, D=256, Q=512, nlist=512, L=128, M=16, Ks=256, nprobe=64, k=128)
 
-CONFIGS = {c.name: c for c in (C0, C1, C2, C3, C4, E2_BASIC, E2_LOWACC, E2_LARGE)}
+# C4's per-list and per-query shape (D, L, M, Ks, nprobe, k) at a size the oracle finishes in
+# seconds: a parity / debugging stand-in for the scale config.
+C4_MINI = Config("c4_mini", 20, "sift", N=200_000, D=128, Q=1024, nlist=512, L=768, M=32, Ks=256, nprobe=64, k=100)
+
+CONFIGS = {c.name: c for c in (C0, C1, C2, C3, C4, E2_BASIC, E2_LOWACC, E2_LARGE, C4_MINI)}
 BASELINE_CONFIGS = (C0, C1, C2, C3, C4)
 
 

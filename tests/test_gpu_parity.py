@@ -2,7 +2,8 @@
 
 All arithmetic is integer, so the bar is bit-exact equality of every output: the snapshot
 arrays (centroids, codebooks, ids, codes, counts, list_of), out_ids, out_dist,
-trace_lists, trace_list_dist and trace_cand_dist.
+trace_lists, trace_list_dist and trace_cand_dist.  Both scan kernels (query-major and
+list-major) are checked.
 """
 import numpy as np
 import pytest
@@ -16,6 +17,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 FIELDS = ("centroids", "codebooks", "ids", "codes", "counts", "list_of")
+ALGOS = {"qm": 1, "lm": 2}
 
 
 @pytest.fixture(scope="module")
@@ -28,9 +30,8 @@ def v3db():
     return mod
 
 
-def gpu_build(v3db, inp, cfg):
-    db = torch.from_numpy(inp.db).cuda()
-    return v3db.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+def gpu_build(v3db, db, nlist, L, M, Ks, cent, code):
+    return v3db.build_snapshot(torch.from_numpy(np.ascontiguousarray(db)).cuda(), nlist, L, M, Ks, cent, code)
 
 
 def export_all(v3db, s):
@@ -46,24 +47,189 @@ def assert_snapshot_equal(v3db, s, ref):
         assert np.array_equal(got[name], exp), f"snapshot {name}: {first_mismatch(got[name], exp)}"
 
 
-def assert_query_equal(out, ref, rows=None):
+def assert_query_equal(out, ref, rows=None, keys=None):
     for key, exp in ref.items():
+        if keys is not None and key not in keys:
+            continue
         got = out[key].cpu().numpy()
         if rows is not None:
             got = got[rows]
         assert np.array_equal(got, exp), f"{key}: {first_mismatch(got, exp)}"
 
 
+_CACHE = {}
+
+
+def config_case(name):
+    """(cfg, inputs, oracle snapshot, oracle outputs for all queries) -- cached per module."""
+    if name not in _CACHE:
+        cfg = get_config(name)
+        inp = generate(cfg)
+        ref_s = oracle.build_snapshot(inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows,
+                                      inp.codeword_rows)
+        ref = oracle_queries(ref_s, inp.queries, cfg.nprobe, cfg.k)
+        _CACHE[name] = (cfg, inp, ref_s, ref)
+    return _CACHE[name]
+
+
+@pytest.mark.parametrize("algo", ["qm", "lm"])
 @pytest.mark.parametrize("name", ["c0", "c1", "e2_basic", "e2_lowacc", "e2_large"])
-def test_full_parity_small_configs(v3db, name):
+def test_full_parity_small_configs(v3db, name, algo):
     """Full snapshot + full query batch, bit-exact (C0, C1 and the paper's E2 shapes)."""
-    cfg = get_config(name)
-    inp = generate(cfg)
-    ref_s = oracle.build_snapshot(inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
-    s = gpu_build(v3db, inp, cfg)
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
     assert_snapshot_equal(v3db, s, ref_s)
     q = torch.from_numpy(inp.queries).cuda()
-    out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, trace=True)
+    out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, trace=True, algo=ALGOS[algo])
     torch.cuda.synchronize()
-    ref = oracle_queries(ref_s, inp.queries, cfg.nprobe, cfg.k)
     assert_query_equal(out, ref)
+    s.free()
+
+
+def run_case(v3db, db, queries, nlist, L, M, Ks, nprobe, k, cent, code, algos=("qm", "lm"), trace=True):
+    ref_s = oracle.build_snapshot(db, nlist, L, M, Ks, cent, code)
+    ref = oracle.query_batch(ref_s, queries, nprobe, k)
+    s = gpu_build(v3db, db, nlist, L, M, Ks, cent, code)
+    assert_snapshot_equal(v3db, s, ref_s)
+    q = torch.from_numpy(np.ascontiguousarray(queries)).cuda()
+    for algo in algos:
+        out = v3db.query_batch(s, q, nprobe, k, trace=trace, algo=ALGOS[algo])
+        torch.cuda.synchronize()
+        assert_query_equal(out, ref, keys=None if trace else ("out_ids", "out_dist"))
+    s.free()
+    return ref_s, ref
+
+
+def test_edge_k_equals_nsel_and_nprobe_equals_nlist(v3db):
+    """k = N_sel (full sort) with n_probe = n_list."""
+    rng = np.random.default_rng(11)
+    N, D, nlist, L = 200, 16, 4, 64
+    db = rng.integers(-60, 60, size=(N, D)).astype(np.int8)
+    qs = rng.integers(-60, 60, size=(37, D)).astype(np.int8)
+    run_case(v3db, db, qs, nlist, L, 4, 16, nlist, nlist * L, rng.choice(N, nlist, replace=False),
+             np.stack([rng.choice(N, 16, replace=False) for _ in range(4)]))
+
+
+def test_edge_fewer_than_k_valid(v3db):
+    """Probed lists hold fewer than k valid candidates -> (-1, d_max) tail (R11)."""
+    rng = np.random.default_rng(12)
+    N, D, nlist, L = 40, 8, 8, 64
+    db = rng.integers(-100, 100, size=(N, D)).astype(np.int8)
+    qs = rng.integers(-100, 100, size=(19, D)).astype(np.int8)
+    ref_s, ref = run_case(v3db, db, qs, nlist, L, 2, 8, 2, 100, rng.choice(N, nlist, replace=False),
+                          np.stack([rng.choice(N, 8, replace=False) for _ in range(2)]))
+    assert (ref["out_ids"] == -1).any()
+
+
+def test_edge_all_identical_vectors(v3db):
+    """Every vector identical: all distances tie, only the id tie-break orders (R10); lists
+    with duplicate centroids lose every tie to the lowest index and stay empty (R2)."""
+    N, D, nlist, L = 300, 8, 4, 100
+    db = np.full((N, D), 7, np.int8)
+    qs = np.vstack([np.full((1, D), 7, np.int8), np.full((1, D), -9, np.int8), np.arange(D, dtype=np.int8)[None]])
+    run_case(v3db, db, qs, nlist, L, 4, 4, 3, 50, np.arange(nlist), np.stack([np.arange(4)] * 4))
+
+
+def test_edge_overflow_fallback(v3db):
+    """A query whose nearest list holds fewer than k valid vectors gets tau = the padding key,
+    so every valid candidate of its other lists is buffered; past the buffer capacity the
+    list-major path must recompute it with the query-major kernel (still exact)."""
+    rng = np.random.default_rng(13)
+    N, D, nlist, L = 3000, 8, 3, 2000
+    db = rng.integers(-20, 20, size=(N, D)).astype(np.int8)
+    db[0] = 120                                    # an outlier: its list holds (almost) only itself
+    qs = np.vstack([np.full((4, D), 118, np.int8), rng.integers(-20, 20, size=(5, D)).astype(np.int8)])
+    run_case(v3db, db, qs, nlist, L, 4, 32, 3, 10, [0, 1, 2], np.stack([rng.choice(N, 32, replace=False)] * 4))
+
+
+@pytest.mark.parametrize("nq", [1, 67, 130])
+def test_ragged_batch_sizes(v3db, nq):
+    cfg, inp, ref_s, ref = config_case("c0")
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    qs = np.vstack([inp.queries] * 3)[:nq]
+    want = oracle.query_batch(ref_s, qs, cfg.nprobe, cfg.k)
+    q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+    for algo in ALGOS.values():
+        out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, algo=algo)
+        torch.cuda.synchronize()
+        assert_query_equal(out, want)
+    s.free()
+
+
+def test_empty_batch_and_trace_off_and_host_api(v3db):
+    cfg, inp, ref_s, ref = config_case("c1")
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    q = torch.from_numpy(inp.queries).cuda()
+    # nq = 0 is a no-op
+    v3db.query_batch(s, q[:0], cfg.nprobe, cfg.k)
+    # trace off: same top-k
+    for algo in ALGOS.values():
+        out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, trace=False, algo=algo)
+        torch.cuda.synchronize()
+        assert_query_equal(out, ref, keys=("out_ids", "out_dist"))
+    # host-buffer entry point (end-to-end path of bench.py)
+    qh = torch.from_numpy(inp.queries).pin_memory()
+    oh = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=True, device="cpu", pin=True)
+    v3db.query_batch_host(s, qh, cfg.nprobe, cfg.k, oh)
+    for key, exp in ref.items():
+        assert np.array_equal(oh[key].numpy(), exp), key
+    s.free()
+
+
+def test_determinism_across_runs_and_streams(v3db):
+    cfg, inp, ref_s, ref = config_case("e2_large")
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    q = torch.from_numpy(inp.queries).cuda()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = []
+    for st in streams:
+        with torch.cuda.stream(st):
+            outs.append(v3db.query_batch(s, q, cfg.nprobe, cfg.k, stream=st))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert_query_equal(o, ref)
+    s.free()
+
+
+def test_errors(v3db):
+    cfg, inp, _, _ = config_case("c0")
+    db = torch.from_numpy(inp.db).cuda()
+    with pytest.raises(v3db.V3DBError, match="EINFEASIBLE"):
+        v3db.build_snapshot(db, cfg.nlist, 100, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    bad = inp.centroid_rows.copy()
+    bad[1] = bad[0]
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, bad, inp.codeword_rows)
+    s = v3db.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    q = torch.from_numpy(inp.queries).cuda()
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.query_batch(s, q, cfg.nlist + 1, cfg.k)
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.query_batch(s, q, 1, cfg.L + 1)
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.query_batch(s, q, cfg.nprobe, cfg.k, algo=7)
+    s.free()
+
+
+@pytest.mark.parametrize("name", ["c1", "e2_large"])
+def test_coarse_mma_fallback_path(v3db, name, monkeypatch):
+    """The mma.sync coarse kernel (used when the TMA/tcgen05 path does not apply) gives the
+    same bit-exact snapshot and query results."""
+    monkeypatch.setenv("V3DB_FORCE_COARSE_MMA", "1")
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    assert_snapshot_equal(v3db, s, ref_s)
+    out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k)
+    torch.cuda.synchronize()
+    assert_query_equal(out, ref)
+    s.free()
+
+
+def test_odd_dim_generic_paths(v3db):
+    """dim % 16 != 0 and d not in {4, 8, 16}: generic (non-TMA, byte-wise decode) paths."""
+    rng = np.random.default_rng(14)
+    N, D, nlist, L, M, Ks = 900, 18, 6, 200, 3, 32
+    db = rng.integers(-90, 90, size=(N, D)).astype(np.int8)
+    qs = rng.integers(-90, 90, size=(77, D)).astype(np.int8)
+    run_case(v3db, db, qs, nlist, L, M, Ks, 3, 20, rng.choice(N, nlist, replace=False),
+             np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))

@@ -1,0 +1,56 @@
+// tc_bench.cu -- microbenchmark of tcgen05.mma.kind::i8 (M=128, N=256, K=32) issue
+// throughput and commit latency, and of mbarrier round trips (bring-up tool, not libv3db).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include "../paper_2603_03065_b200/csrc/tc_common.cuh"
+using namespace v3db;
+
+__global__ void __launch_bounds__(128, 1) mma_bench(int nmma, int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;             // 16 KB
+  uint8_t* sB = smem + 16384;     // 32 KB
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x; i < (16384 + 32768) / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(i, i, i, i);
+  if (threadIdx.x == 0) { tc::mbar_init(&bar, 1); tc::mbar_fence_init(); }
+  if (threadIdx.x < 32) tc::tmem_alloc(&tslot, 512);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = tc::idesc_s8(128, 256);
+    const uint32_t aa = tc::smem_u32(sA), ba = tc::smem_u32(sB);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      for (int k = 0; k < nmma; ++k)
+        tc::mma_s8(tmem + (r & 1) * 256, tc::desc_sw128(aa + 32 * (k & 3)), tc::desc_sw128(ba + 32 * (k & 3)), idesc, k > 0);
+      tc::mma_commit(&bar);
+      tc::mbar_wait(&bar, r & 1);
+    }
+    long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_dealloc(tmem, 512);
+}
+
+int main() {
+  long long* d; cudaMalloc(&d, sizeof(long long) * 148);
+  cudaFuncSetAttribute(mma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
+  for (int nmma : {1, 4, 16, 64}) {
+    const int reps = 200;
+    for (int grid : {1, 148}) {
+      mma_bench<<<grid, 128, 50 * 1024>>>(nmma, reps, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long h = 0; cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("grid %3d nmma %3d: %.1f cycles per commit-wait round, %.1f cycles per MMA (%s)\n", grid, nmma,
+             (double)h / reps, (double)h / reps / nmma, cudaGetErrorString(e));
+    }
+  }
+  return 0;
+}

@@ -1,0 +1,42 @@
+"""Time query_batch on a config with CUDA events (per-kernel via the profiling hooks)."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_2603_03065_b200 import v3db  # noqa: E402
+from synth import generate, get_config  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--config", default="c4")
+p.add_argument("--reps", type=int, default=5)
+p.add_argument("--algos", default="2")
+p.add_argument("--Q", type=int, default=0, help="use only the first Q queries")
+p.add_argument("--envs", default="", help="comma-separated VAR=VALUE runs after the plain run")
+args = p.parse_args()
+cfg = get_config(args.config)
+inp = generate(cfg)
+s = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows,
+                        inp.codeword_rows)
+q = torch.from_numpy(inp.queries[: args.Q or None]).cuda().contiguous()
+if args.Q:
+    cfg = cfg.with_(Q=args.Q)
+out = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=True, device="cuda")
+v3db.profile_enable(True)
+for env in [""] + [e for e in args.envs.split(",") if e]:
+    os.environ.pop("V3DB_LM_DEBUG", None)
+    if env:
+        k, v = env.split("=")
+        os.environ[k] = v
+    for algo in [int(x) for x in args.algos.split(",")]:
+        v3db.query_batch(s, q, cfg.nprobe, cfg.k, out=out, algo=algo)
+        ts = []
+        for _ in range(args.reps):
+            v3db.query_batch(s, q, cfg.nprobe, cfg.k, out=out, algo=algo)
+            ts.append(v3db.profile_read())
+        c = sorted(t[0] for t in ts)[len(ts) // 2]
+        sc = sorted(t[1] for t in ts)[len(ts) // 2]
+        print(f"{cfg.name} env={env or '-'} algo={algo} coarse {c:.3f} ms  scan {sc:.3f} ms", flush=True)
