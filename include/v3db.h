@@ -112,13 +112,13 @@ int v3db_query_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32
                      int32_t k, int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists,
                      int32_t* trace_list_dist, int32_t* trace_cand_dist, void* stream);
 
-/* Scan-kernel selection for v3db_query_batch_ex (results are identical for all). */
-#define V3DB_SCAN_AUTO 0
-#define V3DB_SCAN_QUERY_MAJOR 1 /* per-query LUT in shared memory, stream each probed list */
-#define V3DB_SCAN_LIST_MAJOR 2  /* group (query, list) pairs by list; read each list once  */
+/* Scan-kernel selection for v3db_query_batch_ex (results are bit-identical for all). */
+#define V3DB_SCAN_AUTO 0    /* ROTATED when the snapshot's shape supports it, else GENERIC   */
+#define V3DB_SCAN_GENERIC 1 /* per-query LUT [M][Ks] in shared memory, any shape            */
+#define V3DB_SCAN_ROTATED 2 /* conflict-free rotated LUT (M % 4 == 0, d % 4 == 0, M <= 128) */
 
 /* v3db_query_batch_ex -- v3db_query_batch with an explicit scan kernel (`algo`, one of
- * V3DB_SCAN_*).  EINVAL for an unknown or unsupported algo. */
+ * V3DB_SCAN_*).  EINVAL for an unknown algo, or ROTATED on a snapshot it does not support. */
 int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe,
                         int32_t k, int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists,
                         int32_t* trace_list_dist, int32_t* trace_cand_dist, int32_t algo,

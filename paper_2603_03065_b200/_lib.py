@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "v3db.h")
 
 V3DB_OK, V3DB_EINVAL, V3DB_EINFEASIBLE, V3DB_ENOMEM, V3DB_ECUDA = range(5)
 STATUS_NAMES = {0: "V3DB_OK", 1: "V3DB_EINVAL", 2: "V3DB_EINFEASIBLE", 3: "V3DB_ENOMEM", 4: "V3DB_ECUDA"}
-SCAN_AUTO, SCAN_QUERY_MAJOR, SCAN_LIST_MAJOR = 0, 1, 2
+SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED = 0, 1, 2
 FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_IDS, FIELD_CODES, FIELD_COUNTS, FIELD_LIST_OF = range(6)
 
 _c_i8p = ctypes.c_void_p

@@ -8,6 +8,8 @@
 //   slot_terms          P_{i,j} = ||xhat_ij||^2 + 2 <mu_i, xhat_ij>, the per-slot term of the
 //                       exact identity d~_ij = d_i + P_ij + sum_m A_q[m][c_m] used by the scan
 //                       (DESIGN.md "LUT factorisation"); 0 for padding slots.
+//   rotate_codes        codes_rot: the layout the rotated-LUT scan reads (DESIGN.md "Rotated LUT
+//                       layout"); transpose_codebooks: cbT [Ks][M][d].
 // PQ of residuals: PAPER.md:97-100; fixed-shape lists: PAPER.md:292-294, 331-340.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -120,7 +122,50 @@ __global__ void slot_terms_kernel(const int8_t* __restrict__ mu, const int8_t* _
   }
 }
 
+// Byte g*G + s of slot j holds the code of subspace g*G + (j + s) mod G (lane l = j mod 32 reads
+// table column l + s, which holds that subspace).  kLutW32 additionally pre-compensates the row
+// wrap of columns l + s >= 32: the stored byte is (code - 1) mod 256 there.
+__global__ void rotate_kernel(const uint8_t* __restrict__ codes, int64_t slots, int M, int mode, int G,
+                              uint8_t* __restrict__ out) {
+  const int64_t total = slots * M;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / M;
+    const int pos = static_cast<int>(e - j * M);
+    const int g = pos / G, s = pos - g * G;
+    const int lane = static_cast<int>(j & 31);
+    const int src = g * G + (lane + s) % G;
+    int v = codes[j * M + src];
+    if (mode == kLutW32 && lane + s >= 32) v = (v + 255) & 255;
+    out[e] = static_cast<uint8_t>(v);
+  }
+}
+
+__global__ void transpose_cb_kernel(const int8_t* __restrict__ cb, int M, int Ks, int d, int8_t* __restrict__ cbT) {
+  const int total = M * Ks * d;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int u = e % d, mc = e / d, m = mc / Ks, c = mc - m * Ks;
+    cbT[(static_cast<int64_t>(c) * M + m) * d + u] = cb[e];
+  }
+}
+
 }  // namespace
+
+cudaError_t rotate_codes(const uint8_t* codes, int64_t slots, int M, int mode, int G, uint8_t* codes_rot,
+                         cudaStream_t st) {
+  const int64_t total = slots * M;
+  const int blocks = static_cast<int>((total + 255) / 256 < 16384 ? (total + 255) / 256 : 16384);
+  rotate_kernel<<<blocks, 256, 0, st>>>(codes, slots, M, mode, G, codes_rot);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t transpose_codebooks(const int8_t* cb, int M, int Ks, int d, int8_t* cbT, cudaStream_t st) {
+  const int total = M * Ks * d;
+  transpose_cb_kernel<<<(total + 255) / 256 < 1024 ? (total + 255) / 256 : 1024, 256, 0, st>>>(cb, M, Ks, d, cbT);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t gather_rows(const int8_t* db, int dim, const int32_t* rows, int nrows, int8_t* out, int32_t* norms,
                         cudaStream_t st) {

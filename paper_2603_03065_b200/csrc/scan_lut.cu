@@ -1,4 +1,6 @@
-// scan_lut.cu -- Steps 3-5 of PAPER.md §4.2, query-major: one CTA per query.
+// scan_lut.cu -- Steps 3-5 of PAPER.md §4.2, generic query-major scan: one CTA per query.
+// Serves every shape; the rotated-LUT kernel of scan_rot.cu replaces it where its
+// conflict-free table geometry applies.
 //
 // Step 3 defines, per probed list i, LUT_{i,m,c} = dist(C_{m,c}, (q-mu_i)^{(m)}).
 // Summed over the M sub-blocks selected by a slot's code this is (exact integer identity,
@@ -50,8 +52,7 @@ __global__ void __launch_bounds__(kThreads) scan_qm_kernel(
     const uint8_t* __restrict__ codes, const int32_t* __restrict__ pterm, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ counts, int nprobe, int k, const int32_t* __restrict__ lists,
     const int32_t* __restrict__ ldist, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_dist,
-    int32_t* __restrict__ trace, int rho_begin, int rho_end, int mode, uint64_t* __restrict__ cand_buf, int cap,
-    int* __restrict__ cand_cnt, uint64_t* __restrict__ tau, const int* __restrict__ flags) {
+    int32_t* __restrict__ trace) {
   const int M = MC > 0 ? MC : M_rt;
   const int d = dim / M;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -61,7 +62,6 @@ __global__ void __launch_bounds__(kThreads) scan_qm_kernel(
   int8_t* qs = reinterpret_cast<int8_t*>(probe + nprobe);       // [dim]
 
   const int64_t qi = blockIdx.x;
-  if (mode == kModeFallback && flags[qi] == 0) return;  // only queries whose candidate buffer overflowed
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int u = threadIdx.x; u < dim; u += kThreads) qs[u] = queries[qi * dim + u];
   for (int r = threadIdx.x; r < nprobe; r += kThreads)
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads) scan_qm_kernel(
   // Steps 4-5: stream the probed lists.
   uint64_t* T = tops + warp * k;
   uint64_t thr = ~0ull;
-  for (int rho = rho_begin; rho < rho_end; ++rho) {
+  for (int rho = 0; rho < nprobe; ++rho) {
     const int li = probe[rho].x;
     const int di = probe[rho].y;
     const int cnt = counts[li];
@@ -125,15 +125,6 @@ __global__ void __launch_bounds__(kThreads) scan_qm_kernel(
     }
   }
   __syncthreads();
-  if (mode == kModeSeed) {
-    // seed of the list-major path: the exact top-k of ranks [0, r0) and its k-th key
-    for (int r = threadIdx.x; r < k; r += kThreads) cand_buf[qi * cap + r] = tops[r];
-    if (threadIdx.x == 0) {
-      cand_cnt[qi] = k;
-      tau[qi] = tops[k - 1];
-    }
-    return;
-  }
   for (int r = threadIdx.x; r < k; r += kThreads) {
     const uint64_t key = tops[r];
     out_ids[qi * k + r] = step5_id(key);
@@ -143,9 +134,9 @@ __global__ void __launch_bounds__(kThreads) scan_qm_kernel(
 
 }  // namespace
 
-cudaError_t scan_query_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
-                             const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
-                             int32_t* trace, cudaStream_t st, const QmExtra& x) {
+cudaError_t scan_generic(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
+                         const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
+                         int32_t* trace, cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
   const size_t smem = sizeof(uint64_t) * kWarps * k + sizeof(int32_t) * s->M * s->Ks + sizeof(int2) * nprobe +
                       ((s->dim + 15) & ~15);
@@ -156,8 +147,7 @@ cudaError_t scan_query_major(const v3db_snapshot* s, const int8_t* queries, int6
     if (e != cudaSuccess) return e;                                                                              \
     scan_qm_kernel<MC><<<static_cast<unsigned>(nq), kThreads, smem, st>>>(                                       \
         queries, s->dim, s->M, s->Ks, s->L, s->codebooks, s->codes, s->pterm, s->ids, s->counts, nprobe, k,     \
-        lists, ldist, out_ids, out_dist, trace, x.rho_begin, x.rho_end < 0 ? nprobe : x.rho_end, x.mode,         \
-        x.cand_buf, x.cap, x.cand_cnt, x.tau, x.flags);                                                          \
+        lists, ldist, out_ids, out_dist, trace);                                                                 \
     break;                                                                                                       \
   }
   switch (s->M) {

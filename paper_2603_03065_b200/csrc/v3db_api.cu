@@ -64,6 +64,8 @@ void free_snapshot(v3db_snapshot* s) {
   cudaFree(s->counts);
   cudaFree(s->pterm);
   cudaFree(s->list_of);
+  cudaFree(s->codes_rot);
+  cudaFree(s->cbT);
   delete s;
 }
 
@@ -287,6 +289,14 @@ int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist,
   V3DB_CUDA(v3db::encode_and_place(db, n, dim, s->centroids, s->list_of, d_pos.p, s->codebooks, m, ks, s->codes,
                                    s->ids, st));
   V3DB_CUDA(v3db::slot_terms(s->centroids, s->codebooks, s->codes, s->ids, nlist, L, dim, m, ks, s->pterm, st));
+  // layouts of the rotated-LUT scan
+  s->lut_mode = v3db::plan_lut(m, ks, d, &s->lut_g);
+  if (s->lut_mode != 0) {
+    V3DB_CUDA(cudaMalloc(&s->codes_rot, static_cast<size_t>(slots) * m));
+    V3DB_CUDA(cudaMalloc(&s->cbT, static_cast<size_t>(m) * ks * d));
+    V3DB_CUDA(v3db::rotate_codes(s->codes, slots, m, s->lut_mode, s->lut_g, s->codes_rot, st));
+    V3DB_CUDA(v3db::transpose_codebooks(s->codebooks, m, ks, d, s->cbT, st));
+  }
   V3DB_CUDA(cudaStreamSynchronize(st));
   s->total_valid = n;
   guard.s = nullptr;
@@ -312,13 +322,11 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   g_err.clear();
   int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
   if (rc != V3DB_OK) return rc;
-  if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_QUERY_MAJOR && algo != V3DB_SCAN_LIST_MAJOR)
+  if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_GENERIC && algo != V3DB_SCAN_ROTATED)
     return fail(V3DB_EINVAL, "unsupported scan algo");
-  if (algo == V3DB_SCAN_AUTO) {
-    // list-major pays off when lists are probed by several queries of the batch
-    // the list-major tensor-core scan is still experimental (algo=2 selects it explicitly)
-    algo = V3DB_SCAN_QUERY_MAJOR;
-  }
+  if (algo == V3DB_SCAN_ROTATED && s->lut_mode == 0)
+    return fail(V3DB_EINVAL, "V3DB_SCAN_ROTATED does not support this snapshot's (M, Ks, d)");
+  if (algo == V3DB_SCAN_AUTO) algo = s->lut_mode != 0 ? V3DB_SCAN_ROTATED : V3DB_SCAN_GENERIC;
   if ((rc = check_device(s)) != V3DB_OK) return rc;
   if (nq == 0) return V3DB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -334,10 +342,10 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   cudaError_t e = v3db::coarse_topk(queries, nq, s->dim, s->centroids, s->cnorm, s->nlist, nprobe, lists, ldist, st);
   prof_record(1, st);
   if (e == cudaSuccess) {
-    if (algo == V3DB_SCAN_LIST_MAJOR)
-      e = v3db::scan_list_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+    if (algo == V3DB_SCAN_ROTATED)
+      e = v3db::scan_rotated(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
     else
-      e = v3db::scan_query_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+      e = v3db::scan_generic(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
   }
   prof_record(2, st);
   if (scratch) cudaFreeAsync(scratch, st);

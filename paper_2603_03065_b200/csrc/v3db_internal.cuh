@@ -9,6 +9,9 @@
 //   counts     int32 [nlist]               valid slots (valid slots come first, R7)
 //   pterm      int32 [nlist][L]            P_{i,j} = ||xhat_ij||^2 + 2<mu_i, xhat_ij>
 //   list_of    int32 [n]                   final list of every vector (export/tests)
+//   codes_rot  uint8 [nlist][L][M]         codes re-ordered for the conflict-free rotated LUT
+//                                          scan (scan_rot.cu)
+//   cbT        int8  [Ks][M][d]            codebooks, codeword-major (coalesced LUT build)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -28,6 +31,11 @@ struct v3db_snapshot {
   int32_t* counts = nullptr;
   int32_t* pterm = nullptr;
   int32_t* list_of = nullptr;
+  // rotated-LUT scan (scan_rot.cu): lut_mode 0 = not supported for this shape (generic scan),
+  // kLutP64 / kLutW32 = table geometry; lut_g = subspaces per rotation group.
+  int lut_mode = 0, lut_g = 0;
+  uint8_t* codes_rot = nullptr;
+  int8_t* cbT = nullptr;
 };
 
 namespace v3db {
@@ -58,27 +66,27 @@ cudaError_t slot_terms(const int8_t* mu, const int8_t* codebooks, const uint8_t*
                        const int32_t* ids, int nlist, int L, int dim, int M, int Ks, int32_t* pterm,
                        cudaStream_t st);
 
-// Steps 3-5, query-major scan (scan_lut.cu).  Modes: final top-k over all ranks; seed (ranks
-// [0, rho_end): write the exact top-k keys into cand_buf[q][0..k), cand_cnt[q] = k and the
-// k-th key into tau[q]); fallback (final, only queries with flags[q] != 0, no trace).
-constexpr int kModeFinal = 0, kModeSeed = 1, kModeFallback = 2;
-struct QmExtra {
-  int rho_begin = 0, rho_end = -1, mode = kModeFinal;
-  uint64_t* cand_buf = nullptr;
-  int cap = 0;
-  int* cand_cnt = nullptr;
-  uint64_t* tau = nullptr;
-  const int* flags = nullptr;
-};
-cudaError_t scan_query_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe,
-                             int k, const int32_t* lists, const int32_t* ldist, int32_t* out_ids,
-                             int32_t* out_dist, int32_t* trace_cand, cudaStream_t st,
-                             const QmExtra& x = QmExtra());
+// Rotated-LUT geometry.
+constexpr int kLutP64 = 1;   // G = M <= 32 subspaces, rows of 64 int32 columns (PRMT addressing)
+constexpr int kLutW32 = 2;   // G = gcd(M, 32), M/G groups of 257 rows x 32 columns (wrap addressing)
+constexpr int kW32GroupBytes = 257 * 32 * 4;
+// Chooses the geometry for (M, Ks, d): returns the mode (0 = generic scan) and sets *G.
+int plan_lut(int M, int Ks, int d, int* G);
+// Build: codes_rot from the canonical codes, and cbT.
+cudaError_t rotate_codes(const uint8_t* codes, int64_t slots, int M, int mode, int G, uint8_t* codes_rot,
+                         cudaStream_t st);
+cudaError_t transpose_codebooks(const int8_t* cb, int M, int Ks, int d, int8_t* cbT, cudaStream_t st);
 
-// Steps 3-5, list-major scan (scan_list_major.cu): groups the (query, rank) pairs by list and
-// reads each probed list once per batch; exact top-k via per-query thresholds.
-cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe,
-                            int k, const int32_t* lists, const int32_t* ldist, int32_t* out_ids,
-                            int32_t* out_dist, int32_t* trace_cand, cudaStream_t st);
+// Steps 3-5, generic query-major scan (scan_lut.cu): any shape, per-query LUT [M][Ks] in shared
+// memory (not conflict-free).
+cudaError_t scan_generic(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
+                         const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
+                         int32_t* trace_cand, cudaStream_t st);
+
+// Steps 3-5, rotated-LUT scan (scan_rot.cu): conflict-free LUT lookups, padding chunks skipped,
+// buffered exact top-k.  Requires s->lut_mode != 0.
+cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
+                         const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
+                         int32_t* trace_cand, cudaStream_t st);
 
 }  // namespace v3db

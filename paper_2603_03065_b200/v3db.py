@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 from ._lib import (FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_CODES, FIELD_COUNTS, FIELD_IDS,  # noqa: F401
-                   FIELD_LIST_OF, SCAN_AUTO, SCAN_LIST_MAJOR, SCAN_QUERY_MAJOR, V3DBError)
+                   FIELD_LIST_OF, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, V3DBError)
 
 
 def _stream_ptr(stream) -> ctypes.c_void_p:

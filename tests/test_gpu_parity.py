@@ -2,8 +2,8 @@
 
 All arithmetic is integer, so the bar is bit-exact equality of every output: the snapshot
 arrays (centroids, codebooks, ids, codes, counts, list_of), out_ids, out_dist,
-trace_lists, trace_list_dist and trace_cand_dist.  Both scan kernels (query-major and
-list-major) are checked.
+trace_lists, trace_list_dist and trace_cand_dist.  Both scan kernels (the generic
+query-major LUT scan and the rotated conflict-free LUT scan) are checked.
 """
 import numpy as np
 import pytest
@@ -17,7 +17,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 FIELDS = ("centroids", "codebooks", "ids", "codes", "counts", "list_of")
-ALGOS = {"qm": 1, "lm": 2}
+ALGOS = {"auto": 0, "gen": 1, "rot": 2}
 
 
 @pytest.fixture(scope="module")
@@ -72,8 +72,8 @@ def config_case(name):
     return _CACHE[name]
 
 
-@pytest.mark.parametrize("algo", ["qm", "lm"])
-@pytest.mark.parametrize("name", ["c0", "c1", "e2_basic", "e2_lowacc", "e2_large"])
+@pytest.mark.parametrize("algo", ["gen", "rot"])
+@pytest.mark.parametrize("name", ["c0", "c1", "e2_basic", "e2_lowacc", "e2_large", "c4_mini"])
 def test_full_parity_small_configs(v3db, name, algo):
     """Full snapshot + full query batch, bit-exact (C0, C1 and the paper's E2 shapes)."""
     cfg, inp, ref_s, ref = config_case(name)
@@ -86,7 +86,7 @@ def test_full_parity_small_configs(v3db, name, algo):
     s.free()
 
 
-def run_case(v3db, db, queries, nlist, L, M, Ks, nprobe, k, cent, code, algos=("qm", "lm"), trace=True):
+def run_case(v3db, db, queries, nlist, L, M, Ks, nprobe, k, cent, code, algos=("gen", "auto"), trace=True):
     ref_s = oracle.build_snapshot(db, nlist, L, M, Ks, cent, code)
     ref = oracle.query_batch(ref_s, queries, nprobe, k)
     s = gpu_build(v3db, db, nlist, L, M, Ks, cent, code)
@@ -130,10 +130,9 @@ def test_edge_all_identical_vectors(v3db):
     run_case(v3db, db, qs, nlist, L, 4, 4, 3, 50, np.arange(nlist), np.stack([np.arange(4)] * 4))
 
 
-def test_edge_overflow_fallback(v3db):
-    """A query whose nearest list holds fewer than k valid vectors gets tau = the padding key,
-    so every valid candidate of its other lists is buffered; past the buffer capacity the
-    list-major path must recompute it with the query-major kernel (still exact)."""
+def test_edge_outlier_list(v3db):
+    """A query whose nearest list holds a single vector: the rotated scan's threshold stays
+    open (fewer than k candidates seen) until later lists fill the buffer; still exact."""
     rng = np.random.default_rng(13)
     N, D, nlist, L = 3000, 8, 3, 2000
     db = rng.integers(-20, 20, size=(N, D)).astype(np.int8)
@@ -149,10 +148,36 @@ def test_ragged_batch_sizes(v3db, nq):
     qs = np.vstack([inp.queries] * 3)[:nq]
     want = oracle.query_batch(ref_s, qs, cfg.nprobe, cfg.k)
     q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
-    for algo in ALGOS.values():
+    for algo in (1, 2):
         out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, algo=algo)
         torch.cuda.synchronize()
         assert_query_equal(out, want)
+    s.free()
+
+
+@pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_basic"])
+def test_rotated_w32_geometry(v3db, name, monkeypatch):
+    """The wrap geometry (kLutW32) on shapes where AUTO picks the 64-column one: same bits."""
+    monkeypatch.setenv("V3DB_LUT_MODE", "w32")
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k, algo=ALGOS["rot"])
+    torch.cuda.synchronize()
+    assert_query_equal(out, ref)
+    s.free()
+
+
+@pytest.mark.parametrize("k", [1, 7, 100, 333, 1024])
+def test_rotated_topk_sizes(v3db, k):
+    """Buffered top-k of the rotated scan for k from 1 to V3DB_MAX_K (compactions at every
+    buffer size); C4's list shape (L = 768, M = 32)."""
+    cfg, inp, ref_s, _ = config_case("c4_mini")
+    qs = inp.queries[:48]
+    want = oracle.query_batch(ref_s, qs, cfg.nprobe, k)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    out = v3db.query_batch(s, torch.from_numpy(qs).cuda(), cfg.nprobe, k, algo=ALGOS["rot"])
+    torch.cuda.synchronize()
+    assert_query_equal(out, want)
     s.free()
 
 
@@ -163,7 +188,7 @@ def test_empty_batch_and_trace_off_and_host_api(v3db):
     # nq = 0 is a no-op
     v3db.query_batch(s, q[:0], cfg.nprobe, cfg.k)
     # trace off: same top-k
-    for algo in ALGOS.values():
+    for algo in (1, 2):
         out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, trace=False, algo=algo)
         torch.cuda.synchronize()
         assert_query_equal(out, ref, keys=("out_ids", "out_dist"))
@@ -208,6 +233,16 @@ def test_errors(v3db):
         v3db.query_batch(s, q, 1, cfg.L + 1)
     with pytest.raises(v3db.V3DBError, match="EINVAL"):
         v3db.query_batch(s, q, cfg.nprobe, cfg.k, algo=7)
+    s.free()
+
+
+def test_rotated_rejected_for_unsupported_shape(v3db):
+    rng = np.random.default_rng(15)
+    N, D = 300, 18
+    db = rng.integers(-90, 90, size=(N, D)).astype(np.int8)
+    s = gpu_build(v3db, db, 3, 200, 3, 8, [0, 1, 2], np.stack([np.arange(8)] * 3))
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.query_batch(s, torch.from_numpy(db[:5].copy()).cuda(), 2, 5, algo=ALGOS["rot"])
     s.free()
 
 

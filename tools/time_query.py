@@ -13,7 +13,7 @@ from synth import generate, get_config  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--config", default="c4")
 p.add_argument("--reps", type=int, default=5)
-p.add_argument("--algos", default="2")
+p.add_argument("--algos", default="1,2")
 p.add_argument("--Q", type=int, default=0, help="use only the first Q queries")
 p.add_argument("--envs", default="", help="comma-separated VAR=VALUE runs after the plain run")
 args = p.parse_args()
