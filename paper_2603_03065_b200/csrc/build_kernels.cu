@@ -124,20 +124,27 @@ __global__ void slot_terms_kernel(const int8_t* __restrict__ mu, const int8_t* _
 
 // Byte g*G + s of slot j holds the code of subspace g*G + (j + s) mod G (lane l = j mod 32 reads
 // table column l + s, which holds that subspace).  kLutW32 additionally pre-compensates the row
-// wrap of columns l + s >= 32: the stored byte is (code - 1) mod 256 there.
-__global__ void rotate_kernel(const uint8_t* __restrict__ codes, int64_t slots, int M, int mode, int G,
-                              uint8_t* __restrict__ out) {
-  const int64_t total = slots * M;
+// wrap of columns l + s >= 32: the stored byte is (code - 1) mod 256 there.  Each 32-slot chunk
+// is stored unit-transposed: byte pos of slot j lives at chunk + (pos/U)*32*U + (j%32)*U + pos%U.
+__global__ void rotate_kernel(const uint8_t* __restrict__ codes, const int32_t* __restrict__ pterm, int nlist,
+                              int L, int Lp, int M, int mode, int G, int U, uint8_t* __restrict__ out,
+                              int32_t* __restrict__ pout) {
+  const int64_t total = static_cast<int64_t>(nlist) * Lp * M;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = e / M;
-    const int pos = static_cast<int>(e - j * M);
-    const int g = pos / G, s = pos - g * G;
-    const int lane = static_cast<int>(j & 31);
-    const int src = g * G + (lane + s) % G;
-    int v = codes[j * M + src];
-    if (mode == kLutW32 && lane + s >= 32) v = (v + 255) & 255;
-    out[e] = static_cast<uint8_t>(v);
+    const int64_t sp = e / M;                       // padded slot index i*Lp + jp
+    const int pos = static_cast<int>(e - sp * M);
+    const int i = static_cast<int>(sp / Lp), jp = static_cast<int>(sp - static_cast<int64_t>(i) * Lp);
+    const int lane = jp & 31;
+    int v = 0;
+    if (jp < L) {
+      const int g = pos / G, s = pos - g * G;
+      v = codes[(static_cast<int64_t>(i) * L + jp) * M + g * G + (lane + s) % G];
+      if (mode == kLutW32 && lane + s >= 32) v = (v + 255) & 255;
+    }
+    const int64_t chunk = sp >> 5;                  // (i*Lp + jp) / 32: chunks never straddle lists
+    out[chunk * 32 * M + (pos / U) * 32 * U + lane * U + pos % U] = static_cast<uint8_t>(v);
+    if (pos == 0) pout[sp] = jp < L ? pterm[static_cast<int64_t>(i) * L + jp] : 0;
   }
 }
 
@@ -151,11 +158,12 @@ __global__ void transpose_cb_kernel(const int8_t* __restrict__ cb, int M, int Ks
 
 }  // namespace
 
-cudaError_t rotate_codes(const uint8_t* codes, int64_t slots, int M, int mode, int G, uint8_t* codes_rot,
-                         cudaStream_t st) {
-  const int64_t total = slots * M;
+cudaError_t rotate_codes(const uint8_t* codes, const int32_t* pterm, int nlist, int L, int M, int mode, int G,
+                         uint8_t* codes_rot, int32_t* pterm_rot, cudaStream_t st) {
+  const int Lp = (L + 31) & ~31;
+  const int64_t total = static_cast<int64_t>(nlist) * Lp * M;
   const int blocks = static_cast<int>((total + 255) / 256 < 16384 ? (total + 255) / 256 : 16384);
-  rotate_kernel<<<blocks, 256, 0, st>>>(codes, slots, M, mode, G, codes_rot);
+  rotate_kernel<<<blocks, 256, 0, st>>>(codes, pterm, nlist, L, Lp, M, mode, G, rot_unit(M), codes_rot, pterm_rot);
   note_launch();
   return cudaGetLastError();
 }

@@ -19,15 +19,25 @@
 //            column l+s passes 32 wraps into the next row, which the stored byte pre-compensates
 //            ((code - 1) mod 256; row 256 duplicates row 0):
 //            address = ((byte << 7) | 4l) + immediate.                                2 ALU ops
-// Top-k: candidates with D <= tau go to a shared buffer of (D, slot) keys (warp-aggregated
-// append).  Between rounds (one 32-slot chunk per warp) the CTA compacts the buffer when it could
-// overflow during the next round: item ids are resolved, the buffer is sorted by (D, item) and
-// truncated to k, and tau = D of the k-th key.  Every key excluded by tau has k keys at or below
-// it, so the final top-k is exact.
+//
+// Streaming.  A producer warp (one lane) walks the probed lists'
+// VALID 32-slot chunks in probe order and packs them into CTA-wide stages of SEG chunks; each
+// stage is filled by one cp.async.bulk (TMA bulk copy) of codes and one of P terms per list piece
+// (~1-2 pieces per stage), completion on the stage's `full` mbarrier; the consumer warps split the
+// stage's chunks and release it on its `empty` mbarrier.  codes_rot stores each chunk
+// unit-transposed ([unit][lane][U bytes]) so the lanes' stage reads are conflict-free LDS.128/64/32.
+// Chunks holding only padding are never read: their trace entries (d_max) are written up front.
+//
+// Top-k.  Candidates with D <= tau are appended to a shared buffer
+// (warp-aggregated).  Every R stages the consumer warps meet at one named barrier; if the buffer could overflow
+// during the next epoch it is compacted: item ids are resolved, a 4-pass radix select finds the
+// k-th smallest D, tau = that D and only entries with D <= tau stay (>= k of them, so every
+// dropped key has k keys at or below it).  At the end the survivors are sorted by (D, item).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
 
+#include "tc_common.cuh"
 #include "topk.cuh"
 #include "v3db_internal.cuh"
 
@@ -37,73 +47,75 @@ int plan_lut(int M, int Ks, int d, int* G) {
   *G = 0;
   if (M < 4 || M % 4 != 0 || d % 4 != 0 || Ks < 1 || Ks > 256) return 0;
   const int g = (M % 32 == 0) ? 32 : (M % 16 == 0) ? 16 : (M % 8 == 0) ? 8 : 4;
-  const char* force = getenv("V3DB_LUT_MODE");  // test hook: "w32" forces the wrap geometry
+  const char* force = getenv("V3DB_LUT_MODE");  // test/bench hook: "w32" / "p64" force a geometry
   const bool want_w32 = force && force[0] == 'w';
-  if (!want_w32 && g == M && (M == 4 || M == 8 || M == 16 || M == 32) && Ks * 256 <= 65536) {
+  const bool want_p64 = force && force[0] == 'p';
+  const bool p64_ok = g == M && (M == 4 || M == 8 || M == 16 || M == 32);
+  const bool w32_ok = (M == 8 || M == 16 || M == 24 || M == 32 || M == 48 || M == 64 || M == 96 || M == 128) &&
+                      (M / g) * kW32GroupBytes <= 160 * 1024;
+  // default: P64 (1 ALU op per lookup) while its table is small; W32 (half the table, so more
+  // CTAs and ring stages per SM) for 256-codeword tables
+  if (p64_ok && !want_w32 && (want_p64 || Ks * 256 <= 16384 || !w32_ok)) {
     *G = g;
     return kLutP64;
   }
-  if ((M == 8 || M == 16 || M == 24 || M == 32 || M == 48 || M == 64 || M == 96 || M == 128) &&
-      (M / g) * kW32GroupBytes <= 200 * 1024) {
+  if (w32_ok) {
     *G = g;
     return kLutW32;
   }
   return 0;
 }
 
+int rot_unit(int M) { return M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4; }
+
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
+// Low 16 bits of the shared-window address of dynamic shared memory: the first 1 KB of a CTA's
+// window is reserved on sm_90+ (cudaDevAttrReservedSharedMemoryPerBlock), so it starts at 0x400;
+// checked at kernel entry.
+constexpr uint32_t kSmemLo = 0x400;
+
+// mbarrier phase wait that lets the hardware suspend the warp (instead of spinning) until the
+// phase completes or the hint expires.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ int32_t lds32(uint32_t addr) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 constexpr uint32_t kTauInit = 0x7ffffffeu;  // accept every valid D (< d_max)
 
 template <int M, int MODE>
 struct Geo {
   static constexpr int G = (M % 32 == 0) ? 32 : (M % 16 == 0) ? 16 : (M % 8 == 0) ? 8 : 4;
   static constexpr int NG = M / G;
-  static constexpr int NW = M / 4;  // 32-bit code words per slot
+  static constexpr int NW = M / 4;                                   // 32-bit code words per slot
+  static constexpr int U = M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4;    // bytes per lane per unit
   static constexpr int TGB = (MODE == kLutW32) ? kW32GroupBytes : 0;  // bytes per group table
-  static constexpr int NT = (MODE == kLutW32 && NG * kW32GroupBytes > 100 * 1024) ? 512 : 256;
-  static constexpr int MINB = (MODE == kLutP64) ? 3 : (NT == 512 ? 1 : 2);
+  static constexpr int NT = (MODE == kLutW32 && NG * kW32GroupBytes > 100 * 1024) ? 512 : 256;  // consumers
+  static constexpr int NTOT = NT + 32;                              // + the producer warp
+  static constexpr int MINB = NT == 512 ? 1 : 2;
 };
-
-template <int M>
-__device__ __forceinline__ void load_codes(const uint8_t* p, uint32_t (&w)[M / 4]) {
-  if constexpr (M % 16 == 0) {
-#pragma unroll
-    for (int v = 0; v < M / 16; ++v) {
-      uint4 x;
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
-                   : "l"(p + 16 * v));
-      w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
-    }
-  } else if constexpr (M % 8 == 0) {
-#pragma unroll
-    for (int v = 0; v < M / 8; ++v) {
-      uint2 x;
-      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(x.x), "=r"(x.y) : "l"(p + 8 * v));
-      w[2 * v] = x.x; w[2 * v + 1] = x.y;
-    }
-  } else {
-#pragma unroll
-    for (int v = 0; v < M / 4; ++v)
-      asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(w[v]) : "l"(p + 4 * v));
-  }
-}
-
-__device__ __forceinline__ int32_t ld_nc_i32(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
 
 struct RotArgs {
   const int8_t* queries;
-  int dim, d, Ks, L, nprobe, k, cap;
+  int dim, d, Ks, L, Lp, nprobe, k, cap, NS, SEG, R;
+  uint32_t off_stage, off_desc, off_buf, off_hist, off_probe, off_q, off_int, off_bar, stage_bytes;
   const int8_t* cbT;
-  const uint8_t* codes;   // codes_rot
-  const int32_t* pterm;
-  const int32_t* ids;
+  const uint8_t* codes;   // codes_rot [nlist][Lp/32][unit][lane][U]
+  const int32_t* pterm;   // pterm_rot [nlist][Lp]
+  const int32_t* ids;     // [nlist][L]
   const int32_t* counts;
   const int32_t* lists;
   const int32_t* ldist;
@@ -112,9 +124,17 @@ struct RotArgs {
   int32_t* trace;
 };
 
-// Shared-memory layout (bytes): [LUT tables][buf: cap x u64][probe: nprobe x int4][q: dim][scalars]
-__host__ __device__ inline uint32_t lut_bytes(int mode, int M, int G, int Ks) {
-  return mode == kLutP64 ? static_cast<uint32_t>(Ks) * 256u : static_cast<uint32_t>(M / G) * kW32GroupBytes;
+// Named barrier 1 among the NT consumer threads (the producer warp never joins).
+template <int NT>
+__device__ __forceinline__ void bar_c() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
 }
 
 // Exact sort of buf[0, P) ascending (bitonic network; P a power of two).  All threads call.
@@ -132,103 +152,221 @@ __device__ __forceinline__ void bitonic_sort(uint64_t* buf, int P) {
           buf[hi] = a;
         }
       }
-      __syncthreads();
+      bar_c<NT>();
     }
   }
 }
 
-// Resolve item ids of the unresolved entries [nres, n), sort, keep the first min(n, k), set tau.
-template <int NT>
-__device__ void compact(uint64_t* buf, const int4* probe, int* s_int, const RotArgs& a, int n) {
-  const int nres = s_int[1];
-  for (int e = nres + static_cast<int>(threadIdx.x); e < n; e += NT) {
-    const uint64_t key = buf[e];
-    const uint32_t flat = static_cast<uint32_t>(key);
-    const int rho = static_cast<int>(flat / static_cast<uint32_t>(a.L));
-    const int j = static_cast<int>(flat - static_cast<uint32_t>(rho) * a.L);
-    const int32_t id = __ldg(a.ids + static_cast<int64_t>(probe[rho].x) * a.L + j);
-    buf[e] = (key & 0xffffffff00000000ull) | (static_cast<uint32_t>(id) ^ 0x80000000u);
+// Compaction of buf[0, n): entries [nres, n) hold (D, flat slot) and are resolved to (D, item)
+// keys; if n > k only the entries with D <= (k-th smallest D) stay; if ties at that D leave more
+// than `limit`, the exact k smallest keys are kept (bitonic sort).  Returns the new count and
+// sets *tau (CTA-uniform).  All threads call; n, nres uniform.
+template <int NT, int CAPM>
+__device__ int compact(uint64_t* buf, int* hist, int* s_int, const int4* probe, const RotArgs& a, int n, int nres,
+                       int limit, uint32_t* tau) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t kv[CAPM];
+#pragma unroll
+  for (int r = 0; r < CAPM; ++r) {
+    const int e = tid + r * NT;
+    kv[r] = ~0ull;
+    if (e < n) {
+      uint64_t key = buf[e];
+      if (e >= nres) {
+        const uint32_t flat = static_cast<uint32_t>(key);
+        const int rho = static_cast<int>(flat / static_cast<uint32_t>(a.L));
+        const int j = static_cast<int>(flat - static_cast<uint32_t>(rho) * a.L);
+        const int32_t id = __ldg(a.ids + static_cast<int64_t>(probe[rho].x) * a.L + j);
+        key = (key & 0xffffffff00000000ull) | (static_cast<uint32_t>(id) ^ 0x80000000u);
+      }
+      kv[r] = key;
+    }
   }
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int e = n + static_cast<int>(threadIdx.x); e < P; e += NT) buf[e] = ~0ull;
-  __syncthreads();
-  bitonic_sort<NT>(buf, P);
-  if (threadIdx.x == 0) {
-    const int keep = n < a.k ? n : a.k;
-    s_int[0] = keep;
-    s_int[1] = keep;
-    if (n >= a.k) s_int[2] = static_cast<int>(buf[a.k - 1] >> 32);
+  if (n <= a.k) {  // nothing to select: write the resolved keys back
+    bar_c<NT>();
+#pragma unroll
+    for (int r = 0; r < CAPM; ++r)
+      if (tid + r * NT < n) buf[tid + r * NT] = kv[r];
+    bar_c<NT>();
+    return n;
   }
-  __syncthreads();
+  // 4-pass radix select (8-bit digits) of the k-th smallest D.
+  uint32_t prefix = 0;
+  int kk = a.k;
+#pragma unroll 1
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int b = tid; b < 256; b += NT) hist[b] = 0;
+    bar_c<NT>();
+#pragma unroll
+    for (int r = 0; r < CAPM; ++r) {
+      const uint32_t D = static_cast<uint32_t>(kv[r] >> 32);
+      if (tid + r * NT < n && (pass == 0 || (D >> (shift + 8)) == prefix)) atomicAdd(&hist[(D >> shift) & 255], 1);
+    }
+    bar_c<NT>();
+    if (warp == 0) {
+      int h[8], sum = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        h[b] = hist[lane * 8 + b];
+        sum += h[b];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int cum = incl - sum;  // exclusive prefix of this lane's 8 bins
+      const bool mine = cum < kk && kk <= incl;
+      if (mine) {
+        int bin = lane * 8;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (cum + h[b] >= kk) break;
+          cum += h[b];
+          ++bin;
+        }
+        s_int[8] = bin;
+        s_int[9] = kk - cum;
+      }
+    }
+    bar_c<NT>();
+    prefix = (prefix << 8) | static_cast<uint32_t>(s_int[8]);
+    kk = s_int[9];
+    bar_c<NT>();  // s_int[8..9] reused next pass
+  }
+  const uint32_t tauD = prefix;  // exact k-th smallest D
+  if (tid == 0) s_int[10] = 0;
+  bar_c<NT>();
+#pragma unroll
+  for (int r = 0; r < CAPM; ++r) {
+    const bool keep = tid + r * NT < n && static_cast<uint32_t>(kv[r] >> 32) <= tauD;
+    const uint32_t bal = __ballot_sync(kFull, keep);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&s_int[10], __popc(bal));
+    base = __shfl_sync(kFull, base, 0);
+    if (keep) buf[base + __popc(bal & ((1u << lane) - 1u))] = kv[r];
+  }
+  bar_c<NT>();
+  int kept = s_int[10];
+  *tau = tauD;
+  if (kept > limit) {  // many ties at tauD: exact (D, item) selection
+    int P = 1;
+    while (P < kept) P <<= 1;
+    for (int e = kept + tid; e < P; e += NT) buf[e] = ~0ull;
+    bar_c<NT>();
+    bitonic_sort<NT>(buf, P);
+    kept = a.k;
+  }
+  bar_c<NT>();
+  return kept;
 }
 
-template <int M, int MODE>
-__global__ void __launch_bounds__(Geo<M, MODE>::NT, Geo<M, MODE>::MINB) scan_rot_kernel(const RotArgs a) {
+template <int M, int MODE, int CAPM>
+__global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_rot_kernel(const RotArgs a) {
   using C = Geo<M, MODE>;
-  constexpr int NT = C::NT, W = NT / 32, G = C::G, NG = C::NG, NW = C::NW;
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t lbytes = lut_bytes(MODE, M, G, a.Ks);
-  uint64_t* buf = reinterpret_cast<uint64_t*>(smem + lbytes);
-  int4* probe = reinterpret_cast<int4*>(buf + a.cap);                // (list, d_i, count, 0)
-  int8_t* qs = reinterpret_cast<int8_t*>(probe + a.nprobe);
-  int* s_int = reinterpret_cast<int*>(qs + ((a.dim + 15) & ~15));   // [0] count [1] resolved [2] tau
+  constexpr int NT = C::NT, W = NT / 32, G = C::G, NG = C::NG, NW = C::NW, U = C::U;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* stages = smem + a.off_stage;                        // [NS][SEG*32*M codes | SEG*128 P]
+  int* vcoff = reinterpret_cast<int*>(smem + a.off_desc);      // [nprobe+1] prefix sums of valid chunks
+  uint64_t* buf = reinterpret_cast<uint64_t*>(smem + a.off_buf);
+  int* hist = reinterpret_cast<int*>(smem + a.off_hist);
+  int4* probe = reinterpret_cast<int4*>(smem + a.off_probe);  // (list, d_i, count, 0)
+  int8_t* qs = reinterpret_cast<int8_t*>(smem + a.off_q);
+  int* s_int = reinterpret_cast<int*>(smem + a.off_int);     // [0..2] epoch counters, [8..10] scratch
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  uint64_t* empty = full + a.NS;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t qi = blockIdx.x;
-  const int L = a.L, nprobe = a.nprobe;
+  const int L = a.L, nprobe = a.nprobe, NS = a.NS, SEG = a.SEG;
+  const uint32_t pbase = static_cast<uint32_t>(SEG) * 32u * M;  // P terms inside a stage
 
-  for (int u = tid; u < a.dim; u += NT) qs[u] = a.queries[qi * a.dim + u];
-  for (int r = tid; r < nprobe; r += NT) {
+  for (int u = tid; u < a.dim; u += C::NTOT) qs[u] = a.queries[qi * a.dim + u];
+  for (int r = tid; r < nprobe; r += C::NTOT) {
     const int li = a.lists[qi * nprobe + r];
     probe[r] = make_int4(li, a.ldist[qi * nprobe + r], __ldg(a.counts + li), 0);
   }
+  if (tid < 16) s_int[tid] = 0;
   if (tid == 0) {
-    s_int[0] = 0;
-    s_int[1] = 0;
-    s_int[2] = static_cast<int>(kTauInit);
+    for (int s = 0; s < NS; ++s) {
+      tc::mbar_init(full + s, 1);
+      tc::mbar_init(empty + s, W);
+    }
+  }
+  tc::mbar_fence_init();
+  __syncthreads();
+  // valid-chunk prefix sums: the g-th valid chunk of the query (probe order) is chunk
+  // g - vcoff[rho] of probe rho, vcoff[rho] <= g < vcoff[rho + 1]
+  if (warp == 0) {
+    int carry = 0;
+    for (int r0 = 0; r0 < nprobe; r0 += 32) {
+      const int r = r0 + lane;
+      const int cv = r < nprobe ? (probe[r].z + 31) >> 5 : 0;
+      int incl = cv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (r < nprobe) vcoff[r] = carry + incl - cv;
+      carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) vcoff[nprobe] = carry;
   }
   __syncthreads();
+  const int TV = vcoff[nprobe];               // valid chunks of this query
+  const int NSTG = (TV + SEG - 1) / SEG;      // stages: [t*SEG, min(TV, (t+1)*SEG))
 
-  const int cpl = (L + 31) >> 5;              // 32-slot chunks per list
-  const int nchunks = nprobe * cpl;
-  const int nrounds = (nchunks + W - 1) / W;
-  const uint32_t lane4 = 4u * lane;
-
-  // chunk c = round * W + warp  ->  (rho, jc); advanced incrementally
-  int c = warp, rho = warp / cpl, jc = warp - (warp / cpl) * cpl;
-
-  // prefetch the first chunk while the LUT is built
-  uint32_t cur[NW];
-  int32_t pcur = 0;
-  auto fetch = [&](int c_, int rho_, int jc_, uint32_t(&w)[NW], int32_t& p) {
-#pragma unroll
-    for (int v = 0; v < NW; ++v) w[v] = 0;
-    p = 0;
-    if (c_ < nchunks) {
-      const int4 pr = probe[rho_];
-      const int j = jc_ * 32 + lane;
-      if (j < pr.z) {
-        const int64_t slot = static_cast<int64_t>(pr.x) * L + j;
-        load_codes<M>(a.codes + slot * M, w);
-        p = ld_nc_i32(a.pterm + slot);
+  if (warp == W) {
+    // ------------------------------------------------ producer: one lane issues every stage
+    if (lane == 0) {
+      int rho = 0, s = 0;
+      uint32_t eph = 0;  // parity of the empty-barrier phase to wait for (per ring pass)
+      for (int t = 0; t < NSTG; ++t) {
+        if (t >= NS) mbar_wait_sleep(empty + s, eph);  // consumers released the previous fill
+        uint8_t* st = stages + static_cast<uint32_t>(s) * a.stage_bytes;
+        const int g0 = t * SEG, g1 = min(TV, g0 + SEG);
+        tc::mbar_expect_tx(full + s, static_cast<uint32_t>(g1 - g0) * (32u * M + 128u));
+        // one codes copy and one P copy per piece (a run of valid chunks of one list)
+        for (int g = g0; g < g1;) {
+          while (vcoff[rho + 1] <= g) ++rho;
+          const int jc = g - vcoff[rho];
+          const int m = min(g1 - g, vcoff[rho + 1] - g);
+          const int64_t slot0 = static_cast<int64_t>(probe[rho].x) * a.Lp + jc * 32;
+          const uint32_t i = static_cast<uint32_t>(g - g0);
+          bulk_g2s(st + i * 32u * M, a.codes + slot0 * M, static_cast<uint32_t>(m) * 32u * M, full + s);
+          bulk_g2s(st + pbase + i * 128u, a.pterm + slot0, static_cast<uint32_t>(m) * 128u, full + s);
+          g += m;
+        }
+        if (++s == NS) {
+          s = 0;
+          if (t + 1 > NS) eph ^= 1u;
+        }
       }
     }
-  };
-  fetch(c, rho, jc, cur, pcur);
+    return;
+  }
+
+  // ------------------------------------------------ consumers
+  // trace of chunks that hold only padding: D = d_max (never read from HBM)
+  if (a.trace) {
+    for (int r = warp; r < nprobe; r += W) {
+      const int cv = (probe[r].z + 31) >> 5;
+      int32_t* tr = a.trace + (qi * nprobe + r) * static_cast<int64_t>(L);
+      for (int j = cv * 32 + lane; j < L; j += 32) __stcs(tr + j, kDMax);
+    }
+  }
 
   // Step 3 (factorised): A_q[m][c] = -2 <C_{m,c}, q^{(m)}>, written into the rotated tables.
+  // Four entries per thread per step with their codebook loads issued together (latency-bound
+  // otherwise: one L2 round trip per entry).
   {
     int32_t* T = reinterpret_cast<int32_t*>(smem);
-    const int d = a.d;
-    for (int e = tid; e < M * a.Ks; e += NT) {
+    const int dw = a.d >> 2, MK = M * a.Ks;
+    auto put = [&](int e, int32_t A) {
       const int m = e % M, cc = e / M;
-      const int8_t* cw = a.cbT + (static_cast<int64_t>(cc) * M + m) * d;
-      const int8_t* qm = qs + m * d;
-      int acc = 0;
-      for (int u = 0; u < d; u += 4)
-        acc = __dp4a(*reinterpret_cast<const int*>(cw + u), *reinterpret_cast<const int*>(qm + u), acc);
-      const int32_t A = -2 * acc;
       const int g = m / G, r = m - g * G;
       if constexpr (MODE == kLutP64) {
 #pragma unroll
@@ -241,81 +379,156 @@ __global__ void __launch_bounds__(Geo<M, MODE>::NT, Geo<M, MODE>::MINB) scan_rot
           if (cc == 0) Tg[256 * 32 + col] = A;  // row 256 duplicates row 0 (wrap of code 0)
         }
       }
-    }
-  }
-  __syncthreads();
-
-  uint32_t tau = kTauInit;
-  int n_buf = 0;  // entries in buf (CTA-uniform: counted with __syncthreads_count)
-  const int64_t trace_base = qi * nprobe;
-  for (int round = 0; round < nrounds; ++round) {
-    // next chunk of this warp
-    int c2 = c + W, rho2 = rho, jc2 = jc + W;
-    while (jc2 >= cpl) {
-      jc2 -= cpl;
-      ++rho2;
-    }
-    uint32_t nxt[NW];
-    int32_t pnxt;
-    fetch(c2, rho2, jc2, nxt, pnxt);
-
-    bool pass = false;
-    if (c < nchunks) {
-      const int4 pr = probe[rho];
-      const int j = jc * 32 + lane;
-      int32_t D = kDMax;
-      if (jc * 32 < pr.z) {  // warp-uniform: the chunk holds valid slots
-        int32_t acc = pr.y + pcur;
+    };
+    const int* cbw = reinterpret_cast<const int*>(a.cbT);   // [Ks][M][dw] words
+    const int* qw = reinterpret_cast<const int*>(qs);       // [M][dw] words
+    for (int e0 = tid; e0 < MK; e0 += 4 * NT) {
+      int acc[4] = {0, 0, 0, 0};
+      if (dw == 1) {
+        int cwv[4];
 #pragma unroll
-        for (int g = 0; g < NG; ++g) {
+        for (int x = 0; x < 4; ++x) cwv[x] = e0 + x * NT < MK ? __ldg(cbw + e0 + x * NT) : 0;
 #pragma unroll
-          for (int s = 0; s < G; ++s) {
-            const int pos = g * G + s;
-            const uint32_t w = cur[pos >> 2];
-            uint32_t ad;
-            if constexpr (MODE == kLutP64) {
-              ad = __byte_perm(w, lane4, 0x5504u | ((pos & 3) << 4));
-            } else {
-              const int b = pos & 3;
-              const uint32_t sh = (b == 0) ? (w << 7) : (w >> (8 * b - 7));
-              ad = (sh & 0x7f80u) | lane4;
-            }
-            acc += *reinterpret_cast<const int32_t*>(smem + (g * C::TGB + 4 * s) + ad);
+        for (int x = 0; x < 4; ++x) acc[x] = __dp4a(cwv[x], qw[(e0 + x * NT) % M], 0);
+      } else if (dw == 2) {
+        int2 cwv[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          cwv[x] = e0 + x * NT < MK ? __ldg(reinterpret_cast<const int2*>(cbw) + e0 + x * NT) : make_int2(0, 0);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const int m = (e0 + x * NT) % M;
+          acc[x] = __dp4a(cwv[x].y, qw[2 * m + 1], __dp4a(cwv[x].x, qw[2 * m], 0));
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const int e = e0 + x * NT;
+          if (e < MK) {
+            const int m = e % M;
+            for (int u = 0; u < dw; ++u) acc[x] = __dp4a(__ldg(cbw + static_cast<int64_t>(e) * dw + u), qw[m * dw + u], acc[x]);
           }
         }
-        if (j < pr.z) D = acc;
       }
-      if (a.trace && j < L) __stcs(a.trace + (trace_base + rho) * L + j, D);
-      pass = j < pr.z && static_cast<uint32_t>(D) <= tau;
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        if (e0 + x * NT < MK) put(e0 + x * NT, -2 * acc[x]);
+    }
+  }
+  bar_c<NT>();
+
+  // LUT addressing: the address register is built by one PRMT (P64) or SHF+LOP3 (W32) with the
+  // lane's column and the high half of the shared-window address OR-ed in; the low half of the
+  // dynamic shared-memory base (kSmemLo) and the step offset go into the LDS immediate.
+  const uint32_t sbase = tc::smem_u32(smem);
+  if ((sbase & 0xffffu) != kSmemLo) __trap();  // layout assumption
+  // lane4 = 4 * lane | high half of the window address, kept in ONE register: read back from shared
+  // memory so the compiler cannot split the OR into two instructions per lookup
+  if (tid < 32) s_int[32 + tid] = static_cast<int>(4u * tid | (sbase & 0xffff0000u));
+  bar_c<NT>();
+  const uint32_t lane4 = static_cast<uint32_t>(*reinterpret_cast<volatile int*>(&s_int[32 + lane]));
+  int32_t* trq = a.trace ? a.trace + qi * nprobe * static_cast<int64_t>(L) + lane : nullptr;  // this query's trace
+  const int limit = a.cap - a.R * SEG * 32;  // an epoch appends at most R * SEG * 32 entries
+  uint32_t tau = kTauInit;
+  int n_base = 0, n_res = 0;                 // buffer entries before this epoch / resolved prefix
+  int epoch = 0, in_epoch = 0;
+
+  uint32_t fph = 0;
+  int crho = 0;  // this warp's probe cursor (its chunks g increase monotonically)
+  for (int t = 0, s = 0; t < NSTG; ++t) {
+    mbar_wait_sleep(full + s, fph);
+    const uint8_t* st = stages + static_cast<uint32_t>(s) * a.stage_bytes;
+    const int g0 = t * SEG, n = min(TV, g0 + SEG) - g0;
+    for (int i = warp; i < n; i += W) {
+      const int g = g0 + i;
+      while (vcoff[crho + 1] <= g) ++crho;
+      const int rho = crho, jc = g - vcoff[crho];
+      const int4 pr = probe[rho];
+      const int nv = min(32, pr.z - jc * 32);
+      uint32_t w[NW];
+      const uint8_t* cp = st + static_cast<uint32_t>(i) * 32u * M;
+#pragma unroll
+      for (int u = 0; u < M / U; ++u) {
+        const uint8_t* p = cp + u * 32 * U + lane * U;
+        if constexpr (U == 16) {
+          const uint4 x = *reinterpret_cast<const uint4*>(p);
+          w[4 * u] = x.x; w[4 * u + 1] = x.y; w[4 * u + 2] = x.z; w[4 * u + 3] = x.w;
+        } else if constexpr (U == 8) {
+          const uint2 x = *reinterpret_cast<const uint2*>(p);
+          w[2 * u] = x.x; w[2 * u + 1] = x.y;
+        } else {
+          w[u] = *reinterpret_cast<const uint32_t*>(p);
+        }
+      }
+      int32_t acc = pr.y + *reinterpret_cast<const int32_t*>(st + pbase + static_cast<uint32_t>(i) * 128u + 4 * lane);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+#pragma unroll
+        for (int s2 = 0; s2 < G; ++s2) {
+          const int pos = g * G + s2;
+          const uint32_t wd = w[pos >> 2];
+          uint32_t ad;
+          if constexpr (MODE == kLutP64) {
+            ad = __byte_perm(wd, lane4, 0x7604u | ((pos & 3) << 4));  // code << 8 | lane4
+          } else {
+            const int b = pos & 3;
+            const uint32_t sh = (b == 0) ? (wd << 7) : (wd >> (8 * b - 7));
+            ad = (sh & 0x7f80u) | lane4;
+          }
+          acc += lds32(ad + (kSmemLo + g * C::TGB + 4 * s2));
+        }
+      }
+      // lanes past the list's valid slots read stale stage bytes (always in-table addresses)
+      const bool valid = lane < nv;
+      const int32_t D = valid ? acc : kDMax;
+      const int j = jc * 32 + lane;
+      if (trq && j < L) __stcs(trq + (rho * L + jc * 32), D);
+      const bool pass = valid && static_cast<uint32_t>(D) <= tau;
       const uint32_t bal = __ballot_sync(kFull, pass);
       if (bal) {
         int base = 0;
-        if (lane == 0) base = atomicAdd(&s_int[0], __popc(bal));
+        if (lane == 0) base = atomicAdd(&s_int[epoch % 3], __popc(bal));
         base = __shfl_sync(kFull, base, 0);
         if (pass)
-          buf[base + __popc(bal & ((1u << lane) - 1u))] =
+          buf[n_base + base + __popc(bal & ((1u << lane) - 1u))] =
               (static_cast<uint64_t>(static_cast<uint32_t>(D)) << 32) | static_cast<uint32_t>(rho * L + j);
       }
     }
-    n_buf += __syncthreads_count(pass);           // barrier: this round's appends are visible
-    if (n_buf > a.cap - NT || round == nrounds - 1) {  // CTA-uniform
-      compact<NT>(buf, probe, s_int, a, n_buf);
-      n_buf = n_buf < a.k ? n_buf : a.k;
-      tau = static_cast<uint32_t>(s_int[2]);        // written only inside compact()
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(empty + s);  // this warp is done with the stage
+    if (++s == NS) {
+      s = 0;
+      fph ^= 1u;
     }
-    c = c2;
-    rho = rho2;
-    jc = jc2;
-#pragma unroll
-    for (int v = 0; v < NW; ++v) cur[v] = nxt[v];
-    pcur = pnxt;
+    if (++in_epoch == a.R) {                    // epoch boundary (uniform across consumers)
+      bar_c<NT>();
+      n_base += s_int[epoch % 3];
+      if (tid == 0) s_int[(epoch + 2) % 3] = 0;  // next used in epoch + 2; last read before this barrier
+      ++epoch;
+      in_epoch = 0;
+      if (n_base > limit) {
+        uint32_t t2;
+        n_base = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, n_res, limit, &t2);
+        n_res = n_base;
+        tau = t2;
+      }
+    }
   }
+  bar_c<NT>();
+  n_base += s_int[epoch % 3];
 
-  // Step 5 output: the first k keys of the buffer, (d_max, -1) past the valid candidates (R11).
-  const int kept = n_buf;
+  // Final Step 5: the k smallest (D, item) keys, (d_max, -1) past the valid candidates (R11).
+  uint32_t t2;
+  int n = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, n_res, a.k, &t2);
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int e = n + tid; e < P; e += NT) buf[e] = ~0ull;
+  bar_c<NT>();
+  bitonic_sort<NT>(buf, P);
+  if (n > a.k) n = a.k;
   for (int r = tid; r < a.k; r += NT) {
     int32_t id = -1, dd = kDMax;
-    if (r < kept) {
+    if (r < n) {
       const uint64_t key = buf[r];
       id = step5_id(key);
       dd = static_cast<int32_t>(key >> 32);
@@ -325,20 +538,75 @@ __global__ void __launch_bounds__(Geo<M, MODE>::NT, Geo<M, MODE>::MINB) scan_rot
   }
 }
 
-template <int M, int MODE>
-cudaError_t launch(const RotArgs& a, int64_t nq, size_t smem, cudaStream_t st) {
+template <int M, int MODE, int CAPM>
+cudaError_t launch_cap(const RotArgs& a, int64_t nq, size_t smem, cudaStream_t st) {
   using C = Geo<M, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(scan_rot_kernel<M, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(scan_rot_kernel<M, MODE, CAPM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  scan_rot_kernel<M, MODE><<<static_cast<unsigned>(nq), C::NT, smem, st>>>(a);
+  scan_rot_kernel<M, MODE, CAPM><<<static_cast<unsigned>(nq), C::NTOT, smem, st>>>(a);
   note_launch();
   return cudaGetLastError();
 }
 
-template <int MODE>
-int threads_for(int M, int G) {
-  return (MODE == kLutW32 && (M / G) * kW32GroupBytes > 100 * 1024) ? 512 : 256;
+template <int M, int MODE>
+cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
+  using C = Geo<M, MODE>;
+  constexpr int NT = C::NT;
+  auto al = [](uint32_t x, uint32_t b) { return (x + b - 1) / b * b; };
+  const uint32_t lut = MODE == kLutP64 ? static_cast<uint32_t>(a.Ks) * 256u : C::NG * kW32GroupBytes;
+  const uint32_t chunk = 32u * M + 128u;  // codes + P terms of one 32-slot chunk
+  // (SEG, NS, cap): the first candidate that fits the per-CTA budget.  A bigger candidate buffer
+  // (cap) lets an epoch span more stages (fewer consumer barriers); 2-3 stages in flight suffice.
+  static const int cand[][3] = {{16, 3, 2048}, {16, 3, 1024}, {16, 2, 2048}, {8, 4, 1024}, {16, 2, 1024},
+                                {8, 3, 1024}, {8, 2, 1024}};
+  int SEG = 8, NS = 2, cap = 1024;
+  size_t smem = 0;
+  const char* e_seg = getenv("V3DB_SEG");  // experiments: force (SEG, NS)
+  const char* e_ns = getenv("V3DB_NS");
+  for (const auto& c : cand) {
+    const int seg = e_seg ? atoi(e_seg) : c[0], ns = e_ns ? atoi(e_ns) : c[1];
+    const int cp = a.k + seg * 32 <= c[2] ? c[2] : 2048;
+    const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) +
+                        8u * cp + 256 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
+    SEG = seg;
+    NS = ns;
+    cap = cp;
+    smem = need;
+    if (need <= static_cast<size_t>(smem_budget) || (e_seg && e_ns)) break;
+  }
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  a.SEG = SEG;
+  a.NS = NS;
+  a.cap = cap;
+  a.R = (cap - a.k) / (SEG * 32);  // >= 1: after a compaction at most k entries remain
+  a.stage_bytes = al(SEG * chunk, 128);
+  uint32_t o = al(lut, 128);
+  a.off_stage = o;
+  o += NS * a.stage_bytes;
+  a.off_desc = o;
+  o += al(4u * (a.nprobe + 1), 16);
+  a.off_buf = o;
+  o += 8u * cap;
+  a.off_hist = o;
+  o += 256 * 4;
+  a.off_probe = o;
+  o += 16u * a.nprobe;
+  a.off_q = o;
+  o += al(a.dim, 16);
+  a.off_int = o;
+  o += 256;
+  a.off_bar = o;
+  const int capm = cap / NT;
+  if (capm <= 2) return launch_cap<M, MODE, 2>(a, nq, smem, st);
+  if (capm <= 4) return launch_cap<M, MODE, 4>(a, nq, smem, st);
+  return launch_cap<M, MODE, 8>(a, nq, smem, st);
+}
+
+template <int M, int MODE>
+int budget() {
+  using C = Geo<M, MODE>;
+  return (228 * 1024) / C::MINB - 1024;  // per-CTA share of the SM (1 KB reserved per CTA)
 }
 
 }  // namespace
@@ -348,22 +616,18 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
                          int32_t* trace, cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
   if (s->lut_mode == 0) return cudaErrorInvalidValue;
-  const int nt = s->lut_mode == kLutP64 ? 256 : threads_for<kLutW32>(s->M, s->lut_g);
-  // buffer: after a compaction at most k entries; one round appends at most nt
-  int cap = 512;
-  while (cap < k + 2 * nt) cap <<= 1;
   RotArgs a;
   a.queries = queries;
   a.dim = s->dim;
   a.d = s->d;
   a.Ks = s->Ks;
   a.L = s->L;
+  a.Lp = (s->L + 31) & ~31;
   a.nprobe = nprobe;
   a.k = k;
-  a.cap = cap;
   a.cbT = s->cbT;
   a.codes = s->codes_rot;
-  a.pterm = s->pterm;
+  a.pterm = s->pterm_rot;
   a.ids = s->ids;
   a.counts = s->counts;
   a.lists = lists;
@@ -371,29 +635,28 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
   a.out_ids = out_ids;
   a.out_dist = out_dist;
   a.trace = trace;
-  const size_t smem = lut_bytes(s->lut_mode, s->M, s->lut_g, s->Ks) + sizeof(uint64_t) * cap +
-                      sizeof(int4) * nprobe + ((s->dim + 15) & ~15) + 16;
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+#define V3DB_ROT(MM, MODE) return launch<MM, MODE>(a, nq, budget<MM, MODE>(), st);
   if (s->lut_mode == kLutP64) {
     switch (s->M) {
-      case 4: return launch<4, kLutP64>(a, nq, smem, st);
-      case 8: return launch<8, kLutP64>(a, nq, smem, st);
-      case 16: return launch<16, kLutP64>(a, nq, smem, st);
-      case 32: return launch<32, kLutP64>(a, nq, smem, st);
+      case 4: V3DB_ROT(4, kLutP64)
+      case 8: V3DB_ROT(8, kLutP64)
+      case 16: V3DB_ROT(16, kLutP64)
+      case 32: V3DB_ROT(32, kLutP64)
       default: return cudaErrorInvalidValue;
     }
   }
   switch (s->M) {
-    case 8: return launch<8, kLutW32>(a, nq, smem, st);
-    case 16: return launch<16, kLutW32>(a, nq, smem, st);
-    case 24: return launch<24, kLutW32>(a, nq, smem, st);
-    case 32: return launch<32, kLutW32>(a, nq, smem, st);
-    case 48: return launch<48, kLutW32>(a, nq, smem, st);
-    case 64: return launch<64, kLutW32>(a, nq, smem, st);
-    case 96: return launch<96, kLutW32>(a, nq, smem, st);
-    case 128: return launch<128, kLutW32>(a, nq, smem, st);
+    case 8: V3DB_ROT(8, kLutW32)
+    case 16: V3DB_ROT(16, kLutW32)
+    case 24: V3DB_ROT(24, kLutW32)
+    case 32: V3DB_ROT(32, kLutW32)
+    case 48: V3DB_ROT(48, kLutW32)
+    case 64: V3DB_ROT(64, kLutW32)
+    case 96: V3DB_ROT(96, kLutW32)
+    case 128: V3DB_ROT(128, kLutW32)
     default: return cudaErrorInvalidValue;
   }
+#undef V3DB_ROT
 }
 
 }  // namespace v3db

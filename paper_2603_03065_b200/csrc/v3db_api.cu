@@ -65,6 +65,7 @@ void free_snapshot(v3db_snapshot* s) {
   cudaFree(s->pterm);
   cudaFree(s->list_of);
   cudaFree(s->codes_rot);
+  cudaFree(s->pterm_rot);
   cudaFree(s->cbT);
   delete s;
 }
@@ -292,9 +293,13 @@ int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist,
   // layouts of the rotated-LUT scan
   s->lut_mode = v3db::plan_lut(m, ks, d, &s->lut_g);
   if (s->lut_mode != 0) {
-    V3DB_CUDA(cudaMalloc(&s->codes_rot, static_cast<size_t>(slots) * m));
+    // padded list stride Lp; +256 B so rounded-up bulk copies of the last chunk stay in bounds
+    const int64_t pslots = static_cast<int64_t>(nlist) * ((L + 31) & ~31);
+    V3DB_CUDA(cudaMalloc(&s->codes_rot, static_cast<size_t>(pslots) * m + 256));
+    V3DB_CUDA(cudaMalloc(&s->pterm_rot, sizeof(int32_t) * pslots + 256));
     V3DB_CUDA(cudaMalloc(&s->cbT, static_cast<size_t>(m) * ks * d));
-    V3DB_CUDA(v3db::rotate_codes(s->codes, slots, m, s->lut_mode, s->lut_g, s->codes_rot, st));
+    V3DB_CUDA(v3db::rotate_codes(s->codes, s->pterm, nlist, L, m, s->lut_mode, s->lut_g, s->codes_rot, s->pterm_rot,
+                                 st));
     V3DB_CUDA(v3db::transpose_codebooks(s->codebooks, m, ks, d, s->cbT, st));
   }
   V3DB_CUDA(cudaStreamSynchronize(st));

@@ -9,8 +9,11 @@
 //   counts     int32 [nlist]               valid slots (valid slots come first, R7)
 //   pterm      int32 [nlist][L]            P_{i,j} = ||xhat_ij||^2 + 2<mu_i, xhat_ij>
 //   list_of    int32 [n]                   final list of every vector (export/tests)
-//   codes_rot  uint8 [nlist][L][M]         codes re-ordered for the conflict-free rotated LUT
-//                                          scan (scan_rot.cu)
+//   codes_rot  uint8 [nlist][Lp/32][M/U][32][U]  codes re-ordered for the conflict-free rotated
+//                                          LUT scan: per 32-slot chunk, unit-transposed (U = 16/8/4
+//                                          bytes), bytes rotated per slot (DESIGN.md "Rotated LUT
+//                                          layout"); Lp = L rounded up to 32
+//   pterm_rot  int32 [nlist][Lp]           P_{i,j} with the padded list stride
 //   cbT        int8  [Ks][M][d]            codebooks, codeword-major (coalesced LUT build)
 #pragma once
 #include <cuda_runtime.h>
@@ -35,6 +38,7 @@ struct v3db_snapshot {
   // kLutP64 / kLutW32 = table geometry; lut_g = subspaces per rotation group.
   int lut_mode = 0, lut_g = 0;
   uint8_t* codes_rot = nullptr;
+  int32_t* pterm_rot = nullptr;
   int8_t* cbT = nullptr;
 };
 
@@ -72,9 +76,11 @@ constexpr int kLutW32 = 2;   // G = gcd(M, 32), M/G groups of 257 rows x 32 colu
 constexpr int kW32GroupBytes = 257 * 32 * 4;
 // Chooses the geometry for (M, Ks, d): returns the mode (0 = generic scan) and sets *G.
 int plan_lut(int M, int Ks, int d, int* G);
-// Build: codes_rot from the canonical codes, and cbT.
-cudaError_t rotate_codes(const uint8_t* codes, int64_t slots, int M, int mode, int G, uint8_t* codes_rot,
-                         cudaStream_t st);
+// Bytes per lane per unit of the chunk-transposed codes_rot layout.
+int rot_unit(int M);
+// Build: codes_rot / pterm_rot from the canonical codes / pterm, and cbT.
+cudaError_t rotate_codes(const uint8_t* codes, const int32_t* pterm, int nlist, int L, int M, int mode, int G,
+                         uint8_t* codes_rot, int32_t* pterm_rot, cudaStream_t st);
 cudaError_t transpose_codebooks(const int8_t* cb, int M, int Ks, int d, int8_t* cbT, cudaStream_t st);
 
 // Steps 3-5, generic query-major scan (scan_lut.cu): any shape, per-query LUT [M][Ks] in shared

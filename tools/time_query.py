@@ -15,7 +15,7 @@ p.add_argument("--config", default="c4")
 p.add_argument("--reps", type=int, default=5)
 p.add_argument("--algos", default="1,2")
 p.add_argument("--Q", type=int, default=0, help="use only the first Q queries")
-p.add_argument("--envs", default="", help="comma-separated VAR=VALUE runs after the plain run")
+p.add_argument("--envs", default="", help="comma-separated runs after the plain run, each VAR=VALUE[:VAR=VALUE]")
 args = p.parse_args()
 cfg = get_config(args.config)
 inp = generate(cfg)
@@ -27,10 +27,10 @@ if args.Q:
 out = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=True, device="cuda")
 v3db.profile_enable(True)
 for env in [""] + [e for e in args.envs.split(",") if e]:
-    os.environ.pop("V3DB_LM_DEBUG", None)
-    if env:
-        k, v = env.split("=")
-        os.environ[k] = v
+    for kv in env.split(":"):
+        if kv:
+            k, v = kv.split("=")
+            os.environ[k] = v
     for algo in [int(x) for x in args.algos.split(",")]:
         v3db.query_batch(s, q, cfg.nprobe, cfg.k, out=out, algo=algo)
         ts = []
