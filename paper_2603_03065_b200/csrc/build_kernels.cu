@@ -122,8 +122,9 @@ __global__ void slot_terms_kernel(const int8_t* __restrict__ mu, const int8_t* _
   }
 }
 
-// Byte g*G + s of slot j holds the code of subspace g*G + (j + s) mod G (lane l = j mod 32 reads
-// table column l + s, which holds that subspace).  kLutW32 additionally pre-compensates the row
+// Byte off_g + s of slot j holds the code of subspace off_g + (j + s) mod G_g for rotation group g
+// (lane l = j mod 32 reads table column l + s, which holds that subspace; kLutP64 has the one group
+// [0, M)).  kLutW32 additionally pre-compensates the row
 // wrap of columns l + s >= 32: the stored byte is (code - 1) mod 256 there.  Each 32-slot chunk
 // is stored unit-transposed: byte pos of slot j lives at chunk + (pos/U)*32*U + (j%32)*U + pos%U.
 __global__ void rotate_kernel(const uint8_t* __restrict__ codes, const int32_t* __restrict__ pterm, int nlist,
@@ -138,8 +139,15 @@ __global__ void rotate_kernel(const uint8_t* __restrict__ codes, const int32_t* 
     const int lane = jp & 31;
     int v = 0;
     if (jp < L) {
-      const int g = pos / G, s = pos - g * G;
-      v = codes[(static_cast<int64_t>(i) * L + jp) * M + g * G + (lane + s) % G];
+      int off = 0, Gg = M;
+      if (mode == kLutW32) {
+        int g = 0;
+        while (pos >= rot_goff(M, g + 1) && g + 1 < rot_ngroups(M)) ++g;
+        off = rot_goff(M, g);
+        Gg = rot_gsize(M, g);
+      }
+      const int s = pos - off;
+      v = codes[(static_cast<int64_t>(i) * L + jp) * M + off + (lane + s) % Gg];
       if (mode == kLutW32 && lane + s >= 32) v = (v + 255) & 255;
     }
     const int64_t chunk = sp >> 5;                  // (i*Lp + jp) / 32: chunks never straddle lists

@@ -8,17 +8,17 @@
 // the probed lists' codes; padding slots (f = 0) get D = d_max and whole chunks of padding are
 // never read.  Step 5 keeps an exact top-k on (D, item) keys.
 //
-// Rotated LUT.  Lane l of a warp handles slot j = 32c + l of a
-// chunk.  At step s it reads subspace m = gG + (l + s) mod G (G | 32 subspaces per group) from
+// Rotated LUT.  The M subspaces are split into groups of
+// G in {32, 16, 8, 4} consecutive subspaces (greedy: M = 24 -> 16 + 8).  Lane l of a warp handles
+// slot j = 32c + l of a chunk.  At step s of group g it reads subspace off_g + (l + s) mod G from
 // table COLUMN l + s, so the 32 lanes of every LDS hit 32 distinct banks whatever the codes are.
-// The slot's code bytes are stored pre-rotated (codes_rot, built once) so byte s of the
-// register word is the right code.  Two table geometries:
-//   kLutP64 (G = M <= 32): rows of 64 int32 columns, column col = subspace col mod G;
+// The slot's code bytes are stored pre-rotated (codes_rot, built once) so byte off_g + s of the
+// register words is the right code.  Two table geometries:
+//   kLutP64 (one group, G = M <= 32): rows of 64 int32 columns, column col = subspace col mod G;
 //            address = code*256 + 4l + 4s = PRMT(code byte, 4l) + immediate.        1 ALU op
-//   kLutW32 (G = gcd(M,32), M/G groups): rows of 32 columns, 257 rows per group; a lane whose
-//            column l+s passes 32 wraps into the next row, which the stored byte pre-compensates
-//            ((code - 1) mod 256; row 256 duplicates row 0):
-//            address = ((byte << 7) | 4l) + immediate.                                2 ALU ops
+//   kLutW32 (any M % 4 == 0): per group, 257 rows of 32 columns; a lane whose column l+s passes
+//            32 wraps into the next row, which the stored byte pre-compensates ((code - 1) mod
+//            256; row 256 duplicates row 0):  address = ((byte << 7) | 4l) + immediate.  2 ALU ops
 //
 // Streaming.  A producer warp (one lane) walks the probed lists'
 // VALID 32-slot chunks in probe order and packs them into CTA-wide stages of SEG chunks; each
@@ -45,28 +45,25 @@ namespace v3db {
 
 int plan_lut(int M, int Ks, int d, int* G) {
   *G = 0;
-  if (M < 4 || M % 4 != 0 || d % 4 != 0 || Ks < 1 || Ks > 256) return 0;
-  const int g = (M % 32 == 0) ? 32 : (M % 16 == 0) ? 16 : (M % 8 == 0) ? 8 : 4;
+  if (M < 4 || M % 4 != 0 || M > 128 || d % 4 != 0 || Ks < 1 || Ks > 256) return 0;
   const char* force = getenv("V3DB_LUT_MODE");  // test/bench hook: "w32" / "p64" force a geometry
   const bool want_w32 = force && force[0] == 'w';
   const bool want_p64 = force && force[0] == 'p';
-  const bool p64_ok = g == M && (M == 4 || M == 8 || M == 16 || M == 32);
-  const bool w32_ok = (M == 8 || M == 16 || M == 24 || M == 32 || M == 48 || M == 64 || M == 96 || M == 128) &&
-                      (M / g) * kW32GroupBytes <= 160 * 1024;
-  // default: P64 (1 ALU op per lookup) while its table is small; W32 (half the table, so more
-  // CTAs and ring stages per SM) for 256-codeword tables
+  const bool p64_ok = M == 4 || M == 8 || M == 16 || M == 32;
+  const bool w32_ok = M == 8 || M == 12 || M == 16 || M == 24 || M == 32 || M == 48 || M == 64 || M == 96 || M == 128;
+  // default: P64 (1 ALU op per lookup) while its table is small; W32 (half the table, so room
+  // for deeper TMA stages) for 256-codeword tables
   if (p64_ok && !want_w32 && (want_p64 || Ks * 256 <= 16384 || !w32_ok)) {
-    *G = g;
+    *G = M;
     return kLutP64;
   }
   if (w32_ok) {
-    *G = g;
+    *G = rot_gsize(M, 0);
     return kLutW32;
   }
   return 0;
 }
 
-int rot_unit(int M) { return M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4; }
 
 namespace {
 
@@ -98,12 +95,11 @@ constexpr uint32_t kTauInit = 0x7ffffffeu;  // accept every valid D (< d_max)
 
 template <int M, int MODE>
 struct Geo {
-  static constexpr int G = (M % 32 == 0) ? 32 : (M % 16 == 0) ? 16 : (M % 8 == 0) ? 8 : 4;
-  static constexpr int NG = M / G;
+  static constexpr int NG = rot_ngroups(M);
   static constexpr int NW = M / 4;                                   // 32-bit code words per slot
   static constexpr int U = M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4;    // bytes per lane per unit
   static constexpr int TGB = (MODE == kLutW32) ? kW32GroupBytes : 0;  // bytes per group table
-  static constexpr int NT = (MODE == kLutW32 && NG * kW32GroupBytes > 100 * 1024) ? 512 : 256;  // consumers
+  static constexpr int NT = (MODE == kLutW32 && NG * kW32GroupBytes > 96 * 1024) ? 512 : 256;  // consumers
   static constexpr int NTOT = NT + 32;                              // + the producer warp
   static constexpr int MINB = NT == 512 ? 1 : 2;
 };
@@ -263,10 +259,33 @@ __device__ int compact(uint64_t* buf, int* hist, int* s_int, const int4* probe, 
   return kept;
 }
 
+// Step 4 of one slot per lane: acc += sum over the subspaces of group G_IDX.. of the rotated
+// table entry selected by the slot's code byte (compile-time unrolled per group).
+template <int M, int MODE, int G_IDX>
+__device__ __forceinline__ void lut_sum(const uint32_t (&w)[M / 4], uint32_t lane4, int32_t& acc) {
+  constexpr int off = rot_goff(M, G_IDX), Gg = MODE == kLutP64 ? M : rot_gsize(M, G_IDX);
+  constexpr int TGB = MODE == kLutW32 ? kW32GroupBytes : 0;
+#pragma unroll
+  for (int s2 = 0; s2 < Gg; ++s2) {
+    const int pos = off + s2;
+    const uint32_t wd = w[pos >> 2];
+    uint32_t ad;
+    if constexpr (MODE == kLutP64) {
+      ad = __byte_perm(wd, lane4, 0x7604u | ((pos & 3) << 4));  // code << 8 | lane4
+    } else {
+      const int b = pos & 3;
+      const uint32_t sh = (b == 0) ? (wd << 7) : (wd >> (8 * b - 7));
+      ad = (sh & 0x7f80u) | lane4;
+    }
+    acc += lds32(ad + (kSmemLo + G_IDX * TGB + 4 * s2));
+  }
+  if constexpr (MODE == kLutW32 && G_IDX + 1 < rot_ngroups(M)) lut_sum<M, MODE, G_IDX + 1>(w, lane4, acc);
+}
+
 template <int M, int MODE, int CAPM>
 __global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_rot_kernel(const RotArgs a) {
   using C = Geo<M, MODE>;
-  constexpr int NT = C::NT, W = NT / 32, G = C::G, NG = C::NG, NW = C::NW, U = C::U;
+  constexpr int NT = C::NT, W = NT / 32, NG = C::NG, NW = C::NW, U = C::U;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem + a.off_stage;                        // [NS][SEG*32*M codes | SEG*128 P]
   int* vcoff = reinterpret_cast<int*>(smem + a.off_desc);      // [nprobe+1] prefix sums of valid chunks
@@ -367,14 +386,16 @@ __global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_r
     const int dw = a.d >> 2, MK = M * a.Ks;
     auto put = [&](int e, int32_t A) {
       const int m = e % M, cc = e / M;
-      const int g = m / G, r = m - g * G;
       if constexpr (MODE == kLutP64) {
 #pragma unroll
-        for (int col = r; col < 64; col += G) T[cc * 64 + col] = A;
+        for (int col = m; col < 64; col += M) T[cc * 64 + col] = A;
       } else {
-        int32_t* Tg = T + g * (kW32GroupBytes / 4);
+        int g = 0;
 #pragma unroll
-        for (int col = r; col < 32; col += G) {
+        for (int x = 1; x < NG; ++x) g += m >= rot_goff(M, x) ? 1 : 0;
+        const int Gg = rot_gsize(M, g), r = m - rot_goff(M, g);
+        int32_t* Tg = T + g * (kW32GroupBytes / 4);
+        for (int col = r; col < 32; col += Gg) {
           Tg[cc * 32 + col] = A;
           if (cc == 0) Tg[256 * 32 + col] = A;  // row 256 duplicates row 0 (wrap of code 0)
         }
@@ -461,23 +482,7 @@ __global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_r
         }
       }
       int32_t acc = pr.y + *reinterpret_cast<const int32_t*>(st + pbase + static_cast<uint32_t>(i) * 128u + 4 * lane);
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-#pragma unroll
-        for (int s2 = 0; s2 < G; ++s2) {
-          const int pos = g * G + s2;
-          const uint32_t wd = w[pos >> 2];
-          uint32_t ad;
-          if constexpr (MODE == kLutP64) {
-            ad = __byte_perm(wd, lane4, 0x7604u | ((pos & 3) << 4));  // code << 8 | lane4
-          } else {
-            const int b = pos & 3;
-            const uint32_t sh = (b == 0) ? (wd << 7) : (wd >> (8 * b - 7));
-            ad = (sh & 0x7f80u) | lane4;
-          }
-          acc += lds32(ad + (kSmemLo + g * C::TGB + 4 * s2));
-        }
-      }
+      lut_sum<M, MODE, 0>(w, lane4, acc);
       // lanes past the list's valid slots read stale stage bytes (always in-table addresses)
       const bool valid = lane < nv;
       const int32_t D = valid ? acc : kDMax;
@@ -647,6 +652,7 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
   }
   switch (s->M) {
     case 8: V3DB_ROT(8, kLutW32)
+    case 12: V3DB_ROT(12, kLutW32)
     case 16: V3DB_ROT(16, kLutW32)
     case 24: V3DB_ROT(24, kLutW32)
     case 32: V3DB_ROT(32, kLutW32)

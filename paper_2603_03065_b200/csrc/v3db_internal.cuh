@@ -71,13 +71,45 @@ cudaError_t slot_terms(const int8_t* mu, const int8_t* codebooks, const uint8_t*
                        cudaStream_t st);
 
 // Rotated-LUT geometry.
-constexpr int kLutP64 = 1;   // G = M <= 32 subspaces, rows of 64 int32 columns (PRMT addressing)
-constexpr int kLutW32 = 2;   // G = gcd(M, 32), M/G groups of 257 rows x 32 columns (wrap addressing)
+constexpr int kLutP64 = 1;   // one group of M <= 32 subspaces, rows of 64 int32 columns (PRMT addressing)
+constexpr int kLutW32 = 2;   // rot_ngroups(M) groups of 257 rows x 32 columns (wrap addressing)
 constexpr int kW32GroupBytes = 257 * 32 * 4;
-// Chooses the geometry for (M, Ks, d): returns the mode (0 = generic scan) and sets *G.
+// Chooses the geometry for (M, Ks, d): returns the mode (0 = generic scan) and sets *G (the first
+// group's size; informational).
 int plan_lut(int M, int Ks, int d, int* G);
 // Bytes per lane per unit of the chunk-transposed codes_rot layout.
-int rot_unit(int M);
+__host__ __device__ constexpr int rot_unit(int M) { return M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4; }
+// Rotation groups of the W32 geometry: M (a multiple of 4) split greedily into groups of 32, 16,
+// 8, 4 consecutive subspaces (M = 24 -> 16 + 8).  Group g covers [rot_goff(M,g), +rot_gsize(M,g)).
+__host__ __device__ constexpr int rot_ngroups(int M) {
+  int n = 0;
+  for (int r = M, sz = 32; r > 0;) {
+    if (r >= sz) {
+      r -= sz;
+      ++n;
+    } else {
+      sz >>= 1;
+    }
+  }
+  return n;
+}
+__host__ __device__ constexpr int rot_gsize(int M, int g) {
+  for (int r = M, sz = 32, i = 0; r > 0;) {
+    if (r >= sz) {
+      if (i == g) return sz;
+      r -= sz;
+      ++i;
+    } else {
+      sz >>= 1;
+    }
+  }
+  return 0;
+}
+__host__ __device__ constexpr int rot_goff(int M, int g) {
+  int o = 0;
+  for (int i = 0; i < g; ++i) o += rot_gsize(M, i);
+  return o;
+}
 // Build: codes_rot / pterm_rot from the canonical codes / pterm, and cbT.
 cudaError_t rotate_codes(const uint8_t* codes, const int32_t* pterm, int nlist, int L, int M, int mode, int G,
                          uint8_t* codes_rot, int32_t* pterm_rot, cudaStream_t st);

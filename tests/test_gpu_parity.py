@@ -167,6 +167,18 @@ def test_rotated_w32_geometry(v3db, name, monkeypatch):
     s.free()
 
 
+@pytest.mark.parametrize("M,d,k", [(12, 4, 10), (24, 4, 10), (48, 2 * 4, 100), (96, 8, 100), (128, 4, 37)])
+def test_rotated_group_decompositions(v3db, M, d, k):
+    """W32 rotation groups of every size mix: 12 = 8+4, 24 = 16+8, 48 = 32+16, 96 = 3x32 (512
+    consumer threads), 128 = 4x32; ragged list fill and a ragged last chunk (L % 32 != 0)."""
+    rng = np.random.default_rng(100 + M)
+    N, D, nlist, L, Ks = 3000, M * d, 12, 300, 256
+    db = rng.integers(-100, 100, size=(N, D)).astype(np.int8)
+    qs = rng.integers(-100, 100, size=(41, D)).astype(np.int8)
+    run_case(v3db, db, qs, nlist, L, M, Ks, 5, k, rng.choice(N, nlist, replace=False),
+             np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
+
+
 @pytest.mark.parametrize("k", [1, 7, 100, 333, 1024])
 def test_rotated_topk_sizes(v3db, k):
     """Buffered top-k of the rotated scan for k from 1 to V3DB_MAX_K (compactions at every
