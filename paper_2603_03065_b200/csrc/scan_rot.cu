@@ -93,21 +93,23 @@ __device__ __forceinline__ int32_t lds32(uint32_t addr) {
 }
 constexpr uint32_t kTauInit = 0x7ffffffeu;  // accept every valid D (< d_max)
 
-template <int M, int MODE>
+// VAR selects experimental CTA shapes (V3DB_SCAN_VAR, M = 32 W32 only): 1 = 12 consumer warps,
+// 2 = three CTAs per SM.
+template <int M, int MODE, int VAR = 0>
 struct Geo {
   static constexpr int NG = rot_ngroups(M);
   static constexpr int NW = M / 4;                                   // 32-bit code words per slot
   static constexpr int U = M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4;    // bytes per lane per unit
   static constexpr int TGB = (MODE == kLutW32) ? kW32GroupBytes : 0;  // bytes per group table
-  static constexpr int NT = (MODE == kLutW32 && NG * kW32GroupBytes > 96 * 1024) ? 512 : 256;  // consumers
+  static constexpr int NT = VAR == 1 ? 384 : (MODE == kLutW32 && NG * kW32GroupBytes > 96 * 1024) ? 512 : 256;  // consumers
   static constexpr int NTOT = NT + 32;                              // + the producer warp
-  static constexpr int MINB = NT == 512 ? 1 : 2;
+  static constexpr int MINB = VAR == 2 ? 3 : NT == 512 ? 1 : 2;
 };
 
 struct RotArgs {
   const int8_t* queries;
   int dim, d, Ks, L, Lp, nprobe, k, cap, NS, SEG, R;
-  uint32_t off_stage, off_desc, off_buf, off_hist, off_probe, off_q, off_int, off_bar, stage_bytes;
+  uint32_t off_stage, off_desc, off_vc, off_buf, off_hist, off_probe, off_q, off_int, off_bar, stage_bytes;
   const int8_t* cbT;
   const uint8_t* codes;   // codes_rot [nlist][Lp/32][unit][lane][U]
   const int32_t* pterm;   // pterm_rot [nlist][Lp]
@@ -282,13 +284,14 @@ __device__ __forceinline__ void lut_sum(const uint32_t (&w)[M / 4], uint32_t lan
   if constexpr (MODE == kLutW32 && G_IDX + 1 < rot_ngroups(M)) lut_sum<M, MODE, G_IDX + 1>(w, lane4, acc);
 }
 
-template <int M, int MODE, int CAPM>
-__global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_rot_kernel(const RotArgs a) {
-  using C = Geo<M, MODE>;
+template <int M, int MODE, int CAPM, int VAR>
+__global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MINB) scan_rot_kernel(const RotArgs a) {
+  using C = Geo<M, MODE, VAR>;
   constexpr int NT = C::NT, W = NT / 32, NG = C::NG, NW = C::NW, U = C::U;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem + a.off_stage;                        // [NS][SEG*32*M codes | SEG*128 P]
-  int* vcoff = reinterpret_cast<int*>(smem + a.off_desc);      // [nprobe+1] prefix sums of valid chunks
+  int* vcoff = reinterpret_cast<int*>(smem + a.off_vc);        // [nprobe+1] prefix sums of valid chunks
+  int4* dsc = reinterpret_cast<int4*>(smem + a.off_desc);      // [NS][SEG] chunk descriptors
   uint64_t* buf = reinterpret_cast<uint64_t*>(smem + a.off_buf);
   int* hist = reinterpret_cast<int*>(smem + a.off_hist);
   int4* probe = reinterpret_cast<int4*>(smem + a.off_probe);  // (list, d_i, count, 0)
@@ -353,8 +356,13 @@ __global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_r
           while (vcoff[rho + 1] <= g) ++rho;
           const int jc = g - vcoff[rho];
           const int m = min(g1 - g, vcoff[rho + 1] - g);
-          const int64_t slot0 = static_cast<int64_t>(probe[rho].x) * a.Lp + jc * 32;
+          const int4 pr = probe[rho];
+          const int64_t slot0 = static_cast<int64_t>(pr.x) * a.Lp + jc * 32;
           const uint32_t i = static_cast<uint32_t>(g - g0);
+          // per-chunk descriptors: (d_i, rho*L + 32*jc (trace / flat offset), valid slots, slots)
+          for (int x = 0; x < m; ++x)
+            dsc[s * SEG + i + x] = make_int4(pr.y, rho * L + (jc + x) * 32, min(32, pr.z - (jc + x) * 32),
+                                             min(32, L - (jc + x) * 32));
           bulk_g2s(st + i * 32u * M, a.codes + slot0 * M, static_cast<uint32_t>(m) * 32u * M, full + s);
           bulk_g2s(st + pbase + i * 128u, a.pterm + slot0, static_cast<uint32_t>(m) * 128u, full + s);
           g += m;
@@ -455,48 +463,62 @@ __global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_r
   int epoch = 0, in_epoch = 0;
 
   uint32_t fph = 0;
-  int crho = 0;  // this warp's probe cursor (its chunks g increase monotonically)
+  // one chunk's code words (rotated, chunk-transposed) from the stage
+  auto load_w = [&](const uint8_t* cp, uint32_t(&w)[NW]) {
+#pragma unroll
+    for (int u = 0; u < M / U; ++u) {
+      const uint8_t* p = cp + u * 32 * U + lane * U;
+      if constexpr (U == 16) {
+        const uint4 x = *reinterpret_cast<const uint4*>(p);
+        w[4 * u] = x.x; w[4 * u + 1] = x.y; w[4 * u + 2] = x.z; w[4 * u + 3] = x.w;
+      } else if constexpr (U == 8) {
+        const uint2 x = *reinterpret_cast<const uint2*>(p);
+        w[2 * u] = x.x; w[2 * u + 1] = x.y;
+      } else {
+        w[u] = *reinterpret_cast<const uint32_t*>(p);
+      }
+    }
+  };
+  // masked D to the trace, candidate append (Step 5 buffer)
+  auto emit = [&](const int4 dd, int32_t acc) {
+    const bool valid = lane < dd.z;  // lanes past the valid slots read stale stage bytes
+    const int32_t D = valid ? acc : kDMax;
+    const int off = dd.y + lane;     // rho*L + j
+    if (trq && lane < dd.w) __stcs(trq + dd.y, D);
+    const bool pass = valid && static_cast<uint32_t>(D) <= tau;
+    const uint32_t bal = __ballot_sync(kFull, pass);
+    if (bal) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&s_int[epoch % 3], __popc(bal));
+      base = __shfl_sync(kFull, base, 0);
+      if (pass)
+        buf[n_base + base + __popc(bal & ((1u << lane) - 1u))] =
+            (static_cast<uint64_t>(static_cast<uint32_t>(D)) << 32) | static_cast<uint32_t>(off);
+    }
+  };
   for (int t = 0, s = 0; t < NSTG; ++t) {
     mbar_wait_sleep(full + s, fph);
     const uint8_t* st = stages + static_cast<uint32_t>(s) * a.stage_bytes;
-    const int g0 = t * SEG, n = min(TV, g0 + SEG) - g0;
-    for (int i = warp; i < n; i += W) {
-      const int g = g0 + i;
-      while (vcoff[crho + 1] <= g) ++crho;
-      const int rho = crho, jc = g - vcoff[crho];
-      const int4 pr = probe[rho];
-      const int nv = min(32, pr.z - jc * 32);
-      uint32_t w[NW];
-      const uint8_t* cp = st + static_cast<uint32_t>(i) * 32u * M;
-#pragma unroll
-      for (int u = 0; u < M / U; ++u) {
-        const uint8_t* p = cp + u * 32 * U + lane * U;
-        if constexpr (U == 16) {
-          const uint4 x = *reinterpret_cast<const uint4*>(p);
-          w[4 * u] = x.x; w[4 * u + 1] = x.y; w[4 * u + 2] = x.z; w[4 * u + 3] = x.w;
-        } else if constexpr (U == 8) {
-          const uint2 x = *reinterpret_cast<const uint2*>(p);
-          w[2 * u] = x.x; w[2 * u + 1] = x.y;
-        } else {
-          w[u] = *reinterpret_cast<const uint32_t*>(p);
-        }
-      }
-      int32_t acc = pr.y + *reinterpret_cast<const int32_t*>(st + pbase + static_cast<uint32_t>(i) * 128u + 4 * lane);
-      lut_sum<M, MODE, 0>(w, lane4, acc);
-      // lanes past the list's valid slots read stale stage bytes (always in-table addresses)
-      const bool valid = lane < nv;
-      const int32_t D = valid ? acc : kDMax;
-      const int j = jc * 32 + lane;
-      if (trq && j < L) __stcs(trq + (rho * L + jc * 32), D);
-      const bool pass = valid && static_cast<uint32_t>(D) <= tau;
-      const uint32_t bal = __ballot_sync(kFull, pass);
-      if (bal) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&s_int[epoch % 3], __popc(bal));
-        base = __shfl_sync(kFull, base, 0);
-        if (pass)
-          buf[n_base + base + __popc(bal & ((1u << lane) - 1u))] =
-              (static_cast<uint64_t>(static_cast<uint32_t>(D)) << 32) | static_cast<uint32_t>(rho * L + j);
+    const int4* ds = dsc + s * SEG;
+    const int n = min(TV, t * SEG + SEG) - t * SEG;
+    // two chunks (i, i + W) per pass: their loads and 2M lookups interleave
+    for (int i = warp; i < n; i += 2 * W) {
+      const bool two = i + W < n;  // warp-uniform
+      const int4 d0 = ds[i];
+      uint32_t w0[NW], w1[NW];
+      load_w(st + static_cast<uint32_t>(i) * 32u * M, w0);
+      int32_t acc0 = d0.x + *reinterpret_cast<const int32_t*>(st + pbase + static_cast<uint32_t>(i) * 128u + 4 * lane);
+      if (two) {
+        const int4 d1 = ds[i + W];
+        load_w(st + static_cast<uint32_t>(i + W) * 32u * M, w1);
+        int32_t acc1 = d1.x + *reinterpret_cast<const int32_t*>(st + pbase + static_cast<uint32_t>(i + W) * 128u + 4 * lane);
+        lut_sum<M, MODE, 0>(w0, lane4, acc0);
+        lut_sum<M, MODE, 0>(w1, lane4, acc1);
+        emit(d0, acc0);
+        emit(d1, acc1);
+      } else {
+        lut_sum<M, MODE, 0>(w0, lane4, acc0);
+        emit(d0, acc0);
       }
     }
     __syncwarp();
@@ -543,20 +565,20 @@ __global__ void __launch_bounds__(Geo<M, MODE>::NTOT, Geo<M, MODE>::MINB) scan_r
   }
 }
 
-template <int M, int MODE, int CAPM>
+template <int M, int MODE, int CAPM, int VAR>
 cudaError_t launch_cap(const RotArgs& a, int64_t nq, size_t smem, cudaStream_t st) {
-  using C = Geo<M, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(scan_rot_kernel<M, MODE, CAPM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  using C = Geo<M, MODE, VAR>;
+  cudaError_t e = cudaFuncSetAttribute(scan_rot_kernel<M, MODE, CAPM, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  scan_rot_kernel<M, MODE, CAPM><<<static_cast<unsigned>(nq), C::NTOT, smem, st>>>(a);
+  scan_rot_kernel<M, MODE, CAPM, VAR><<<static_cast<unsigned>(nq), C::NTOT, smem, st>>>(a);
   note_launch();
   return cudaGetLastError();
 }
 
-template <int M, int MODE>
+template <int M, int MODE, int VAR = 0>
 cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
-  using C = Geo<M, MODE>;
+  using C = Geo<M, MODE, VAR>;
   constexpr int NT = C::NT;
   auto al = [](uint32_t x, uint32_t b) { return (x + b - 1) / b * b; };
   const uint32_t lut = MODE == kLutP64 ? static_cast<uint32_t>(a.Ks) * 256u : C::NG * kW32GroupBytes;
@@ -572,7 +594,7 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   for (const auto& c : cand) {
     const int seg = e_seg ? atoi(e_seg) : c[0], ns = e_ns ? atoi(e_ns) : c[1];
     const int cp = a.k + seg * 32 <= c[2] ? c[2] : 2048;
-    const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) +
+    const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) + 16u * ns * seg +
                         8u * cp + 256 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
     SEG = seg;
     NS = ns;
@@ -590,6 +612,8 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   a.off_stage = o;
   o += NS * a.stage_bytes;
   a.off_desc = o;
+  o += 16u * NS * SEG;
+  a.off_vc = o;
   o += al(4u * (a.nprobe + 1), 16);
   a.off_buf = o;
   o += 8u * cap;
@@ -603,14 +627,14 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   o += 256;
   a.off_bar = o;
   const int capm = cap / NT;
-  if (capm <= 2) return launch_cap<M, MODE, 2>(a, nq, smem, st);
-  if (capm <= 4) return launch_cap<M, MODE, 4>(a, nq, smem, st);
-  return launch_cap<M, MODE, 8>(a, nq, smem, st);
+  if (capm <= 2) return launch_cap<M, MODE, 2, VAR>(a, nq, smem, st);
+  if (capm <= 4) return launch_cap<M, MODE, 4, VAR>(a, nq, smem, st);
+  return launch_cap<M, MODE, 8, VAR>(a, nq, smem, st);
 }
 
-template <int M, int MODE>
+template <int M, int MODE, int VAR = 0>
 int budget() {
-  using C = Geo<M, MODE>;
+  using C = Geo<M, MODE, VAR>;
   return (228 * 1024) / C::MINB - 1024;  // per-CTA share of the SM (1 KB reserved per CTA)
 }
 
@@ -655,7 +679,12 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
     case 12: V3DB_ROT(12, kLutW32)
     case 16: V3DB_ROT(16, kLutW32)
     case 24: V3DB_ROT(24, kLutW32)
-    case 32: V3DB_ROT(32, kLutW32)
+    case 32: {
+      const char* var = getenv("V3DB_SCAN_VAR");
+      if (var && var[0] == '1') return launch<32, kLutW32, 1>(a, nq, budget<32, kLutW32, 1>(), st);
+      if (var && var[0] == '2') return launch<32, kLutW32, 2>(a, nq, budget<32, kLutW32, 2>(), st);
+      V3DB_ROT(32, kLutW32)
+    }
     case 48: V3DB_ROT(48, kLutW32)
     case 64: V3DB_ROT(64, kLutW32)
     case 96: V3DB_ROT(96, kLutW32)
