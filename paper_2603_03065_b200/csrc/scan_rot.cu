@@ -100,7 +100,6 @@ struct Geo {
   static constexpr int NG = rot_ngroups(M);
   static constexpr int NW = M / 4;                                   // 32-bit code words per slot
   static constexpr int U = M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4;    // bytes per lane per unit
-  static constexpr int TGB = (MODE == kLutW32) ? kW32GroupBytes : 0;  // bytes per group table
   static constexpr int NT = VAR == 1 ? 384 : (MODE == kLutW32 && NG * kW32GroupBytes > 96 * 1024) ? 512 : 256;  // consumers
   static constexpr int NTOT = NT + 32;                              // + the producer warp
   static constexpr int MINB = VAR == 2 ? 3 : NT == 512 ? 1 : 2;
