@@ -39,17 +39,19 @@ cudaError_t coarse_topk_mma(const int8_t* X, int64_t n, int dim, const int8_t* m
 
 namespace {
 
-constexpr int kRows = 128;        // rows per CTA (UMMA M)
+constexpr int kRows = 128;        // rows per tile (UMMA M)
 constexpr int kChunk = 256;       // centroids per MMA chunk (UMMA N)
 constexpr int kPanel = 128;       // bytes of K per swizzled panel
-constexpr int kEpiWarps = 8;      // warps 0-7 epilogue (TMEM lanes 32*(w%4), column half w/4)
-constexpr int kThreads = 32 * (kEpiWarps + 1);  // + warp 8: TMA producer / MMA issuer
+constexpr int kEpiWarps = 16;     // epilogue: warp w -> TMEM lanes 32*(w%4), columns 64*(w/4) of a chunk
+constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+constexpr int kThreads = 32 * (kEpiWarps + 2);
 constexpr uint32_t kAPanelBytes = kRows * kPanel;     // 16 KB
 constexpr uint32_t kBStageBytes = kChunk * kPanel;    // 32 KB
 
 struct CoarseArgs {
-  int64_t n;
-  int dim, nlist, kp, stages, nsplit, G, ngroups, capc;
+  int64_t n, items;  // rows, work items (row tile x chunk)
+  int dim, nlist, kp, stages, nchunks, G, ngroups, capc;
+  const int8_t* X;
   const int32_t* cnorm;
   int32_t* gmin;        // pass 1: [n][ngroups] group-minimum distances
   const int32_t* tau;   // pass 2: [n] threshold distance
@@ -57,6 +59,10 @@ struct CoarseArgs {
   int* ccnt;            // pass 2: [n] candidate counts
 };
 
+// Persistent: CTA b owns the contiguous work items [b*per, (b+1)*per) of the row-major
+// (row tile, chunk) order, so a CTA switches row tiles at most a few times.  Warp 16 issues the
+// TMA loads (A once per row tile, B per (chunk, K panel) into a ring), warp 17 issues the MMAs
+// into two TMEM accumulators, warps 0-15 run the epilogue (TMEM -> registers -> distances).
 template <int PASS>
 __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_constant__ CUtensorMap tmX,
                                                                 const __grid_constant__ CUtensorMap tmMu,
@@ -65,24 +71,23 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;                                   // kp panels of [128][128]
   uint8_t* sB = smem + a.kp * kAPanelBytes;             // stages of [256][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + a.stages * kBStageBytes);
+  int* sCn = reinterpret_cast<int*>(sB + a.stages * kBStageBytes);  // [kEpiWarps][64] ||mu||^2
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sCn + kEpiWarps * 64);
   uint64_t* a_full = bars;
-  uint64_t* full = bars + 1;                            // [stages]
+  uint64_t* a_empty = bars + 1;
+  uint64_t* full = bars + 2;                            // [stages]
   uint64_t* empty = full + a.stages;                    // [stages]
   uint64_t* accf = empty + a.stages;                    // [2]
   uint64_t* acce = accf + 2;                            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
-  int* sCn = reinterpret_cast<int*>(bars + 32);         // [2][kChunk] ||mu||^2 of the chunk
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kRows;
-  const int nchunks = (a.nlist + kChunk - 1) / kChunk;
-  const int cpc = (nchunks + a.nsplit - 1) / a.nsplit;
-  const int c_begin = blockIdx.y * cpc;
-  const int nch = max(0, min(nchunks, c_begin + cpc) - c_begin);
+  const int64_t per = (a.items + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = blockIdx.x * per, i1 = min(a.items, i0 + per);
 
-  if (tid == 32 * kEpiWarps) {
+  if (tid == 0) {
     tc::mbar_init(a_full, 1);
+    tc::mbar_init(a_empty, 1);
     for (int s = 0; s < a.stages; ++s) {
       tc::mbar_init(full + s, 1);
       tc::mbar_init(empty + s, 1);
@@ -99,31 +104,55 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  if (nch > 0) {
-    if (warp == kEpiWarps) {
-      if (lane == 0) {
-        tc::tma_prefetch(&tmX);
-        tc::tma_prefetch(&tmMu);
-        tc::mbar_expect_tx(a_full, a.kp * kAPanelBytes);
-        for (int p = 0; p < a.kp; ++p) tc::tma_load_2d(sA + p * kAPanelBytes, &tmX, a_full, p * kPanel, (int)row0);
-        const int n_it = nch * a.kp;
-        auto load_b = [&](int it) {
-          const int s = it % a.stages, c = c_begin + it / a.kp, p = it % a.kp;
+  if (warp == kProdWarp) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0 && i0 < i1) {
+      tc::tma_prefetch(&tmX);
+      tc::tma_prefetch(&tmMu);
+      int64_t cur_rt = -1;
+      int nA = 0, s = 0, u = 0;  // A loads so far; B stage index / ring pass
+      for (int64_t it = i0; it < i1; ++it) {
+        const int64_t rt = it / a.nchunks;
+        const int c = static_cast<int>(it - rt * a.nchunks);
+        if (rt != cur_rt) {
+          if (nA > 0) tc::mbar_wait(a_empty, (nA - 1) & 1);  // every MMA reading the old tile is done
+          tc::mbar_expect_tx(a_full, a.kp * kAPanelBytes);
+          for (int p = 0; p < a.kp; ++p) tc::tma_load_2d(sA + p * kAPanelBytes, &tmX, a_full, p * kPanel, (int)(rt * kRows));
+          ++nA;
+          cur_rt = rt;
+        }
+        for (int p = 0; p < a.kp; ++p) {
+          if (u > 0) tc::mbar_wait(empty + s, (u - 1) & 1);
           tc::mbar_expect_tx(full + s, kBStageBytes);
           tc::tma_load_2d(sB + s * kBStageBytes, &tmMu, full + s, p * kPanel, c * kChunk);
-        };
-        for (int it = 0; it < min(a.stages, n_it); ++it) load_b(it);
-        tc::mbar_wait(a_full, 0);
-        tc::fence_after_sync();
-        constexpr uint32_t idesc = tc::idesc_s8(kRows, kChunk);
-        for (int it = 0; it < n_it; ++it) {
-          const int c = it / a.kp, p = it % a.kp, s = it % a.stages;
-          const int acc = c & 1, use = c >> 1;
-          if (p == 0 && use > 0) {
-            tc::mbar_wait(acce + acc, (use - 1) & 1);
-            tc::fence_after_sync();
+          if (++s == a.stages) {
+            s = 0;
+            ++u;
           }
-          tc::mbar_wait(full + s, (it / a.stages) & 1);
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0 && i0 < i1) {
+      constexpr uint32_t idesc = tc::idesc_s8(kRows, kChunk);
+      int64_t cur_rt = -1;
+      int nA = 0, s = 0, u = 0;
+      for (int64_t it = i0; it < i1; ++it) {
+        const int64_t rt = it / a.nchunks;
+        const int j = static_cast<int>(it - i0), acc = j & 1, use = j >> 1;
+        if (rt != cur_rt) {
+          tc::mbar_wait(a_full, nA & 1);
+          tc::fence_after_sync();
+          ++nA;
+          cur_rt = rt;
+        }
+        if (use > 0) {  // the epilogue drained this accumulator
+          tc::mbar_wait(acce + acc, (use - 1) & 1);
+          tc::fence_after_sync();
+        }
+        for (int p = 0; p < a.kp; ++p) {
+          tc::mbar_wait(full + s, u & 1);
           tc::fence_after_sync();
           const int nk = min(4, (a.dim - p * kPanel + 31) / 32);
           const uint32_t a_addr = tc::smem_u32(sA + p * kAPanelBytes);
@@ -132,73 +161,105 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
             tc::mma_s8(tmem + acc * kChunk, tc::desc_sw128(a_addr + k * 32), tc::desc_sw128(b_addr + k * 32), idesc,
                        (p | k) != 0);
           tc::mma_commit(empty + s);
-          if (p == a.kp - 1) tc::mma_commit(accf + acc);
-          if (it >= 1 && it - 1 + a.stages < n_it) {  // refill the stage of the previous iteration
-            const int pit = it - 1, ps = pit % a.stages;
-            tc::mbar_wait(empty + ps, (pit / a.stages) & 1);
-            load_b(pit + a.stages);
+          if (++s == a.stages) {
+            s = 0;
+            ++u;
           }
         }
+        tc::mma_commit(accf + acc);
+        // last item of this row tile in our range: the A buffer is free once these MMAs finish
+        if (it + 1 == i1 || (it + 1) / a.nchunks != rt) tc::mma_commit(a_empty);
       }
-    } else {
-      // ---------------- epilogue: thread r owns row row0 + r, half h of each chunk ----------------
-      const int r = (warp & 3) * 32 + lane, half = warp >> 2;
-      const int64_t row = row0 + r;
-      const bool live = row < a.n;
-      const int et = warp * 32 + lane;  // 0..255
-      // ||mu||^2 of the first chunk into sCn[0]
-      {
-        const int col = c_begin * kChunk + et;
-        sCn[et] = col < a.nlist ? __ldg(a.cnorm + col) : 0;
-      }
-      tc::mbar_wait(a_full, 0);
-      int xn = 0;
-      for (int p = 0; p < a.kp; ++p)
-        for (int c = 0; c < 8; ++c) {
-          const uint4 v = *reinterpret_cast<const uint4*>(sA + p * kAPanelBytes + tc::sw128_offset(r, c));
-          xn = __dp4a(static_cast<int>(v.x), static_cast<int>(v.x), xn);
-          xn = __dp4a(static_cast<int>(v.y), static_cast<int>(v.y), xn);
-          xn = __dp4a(static_cast<int>(v.z), static_cast<int>(v.z), xn);
-          xn = __dp4a(static_cast<int>(v.w), static_cast<int>(v.w), xn);
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 0-15)
+    const int q = warp & 3, h = warp >> 2;       // TMEM lane quadrant, 64-column quarter
+    const int r = q * 32 + lane;                  // row within the tile
+    int* cn = sCn + warp * 64;
+    int64_t cur_rt = -1;
+    int xn = 0, tau_d = 0;
+    int64_t row = 0;
+    bool live = false;
+    for (int64_t it = i0; it < i1; ++it) {
+      const int64_t rt = it / a.nchunks;
+      const int c = static_cast<int>(it - rt * a.nchunks);
+      const int j = static_cast<int>(it - i0), acc = j & 1, use = j >> 1;
+      const int col0 = c * kChunk + h * 64;       // first list of this warp's 64 columns
+      // ||mu||^2 of the 64 columns (warp-uniform per column: read back as broadcasts)
+      __syncwarp();
+      cn[lane] = col0 + lane < a.nlist ? __ldg(a.cnorm + col0 + lane) : 0;
+      cn[lane + 32] = col0 + 32 + lane < a.nlist ? __ldg(a.cnorm + col0 + 32 + lane) : 0;
+      if (rt != cur_rt) {  // ||x||^2 of this thread's row (from global: the A tile may be reloaded)
+        cur_rt = rt;
+        row = rt * kRows + r;
+        live = row < a.n;
+        xn = 0;
+        if (live) {
+          const int8_t* xr = a.X + row * a.dim;
+          for (int u2 = 0; u2 < a.dim; u2 += 4) {
+            const int v = *reinterpret_cast<const int*>(xr + u2);
+            xn = __dp4a(v, v, xn);
+          }
+          if (PASS == 2) tau_d = a.tau[row];
         }
-      int tau_d = 0;
-      if (PASS == 2 && live) tau_d = a.tau[row];
-      for (int c = 0; c < nch; ++c) {
-        const int acc = c & 1, use = c >> 1;
-        // prefetch the next chunk's norms (published by the named barrier below)
-        const int ncol = (c_begin + c + 1) * kChunk + et;
-        const int cn_next = (c + 1 < nch && ncol < a.nlist) ? __ldg(a.cnorm + ncol) : 0;
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps));   // sCn[c&1] complete
-        const int* cn = sCn + (c & 1) * kChunk + half * (kChunk / 2);
-        tc::mbar_wait(accf + acc, use & 1);
-        tc::fence_after_sync();
-        const int colbase = (c_begin + c) * kChunk + half * (kChunk / 2);
-#pragma unroll 1
-        for (int b = 0; b < kChunk / 64; ++b) {
-          const int col0 = colbase + b * 32;
-          if (col0 >= a.nlist) break;  // warp-uniform
-          uint32_t v[32];
-          tc::tmem_ld32(tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + acc * kChunk +
-                            half * (kChunk / 2) + b * 32, v);
-          tc::tmem_ld_wait();
-          if (!live) continue;
-          const int* cnb = cn + b * 32;
-          if (PASS == 1) {
+      }
+      tc::mbar_wait(accf + acc, use & 1);
+      tc::fence_after_sync();
+      uint32_t v0[32], v1[32];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kChunk + h * 64;
+      tc::tmem_ld32(taddr, v0);
+      tc::tmem_ld32(taddr + 32, v1);
+      tc::tmem_ld_wait();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acce + acc);  // accumulator columns consumed
+      if (!live || col0 >= a.nlist) continue;
+      auto block = [&](const uint32_t(&v)[32], int cb) {
+        const int4* c4 = reinterpret_cast<const int4*>(cn + cb);
+        if (PASS == 1) {
+          const bool full_cols = col0 + cb + 32 <= a.nlist;  // padded columns (v = 0) must not count
+          if (a.G >= 4) {
             int best = 0x7fffffff;
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-              if (col0 + u < a.nlist) best = min(best, xn + cnb[u] - 2 * static_cast<int>(v[u]));
-              if (((u + 1) & (a.G - 1)) == 0) {  // end of a group of G lists
-                const int gstart = col0 + u + 1 - a.G;
-                if (gstart < a.nlist) a.gmin[row * a.ngroups + gstart / a.G] = best;
+            for (int u4 = 0; u4 < 8; ++u4) {
+              const int4 cc = c4[u4];
+              int e0 = cc.x - 2 * static_cast<int>(v[4 * u4]), e1 = cc.y - 2 * static_cast<int>(v[4 * u4 + 1]);
+              int e2 = cc.z - 2 * static_cast<int>(v[4 * u4 + 2]), e3 = cc.w - 2 * static_cast<int>(v[4 * u4 + 3]);
+              if (!full_cols) {
+                const int col = col0 + cb + 4 * u4;
+                if (col >= a.nlist) e0 = 0x7fffffff;
+                if (col + 1 >= a.nlist) e1 = 0x7fffffff;
+                if (col + 2 >= a.nlist) e2 = 0x7fffffff;
+                if (col + 3 >= a.nlist) e3 = 0x7fffffff;
+              }
+              best = min(best, min(min(e0, e1), min(e2, e3)));
+              if (((4 * u4 + 4) & (a.G - 1)) == 0) {  // end of a group of G lists
+                const int gstart = col0 + cb + 4 * u4 + 4 - a.G;
+                if (gstart < a.nlist) a.gmin[row * a.ngroups + gstart / a.G] = best + xn;
                 best = 0x7fffffff;
               }
             }
-          } else {
-#pragma unroll
+          } else {  // G in {1, 2}: small nlist
+            int best = 0x7fffffff;
             for (int u = 0; u < 32; ++u) {
-              const int col = col0 + u;
-              const int d = xn + cnb[u] - 2 * static_cast<int>(v[u]);
+              const int col = col0 + cb + u;
+              if (col < a.nlist) best = min(best, cn[cb + u] - 2 * static_cast<int>(v[u]));
+              if (((u + 1) & (a.G - 1)) == 0) {
+                const int gstart = col + 1 - a.G;
+                if (gstart < a.nlist) a.gmin[row * a.ngroups + gstart / a.G] = best + xn;
+                best = 0x7fffffff;
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u4 = 0; u4 < 8; ++u4) {
+            const int4 cc = c4[u4];
+            const int ev[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const int col = col0 + cb + 4 * u4 + x;
+              const int d = xn + ev[x] - 2 * static_cast<int>(v[4 * u4 + x]);
               if (d <= tau_d && col < a.nlist) {
                 const int pos = atomicAdd(a.ccnt + row, 1);
                 if (pos < a.capc) a.cand[row * a.capc + pos] = step2_key(d, col);
@@ -206,11 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
             }
           }
         }
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(acce + acc);
-        sCn[((c + 1) & 1) * kChunk + et] = cn_next;
-      }
+      };
+      block(v0, 0);
+      block(v1, 32);
     }
   }
   tc::fence_before_sync();
@@ -218,20 +277,66 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
   if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
-// tau_row = R-th smallest group minimum (distance only); resets the candidate counters.
-template <int KR>
+// tau_row = the R-th smallest of the row's group minima (exact 4-pass radix select, one warp per
+// row); resets the candidate counters.  >= the row's true R-th smallest distance: R distinct lists
+// reach it.  Fewer than R groups: no filtering.
 __global__ void __launch_bounds__(256) tau_kernel(int64_t n, int ngroups, int R, const int32_t* __restrict__ gmin,
                                                  int32_t* __restrict__ tau, int* __restrict__ ccnt) {
+  __shared__ int hist[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
   if (row >= n) return;
-  WarpTopK<KR> top;
-  top.init(R);
+  int* hw = hist[warp];
   const int32_t* g = gmin + row * ngroups;
-  for (int b = 0; b < ngroups; b += 32)
-    top.offer((b + lane < ngroups) ? step2_key(g[b + lane], b + lane) : ~0ull);
+  if (ngroups < R) {
+    if (lane == 0) {
+      tau[row] = 0x7fffffff;
+      ccnt[row] = 0;
+    }
+    return;
+  }
+  uint32_t prefix = 0;
+  int kk = R;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int b = lane; b < 256; b += 32) hw[b] = 0;
+    __syncwarp();
+    for (int i = lane; i < ngroups; i += 32) {
+      const uint32_t v = static_cast<uint32_t>(g[i]);
+      if (pass == 0 || (v >> (shift + 8)) == prefix) atomicAdd(&hw[(v >> shift) & 255], 1);
+    }
+    __syncwarp();
+    int hb[8], sum = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      hb[b] = hw[lane * 8 + b];
+      sum += hb[b];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int cum = incl - sum, bin = -1, newk = 0;
+    if (cum < kk && kk <= incl) {
+      bin = lane * 8;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        if (cum + hb[b] >= kk) break;
+        cum += hb[b];
+        ++bin;
+      }
+      newk = kk - cum;
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, bin >= 0)) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    kk = __shfl_sync(0xffffffffu, newk, src);
+    __syncwarp();
+    prefix = (prefix << 8) | static_cast<uint32_t>(bin);
+  }
   if (lane == 0) {
-    tau[row] = static_cast<int32_t>(top.thr >> 32);
+    tau[row] = static_cast<int32_t>(prefix);
     ccnt[row] = 0;
   }
 }
@@ -331,7 +436,8 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
                         int R, int32_t* out_idx, int32_t* out_dist, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int kp = (dim + kPanel - 1) / kPanel;
-  const int stages = std::min(4, static_cast<int>((200 * 1024 - kp * kAPanelBytes) / kBStageBytes));
+  const size_t fixed = 1024 + static_cast<size_t>(kp) * kAPanelBytes + kEpiWarps * 64 * 4 + 64 * 8;
+  const int stages = static_cast<int>(std::min<size_t>(6, (227 * 1024 - fixed) / kBStageBytes));
   const char* force = getenv("V3DB_FORCE_COARSE_MMA");
   const bool tc_ok = dim % 16 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(mu) % 16 == 0 && stages >= 2 && !(force && force[0] == '1');
@@ -339,10 +445,11 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   if (!tc_ok || !make_tmap_i8(&tmX, X, n, dim, kRows, kPanel) || !make_tmap_i8(&tmMu, mu, nlist, dim, kChunk, kPanel))
     return coarse_topk_mma(X, n, dim, mu, cnorm, nlist, R, out_idx, out_dist, st);
 
+  // group size G: a power of two <= 32 with >= 2R groups when nlist allows
   int G = 1;
   while (G * 2 <= 32 && static_cast<int64_t>(G * 2) * 2 * R <= nlist) G *= 2;
   const int ngroups = (nlist + G - 1) / G;
-  const int capc = 4 * R + 128;
+  const int capc = ngroups < R ? std::max(nlist, 4 * R + 128) : 4 * R + 128;
 
   int dev = 0, sms = 148;
   cudaError_t e = cudaGetDevice(&dev);
@@ -350,7 +457,8 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   if (e != cudaSuccess) return e;
   const int64_t rtiles = (n + kRows - 1) / kRows;
   const int nchunks = (nlist + kChunk - 1) / kChunk;
-  const int nsplit = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nchunks, (2 * sms + rtiles - 1) / rtiles)));
+  const int64_t items = rtiles * nchunks;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(items, sms));
 
   const size_t b_g = align256(sizeof(int32_t) * n * ngroups), b_t = align256(sizeof(int32_t) * n),
                b_c = align256(sizeof(uint64_t) * n * capc), b_n = align256(sizeof(int) * n);
@@ -359,14 +467,16 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   if (e != cudaSuccess) return e;
   CoarseArgs a;
   a.n = n;
+  a.items = items;
   a.dim = dim;
   a.nlist = nlist;
   a.kp = kp;
   a.stages = stages;
-  a.nsplit = nsplit;
+  a.nchunks = nchunks;
   a.G = G;
   a.ngroups = ngroups;
   a.capc = capc;
+  a.X = X;
   a.cnorm = cnorm;
   a.gmin = reinterpret_cast<int32_t*>(base);
   a.tau = reinterpret_cast<int32_t*>(base + b_g);
@@ -374,8 +484,7 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   a.ccnt = reinterpret_cast<int*>(base + b_g + b_t + b_c);
   int* flags = reinterpret_cast<int*>(base + b_g + b_t + b_c + b_n);
 
-  const size_t smem = 1024 + kp * kAPanelBytes + stages * kBStageBytes + 32 * 8 + 2 * kChunk * 4;
-  const dim3 grid(static_cast<unsigned>(rtiles), nsplit);
+  const size_t smem = fixed + static_cast<size_t>(stages) * kBStageBytes;
   const unsigned rb = static_cast<unsigned>((n + 7) / 8);
   e = cudaFuncSetAttribute(coarse_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(coarse_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -385,7 +494,7 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
       cudaFreeAsync(base, st);
       return e;
     }
-    dispatch_kr(R, [&]<int KR>() { tau_kernel<KR><<<rb, 256, 0, st>>>(n, ngroups, R, a.gmin, const_cast<int32_t*>(a.tau), a.ccnt); });
+    tau_kernel<<<rb, 256, 0, st>>>(n, ngroups, R, a.gmin, const_cast<int32_t*>(a.tau), a.ccnt);
     coarse_tc_kernel<2><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
     dispatch_kr(R, [&]<int KR>() {
       select_kernel<KR><<<rb, 256, 0, st>>>(n, R, capc, a.cand, a.ccnt, out_idx, out_dist, flags);
