@@ -63,7 +63,8 @@ struct CoarseArgs {
 // (row tile, chunk) order, so a CTA switches row tiles at most a few times.  Warp 16 issues the
 // TMA loads (A once per row tile, B per (chunk, K panel) into a ring), warp 17 issues the MMAs
 // into two TMEM accumulators, warps 0-15 run the epilogue (TMEM -> registers -> distances).
-template <int PASS>
+// GT: compile-time group size (32, 16, 8, 4) or 0 = runtime a.G (any power of two <= 32).
+template <int PASS, int GT>
 __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_constant__ CUtensorMap tmX,
                                                                 const __grid_constant__ CUtensorMap tmMu,
                                                                 const CoarseArgs a) {
@@ -205,71 +206,81 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
       }
       tc::mbar_wait(accf + acc, use & 1);
       tc::fence_after_sync();
-      uint32_t v0[32], v1[32];
+      uint32_t v[32];
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kChunk + h * 64;
-      tc::tmem_ld32(taddr, v0);
-      tc::tmem_ld32(taddr + 32, v1);
-      tc::tmem_ld_wait();
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(acce + acc);  // accumulator columns consumed
-      if (!live || col0 >= a.nlist) continue;
-      auto block = [&](const uint32_t(&v)[32], int cb) {
+      const bool work = live && col0 < a.nlist;
+      int gacc = 0x7fffffff;  // GT == 0 with G > 4: running minimum across the 4-element folds
+      // In place: v[u] <- e = ||mu||^2 - 2 <x, mu> of one 32-column block (d = xn + e); padded
+      // columns -> +inf.  Then Pass 1 stores group minima, Pass 2 appends candidates d <= tau.
+      auto block = [&](int cb) {
         const int4* c4 = reinterpret_cast<const int4*>(cn + cb);
-        if (PASS == 1) {
-          const bool full_cols = col0 + cb + 32 <= a.nlist;  // padded columns (v = 0) must not count
-          if (a.G >= 4) {
-            int best = 0x7fffffff;
 #pragma unroll
-            for (int u4 = 0; u4 < 8; ++u4) {
-              const int4 cc = c4[u4];
-              int e0 = cc.x - 2 * static_cast<int>(v[4 * u4]), e1 = cc.y - 2 * static_cast<int>(v[4 * u4 + 1]);
-              int e2 = cc.z - 2 * static_cast<int>(v[4 * u4 + 2]), e3 = cc.w - 2 * static_cast<int>(v[4 * u4 + 3]);
-              if (!full_cols) {
-                const int col = col0 + cb + 4 * u4;
-                if (col >= a.nlist) e0 = 0x7fffffff;
-                if (col + 1 >= a.nlist) e1 = 0x7fffffff;
-                if (col + 2 >= a.nlist) e2 = 0x7fffffff;
-                if (col + 3 >= a.nlist) e3 = 0x7fffffff;
-              }
-              best = min(best, min(min(e0, e1), min(e2, e3)));
-              if (((4 * u4 + 4) & (a.G - 1)) == 0) {  // end of a group of G lists
-                const int gstart = col0 + cb + 4 * u4 + 4 - a.G;
-                if (gstart < a.nlist) a.gmin[row * a.ngroups + gstart / a.G] = best + xn;
-                best = 0x7fffffff;
-              }
+        for (int u4 = 0; u4 < 8; ++u4) {
+          const int4 cc = c4[u4];
+          v[4 * u4] = static_cast<uint32_t>(cc.x - 2 * static_cast<int>(v[4 * u4]));
+          v[4 * u4 + 1] = static_cast<uint32_t>(cc.y - 2 * static_cast<int>(v[4 * u4 + 1]));
+          v[4 * u4 + 2] = static_cast<uint32_t>(cc.z - 2 * static_cast<int>(v[4 * u4 + 2]));
+          v[4 * u4 + 3] = static_cast<uint32_t>(cc.w - 2 * static_cast<int>(v[4 * u4 + 3]));
+        }
+        if (col0 + cb + 32 > a.nlist) {
+#pragma unroll
+          for (int u = 0; u < 32; ++u)
+            if (col0 + cb + u >= a.nlist) v[u] = 0x7fffffffu;
+        }
+        auto E = [&](int u) { return static_cast<int>(v[u]); };
+        if constexpr (PASS == 1) {
+          if constexpr (GT > 0) {
+#pragma unroll
+            for (int g0 = 0; g0 < 32; g0 += GT) {
+              int best = min(min(E(g0), E(g0 + 1)), min(E(g0 + 2), E(g0 + 3)));
+#pragma unroll
+              for (int u = 4; u < GT; u += 2) best = min(best, min(E(g0 + u), E(g0 + u + 1)));
+              const int gstart = col0 + cb + g0;
+              if (gstart < a.nlist) a.gmin[row * a.ngroups + gstart / GT] = best + xn;
             }
-          } else {  // G in {1, 2}: small nlist
-            int best = 0x7fffffff;
+          } else {
+            const int G = a.G;  // any power of two <= 32
             for (int u = 0; u < 32; ++u) {
-              const int col = col0 + cb + u;
-              if (col < a.nlist) best = min(best, cn[cb + u] - 2 * static_cast<int>(v[u]));
-              if (((u + 1) & (a.G - 1)) == 0) {
-                const int gstart = col + 1 - a.G;
-                if (gstart < a.nlist) a.gmin[row * a.ngroups + gstart / a.G] = best + xn;
-                best = 0x7fffffff;
+              gacc = min(gacc, E(u));
+              if (((u + 1) & (G - 1)) == 0) {
+                const int gstart = col0 + cb + u + 1 - G;
+                if (gstart < a.nlist) a.gmin[row * a.ngroups + gstart / G] = gacc + xn;
+                gacc = 0x7fffffff;
               }
             }
           }
         } else {
+          // a block whose minimum is above tau has no candidate (the common case); otherwise one
+          // atomic reserves room for all of the block's candidates
+          int mn = min(min(E(0), E(1)), min(E(2), E(3)));
 #pragma unroll
-          for (int u4 = 0; u4 < 8; ++u4) {
-            const int4 cc = c4[u4];
-            const int ev[4] = {cc.x, cc.y, cc.z, cc.w};
+          for (int u = 4; u < 32; u += 2) mn = min(mn, min(E(u), E(u + 1)));
+          const int lim = tau_d - xn;
+          if (mn <= lim) {
+            uint32_t mask = 0;
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-              const int col = col0 + cb + 4 * u4 + x;
-              const int d = xn + ev[x] - 2 * static_cast<int>(v[4 * u4 + x]);
-              if (d <= tau_d && col < a.nlist) {
-                const int pos = atomicAdd(a.ccnt + row, 1);
-                if (pos < a.capc) a.cand[row * a.capc + pos] = step2_key(d, col);
+            for (int u = 0; u < 32; ++u) mask |= (E(u) <= lim ? 1u : 0u) << u;
+            int pos = atomicAdd(a.ccnt + row, __popc(mask));
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+              if ((mask >> u) & 1u) {
+                if (pos < a.capc) a.cand[row * a.capc + pos] = step2_key(E(u) + xn, col0 + cb + u);
+                ++pos;
               }
             }
           }
         }
       };
-      block(v0, 0);
-      block(v1, 32);
+      // two 32-column TMEM loads, processed one after the other (32 live registers)
+      tc::tmem_ld32(taddr, v);
+      tc::tmem_ld_wait();
+      if (work) block(0);
+      tc::tmem_ld32(taddr + 32, v);
+      tc::tmem_ld_wait();
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acce + acc);  // accumulator columns consumed
+      if (work) block(32);
     }
   }
   tc::fence_before_sync();
@@ -486,16 +497,28 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
 
   const size_t smem = fixed + static_cast<size_t>(stages) * kBStageBytes;
   const unsigned rb = static_cast<unsigned>((n + 7) / 8);
-  e = cudaFuncSetAttribute(coarse_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(coarse_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto pass1 = [&]<int GT>() {
+    cudaError_t e1 = cudaFuncSetAttribute(coarse_tc_kernel<1, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e1 == cudaSuccess) coarse_tc_kernel<1, GT><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
+    return e1;
+  };
+  e = cudaFuncSetAttribute(coarse_tc_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) {
-    coarse_tc_kernel<1><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
+    switch (G) {
+      case 32: e = pass1.template operator()<32>(); break;
+      case 16: e = pass1.template operator()<16>(); break;
+      case 8: e = pass1.template operator()<8>(); break;
+      case 4: e = pass1.template operator()<4>(); break;
+      default: e = pass1.template operator()<0>(); break;
+    }
+  }
+  if (e == cudaSuccess) {
     if ((e = debug_sync(st, "coarse pass 1")) != cudaSuccess) {
       cudaFreeAsync(base, st);
       return e;
     }
     tau_kernel<<<rb, 256, 0, st>>>(n, ngroups, R, a.gmin, const_cast<int32_t*>(a.tau), a.ccnt);
-    coarse_tc_kernel<2><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
+    coarse_tc_kernel<2, 0><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
     dispatch_kr(R, [&]<int KR>() {
       select_kernel<KR><<<rb, 256, 0, st>>>(n, R, capc, a.cand, a.ccnt, out_idx, out_dist, flags);
       fallback_kernel<KR><<<rb, 256, 0, st>>>(X, n, dim, mu, nlist, R, flags, out_idx, out_dist);
