@@ -26,7 +26,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth import generate, get_config  # noqa: E402
+from synth import generate, get_config, rank_queries  # noqa: E402
 
 METRIC = "queries/sec and scan HBM GB/s (fraction of roofline) at nprobe, k, 1 B200"
 FALLBACK_HBM_GBS = 6650.0
@@ -229,17 +229,15 @@ def main():
         return
 
     import torch
-    import torch.distributed as dist
+    from paper_2603_03065_b200 import dist as pdist
     from paper_2603_03065_b200 import v3db
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    pdist.init(world, "nccl", dev)
 
     def barrier():
-        if world > 1:
-            dist.barrier()
+        pdist.barrier(world)
 
     cfg = get_config(args.config)
     trace = args.trace == "on"
@@ -254,7 +252,8 @@ def main():
     del db
     counts = v3db.snapshot_export(snap, v3db.FIELD_COUNTS)
 
-    q = torch.from_numpy(inp.queries).to(dev)
+    queries = rank_queries(cfg, rank)        # replicas: an independent batch per rank (weak scaling)
+    q = torch.from_numpy(queries).to(dev)
     out = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=True, device=dev)
     if not trace:
         for key in ("trace_cand_dist",):
@@ -286,11 +285,7 @@ def main():
         torch.cuda.cudart().cudaProfilerStop()
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot_ms = float(np.sum(step_ms))
-    if world > 1:
-        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = pdist.max_over_ranks(float(np.sum(step_ms)), world, dev)
     ms_per_step = tot_ms / args.steps
     qps = cfg.Q * world / (ms_per_step / 1e3)
     coarse_ms = float(np.mean([a for a, _ in kt]))
@@ -322,7 +317,7 @@ def main():
 
     # End-to-end through the C ABI with HOST buffers (H2D queries, D2H outputs inside).
     if not args.no_e2e:
-        qh = torch.from_numpy(inp.queries).pin_memory()
+        qh = torch.from_numpy(queries).pin_memory()
         oh = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=trace, device="cpu", pin=True)
         v3db.query_batch_host(snap, qh, cfg.nprobe, cfg.k, oh)
         n_e2e = max(1, min(args.steps, 5))
@@ -330,11 +325,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(n_e2e):
             v3db.query_batch_host(snap, qh, cfg.nprobe, cfg.k, oh)
-        e2e_s = (time.perf_counter() - t0) / n_e2e
-        if world > 1:
-            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+        e2e_s = pdist.max_over_ranks((time.perf_counter() - t0) / n_e2e, world, dev)
         d2h = sum(v.numel() * 4 for v in oh.values())
         result["e2e"] = {"value": cfg.Q * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": qh.numel(),
                          "d2h_bytes_per_step": d2h, "steps": n_e2e}
@@ -355,8 +346,7 @@ def main():
     if rank == 0:
         print(json.dumps(result), flush=True)
     snap.free()
-    if world > 1:
-        dist.destroy_process_group()
+    pdist.shutdown(world)
 
 
 if __name__ == "__main__":

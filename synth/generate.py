@@ -22,6 +22,7 @@ from .configs import Config
 ROOT_SEED = 20260303
 CHUNK = 1 << 20
 STREAM_MIX, STREAM_DB, STREAM_Q, STREAM_CENT, STREAM_CODE = 0, 1, 2, 3, 4
+STREAM_Q_RANK = 100  # + rank: the independent query batch of rank > 0 in a multi-GPU run
 
 
 def _rng(cfg_id: int, stream: int, chunk: int = 0) -> np.random.Generator:
@@ -103,3 +104,11 @@ def generate(cfg: Config) -> Inputs:
     q = gen_vectors(cfg, STREAM_Q, cfg.Q)
     cent, code = sample_rows(cfg)
     return Inputs(cfg, db, q, cent, code)
+
+
+def rank_queries(cfg: Config, rank: int) -> np.ndarray:
+    """The query batch of rank `rank` of a multi-GPU (replica) run: rank 0 gets the config's own
+    queries, rank r > 0 an independent draw from the same mixture (stream 100 + r)."""
+    if rank == 0:
+        return generate(cfg).queries
+    return gen_vectors(cfg, STREAM_Q_RANK + rank, cfg.Q)

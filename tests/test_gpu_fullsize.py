@@ -1,0 +1,62 @@
+"""GPU parity at BASELINE.json's full sizes (C1-C4), in the launch configuration bench.py times
+(the whole query batch, V3DB_SCAN_AUTO, trace on), on sampled outputs the oracle computes one by
+one.
+
+At these sizes the oracle's own build is too slow to run in a test (C4: 2.1e13 MACs to rank), so
+the GPU-built snapshot is verified directly against the build rules instead (SURVEY.md §8(c)
+B1-B6, pins P7/P8): exact structure, every centroid and codeword, the greedy placement replayed
+for sampled vectors, the PQ codes of sampled slots by brute force.  The oracle's query (Steps
+1-5) then runs on that verified snapshot for sampled queries and every output
+row -- top-k ids and distances, probed lists, their distances and the full candidate trace -- must
+equal the GPU's bit for bit.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import generate, get_config
+
+from .gpu_util import first_mismatch
+from .snapshot_checks import check_snapshot
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def v3db():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_03065_b200 import build as libbuild
+    libbuild.build()
+    from paper_2603_03065_b200 import v3db as mod
+    return mod
+
+
+def export(v3db, s):
+    f = {"centroids": v3db.FIELD_CENTROIDS, "codebooks": v3db.FIELD_CODEBOOKS, "ids": v3db.FIELD_IDS,
+         "codes": v3db.FIELD_CODES, "counts": v3db.FIELD_COUNTS, "list_of": v3db.FIELD_LIST_OF}
+    return {k: v3db.snapshot_export(s, v) for k, v in f.items()}
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_full_size_sampled_parity(v3db, name):
+    cfg = get_config(name)
+    inp = generate(cfg)
+    rng = np.random.default_rng(2026)
+    s = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows,
+                            inp.codeword_rows)
+    snap = export(v3db, s)
+    check_snapshot(cfg, inp, snap, rng)
+    # the bench's launch: the whole batch, AUTO scan, trace on
+    q = torch.from_numpy(inp.queries).cuda()
+    out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, trace=True)
+    torch.cuda.synchronize()
+    s.free()
+    ref_snap = oracle.Snapshot(snap["centroids"], snap["codebooks"], snap["ids"], snap["codes"], snap["counts"],
+                               snap["list_of"])
+    sample = np.unique(np.concatenate([rng.choice(cfg.Q, 40, replace=False), [0, cfg.Q - 1]]))
+    ref = oracle.query_batch(ref_snap, inp.queries, cfg.nprobe, cfg.k, rows=sample)
+    for key, exp in ref.items():
+        got = out[key][torch.from_numpy(sample).cuda()].cpu().numpy()
+        assert np.array_equal(got, exp), f"{name} {key}: {first_mismatch(got, exp)}"
