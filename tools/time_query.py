@@ -15,6 +15,8 @@ p.add_argument("--config", default="c4")
 p.add_argument("--reps", type=int, default=5)
 p.add_argument("--algos", default="1,2")
 p.add_argument("--Q", type=int, default=0, help="use only the first Q queries")
+p.add_argument("--k", type=int, default=0, help="override k")
+p.add_argument("--trace", default="on")
 p.add_argument("--envs", default="", help="comma-separated runs after the plain run, each VAR=VALUE[:VAR=VALUE]")
 args = p.parse_args()
 cfg = get_config(args.config)
@@ -24,7 +26,9 @@ s = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M
 q = torch.from_numpy(inp.queries[: args.Q or None]).cuda().contiguous()
 if args.Q:
     cfg = cfg.with_(Q=args.Q)
-out = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=True, device="cuda")
+if args.k:
+    cfg = cfg.with_(k=args.k)
+out = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=args.trace == "on", device="cuda")
 v3db.profile_enable(True)
 for env in [""] + [e for e in args.envs.split(",") if e]:
     for kv in env.split(":"):
