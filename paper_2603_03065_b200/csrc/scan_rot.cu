@@ -154,114 +154,106 @@ __device__ __forceinline__ void bitonic_sort(uint64_t* buf, int P) {
   }
 }
 
-// Compaction of buf[0, n): entries [nres, n) hold (D, flat slot) and are resolved to (D, item)
-// keys; if n > k only the entries with D <= (k-th smallest D) stay; if ties at that D leave more
-// than `limit`, the exact k smallest keys are kept (bitonic sort).  Returns the new count and
-// sets *tau (CTA-uniform).  All threads call; n, nres uniform.
+// Buffer keys: (D << 32) | low.  low = flat slot rho*L + j (< 2^31, bit 31 clear) until the item is
+// resolved, then id ^ 0x80000000 (bit 31 set for every id >= 0; padding is never buffered) -- the
+// Step-5 key of R10.  Items are resolved only where the (D, id) order is needed: ties that would
+// overflow the buffer, and the final sort.
+__device__ __forceinline__ uint64_t resolve_key(uint64_t key, const int4* probe, const RotArgs& a) {
+  const uint32_t lo = static_cast<uint32_t>(key);
+  if (lo & 0x80000000u) return key;
+  const int rho = static_cast<int>(lo / static_cast<uint32_t>(a.L));
+  const int j = static_cast<int>(lo - static_cast<uint32_t>(rho) * a.L);
+  const int32_t id = __ldg(a.ids + static_cast<int64_t>(probe[rho].x) * a.L + j);
+  return (key & 0xffffffff00000000ull) | (static_cast<uint32_t>(id) ^ 0x80000000u);
+}
+
+// Compaction of buf[0, n) (all consumer threads; n uniform): if n > k only the entries with
+// D <= (the k-th smallest D, exact 4-pass 8-bit radix select) stay -- at least k of them, so every
+// dropped key has k keys at or below it.  If ties at that D leave more than `limit`, or `final`,
+// the items are resolved and sorted by (D, id) and the first min(n, k) kept (sorted).  Returns the
+// new count; *tau = the D threshold for later appends.
 template <int NT, int CAPM>
-__device__ int compact(uint64_t* buf, int* hist, int* s_int, const int4* probe, const RotArgs& a, int n, int nres,
-                       int limit, uint32_t* tau) {
+__device__ int compact(uint64_t* buf, int* hist, int* s_int, const int4* probe, const RotArgs& a, int n, int limit,
+                       bool final, uint32_t* tau) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint64_t kv[CAPM];
 #pragma unroll
-  for (int r = 0; r < CAPM; ++r) {
-    const int e = tid + r * NT;
-    kv[r] = ~0ull;
-    if (e < n) {
-      uint64_t key = buf[e];
-      if (e >= nres) {
-        const uint32_t flat = static_cast<uint32_t>(key);
-        const int rho = static_cast<int>(flat / static_cast<uint32_t>(a.L));
-        const int j = static_cast<int>(flat - static_cast<uint32_t>(rho) * a.L);
-        const int32_t id = __ldg(a.ids + static_cast<int64_t>(probe[rho].x) * a.L + j);
-        key = (key & 0xffffffff00000000ull) | (static_cast<uint32_t>(id) ^ 0x80000000u);
-      }
-      kv[r] = key;
-    }
-  }
-  if (n <= a.k) {  // nothing to select: write the resolved keys back
-    bar_c<NT>();
-#pragma unroll
-    for (int r = 0; r < CAPM; ++r)
-      if (tid + r * NT < n) buf[tid + r * NT] = kv[r];
-    bar_c<NT>();
-    return n;
-  }
-  // 4-pass radix select (8-bit digits) of the k-th smallest D.
-  uint32_t prefix = 0;
-  int kk = a.k;
+  for (int r = 0; r < CAPM; ++r) kv[r] = tid + r * NT < n ? buf[tid + r * NT] : ~0ull;
+  int kept = n;
+  if (n > a.k) {
+    // 4-pass radix select (8-bit digits) of the k-th smallest D.
+    uint32_t prefix = 0;
+    int kk = a.k;
 #pragma unroll 1
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
-    for (int b = tid; b < 256; b += NT) hist[b] = 0;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      for (int b = tid; b < 256; b += NT) hist[b] = 0;
+      bar_c<NT>();
+#pragma unroll
+      for (int r = 0; r < CAPM; ++r) {
+        const uint32_t D = static_cast<uint32_t>(kv[r] >> 32);
+        if (tid + r * NT < n && (pass == 0 || (D >> (shift + 8)) == prefix)) atomicAdd(&hist[(D >> shift) & 255], 1);
+      }
+      bar_c<NT>();
+      if (warp == 0) {
+        int h[8], sum = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          h[b] = hist[lane * 8 + b];
+          sum += h[b];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += v;
+        }
+        int cum = incl - sum;  // exclusive prefix of this lane's 8 bins
+        if (cum < kk && kk <= incl) {
+          int bin = lane * 8;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (cum + h[b] >= kk) break;
+            cum += h[b];
+            ++bin;
+          }
+          s_int[8] = bin;
+          s_int[9] = kk - cum;
+        }
+      }
+      bar_c<NT>();
+      prefix = (prefix << 8) | static_cast<uint32_t>(s_int[8]);
+      kk = s_int[9];
+      bar_c<NT>();  // s_int[8..9] reused next pass
+    }
+    *tau = prefix;  // exact k-th smallest D
+    if (tid == 0) s_int[10] = 0;
     bar_c<NT>();
 #pragma unroll
     for (int r = 0; r < CAPM; ++r) {
-      const uint32_t D = static_cast<uint32_t>(kv[r] >> 32);
-      if (tid + r * NT < n && (pass == 0 || (D >> (shift + 8)) == prefix)) atomicAdd(&hist[(D >> shift) & 255], 1);
+      const bool keep = tid + r * NT < n && static_cast<uint32_t>(kv[r] >> 32) <= prefix;
+      const uint32_t bal = __ballot_sync(kFull, keep);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&s_int[10], __popc(bal));
+      base = __shfl_sync(kFull, base, 0);
+      if (keep) buf[base + __popc(bal & ((1u << lane) - 1u))] = kv[r];
     }
     bar_c<NT>();
-    if (warp == 0) {
-      int h[8], sum = 0;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        h[b] = hist[lane * 8 + b];
-        sum += h[b];
-      }
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
-      }
-      int cum = incl - sum;  // exclusive prefix of this lane's 8 bins
-      const bool mine = cum < kk && kk <= incl;
-      if (mine) {
-        int bin = lane * 8;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (cum + h[b] >= kk) break;
-          cum += h[b];
-          ++bin;
-        }
-        s_int[8] = bin;
-        s_int[9] = kk - cum;
-      }
-    }
-    bar_c<NT>();
-    prefix = (prefix << 8) | static_cast<uint32_t>(s_int[8]);
-    kk = s_int[9];
-    bar_c<NT>();  // s_int[8..9] reused next pass
+    kept = s_int[10];
   }
-  const uint32_t tauD = prefix;  // exact k-th smallest D
-  if (tid == 0) s_int[10] = 0;
-  bar_c<NT>();
-#pragma unroll
-  for (int r = 0; r < CAPM; ++r) {
-    const bool keep = tid + r * NT < n && static_cast<uint32_t>(kv[r] >> 32) <= tauD;
-    const uint32_t bal = __ballot_sync(kFull, keep);
-    int base = 0;
-    if (lane == 0 && bal) base = atomicAdd(&s_int[10], __popc(bal));
-    base = __shfl_sync(kFull, base, 0);
-    if (keep) buf[base + __popc(bal & ((1u << lane) - 1u))] = kv[r];
-  }
-  bar_c<NT>();
-  int kept = s_int[10];
-  *tau = tauD;
-  if (kept > limit) {  // many ties at tauD: exact (D, item) selection
+  if (final || kept > limit) {  // exact (D, id) order: resolve, sort, keep the first min(kept, k)
+    for (int e = tid; e < kept; e += NT) buf[e] = resolve_key(buf[e], probe, a);
     int P = 1;
     while (P < kept) P <<= 1;
     for (int e = kept + tid; e < P; e += NT) buf[e] = ~0ull;
     bar_c<NT>();
     bitonic_sort<NT>(buf, P);
-    kept = a.k;
+    if (kept > a.k) kept = a.k;
   }
   bar_c<NT>();
   return kept;
 }
 
-// Step 4 of one slot per lane: acc += sum over the subspaces of group G_IDX.. of the rotated
-// table entry selected by the slot's code byte (compile-time unrolled per group).
 template <int M, int MODE, int G_IDX>
 __device__ __forceinline__ void lut_sum(const uint32_t (&w)[M / 4], uint32_t lane4, int32_t& acc) {
   constexpr int off = rot_goff(M, G_IDX), Gg = MODE == kLutP64 ? M : rot_gsize(M, G_IDX);
@@ -458,7 +450,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   int32_t* trq = a.trace ? a.trace + qi * nprobe * static_cast<int64_t>(L) + lane : nullptr;  // this query's trace
   const int limit = a.cap - a.R * SEG * 32;  // an epoch appends at most R * SEG * 32 entries
   uint32_t tau = kTauInit;
-  int n_base = 0, n_res = 0;                 // buffer entries before this epoch / resolved prefix
+  int n_base = 0;                            // buffer entries before this epoch
   int epoch = 0, in_epoch = 0;
 
   uint32_t fph = 0;
@@ -526,16 +518,17 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
       s = 0;
       fph ^= 1u;
     }
-    if (++in_epoch == a.R) {                    // epoch boundary (uniform across consumers)
+    // epoch boundary (uniform across consumers): every R stages, and after the first stage so
+    // that tau is set early (before it, every valid candidate is appended)
+    if (++in_epoch == a.R || (t == 0 && a.R > 1)) {
       bar_c<NT>();
       n_base += s_int[epoch % 3];
       if (tid == 0) s_int[(epoch + 2) % 3] = 0;  // next used in epoch + 2; last read before this barrier
       ++epoch;
       in_epoch = 0;
-      if (n_base > limit) {
-        uint32_t t2;
-        n_base = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, n_res, limit, &t2);
-        n_res = n_base;
+      if (n_base > limit || (tau == kTauInit && n_base > a.k)) {
+        uint32_t t2 = tau;
+        n_base = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, limit, false, &t2);
         tau = t2;
       }
     }
@@ -544,14 +537,8 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   n_base += s_int[epoch % 3];
 
   // Final Step 5: the k smallest (D, item) keys, (d_max, -1) past the valid candidates (R11).
-  uint32_t t2;
-  int n = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, n_res, a.k, &t2);
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int e = n + tid; e < P; e += NT) buf[e] = ~0ull;
-  bar_c<NT>();
-  bitonic_sort<NT>(buf, P);
-  if (n > a.k) n = a.k;
+  uint32_t t2 = tau;
+  const int n = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, a.k, true, &t2);
   for (int r = tid; r < a.k; r += NT) {
     int32_t id = -1, dd = kDMax;
     if (r < n) {
