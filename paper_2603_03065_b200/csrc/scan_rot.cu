@@ -119,6 +119,7 @@ struct RotArgs {
   int32_t* out_ids;
   int32_t* out_dist;
   int32_t* trace;
+  const int32_t* order;   // [nq] query processed by CTA b (L2-aware schedule), or null = identity
 };
 
 // Named barrier 1 among the NT consumer threads (the producer warp never joins).
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   uint64_t* empty = full + a.NS;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t qi = blockIdx.x;
+  const int64_t qi = a.order ? a.order[blockIdx.x] : blockIdx.x;
   const int L = a.L, nprobe = a.nprobe, NS = a.NS, SEG = a.SEG;
   const uint32_t pbase = static_cast<uint32_t>(SEG) * 32u * M;  // P terms inside a stage
 
@@ -624,32 +625,51 @@ int budget() {
   return (228 * 1024) / C::MINB - 1024;  // per-CTA share of the SM (1 KB reserved per CTA)
 }
 
-}  // namespace
+// L2-aware schedule: CTAs run in blockIdx order, ~300 at a time, so
+// queries whose probe sets overlap should be adjacent.  List ids are a random sample of the
+// database, so min(probe list ids) is a MinHash of the probe set: two queries get the same key with
+// probability = the Jaccard similarity of their probe sets.  A counting sort by that key groups
+// them; the results do not depend on the order (each CTA writes its own query's rows).
+__global__ void minhash_kernel(const int32_t* __restrict__ lists, int64_t nq, int nprobe, int32_t* __restrict__ key,
+                               int* __restrict__ hist) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q >= nq) return;
+  int m = 0x7fffffff;
+  for (int r = 0; r < nprobe; ++r) m = min(m, __ldg(lists + q * nprobe + r));
+  key[q] = m;
+  atomicAdd(hist + m, 1);
+}
 
-cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
-                         const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
-                         int32_t* trace, cudaStream_t st) {
-  if (nq <= 0) return cudaSuccess;
-  if (s->lut_mode == 0) return cudaErrorInvalidValue;
-  RotArgs a;
-  a.queries = queries;
-  a.dim = s->dim;
-  a.d = s->d;
-  a.Ks = s->Ks;
-  a.L = s->L;
-  a.Lp = (s->L + 31) & ~31;
-  a.nprobe = nprobe;
-  a.k = k;
-  a.cbT = s->cbT;
-  a.codes = s->codes_rot;
-  a.pterm = s->pterm_rot;
-  a.ids = s->ids;
-  a.counts = s->counts;
-  a.lists = lists;
-  a.ldist = ldist;
-  a.out_ids = out_ids;
-  a.out_dist = out_dist;
-  a.trace = trace;
+// exclusive scan of hist[0, n) in place (one CTA of 1024 threads)
+__global__ void __launch_bounds__(1024) scan_hist_kernel(int* __restrict__ hist, int n) {
+  __shared__ int part[1024];
+  const int per = (n + 1023) / 1024, b = threadIdx.x * per, e = min(n, b + per);
+  int sum = 0;
+  for (int i = b; i < e; ++i) sum += hist[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int run = part[threadIdx.x] - sum;
+  for (int i = b; i < e; ++i) {
+    const int c = hist[i];
+    hist[i] = run;
+    run += c;
+  }
+}
+
+__global__ void scatter_kernel(const int32_t* __restrict__ key, int64_t nq, int* __restrict__ offs,
+                               int32_t* __restrict__ order) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q >= nq) return;
+  order[atomicAdd(offs + key[q], 1)] = static_cast<int32_t>(q);
+}
+
+cudaError_t scan_dispatch(const v3db_snapshot* s, RotArgs& a, int64_t nq, cudaStream_t st) {
 #define V3DB_ROT(MM, MODE) return launch<MM, MODE>(a, nq, budget<MM, MODE>(), st);
   if (s->lut_mode == kLutP64) {
     switch (s->M) {
@@ -678,6 +698,65 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
     default: return cudaErrorInvalidValue;
   }
 #undef V3DB_ROT
+}
+
+
+}  // namespace
+
+cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
+                         const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
+                         int32_t* trace, cudaStream_t st) {
+  if (nq <= 0) return cudaSuccess;
+  if (s->lut_mode == 0) return cudaErrorInvalidValue;
+  RotArgs a;
+  a.queries = queries;
+  a.dim = s->dim;
+  a.d = s->d;
+  a.Ks = s->Ks;
+  a.L = s->L;
+  a.Lp = (s->L + 31) & ~31;
+  a.nprobe = nprobe;
+  a.k = k;
+  a.cbT = s->cbT;
+  a.codes = s->codes_rot;
+  a.pterm = s->pterm_rot;
+  a.ids = s->ids;
+  a.counts = s->counts;
+  a.lists = lists;
+  a.ldist = ldist;
+  a.out_ids = out_ids;
+  a.out_dist = out_dist;
+  a.trace = trace;
+  a.order = nullptr;
+  // L2-aware schedule when the probed lists do not fit in L2 anyway and the batch is large
+  const char* sched = getenv("V3DB_SCHED");
+  const bool want = sched ? sched[0] == '1'
+                          : (nq >= 2048 && static_cast<int64_t>(s->nlist) * s->L * s->M > (int64_t(64) << 20));
+  void* sbuf = nullptr;
+  if (want) {
+    cudaError_t e = cudaMallocAsync(&sbuf, sizeof(int32_t) * (2 * nq + s->nlist), st);
+    if (e != cudaSuccess) return e;
+    int32_t* key = static_cast<int32_t*>(sbuf);
+    int32_t* order = key + nq;
+    int* hist = order + nq;
+    e = cudaMemsetAsync(hist, 0, sizeof(int) * s->nlist, st);
+    if (e == cudaSuccess) {
+      const unsigned g = static_cast<unsigned>((nq + 255) / 256);
+      minhash_kernel<<<g, 256, 0, st>>>(lists, nq, nprobe, key, hist);
+      scan_hist_kernel<<<1, 1024, 0, st>>>(hist, s->nlist);
+      scatter_kernel<<<g, 256, 0, st>>>(key, nq, hist, order);
+      note_launch(3);
+      e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) {
+      cudaFreeAsync(sbuf, st);
+      return e;
+    }
+    a.order = order;
+  }
+  cudaError_t res = scan_dispatch(s, a, nq, st);
+  if (sbuf) cudaFreeAsync(sbuf, st);
+  return res;
 }
 
 }  // namespace v3db
