@@ -576,11 +576,12 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
                                 {8, 3, 1024}, {8, 2, 1024}};
   int SEG = 8, NS = 2, cap = 1024;
   size_t smem = 0;
-  const char* e_seg = getenv("V3DB_SEG");  // experiments: force (SEG, NS)
+  const char* e_seg = getenv("V3DB_SEG");  // experiments: force (SEG, NS, cap)
   const char* e_ns = getenv("V3DB_NS");
+  const char* e_cap = getenv("V3DB_CAP");
   for (const auto& c : cand) {
     const int seg = e_seg ? atoi(e_seg) : c[0], ns = e_ns ? atoi(e_ns) : c[1];
-    const int cp = a.k + seg * 32 <= c[2] ? c[2] : 2048;
+    const int cp = e_cap ? atoi(e_cap) : (a.k + seg * 32 <= c[2] ? c[2] : 2048);
     const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) + 16u * ns * seg +
                         8u * cp + 256 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
     SEG = seg;
@@ -616,7 +617,8 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   const int capm = cap / NT;
   if (capm <= 2) return launch_cap<M, MODE, 2, VAR>(a, nq, smem, st);
   if (capm <= 4) return launch_cap<M, MODE, 4, VAR>(a, nq, smem, st);
-  return launch_cap<M, MODE, 8, VAR>(a, nq, smem, st);
+  if (capm <= 8) return launch_cap<M, MODE, 8, VAR>(a, nq, smem, st);
+  return launch_cap<M, MODE, 16, VAR>(a, nq, smem, st);
 }
 
 template <int M, int MODE, int VAR = 0>
