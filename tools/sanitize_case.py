@@ -27,7 +27,7 @@ for name, nq in (("c0", 64), ("e2_basic", 40), ("c4_mini", 24), ("e2_large", 16)
             os.environ.pop("V3DB_LUT_MODE", None)
         s = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows,
                                 inp.codeword_rows)
-        for algo in (1, 2):
+        for algo in (1, 0):
             out = v3db.query_batch(s, torch.from_numpy(qs).cuda(), cfg.nprobe, cfg.k, algo=algo)
             torch.cuda.synchronize()
             for key, exp in ref.items():
