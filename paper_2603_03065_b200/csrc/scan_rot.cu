@@ -29,10 +29,11 @@
 // Chunks holding only padding are never read: their trace entries (d_max) are written up front.
 //
 // Top-k.  Candidates with D <= tau are appended to a shared buffer
-// (warp-aggregated).  Every R stages the consumer warps meet at one named barrier; if the buffer could overflow
-// during the next epoch it is compacted: item ids are resolved, a 4-pass radix select finds the
-// k-th smallest D, tau = that D and only entries with D <= tau stay (>= k of them, so every
-// dropped key has k keys at or below it).  At the end the survivors are sorted by (D, item).
+// (warp-aggregated).  When an append lifts the count above a high-water mark, a compaction is
+// requested and every consumer warp joins it at its next stage end (no periodic barrier): a
+// 4-pass radix select finds the k-th smallest D, tau = that D and only entries with D <= tau stay
+// (>= k of them, so every dropped key has k keys at or below it).  Item ids are resolved only for
+// tie overflow and for the final (D, id) sort.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -107,7 +108,7 @@ struct Geo {
 
 struct RotArgs {
   const int8_t* queries;
-  int dim, d, Ks, L, Lp, nprobe, k, cap, NS, SEG, R;
+  int dim, d, Ks, L, Lp, nprobe, k, cap, NS, SEG;
   uint32_t off_stage, off_desc, off_vc, off_buf, off_hist, off_probe, off_q, off_int, off_bar, stage_bytes;
   const int8_t* cbT;
   const uint8_t* codes;   // codes_rot [nlist][Lp/32][unit][lane][U]
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   int* hist = reinterpret_cast<int*>(smem + a.off_hist);
   int4* probe = reinterpret_cast<int4*>(smem + a.off_probe);  // (list, d_i, count, 0)
   int8_t* qs = reinterpret_cast<int8_t*>(smem + a.off_q);
-  int* s_int = reinterpret_cast<int*>(smem + a.off_int);     // [0..2] epoch counters, [8..10] scratch
+  int* s_int = reinterpret_cast<int*>(smem + a.off_int);     // [0] count [1] request [2] done, [8..10] scratch
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.NS;
 
@@ -449,10 +450,25 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   bar_c<NT>();
   const uint32_t lane4 = static_cast<uint32_t>(*reinterpret_cast<volatile int*>(&s_int[32 + lane]));
   int32_t* trq = a.trace ? a.trace + qi * nprobe * static_cast<int64_t>(L) + lane : nullptr;  // this query's trace
-  const int limit = a.cap - a.R * SEG * 32;  // an epoch appends at most R * SEG * 32 entries
+  // Candidate buffer: s_int[0] = entries (monotonic between compactions), s_int[1] = compaction
+  // requested, s_int[2] = consumer warps done.  A warp whose append lifts the count above `hw`
+  // (or above k before tau is set) requests a compaction; every consumer warp joins at its next
+  // stage end (warps drift by less than NS stages and append at most 2 chunks per stage, so at
+  // most 2 * SEG * 32 more entries arrive before all have joined -- the headroom above hw).
+  const int hw = a.cap - 2 * SEG * 32;
   uint32_t tau = kTauInit;
-  int n_base = 0;                            // buffer entries before this epoch
-  int epoch = 0, in_epoch = 0;
+  volatile int* vs = s_int;
+  auto collective_compact = [&]() {  // all consumer threads
+    bar_c<NT>();                     // every warp stopped appending
+    uint32_t t2 = tau;
+    const int kept = compact<NT, CAPM>(buf, hist, s_int, probe, a, s_int[0], hw, false, &t2);
+    tau = t2;
+    if (tid == 0) {
+      s_int[0] = kept;
+      s_int[1] = 0;
+    }
+    bar_c<NT>();
+  };
 
   uint32_t fph = 0;
   // one chunk's code words (rotated, chunk-transposed) from the stage
@@ -481,10 +497,14 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
     const uint32_t bal = __ballot_sync(kFull, pass);
     if (bal) {
       int base = 0;
-      if (lane == 0) base = atomicAdd(&s_int[epoch % 3], __popc(bal));
+      if (lane == 0) {
+        const int cnt = __popc(bal);
+        base = atomicAdd(&s_int[0], cnt);
+        if (base + cnt > (tau == kTauInit ? min(hw, 4 * a.k) : hw)) vs[1] = 1;
+      }
       base = __shfl_sync(kFull, base, 0);
       if (pass)
-        buf[n_base + base + __popc(bal & ((1u << lane) - 1u))] =
+        buf[base + __popc(bal & ((1u << lane) - 1u))] =
             (static_cast<uint64_t>(static_cast<uint32_t>(D)) << 32) | static_cast<uint32_t>(off);
     }
   };
@@ -519,23 +539,23 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
       s = 0;
       fph ^= 1u;
     }
-    // epoch boundary (uniform across consumers): every R stages, and after the first stage so
-    // that tau is set early (before it, every valid candidate is appended)
-    if (++in_epoch == a.R || (t == 0 && a.R > 1)) {
-      bar_c<NT>();
-      n_base += s_int[epoch % 3];
-      if (tid == 0) s_int[(epoch + 2) % 3] = 0;  // next used in epoch + 2; last read before this barrier
-      ++epoch;
-      in_epoch = 0;
-      if (n_base > limit || (tau == kTauInit && n_base > a.k)) {
-        uint32_t t2 = tau;
-        n_base = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, limit, false, &t2);
-        tau = t2;
-      }
+    if (vs[1]) collective_compact();  // warp-uniform (one broadcast read)
+  }
+  // wait for the other consumer warps, joining any compaction they request meanwhile
+  __syncwarp();
+  if (lane == 0) atomicAdd(&s_int[2], 1);
+  for (;;) {
+    __syncwarp();
+    const int req = vs[1], done = vs[2];
+    if (req) {
+      collective_compact();
+      continue;
     }
+    if (done == W) break;
+    __nanosleep(64);
   }
   bar_c<NT>();
-  n_base += s_int[epoch % 3];
+  const int n_base = s_int[0];
 
   // Final Step 5: the k smallest (D, item) keys, (d_max, -1) past the valid candidates (R11).
   uint32_t t2 = tau;
@@ -570,8 +590,7 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   auto al = [](uint32_t x, uint32_t b) { return (x + b - 1) / b * b; };
   const uint32_t lut = MODE == kLutP64 ? static_cast<uint32_t>(a.Ks) * 256u : C::NG * kW32GroupBytes;
   const uint32_t chunk = 32u * M + 128u;  // codes + P terms of one 32-slot chunk
-  // (SEG, NS, cap): the first candidate that fits the per-CTA budget.  A bigger candidate buffer
-  // (cap) lets an epoch span more stages (fewer consumer barriers); 2-3 stages in flight suffice.
+  // (SEG, NS, cap): the first candidate that fits the per-CTA budget; 2-3 stages in flight suffice.
   static const int cand[][3] = {{16, 3, 2048}, {16, 3, 1024}, {16, 2, 2048}, {8, 4, 1024}, {16, 2, 1024},
                                 {8, 3, 1024}, {8, 2, 1024}};
   int SEG = 8, NS = 2, cap = 1024;
@@ -581,7 +600,8 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   const char* e_cap = getenv("V3DB_CAP");
   for (const auto& c : cand) {
     const int seg = e_seg ? atoi(e_seg) : c[0], ns = e_ns ? atoi(e_ns) : c[1];
-    const int cp = e_cap ? atoi(e_cap) : (a.k + seg * 32 <= c[2] ? c[2] : 2048);
+    // headroom: 2 stages of appends above the high-water mark, which must be >= k
+    const int cp = e_cap ? atoi(e_cap) : (a.k + 2 * seg * 32 <= c[2] ? c[2] : 4096);
     const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) + 16u * ns * seg +
                         8u * cp + 256 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
     SEG = seg;
@@ -594,7 +614,6 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   a.SEG = SEG;
   a.NS = NS;
   a.cap = cap;
-  a.R = (cap - a.k) / (SEG * 32);  // >= 1: after a compaction at most k entries remain
   a.stage_bytes = al(SEG * chunk, 128);
   uint32_t o = al(lut, 128);
   a.off_stage = o;
