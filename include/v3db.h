@@ -135,6 +135,26 @@ int v3db_query_batch_host(v3db_snapshot_t s, const int8_t* queries, int64_t nq, 
                           int32_t k, int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists,
                           int32_t* trace_list_dist, int32_t* trace_cand_dist, void* stream);
 
+/*
+ * v3db_witness_batch -- the prover witness of nq (challenged) queries: the values the
+ * multiset-based design takes from the off-circuit run of Steps 1-5 (§4.7,
+ * PAPER.md:614-657).  Per query, all in DEVICE memory, any may be NULL:
+ *   list_order [nq][nlist], list_dist [nq][nlist]   S^sorted_{idx,dist}: every list i with its
+ *                          d_i = dist(q, mu_i), ascending (d_i, i) (R9); the first
+ *                          nprobe are P(q) (equal to v3db_query_batch's trace_lists)
+ *   lut_sel [nq][nprobe][L][M]   l^{(m)}_{i,j} = LUT_{i,m,v^{(m)}_{i,j}}: the literal Step-3 entry
+ *                           selected by each probed slot's code, padding slots
+ *                          included (code 0)
+ *   cand_items [nq][nprobe*L], cand_dist [nq][nprobe*L]   S^sorted_{item,dist}: all N_sel
+ *                          candidates (item, D) ascending (D, item) (R10); the
+ *                          first k are v3db_query_batch's out_ids / out_dist
+ * nq in [0, 65535].  Asynchronous on `stream`.  Errors: EINVAL (NULL handle/queries, nq or nprobe out
+ * of range), ENOMEM, ECUDA.  Not on the query hot path (on demand, a few MB per query).
+ */
+int v3db_witness_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe,
+                       int32_t* list_order, int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items,
+                       int32_t* cand_dist, void* stream);
+
 /* v3db_free -- release a snapshot.  NULL-safe.  The caller must not free a snapshot with
  * query work still in flight on any stream. */
 void v3db_free(v3db_snapshot_t s);

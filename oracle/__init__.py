@@ -18,4 +18,5 @@ from .v3db_oracle import (  # noqa: F401
     step3_adc_tables,
     step4_candidate_distances,
     step5_topk,
+    witness,
 )

@@ -298,3 +298,29 @@ def query_batch(s: Snapshot, queries, nprobe: int, k: int, rows=None) -> dict:
         out["trace_list_dist"][a] = dp
         out["trace_cand_dist"][a] = cand
     return out
+
+
+# ----------------------------------------------------------------------------------------
+# Prover witness of one query (§4.7, "Multiset-Based Design")
+# ----------------------------------------------------------------------------------------
+
+def witness(q, s: Snapshot, nprobe: int):
+    """The witness values the multiset-based prover takes from the off-circuit run of the query
+    (PAPER.md:617-618):
+      * S^sorted_{idx,dist}: all n_list pairs (i, d_i) sorted (PAPER.md:625-629), ties by i (R9);
+      * the selected LUT entries l^{(m)}_{i,j} = LUT_{i,m,v^{(m)}_{i,j}} for i in P(q), j in [n],
+        m in [M] (PAPER.md:639-644), literal Step-3 tables, padding slots included (their code 0);
+      * S^sorted_{item,dist}: all N_sel candidate pairs (item, D) sorted, ties by
+        item (R10).
+    Returns (order[nlist], order_dist[nlist], ell[nprobe][L][M], items[N_sel], dists[N_sel])."""
+    d = step1_centroid_distances(q, s)
+    order = np.lexsort((np.arange(s.nlist), d))            # primary key d, secondary i
+    probes = order[:nprobe]
+    lut = step3_adc_tables(q, s, probes)                     # [nprobe][M][Ks]
+    m_idx = np.arange(s.M)[None, :]
+    ell = np.stack([lut[rho][m_idx, s.codes[i].astype(np.int64)] for rho, i in enumerate(probes)])
+    cand = step4_candidate_distances(s, probes, lut)         # [nprobe][L]
+    items = s.ids[probes].reshape(-1).astype(np.int64)
+    dists = cand.reshape(-1)
+    o2 = np.lexsort((items, dists))
+    return order, d[order], ell, items[o2], dists[o2]

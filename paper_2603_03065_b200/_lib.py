@@ -34,6 +34,8 @@ _SIGS = {
     "v3db_query_batch_host": (ctypes.c_int, [ctypes.c_void_p, _c_i8p, ctypes.c_int64, ctypes.c_int32,
                                              ctypes.c_int32, _c_i32p, _c_i32p, _c_i32p, _c_i32p, _c_i32p,
                                              ctypes.c_void_p]),
+    "v3db_witness_batch": (ctypes.c_int, [ctypes.c_void_p, _c_i8p, ctypes.c_int64, ctypes.c_int32, _c_i32p, _c_i32p,
+                                          _c_i32p, _c_i32p, _c_i32p, ctypes.c_void_p]),
     "v3db_free": (None, [ctypes.c_void_p]),
     "v3db_snapshot_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "v3db_snapshot_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t]),

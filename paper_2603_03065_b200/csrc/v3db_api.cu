@@ -415,6 +415,23 @@ int v3db_query_batch_host(v3db_snapshot_t s, const int8_t* queries, int64_t nq, 
   return V3DB_OK;
 }
 
+int v3db_witness_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe, int32_t* list_order,
+                       int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items, int32_t* cand_dist, void* stream) {
+  g_err.clear();
+  if (!s) return fail(V3DB_EINVAL, "NULL snapshot");
+  if (nq < 0 || nq > 65535) return fail(V3DB_EINVAL, "nq out of range [0, 65535] (witnesses are per challenged query)");
+  if (nq > 0 && !queries) return fail(V3DB_EINVAL, "NULL queries");
+  if (nprobe < 1 || nprobe > s->nlist || nprobe > V3DB_MAX_NPROBE)
+    return fail(V3DB_EINVAL, "nprobe out of range [1, min(nlist, V3DB_MAX_NPROBE)]");
+  int rc = check_device(s);
+  if (rc != V3DB_OK) return rc;
+  if (nq == 0) return V3DB_OK;
+  cudaError_t e = v3db::witness_batch(s, queries, nq, nprobe, list_order, list_dist, lut_sel, cand_items, cand_dist,
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "v3db_witness_batch");
+  return V3DB_OK;
+}
+
 int v3db_snapshot_info(v3db_snapshot_t s, int64_t* out8) {
   g_err.clear();
   if (!s || !out8) return fail(V3DB_EINVAL, "NULL pointer");

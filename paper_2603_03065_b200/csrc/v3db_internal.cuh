@@ -127,4 +127,9 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
                          const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
                          int32_t* trace_cand, cudaStream_t st);
 
+// Prover witness of a batch of queries (witness.cu; §4.7).  Outputs may be null.
+cudaError_t witness_batch(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int32_t* list_order,
+                          int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items, int32_t* cand_dist,
+                          cudaStream_t st);
+
 }  // namespace v3db

@@ -135,6 +135,25 @@ def query_batch_host(s: Snapshot, queries: torch.Tensor, nprobe: int, k: int, ou
     return out
 
 
+def witness_batch(s: Snapshot, queries: torch.Tensor, nprobe: int, lut_sel: bool = True, stream=None) -> dict:
+    """v3db_witness_batch: the prover witness of each query (§4.7) as CUDA int32 tensors:
+    list_order/list_dist [nq][nlist] (S^sorted_idx,dist), lut_sel [nq][nprobe][L][M] (selected LUT
+    entries), cand_items/cand_dist [nq][nprobe*L] (S^sorted_item,dist)."""
+    lib = _lib.load()
+    nq = queries.shape[0]
+    _need(queries, torch.int8, "cuda", (nq, s.dim), "queries")
+    kw = dict(dtype=torch.int32, device=queries.device)
+    nsel = nprobe * s.list_cap
+    out = {"list_order": torch.empty((nq, s.nlist), **kw), "list_dist": torch.empty((nq, s.nlist), **kw),
+           "cand_items": torch.empty((nq, nsel), **kw), "cand_dist": torch.empty((nq, nsel), **kw)}
+    if lut_sel:
+        out["lut_sel"] = torch.empty((nq, nprobe, s.list_cap, s.m), **kw)
+    _lib.check(lib.v3db_witness_batch(s.handle, _ptr(queries), nq, nprobe, _ptr(out["list_order"]),
+                                      _ptr(out["list_dist"]), _ptr(out.get("lut_sel")), _ptr(out["cand_items"]),
+                                      _ptr(out["cand_dist"]), _stream_ptr(stream)))
+    return out
+
+
 _INFO_KEYS = ("n", "dim", "nlist", "list_cap", "m", "ks", "d", "total_valid")
 
 

@@ -51,6 +51,8 @@ def test_full_size_sampled_parity(v3db, name):
     # the bench's launch: the whole batch, AUTO scan, trace on
     q = torch.from_numpy(inp.queries).cuda()
     out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, trace=True)
+    wq = [int(rng.integers(cfg.Q)) for _ in range(2)]          # two "challenged" queries (NEXT-2)
+    w = v3db.witness_batch(s, q[wq].contiguous(), cfg.nprobe)
     torch.cuda.synchronize()
     s.free()
     ref_snap = oracle.Snapshot(snap["centroids"], snap["codebooks"], snap["ids"], snap["codes"], snap["counts"],
@@ -60,3 +62,8 @@ def test_full_size_sampled_parity(v3db, name):
     for key, exp in ref.items():
         got = out[key][torch.from_numpy(sample).cuda()].cpu().numpy()
         assert np.array_equal(got, exp), f"{name} {key}: {first_mismatch(got, exp)}"
+    for a, qi in enumerate(wq):
+        exp = oracle.witness(inp.queries[qi], ref_snap, cfg.nprobe)
+        for key, e in zip(("list_order", "list_dist", "lut_sel", "cand_items", "cand_dist"), exp):
+            got = w[key][a].cpu().numpy()
+            assert np.array_equal(got, e), f"{name} witness {key}: {first_mismatch(got, e)}"

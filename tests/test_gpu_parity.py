@@ -280,3 +280,27 @@ def test_odd_dim_generic_paths(v3db):
     qs = rng.integers(-90, 90, size=(77, D)).astype(np.int8)
     run_case(v3db, db, qs, nlist, L, M, Ks, 3, 20, rng.choice(N, nlist, replace=False),
              np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
+
+
+@pytest.mark.parametrize("name,nq", [("c0", 64), ("e2_lowacc", 16), ("e2_basic", 12), ("c4_mini", 6)])
+def test_witness_batch(v3db, name, nq):
+    """NEXT-2: the prover witness (§4.7) -- S^sorted_idx,dist, the selected literal LUT
+    entries and S^sorted_item,dist -- bit-exact against oracle.witness, and consistent with the
+    query path's trace and top-k."""
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    q = torch.from_numpy(np.ascontiguousarray(inp.queries[:nq])).cuda()
+    w = v3db.witness_batch(s, q, cfg.nprobe)
+    out = v3db.query_batch(s, q, cfg.nprobe, cfg.k)
+    torch.cuda.synchronize()
+    got = {k2: v.cpu().numpy() for k2, v in w.items()}
+    for a in range(nq):
+        order, od, ell, items, dists = oracle.witness(inp.queries[a], ref_s, cfg.nprobe)
+        assert np.array_equal(got["list_order"][a], order), (a, first_mismatch(got["list_order"][a], order))
+        assert np.array_equal(got["list_dist"][a], od), a
+        assert np.array_equal(got["lut_sel"][a], ell), (a, first_mismatch(got["lut_sel"][a], ell))
+        assert np.array_equal(got["cand_items"][a], items), (a, first_mismatch(got["cand_items"][a], items))
+        assert np.array_equal(got["cand_dist"][a], dists), a
+    assert np.array_equal(got["list_order"][:, :cfg.nprobe], out["trace_lists"].cpu().numpy())
+    assert np.array_equal(got["cand_items"][:, :cfg.k], out["out_ids"].cpu().numpy())
+    s.free()

@@ -287,3 +287,36 @@ def test_build_errors():
         oracle.build_snapshot(db, 2, 8, 2, 2, [0, 0], [[0, 1], [2, 3]])       # duplicate centroid rows
     with pytest.raises(ValueError):
         oracle.build_snapshot(db, 2, 8, 3, 2, [0, 1], [[0, 1], [2, 3], [4, 5]])  # D % M != 0
+
+
+# ---------------------------------------------------------------- prover witness (NEXT-2)
+
+def test_witness_consistent_with_pinned_steps():
+    """The witness against the already-pinned steps and the paper's own checks:
+    S^sorted_{idx,dist} is a permutation of [n_list] in nondecreasing d whose first n_probe entries
+    are Step 2's P(q); every selected entry equals dist(C_{m,code}, (q-mu_i)^(m))
+    recomputed by brute force and the entries of a valid slot sum to its Step-4 distance (the
+    multiset-inclusion statement of PAPER.md:640-648); S^sorted_{item,dist} is the multiset of
+    S^orig in nondecreasing D whose first k pairs are Step 5's output."""
+    rng = np.random.default_rng(21)
+    db, s = _random_snapshot(rng, N=400, D=8, nlist=7, L=80, M=4, Ks=8, lo=-40, hi=40)
+    M, Ks, d = s.codebooks.shape
+    for _ in range(6):
+        q = rng.integers(-128, 128, size=s.D).astype(np.int8)
+        nprobe, k = int(rng.integers(1, s.nlist + 1)), int(rng.integers(1, 30))
+        order, od, ell, items, dists = oracle.witness(q, s, nprobe)
+        ids, dd, probes, dP, cand = oracle.query(q, s, nprobe, k)
+        assert sorted(order.tolist()) == list(range(s.nlist)) and (np.diff(od) >= 0).all()
+        assert order[:nprobe].tolist() == probes.tolist()
+        assert od.tolist() == [oracle.dist(q, s.centroids[i]) for i in order]
+        for rho, i in enumerate(probes):
+            res = q.astype(np.int64) - s.centroids[i].astype(np.int64)
+            for j in range(0, s.L, 9):
+                for m in range(M):
+                    c = int(s.codes[i, j, m])
+                    assert ell[rho, j, m] == oracle.dist(s.codebooks[m, c], res[m * d:(m + 1) * d])
+                if s.ids[i, j] != -1:
+                    assert ell[rho, j].sum() == cand[rho, j]
+        orig = sorted(zip(s.ids[probes].reshape(-1).tolist(), cand.reshape(-1).tolist()))
+        assert sorted(zip(items.tolist(), dists.tolist())) == orig and (np.diff(dists) >= 0).all()
+        assert items[:k].tolist() == ids.tolist() and dists[:k].tolist() == dd.tolist()
