@@ -82,6 +82,28 @@ int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist,
                         int32_t m, int32_t ks, const int32_t* centroid_rows,
                         const int32_t* codeword_rows, void* stream, v3db_snapshot_t* out);
 
+/* Shaping rules for v3db_build_snapshot_ex (B2). */
+#define V3DB_SHAPE_GREEDY 0    /* BASELINE.json: nearest list, overflow to the next-nearest with room  */
+#define V3DB_SHAPE_REBALANCE 1 /* the paper's Alg. 1 on the nearest-centroid lists  */
+
+/*
+ * v3db_build_snapshot_ex -- v3db_build_snapshot with an explicit shaping rule:
+ *   V3DB_SHAPE_GREEDY     B2 as above (what v3db_build_snapshot does);
+ *   V3DB_SHAPE_REBALANCE  capacity-constrained cluster rebalancing, Alg. 1 of PAPER.md:296-325:
+ *                         start from every vector's nearest list (lowest index on ties); while a
+ *                         list holds more than list_cap vectors: for every vector v of an overfull
+ *                         list i take t* = its nearest list with room (lowest index on ties) and
+ *                         Delta = dist(v, mu_t*) - dist(v, mu_i); sort these moves by Delta (stable
+ *                         over (i, v) ascending); apply each in order if i is still overfull and t*
+ *                         still has room.  B3-B6 are unchanged.
+ *   stats    HOST int64 [2] or NULL <- {vectors moved from their nearest list, rounds of the loop}.
+ * Errors as v3db_build_snapshot, plus EINVAL for an unknown rule.
+ */
+int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap,
+                           int32_t m, int32_t ks, const int32_t* centroid_rows,
+                           const int32_t* codeword_rows, int32_t rule, int64_t* stats, void* stream,
+                           v3db_snapshot_t* out);
+
 /*
  * v3db_query_batch -- Steps 1-5 of PAPER.md:351-428 for nq queries, all on the GPU.
  *   Step 1 d_i = dist(q, mu_i) for every list

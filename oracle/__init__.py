@@ -9,6 +9,7 @@ legs may import it.  It shares no code with the CUDA path
 from .v3db_oracle import (  # noqa: F401
     D_MAX,
     Snapshot,
+    assign_rebalance,
     build_snapshot,
     dist,
     query,

@@ -127,6 +127,48 @@ def assign_greedy(db: np.ndarray, mu: np.ndarray, L: int, chunk: int = 4096) -> 
     return list_of
 
 
+def nearest_lists(db: np.ndarray, mu: np.ndarray, chunk: int = 4096) -> np.ndarray:
+    """argmin_i (dist(db[t], mu_i), i) for every t: the initial assignment (R2)."""
+    out = np.empty(db.shape[0], dtype=np.int64)
+    for lo in range(0, db.shape[0], chunk):
+        out[lo:lo + chunk] = np.argmin(_rank_keys(db[lo:lo + chunk], mu), axis=1)
+    return out
+
+
+def assign_rebalance(db: np.ndarray, mu: np.ndarray, L: int, return_rounds: bool = False):
+    """Alg. 1 ("Capacity-constrained cluster rebalancing"), literally, on the
+    nearest-centroid assignment.  Readings (R17): t* ties -> lowest list index; "sort M
+    by increasing Delta" is a stable sort of M built in (cluster i ascending, v ascending) order, so
+    ties keep that order.  Returns list_of (and the number of rounds)."""
+    N = db.shape[0]
+    nlist = mu.shape[0]
+    assert N <= nlist * L, "infeasible: N > nlist * L"
+    list_of = nearest_lists(db, mu)
+    counts = np.bincount(list_of, minlength=nlist)
+    rounds = 0
+    while (counts > L).any():                                   # while exists i with n_i > n
+        rounds += 1
+        O = np.nonzero(counts > L)[0]                           # overfull clusters
+        F = np.nonzero(counts < L)[0]                           # free clusters
+        vs = np.concatenate([np.nonzero(list_of == i)[0] for i in O])   # (i ascending, v ascending)
+        src = list_of[vs]
+        key_f = _rank_keys(db[vs], mu[F])                       # dist(v, mu_t) - ||v||^2, t in F
+        tpos = np.argmin(key_f, axis=1)                         # lowest t on ties (F ascending)
+        tstar = F[tpos]
+        e_t = np.rint(key_f[np.arange(len(vs)), tpos]).astype(np.int64)
+        mun = (mu.astype(np.int64) ** 2).sum(1)
+        e_i = mun[src] - 2 * (db[vs].astype(np.int64) * mu[src].astype(np.int64)).sum(1)
+        delta = e_t - e_i                                        # Delta(v, i) (the ||v||^2 terms cancel)
+        order = np.argsort(delta, kind="stable")                 # sort M by increasing Delta
+        for a in order.tolist():                                 # apply the guarded moves in order
+            v, i, t = int(vs[a]), int(src[a]), int(tstar[a])
+            if counts[i] > L and counts[t] < L and list_of[v] == i:
+                list_of[v] = t
+                counts[i] -= 1
+                counts[t] += 1
+    return (list_of.astype(np.int32), rounds) if return_rounds else list_of.astype(np.int32)
+
+
 def encode(residuals: np.ndarray, codebooks: np.ndarray, chunk: int = 65536) -> np.ndarray:
     """B5: code_t[m] = argmin_c sum_u (r_t[m d + u] - C_{m,c,u})^2, lowest c on ties (R6).
 
@@ -156,8 +198,11 @@ def encode(residuals: np.ndarray, codebooks: np.ndarray, chunk: int = 65536) -> 
     return codes
 
 
-def build_snapshot(db, nlist: int, L: int, M: int, Ks: int, centroid_rows, codeword_rows) -> Snapshot:
-    """Index shaping B1-B6."""
+def build_snapshot(db, nlist: int, L: int, M: int, Ks: int, centroid_rows, codeword_rows,
+                   rule: str = "greedy") -> Snapshot:
+    """Index shaping B1-B6.  `rule` selects
+    B2: "greedy" (BASELINE.json's streaming overflow rule, R1) or "rebalance" (the paper's Alg. 1,
+    PAPER.md:296-325, on the nearest-centroid assignment)."""
     db = np.ascontiguousarray(db, dtype=np.int8)
     N, D = db.shape
     centroid_rows = np.asarray(centroid_rows, dtype=np.int64)
@@ -179,7 +224,12 @@ def build_snapshot(db, nlist: int, L: int, M: int, Ks: int, centroid_rows, codew
     mu = db[centroid_rows].copy()
 
     # B2: nearest list, lowest index on ties, overflow to the next-nearest list with room (R1, R2)
-    list_of = assign_greedy(db, mu, L)
+    if rule == "greedy":
+        list_of = assign_greedy(db, mu, L)
+    elif rule == "rebalance":
+        list_of = assign_rebalance(db, mu, L)
+    else:
+        raise ValueError(f"unknown shaping rule {rule!r}")
 
     # B3: residual r_t = db[t] - mu_{list_of[t]} as int16 in [-255, 255], not clamped (R4, R5)
     resid = db.astype(np.int16) - mu[list_of].astype(np.int16)

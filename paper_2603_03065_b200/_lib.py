@@ -17,6 +17,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "v3db.h")
 V3DB_OK, V3DB_EINVAL, V3DB_EINFEASIBLE, V3DB_ENOMEM, V3DB_ECUDA = range(5)
 STATUS_NAMES = {0: "V3DB_OK", 1: "V3DB_EINVAL", 2: "V3DB_EINFEASIBLE", 3: "V3DB_ENOMEM", 4: "V3DB_ECUDA"}
 SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED = 0, 1, 2
+SHAPE_GREEDY, SHAPE_REBALANCE = 0, 1
 FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_IDS, FIELD_CODES, FIELD_COUNTS, FIELD_LIST_OF = range(6)
 
 _c_i8p = ctypes.c_void_p
@@ -26,6 +27,9 @@ _SIGS = {
     "v3db_build_snapshot": (ctypes.c_int, [_c_i8p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                            ctypes.c_int32, ctypes.c_int32, _c_i32p, _c_i32p, ctypes.c_void_p,
                                            ctypes.POINTER(ctypes.c_void_p)]),
+    "v3db_build_snapshot_ex": (ctypes.c_int, [_c_i8p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_int32, ctypes.c_int32, _c_i32p, _c_i32p, ctypes.c_int32,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "v3db_query_batch": (ctypes.c_int, [ctypes.c_void_p, _c_i8p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                         _c_i32p, _c_i32p, _c_i32p, _c_i32p, _c_i32p, ctypes.c_void_p]),
     "v3db_query_batch_ex": (ctypes.c_int, [ctypes.c_void_p, _c_i8p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,

@@ -164,7 +164,52 @@ __global__ void transpose_cb_kernel(const int8_t* __restrict__ cb, int M, int Ks
   }
 }
 
+__global__ void pair_dist_kernel(const int8_t* __restrict__ X, int64_t n, int dim, const int8_t* __restrict__ mu,
+                                 const int32_t* __restrict__ lists, int32_t* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  (void)warp;
+  if (r >= n) return;
+  const int8_t* x = X + r * dim;
+  const int8_t* m = mu + static_cast<int64_t>(lists[r]) * dim;
+  int acc = 0;
+  for (int u = lane; u < dim; u += 32) {
+    const int df = static_cast<int>(x[u]) - static_cast<int>(m[u]);
+    acc += df * df;
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  if (lane == 0) out[r] = acc;
+}
+
+__global__ void delta_keys_kernel(const int32_t* __restrict__ e_t, const int32_t* __restrict__ e_i, int64_t n,
+                                  int64_t P, uint64_t* __restrict__ keys) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < P;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t key = ~0ull;
+    if (r < n) {
+      const uint32_t d = static_cast<uint32_t>(e_t[r] - e_i[r]) ^ 0x80000000u;  // signed -> unsigned order
+      key = (static_cast<uint64_t>(d) << 32) | static_cast<uint32_t>(r);
+    }
+    keys[r] = key;
+  }
+}
+
 }  // namespace
+
+cudaError_t pair_dist(const int8_t* X, int64_t n, int dim, const int8_t* mu, const int32_t* lists, int32_t* out,
+                      cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  pair_dist_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, st>>>(X, n, dim, mu, lists, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t delta_keys(const int32_t* e_t, const int32_t* e_i, int64_t n, int64_t P, uint64_t* keys, cudaStream_t st) {
+  const int blocks = static_cast<int>((P + 255) / 256 < 16384 ? (P + 255) / 256 : 16384);
+  delta_keys_kernel<<<blocks, 256, 0, st>>>(e_t, e_i, n, P, keys);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t rotate_codes(const uint8_t* codes, const int32_t* pterm, int nlist, int L, int M, int mode, int G,
                          uint8_t* codes_rot, int32_t* pterm_rot, cudaStream_t st) {

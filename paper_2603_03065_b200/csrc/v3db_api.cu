@@ -122,6 +122,99 @@ void keep_pool_memory(int dev) {
   }
 }
 
+// Alg. 1 (capacity-constrained rebalancing) on the nearest-centroid assignment;
+// readings R17: t* ties -> lowest list, M sorted stably by Delta over (cluster, vector)
+// construction order.  GPU: nearest lists, t* over the free lists (the coarse top-1 kernel against
+// the gathered free centroids), Delta, the sort; host: the guarded sequential apply.
+int place_rebalance(const int8_t* db, int64_t n, int dim, int nlist, int L, const int8_t* mu, const int32_t* cnorm,
+                    cudaStream_t st, std::vector<int32_t>& list_of, std::vector<int32_t>& counts, int64_t* moved,
+                    int64_t* rounds) {
+  const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 20);
+  {
+    DevBuf<int32_t> d_idx, d_dist;
+    V3DB_CUDA(d_idx.alloc(chunk));
+    V3DB_CUDA(d_dist.alloc(chunk));
+    for (int64_t lo = 0; lo < n; lo += chunk) {
+      const int64_t rows = std::min(chunk, n - lo);
+      V3DB_CUDA(v3db::coarse_topk(db + lo * dim, rows, dim, mu, cnorm, nlist, 1, d_idx.p, d_dist.p, st));
+      V3DB_CUDA(cudaMemcpyAsync(list_of.data() + lo, d_idx.p, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost, st));
+    }
+    V3DB_CUDA(cudaStreamSynchronize(st));
+  }
+  const std::vector<int32_t> init = list_of;
+  std::fill(counts.begin(), counts.end(), 0);
+  for (int64_t t = 0; t < n; ++t) ++counts[list_of[t]];
+  *rounds = 0;
+  for (;;) {
+    std::vector<int32_t> F;
+    std::vector<char> over(nlist, 0);
+    bool any = false;
+    for (int i = 0; i < nlist; ++i) {
+      if (counts[i] > L) over[i] = 1, any = true;
+      if (counts[i] < L) F.push_back(i);
+    }
+    if (!any) break;
+    if (F.empty()) return fail(V3DB_EINFEASIBLE, "no free list (internal)");
+    ++*rounds;
+    // M in (cluster ascending, vector ascending) order: counting sort of the overfull members
+    std::vector<int64_t> start(nlist + 1, 0);
+    for (int64_t t = 0; t < n; ++t)
+      if (over[list_of[t]]) ++start[list_of[t] + 1];
+    for (int i = 0; i < nlist; ++i) start[i + 1] += start[i];
+    const int64_t mm = start[nlist];
+    std::vector<int32_t> vs(mm), src(mm);
+    for (int64_t t = 0; t < n; ++t) {
+      const int32_t i = list_of[t];
+      if (over[i]) {
+        vs[start[i]] = static_cast<int32_t>(t);
+        src[start[i]++] = i;
+      }
+    }
+    int64_t P = 1;
+    while (P < mm) P <<= 1;
+    DevBuf<int32_t> d_F, d_cnF, d_vs, d_src, d_tpos, d_et, d_ei;
+    DevBuf<int8_t> d_muF, d_X;
+    DevBuf<uint64_t> d_keys;
+    const int nf = static_cast<int>(F.size());
+    V3DB_CUDA(d_F.alloc(nf));
+    V3DB_CUDA(d_cnF.alloc(nf));
+    V3DB_CUDA(d_muF.alloc(static_cast<size_t>(nf) * dim));
+    V3DB_CUDA(d_vs.alloc(mm));
+    V3DB_CUDA(d_src.alloc(mm));
+    V3DB_CUDA(d_tpos.alloc(mm));
+    V3DB_CUDA(d_et.alloc(mm));
+    V3DB_CUDA(d_ei.alloc(mm));
+    V3DB_CUDA(d_X.alloc(static_cast<size_t>(mm) * dim));
+    V3DB_CUDA(d_keys.alloc(P));
+    V3DB_CUDA(cudaMemcpyAsync(d_F.p, F.data(), sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+    V3DB_CUDA(cudaMemcpyAsync(d_vs.p, vs.data(), sizeof(int32_t) * mm, cudaMemcpyHostToDevice, st));
+    V3DB_CUDA(cudaMemcpyAsync(d_src.p, src.data(), sizeof(int32_t) * mm, cudaMemcpyHostToDevice, st));
+    V3DB_CUDA(v3db::gather_rows(mu, dim, d_F.p, nf, d_muF.p, d_cnF.p, st));       // free centroids
+    V3DB_CUDA(v3db::gather_rows(db, dim, d_vs.p, static_cast<int>(mm), d_X.p, nullptr, st));  // candidate vectors
+    V3DB_CUDA(v3db::pair_dist(d_X.p, mm, dim, mu, d_src.p, d_ei.p, st));           // ||v - mu_i||^2
+    V3DB_CUDA(v3db::coarse_topk(d_X.p, mm, dim, d_muF.p, d_cnF.p, nf, 1, d_tpos.p, d_et.p, st));  // t*, ||v - mu_t*||^2
+    V3DB_CUDA(v3db::delta_keys(d_et.p, d_ei.p, mm, P, d_keys.p, st));
+    V3DB_CUDA(v3db::segmented_sort(d_keys.p, 1, static_cast<int>(P), st));       // sort M by (Delta, position)
+    std::vector<uint64_t> keys(mm);
+    std::vector<int32_t> tpos(mm);
+    V3DB_CUDA(cudaMemcpyAsync(keys.data(), d_keys.p, sizeof(uint64_t) * mm, cudaMemcpyDeviceToHost, st));
+    V3DB_CUDA(cudaMemcpyAsync(tpos.data(), d_tpos.p, sizeof(int32_t) * mm, cudaMemcpyDeviceToHost, st));
+    V3DB_CUDA(cudaStreamSynchronize(st));
+    for (int64_t a = 0; a < mm; ++a) {  // the guarded moves, in order
+      const int64_t r = static_cast<int64_t>(keys[a] & 0xffffffffu);
+      const int32_t v = vs[r], i = src[r], t = F[tpos[r]];
+      if (counts[i] > L && counts[t] < L && list_of[v] == i) {
+        list_of[v] = t;
+        --counts[i];
+        ++counts[t];
+      }
+    }
+  }
+  *moved = 0;
+  for (int64_t t = 0; t < n; ++t) *moved += list_of[t] != init[t];
+  return V3DB_OK;
+}
+
 extern "C" {
 
 int v3db_profile_enable(int32_t on) {
@@ -158,7 +251,15 @@ void v3db_free(v3db_snapshot_t s) { free_snapshot(s); }
 int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
                         int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, void* stream,
                         v3db_snapshot_t* out) {
+  return v3db_build_snapshot_ex(db, n, dim, nlist, list_cap, m, ks, centroid_rows, codeword_rows, V3DB_SHAPE_GREEDY,
+                                nullptr, stream, out);
+}
+
+int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
+                           int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, int32_t rule,
+                           int64_t* stats, void* stream, v3db_snapshot_t* out) {
   g_err.clear();
+  if (rule != V3DB_SHAPE_GREEDY && rule != V3DB_SHAPE_REBALANCE) return fail(V3DB_EINVAL, "unknown shaping rule");
   if (!db || !centroid_rows || !codeword_rows || !out) return fail(V3DB_EINVAL, "NULL required pointer");
   if (dim < 1 || dim > V3DB_MAX_DIM) return fail(V3DB_EINVAL, "dim out of range [1, V3DB_MAX_DIM]");
   if (m < 1 || dim % m) return fail(V3DB_EINVAL, "dim must be a positive multiple of m (D = Md, PAPER.md:331)");
@@ -220,61 +321,77 @@ int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist,
   V3DB_CUDA(cudaMemcpyAsync(d_rows.p, centroid_rows, sizeof(int32_t) * nlist, cudaMemcpyHostToDevice, st));
   V3DB_CUDA(v3db::gather_rows(db, dim, d_rows.p, nlist, s->centroids, s->cnorm, st));
 
-  // B2: GPU ranks each vector's R nearest lists by (e, i); host places in ascending t.
-  const int R = std::min(nlist, 64);
-  const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 18);
-  DevBuf<int32_t> d_rank, d_rdist;
-  HostPinned<int32_t> h_rank;
-  V3DB_CUDA(d_rank.alloc(static_cast<size_t>(chunk) * R));
-  V3DB_CUDA(d_rdist.alloc(static_cast<size_t>(chunk) * R));
-  V3DB_CUDA(h_rank.alloc(static_cast<size_t>(chunk) * R));
   std::vector<int32_t> list_of(n), flat_pos(n), counts(nlist, 0);
-  std::vector<int8_t> mu_host;
-  std::vector<int8_t> row(dim);
-  int64_t fallbacks = 0;
-  for (int64_t lo = 0; lo < n; lo += chunk) {
-    const int64_t rows = std::min(chunk, n - lo);
-    V3DB_CUDA(v3db::coarse_topk(db + lo * dim, rows, dim, s->centroids, s->cnorm, nlist, R, d_rank.p, d_rdist.p, st));
-    V3DB_CUDA(cudaMemcpyAsync(h_rank.p, d_rank.p, sizeof(int32_t) * rows * R, cudaMemcpyDeviceToHost, st));
-    V3DB_CUDA(cudaStreamSynchronize(st));
-    for (int64_t r = 0; r < rows; ++r) {
-      const int64_t t = lo + r;
-      int chosen = -1;
-      const int32_t* rk = h_rank.p + r * R;
-      for (int a = 0; a < R; ++a) {
-        if (counts[rk[a]] < L) {
-          chosen = rk[a];
-          break;
-        }
-      }
-      if (chosen < 0) {  // all R nearest lists are full: exact full ranking on the host
-        ++fallbacks;
-        if (mu_host.empty()) {
-          mu_host.resize(static_cast<size_t>(nlist) * dim);
-          V3DB_CUDA(cudaMemcpy(mu_host.data(), s->centroids, mu_host.size(), cudaMemcpyDeviceToHost));
-        }
-        V3DB_CUDA(cudaMemcpy(row.data(), db + t * dim, dim, cudaMemcpyDeviceToHost));
-        int64_t best = INT64_MAX;
-        for (int i = 0; i < nlist; ++i) {
-          if (counts[i] >= L) continue;
-          int64_t e = 0;
-          for (int u = 0; u < dim; ++u) {
-            const int64_t df = int64_t(row[u]) - int64_t(mu_host[static_cast<size_t>(i) * dim + u]);
-            e += df * df;
-          }
-          if (e < best) {  // strict: lowest index on ties
-            best = e;
-            chosen = i;
+  int64_t moved = 0, rounds = 0;
+  if (rule == V3DB_SHAPE_GREEDY) {
+    // B2: GPU ranks each vector's R nearest lists by (e, i); host places in ascending t.
+    const int R = std::min(nlist, 64);
+    const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 18);
+    DevBuf<int32_t> d_rank, d_rdist;
+    HostPinned<int32_t> h_rank;
+    V3DB_CUDA(d_rank.alloc(static_cast<size_t>(chunk) * R));
+    V3DB_CUDA(d_rdist.alloc(static_cast<size_t>(chunk) * R));
+    V3DB_CUDA(h_rank.alloc(static_cast<size_t>(chunk) * R));
+    std::vector<int8_t> mu_host;
+    std::vector<int8_t> row(dim);
+    int64_t fallbacks = 0;
+    for (int64_t lo = 0; lo < n; lo += chunk) {
+      const int64_t rows = std::min(chunk, n - lo);
+      V3DB_CUDA(v3db::coarse_topk(db + lo * dim, rows, dim, s->centroids, s->cnorm, nlist, R, d_rank.p, d_rdist.p, st));
+      V3DB_CUDA(cudaMemcpyAsync(h_rank.p, d_rank.p, sizeof(int32_t) * rows * R, cudaMemcpyDeviceToHost, st));
+      V3DB_CUDA(cudaStreamSynchronize(st));
+      for (int64_t r = 0; r < rows; ++r) {
+        const int64_t t = lo + r;
+        int chosen = -1;
+        const int32_t* rk = h_rank.p + r * R;
+        for (int a = 0; a < R; ++a) {
+          if (counts[rk[a]] < L) {
+            chosen = rk[a];
+            break;
           }
         }
-        if (chosen < 0) return fail(V3DB_EINFEASIBLE, "no list with room (internal)");
+        if (chosen < 0) {  // all R nearest lists are full: exact full ranking on the host
+          ++fallbacks;
+          if (mu_host.empty()) {
+            mu_host.resize(static_cast<size_t>(nlist) * dim);
+            V3DB_CUDA(cudaMemcpy(mu_host.data(), s->centroids, mu_host.size(), cudaMemcpyDeviceToHost));
+          }
+          V3DB_CUDA(cudaMemcpy(row.data(), db + t * dim, dim, cudaMemcpyDeviceToHost));
+          int64_t best = INT64_MAX;
+          for (int i = 0; i < nlist; ++i) {
+            if (counts[i] >= L) continue;
+            int64_t e = 0;
+            for (int u = 0; u < dim; ++u) {
+              const int64_t df = int64_t(row[u]) - int64_t(mu_host[static_cast<size_t>(i) * dim + u]);
+              e += df * df;
+            }
+            if (e < best) {  // strict: lowest index on ties
+              best = e;
+              chosen = i;
+            }
+          }
+          if (chosen < 0) return fail(V3DB_EINFEASIBLE, "no list with room (internal)");
+        }
+        list_of[t] = chosen;
+        flat_pos[t] = chosen * L + counts[chosen];  // B6: members in ascending t
+        ++counts[chosen];
       }
-      list_of[t] = chosen;
-      flat_pos[t] = chosen * L + counts[chosen];  // B6: members in ascending t
-      ++counts[chosen];
+    }
+    (void)fallbacks;
+
+  } else {
+    int rc = place_rebalance(db, n, dim, nlist, L, s->centroids, s->cnorm, st, list_of, counts, &moved, &rounds);
+    if (rc != V3DB_OK) return rc;
+    std::fill(counts.begin(), counts.end(), 0);
+    for (int64_t t = 0; t < n; ++t) {  // B6: members in ascending t
+      const int32_t i = list_of[t];
+      flat_pos[t] = i * L + counts[i]++;
     }
   }
-  (void)fallbacks;
+  if (stats) {
+    stats[0] = moved;
+    stats[1] = rounds;
+  }
 
   // B3-B6 on the GPU.
   DevBuf<int32_t> d_pos, d_cwrows;

@@ -127,6 +127,15 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
                          const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
                          int32_t* trace_cand, cudaStream_t st);
 
+// Ascending sort of nseg segments of P (a power of two) 64-bit keys (witness.cu).
+cudaError_t segmented_sort(uint64_t* keys, int64_t nseg, int P, cudaStream_t st);
+
+// Alg. 1 support (build_kernels.cu): dist(X[r], mu[lists[r]]) for every row r.
+cudaError_t pair_dist(const int8_t* X, int64_t n, int dim, const int8_t* mu, const int32_t* lists, int32_t* out,
+                      cudaStream_t st);
+// keys[r] = (uint32(delta[r] + 2^31) << 32) | r, delta = e_t - e_i; P - n padding keys = ~0.
+cudaError_t delta_keys(const int32_t* e_t, const int32_t* e_i, int64_t n, int64_t P, uint64_t* keys, cudaStream_t st);
+
 // Prover witness of a batch of queries (witness.cu; §4.7).  Outputs may be null.
 cudaError_t witness_batch(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int32_t* list_order,
                           int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items, int32_t* cand_dist,

@@ -59,17 +59,6 @@ __global__ void bitonic_step_kernel(uint64_t* __restrict__ keys, int64_t pairs, 
   }
 }
 
-cudaError_t segmented_sort(uint64_t* keys, int64_t nseg, int P, cudaStream_t st) {
-  const int64_t pairs = nseg * (P / 2);
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((pairs + 255) / 256, 148 * 16));
-  for (int size = 2; size <= P; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      bitonic_step_kernel<<<grid, 256, 0, st>>>(keys, pairs, P, size, stride);
-      note_launch();
-    }
-  return cudaGetLastError();
-}
-
 // Per (query, probe rank): the literal Step-3 table LUT_{i,m,c} = dist(C_{m,c}, (q - mu_i)^{(m)})
 // in shared memory, then for every slot j the selected entries l^{(m)}_{i,j} (Step 4 witness) and
 // the Step-5 key of the masked candidate distance D_{i,j}.
@@ -144,6 +133,18 @@ int pow2_at_least(int64_t n) {
 }
 
 }  // namespace
+
+// Ascending sort of every P-key segment (P a power of two): bitonic network, one launch per step.
+cudaError_t segmented_sort(uint64_t* keys, int64_t nseg, int P, cudaStream_t st) {
+  const int64_t pairs = nseg * (P / 2);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((pairs + 255) / 256, 148 * 16));
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      bitonic_step_kernel<<<grid, 256, 0, st>>>(keys, pairs, P, size, stride);
+      note_launch();
+    }
+  return cudaGetLastError();
+}
 
 cudaError_t witness_batch(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int32_t* list_order,
                           int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items, int32_t* cand_dist,

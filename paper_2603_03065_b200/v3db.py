@@ -16,7 +16,8 @@ import torch
 
 from . import _lib
 from ._lib import (FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_CODES, FIELD_COUNTS, FIELD_IDS,  # noqa: F401
-                   FIELD_LIST_OF, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, V3DBError)
+                   FIELD_LIST_OF, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, SHAPE_GREEDY, SHAPE_REBALANCE,
+                   V3DBError)
 
 
 def _stream_ptr(stream) -> ctypes.c_void_p:
@@ -67,8 +68,10 @@ class Snapshot:
 
 
 def build_snapshot(db: torch.Tensor, nlist: int, list_cap: int, m: int, ks: int, centroid_rows, codeword_rows,
-                   stream=None) -> Snapshot:
-    """v3db_build_snapshot: db is a CUDA int8 [n][dim] tensor; the row samples are host arrays."""
+                   stream=None, rule: int = 0, stats: dict | None = None) -> Snapshot:
+    """v3db_build_snapshot(_ex): db is a CUDA int8 [n][dim] tensor; the row samples are host arrays.
+    rule = SHAPE_GREEDY (BASELINE.json) or SHAPE_REBALANCE (the paper's Alg. 1); `stats`, if given,
+    receives {"moved", "rounds"}."""
     lib = _lib.load()
     if db.dtype != torch.int8 or db.device.type != "cuda" or db.dim() != 2 or not db.is_contiguous():
         raise ValueError("db must be a contiguous CUDA int8 [n][dim] tensor")
@@ -77,9 +80,13 @@ def build_snapshot(db: torch.Tensor, nlist: int, list_cap: int, m: int, ks: int,
     if cent.size != nlist or code.size != m * ks:
         raise ValueError("centroid_rows must have nlist entries and codeword_rows m*ks entries")
     h = ctypes.c_void_p()
-    _lib.check(lib.v3db_build_snapshot(_ptr(db), db.shape[0], db.shape[1], nlist, list_cap, m, ks,
-                                       cent.ctypes.data_as(ctypes.c_void_p), code.ctypes.data_as(ctypes.c_void_p),
-                                       _stream_ptr(stream), ctypes.byref(h)))
+    st = (ctypes.c_int64 * 2)()
+    _lib.check(lib.v3db_build_snapshot_ex(_ptr(db), db.shape[0], db.shape[1], nlist, list_cap, m, ks,
+                                          cent.ctypes.data_as(ctypes.c_void_p), code.ctypes.data_as(ctypes.c_void_p),
+                                          rule, ctypes.cast(st, ctypes.c_void_p), _stream_ptr(stream),
+                                          ctypes.byref(h)))
+    if stats is not None:
+        stats.update(moved=int(st[0]), rounds=int(st[1]))
     return Snapshot(h)
 
 

@@ -304,3 +304,41 @@ def test_witness_batch(v3db, name, nq):
     assert np.array_equal(got["list_order"][:, :cfg.nprobe], out["trace_lists"].cpu().numpy())
     assert np.array_equal(got["cand_items"][:, :cfg.k], out["out_ids"].cpu().numpy())
     s.free()
+
+
+@pytest.mark.parametrize("db,rows,L,expect", [
+    ([3, 2, 1, 0, 10, 11, 20], [3, 4, 6], 3, [1, 0, 0, 0, 1, 1, 2]),
+    ([0, 1, 2, 3, 4, 10, 11, 30], [0, 5, 7], 3, [0, 0, 0, 2, 1, 1, 1, 2]),
+])
+def test_rebalance_hand_examples_gpu(v3db, db, rows, L, expect):
+    """NEXT-3: the paper's Alg. 1 on the hand-derived cases of tests/golden/rebalance_example.md."""
+    x = np.array(db, np.int8)[:, None]
+    stats = {}
+    s = v3db.build_snapshot(torch.from_numpy(x).cuda(), len(rows), L, 1, 2, rows, [[0, 1]], rule=v3db.SHAPE_REBALANCE,
+                            stats=stats)
+    assert v3db.snapshot_export(s, v3db.FIELD_LIST_OF).tolist() == expect
+    init = np.argmin((x.astype(np.int64) - x[rows].astype(np.int64).T) ** 2, axis=1)
+    assert stats["moved"] == int((np.array(expect) != init).sum())
+    s.free()
+
+
+@pytest.mark.parametrize("name", ["c0_tight", "c1", "e2_basic", "e2_large"])
+def test_rebalance_parity(v3db, name):
+    """NEXT-3: snapshot shaped by Alg. 1 on the GPU == oracle, bit for bit, and
+    the query path on it."""
+    cfg = get_config("c0").with_(L=520) if name == "c0_tight" else get_config(name)
+    inp = generate(cfg)
+    ref_s = oracle.build_snapshot(inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows,
+                                  rule="rebalance")
+    stats = {}
+    s = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows,
+                            inp.codeword_rows, rule=v3db.SHAPE_REBALANCE, stats=stats)
+    assert_snapshot_equal(v3db, s, ref_s)
+    init = oracle.v3db_oracle.nearest_lists(inp.db, ref_s.centroids)
+    assert stats["moved"] == int((ref_s.list_of != init).sum())
+    qs = inp.queries[:128]
+    want = oracle.query_batch(ref_s, qs, cfg.nprobe, cfg.k)
+    out = v3db.query_batch(s, torch.from_numpy(np.ascontiguousarray(qs)).cuda(), cfg.nprobe, cfg.k)
+    torch.cuda.synchronize()
+    assert_query_equal(out, want)
+    s.free()

@@ -320,3 +320,37 @@ def test_witness_consistent_with_pinned_steps():
         orig = sorted(zip(s.ids[probes].reshape(-1).tolist(), cand.reshape(-1).tolist()))
         assert sorted(zip(items.tolist(), dists.tolist())) == orig and (np.diff(dists) >= 0).all()
         assert items[:k].tolist() == ids.tolist() and dists[:k].tolist() == dd.tolist()
+
+
+# ---------------------------------------------------------------- Alg. 1 rebalancing (NEXT-3)
+
+@pytest.mark.parametrize("db,rows,L,expect,rounds", [
+    ([3, 2, 1, 0, 10, 11, 20], [3, 4, 6], 3, [1, 0, 0, 0, 1, 1, 2], 1),
+    ([0, 1, 2, 3, 4, 10, 11, 30], [0, 5, 7], 3, [0, 0, 0, 2, 1, 1, 1, 2], 2),
+])
+def test_rebalance_hand_examples(db, rows, L, expect, rounds):
+    """Alg. 1 on the two 1-D cases derived by hand in
+    tests/golden/rebalance_example.md."""
+    x = np.array(db, np.int8)[:, None]
+    got, r = vo.assign_rebalance(x, x[rows], L, return_rounds=True)
+    assert got.tolist() == expect and r == rounds
+
+
+def test_rebalance_invariants_and_no_op():
+    """Alg. 1 ensures |X_i| <= n, conserves the vectors, leaves an assignment with no
+    overfull list unchanged (the while loop does not run), and only moves vectors out of lists that
+    were overfull in the initial assignment."""
+    rng = np.random.default_rng(31)
+    for trial in range(20):
+        N, D, nlist = int(rng.integers(20, 200)), int(rng.integers(1, 5)), int(rng.integers(2, 9))
+        L = int(np.ceil(N / nlist)) + int(rng.integers(0, 3))
+        db = rng.integers(-6, 7, size=(N, D)).astype(np.int8)
+        mu = db[rng.choice(N, nlist, replace=False)]
+        init = vo.nearest_lists(db, mu)
+        got = vo.assign_rebalance(db, mu, L)
+        counts0 = np.bincount(init, minlength=nlist)
+        assert (np.bincount(got, minlength=nlist) <= L).all()
+        moved = got != init
+        assert (counts0[init[moved]] > L).all()
+        if (counts0 <= L).all():
+            assert not moved.any()
