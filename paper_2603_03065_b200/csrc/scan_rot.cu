@@ -296,7 +296,6 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t qi = a.order ? a.order[blockIdx.x] : blockIdx.x;
   const int L = a.L, nprobe = a.nprobe, NS = a.NS, SEG = a.SEG;
-  const uint32_t pbase = static_cast<uint32_t>(SEG) * 32u * M;  // P terms inside a stage
 
   for (int u = tid; u < a.dim; u += C::NTOT) qs[u] = a.queries[qi * a.dim + u];
   for (int r = tid; r < nprobe; r += C::NTOT) {
@@ -343,8 +342,8 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
         if (t >= NS) mbar_wait_sleep(empty + s, eph);  // consumers released the previous fill
         uint8_t* st = stages + static_cast<uint32_t>(s) * a.stage_bytes;
         const int g0 = t * SEG, g1 = min(TV, g0 + SEG);
-        tc::mbar_expect_tx(full + s, static_cast<uint32_t>(g1 - g0) * (32u * M + 128u));
-        // one codes copy and one P copy per piece (a run of valid chunks of one list)
+        tc::mbar_expect_tx(full + s, static_cast<uint32_t>(g1 - g0) * 32u * M);
+        // one codes copy per piece (a run of valid chunks of one list)
         for (int g = g0; g < g1;) {
           while (vcoff[rho + 1] <= g) ++rho;
           const int jc = g - vcoff[rho];
@@ -352,12 +351,13 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
           const int4 pr = probe[rho];
           const int64_t slot0 = static_cast<int64_t>(pr.x) * a.Lp + jc * 32;
           const uint32_t i = static_cast<uint32_t>(g - g0);
-          // per-chunk descriptors: (d_i, rho*L + 32*jc (trace / flat offset), valid slots, slots)
+          // per-chunk descriptors: (d_i, rho*L + 32*jc (trace / flat offset), valid slots | slots << 8,
+          // P-term offset list*Lp + 32*jc)
           for (int x = 0; x < m; ++x)
-            dsc[s * SEG + i + x] = make_int4(pr.y, rho * L + (jc + x) * 32, min(32, pr.z - (jc + x) * 32),
-                                             min(32, L - (jc + x) * 32));
+            dsc[s * SEG + i + x] = make_int4(pr.y, rho * L + (jc + x) * 32,
+                                             min(32, pr.z - (jc + x) * 32) | (min(32, L - (jc + x) * 32) << 8),
+                                             static_cast<int>(slot0) + x * 32);
           bulk_g2s(st + i * 32u * M, a.codes + slot0 * M, static_cast<uint32_t>(m) * 32u * M, full + s);
-          bulk_g2s(st + pbase + i * 128u, a.pterm + slot0, static_cast<uint32_t>(m) * 128u, full + s);
           g += m;
         }
         if (++s == NS) {
@@ -453,9 +453,9 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   // Candidate buffer: s_int[0] = entries (monotonic between compactions), s_int[1] = compaction
   // requested, s_int[2] = consumer warps done.  A warp whose append lifts the count above `hw`
   // (or above k before tau is set) requests a compaction; every consumer warp joins at its next
-  // stage end (warps drift by less than NS stages and append at most 2 chunks per stage, so at
-  // most 2 * SEG * 32 more entries arrive before all have joined -- the headroom above hw).
-  const int hw = a.cap - 2 * SEG * 32;
+  // stage end, so after the request each warp appends at most its share of one stage
+  // (ceil(SEG/W) chunks): W * ceil(SEG/W) * 32 entries of headroom above hw.
+  const int hw = a.cap - W * ((SEG + W - 1) / W) * 32;
   uint32_t tau = kTauInit;
   volatile int* vs = s_int;
   auto collective_compact = [&]() {  // all consumer threads
@@ -489,10 +489,10 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   };
   // masked D to the trace, candidate append (Step 5 buffer)
   auto emit = [&](const int4 dd, int32_t acc) {
-    const bool valid = lane < dd.z;  // lanes past the valid slots read stale stage bytes
+    const bool valid = lane < (dd.z & 0xff);  // lanes past the valid slots read stale stage bytes
     const int32_t D = valid ? acc : kDMax;
-    const int off = dd.y + lane;     // rho*L + j
-    if (trq && lane < dd.w) __stcs(trq + dd.y, D);
+    const int off = dd.y + lane;               // rho*L + j
+    if (trq && lane < (dd.z >> 8)) __stcs(trq + dd.y, D);
     const bool pass = valid && static_cast<uint32_t>(D) <= tau;
     const uint32_t bal = __ballot_sync(kFull, pass);
     if (bal) {
@@ -517,20 +517,23 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
     for (int i = warp; i < n; i += 2 * W) {
       const bool two = i + W < n;  // warp-uniform
       const int4 d0 = ds[i];
+      const int4 d1 = ds[two ? i + W : i];
+      // P terms straight from global memory (L2), issued first: used after the lookups
+      const int32_t p0 = __ldg(a.pterm + d0.w + lane);
+      const int32_t p1 = two ? __ldg(a.pterm + d1.w + lane) : 0;
       uint32_t w0[NW], w1[NW];
       load_w(st + static_cast<uint32_t>(i) * 32u * M, w0);
-      int32_t acc0 = d0.x + *reinterpret_cast<const int32_t*>(st + pbase + static_cast<uint32_t>(i) * 128u + 4 * lane);
+      int32_t acc0 = d0.x;
       if (two) {
-        const int4 d1 = ds[i + W];
         load_w(st + static_cast<uint32_t>(i + W) * 32u * M, w1);
-        int32_t acc1 = d1.x + *reinterpret_cast<const int32_t*>(st + pbase + static_cast<uint32_t>(i + W) * 128u + 4 * lane);
+        int32_t acc1 = d1.x;
         lut_sum<M, MODE, 0>(w0, lane4, acc0);
         lut_sum<M, MODE, 0>(w1, lane4, acc1);
-        emit(d0, acc0);
-        emit(d1, acc1);
+        emit(d0, acc0 + p0);
+        emit(d1, acc1 + p1);
       } else {
         lut_sum<M, MODE, 0>(w0, lane4, acc0);
-        emit(d0, acc0);
+        emit(d0, acc0 + p0);
       }
     }
     __syncwarp();
@@ -589,10 +592,10 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   constexpr int NT = C::NT;
   auto al = [](uint32_t x, uint32_t b) { return (x + b - 1) / b * b; };
   const uint32_t lut = MODE == kLutP64 ? static_cast<uint32_t>(a.Ks) * 256u : C::NG * kW32GroupBytes;
-  const uint32_t chunk = 32u * M + 128u;  // codes + P terms of one 32-slot chunk
+  const uint32_t chunk = 32u * M;  // codes of one 32-slot chunk (P terms are read from L2)
   // (SEG, NS, cap): the first candidate that fits the per-CTA budget; 2-3 stages in flight suffice.
-  static const int cand[][3] = {{16, 3, 2048}, {16, 3, 1024}, {16, 2, 2048}, {8, 4, 1024}, {16, 2, 1024},
-                                {8, 3, 1024}, {8, 2, 1024}};
+  static const int cand[][3] = {{16, 4, 1024}, {16, 3, 1024}, {16, 2, 1024}, {8, 4, 1024}, {8, 3, 1024},
+                                {8, 2, 1024}};
   int SEG = 8, NS = 2, cap = 1024;
   size_t smem = 0;
   const char* e_seg = getenv("V3DB_SEG");  // experiments: force (SEG, NS, cap)
@@ -600,8 +603,10 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   const char* e_cap = getenv("V3DB_CAP");
   for (const auto& c : cand) {
     const int seg = e_seg ? atoi(e_seg) : c[0], ns = e_ns ? atoi(e_ns) : c[1];
-    // headroom: 2 stages of appends above the high-water mark, which must be >= k
-    const int cp = e_cap ? atoi(e_cap) : (a.k + 2 * seg * 32 <= c[2] ? c[2] : 4096);
+    // headroom: one stage share of every consumer warp above the high-water mark, which must be >= k
+    const int head = (NT / 32) * ((seg + NT / 32 - 1) / (NT / 32)) * 32;
+    int cp = e_cap ? atoi(e_cap) : c[2];
+    while (cp < a.k + head) cp *= 2;
     const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) + 16u * ns * seg +
                         8u * cp + 256 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
     SEG = seg;

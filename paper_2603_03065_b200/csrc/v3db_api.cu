@@ -409,6 +409,7 @@ int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nli
   V3DB_CUDA(v3db::slot_terms(s->centroids, s->codebooks, s->codes, s->ids, nlist, L, dim, m, ks, s->pterm, st));
   // layouts of the rotated-LUT scan
   s->lut_mode = v3db::plan_lut(m, ks, d, &s->lut_g);
+  if (static_cast<int64_t>(nlist) * ((L + 31) & ~31) >= (int64_t(1) << 31)) s->lut_mode = 0;  // 32-bit slot offsets
   if (s->lut_mode != 0) {
     // padded list stride Lp; +256 B so rounded-up bulk copies of the last chunk stay in bounds
     const int64_t pslots = static_cast<int64_t>(nlist) * ((L + 31) & ~31);
