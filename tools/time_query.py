@@ -16,6 +16,7 @@ p.add_argument("--reps", type=int, default=5)
 p.add_argument("--algos", default="1,2")
 p.add_argument("--Q", type=int, default=0, help="use only the first Q queries")
 p.add_argument("--k", type=int, default=0, help="override k")
+p.add_argument("--nprobe", type=int, default=0, help="override nprobe")
 p.add_argument("--trace", default="on")
 p.add_argument("--envs", default="", help="comma-separated runs after the plain run, each VAR=VALUE[:VAR=VALUE]")
 args = p.parse_args()
@@ -28,6 +29,8 @@ if args.Q:
     cfg = cfg.with_(Q=args.Q)
 if args.k:
     cfg = cfg.with_(k=args.k)
+if args.nprobe:
+    cfg = cfg.with_(nprobe=args.nprobe)
 out = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=args.trace == "on", device="cuda")
 v3db.profile_enable(True)
 for env in [""] + [e for e in args.envs.split(",") if e]:
