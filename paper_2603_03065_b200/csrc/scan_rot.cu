@@ -94,16 +94,14 @@ __device__ __forceinline__ int32_t lds32(uint32_t addr) {
 }
 constexpr uint32_t kTauInit = 0x7ffffffeu;  // accept every valid D (< d_max)
 
-// VAR selects experimental CTA shapes (V3DB_SCAN_VAR, M = 32 W32 only): 1 = 12 consumer warps,
-// 2 = three CTAs per SM.
 template <int M, int MODE, int VAR = 0>
 struct Geo {
   static constexpr int NG = rot_ngroups(M);
   static constexpr int NW = M / 4;                                   // 32-bit code words per slot
   static constexpr int U = M % 16 == 0 ? 16 : M % 8 == 0 ? 8 : 4;    // bytes per lane per unit
-  static constexpr int NT = VAR == 1 ? 384 : (MODE == kLutW32 && NG * kW32GroupBytes > 96 * 1024) ? 512 : 256;  // consumers
+  static constexpr int NT = (MODE == kLutW32 && NG * kW32GroupBytes > 96 * 1024) ? 512 : 256;  // consumers
   static constexpr int NTOT = NT + 32;                              // + the producer warp
-  static constexpr int MINB = VAR == 2 ? 3 : NT == 512 ? 1 : 2;
+  static constexpr int MINB = NT == 512 ? 1 : 2;
 };
 
 struct RotArgs {
@@ -243,14 +241,16 @@ __device__ int compact(uint64_t* buf, int* hist, int* s_int, const int4* probe, 
     bar_c<NT>();
     kept = s_int[10];
   }
-  if (final || kept > limit) {  // exact (D, id) order: resolve, sort, keep the first min(kept, k)
+  if (final) {  // resolve: the caller orders the survivors by (D, id) (rank_scatter)
+    for (int e = tid; e < kept; e += NT) buf[e] = resolve_key(buf[e], probe, a);
+  } else if (kept > limit) {  // ties: exact (D, id) order, keep the first k
     for (int e = tid; e < kept; e += NT) buf[e] = resolve_key(buf[e], probe, a);
     int P = 1;
     while (P < kept) P <<= 1;
     for (int e = kept + tid; e < P; e += NT) buf[e] = ~0ull;
     bar_c<NT>();
     bitonic_sort<NT>(buf, P);
-    if (kept > a.k) kept = a.k;
+    kept = a.k;
   }
   bar_c<NT>();
   return kept;
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   }
 
   // Step 3 (factorised): A_q[m][c] = -2 <C_{m,c}, q^{(m)}>, written into the rotated tables.
-  // Four entries per thread per step with their codebook loads issued together (latency-bound
+  // Eight entries per thread per step with their codebook loads issued together (latency-bound
   // otherwise: one L2 round trip per entry).
   {
     int32_t* T = reinterpret_cast<int32_t*>(smem);
@@ -404,27 +404,30 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
     };
     const int* cbw = reinterpret_cast<const int*>(a.cbT);   // [Ks][M][dw] words
     const int* qw = reinterpret_cast<const int*>(qs);       // [M][dw] words
-    for (int e0 = tid; e0 < MK; e0 += 4 * NT) {
-      int acc[4] = {0, 0, 0, 0};
+    constexpr int UB = 8;
+    for (int e0 = tid; e0 < MK; e0 += UB * NT) {
+      int acc[UB];
+#pragma unroll
+      for (int x = 0; x < UB; ++x) acc[x] = 0;
       if (dw == 1) {
-        int cwv[4];
+        int cwv[UB];
 #pragma unroll
-        for (int x = 0; x < 4; ++x) cwv[x] = e0 + x * NT < MK ? __ldg(cbw + e0 + x * NT) : 0;
+        for (int x = 0; x < UB; ++x) cwv[x] = e0 + x * NT < MK ? __ldg(cbw + e0 + x * NT) : 0;
 #pragma unroll
-        for (int x = 0; x < 4; ++x) acc[x] = __dp4a(cwv[x], qw[(e0 + x * NT) % M], 0);
+        for (int x = 0; x < UB; ++x) acc[x] = __dp4a(cwv[x], qw[(e0 + x * NT) % M], 0);
       } else if (dw == 2) {
-        int2 cwv[4];
+        int2 cwv[UB];
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < UB; ++x)
           cwv[x] = e0 + x * NT < MK ? __ldg(reinterpret_cast<const int2*>(cbw) + e0 + x * NT) : make_int2(0, 0);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
+        for (int x = 0; x < UB; ++x) {
           const int m = (e0 + x * NT) % M;
           acc[x] = __dp4a(cwv[x].y, qw[2 * m + 1], __dp4a(cwv[x].x, qw[2 * m], 0));
         }
       } else {
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
+        for (int x = 0; x < UB; ++x) {
           const int e = e0 + x * NT;
           if (e < MK) {
             const int m = e % M;
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
         }
       }
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < UB; ++x)
         if (e0 + x * NT < MK) put(e0 + x * NT, -2 * acc[x]);
     }
   }
@@ -561,17 +564,21 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   const int n_base = s_int[0];
 
   // Final Step 5: the k smallest (D, item) keys, (d_max, -1) past the valid candidates (R11).
+  // The survivors (resolved, distinct keys) are placed by rank: one pass, one barrier.
   uint32_t t2 = tau;
   const int n = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, a.k, true, &t2);
-  for (int r = tid; r < a.k; r += NT) {
-    int32_t id = -1, dd = kDMax;
-    if (r < n) {
-      const uint64_t key = buf[r];
-      id = step5_id(key);
-      dd = static_cast<int32_t>(key >> 32);
+  for (int e = tid; e < n; e += NT) {
+    const uint64_t key = buf[e];
+    int rank = 0;
+    for (int f = 0; f < n; ++f) rank += buf[f] < key ? 1 : 0;  // broadcast reads
+    if (rank < a.k) {
+      a.out_ids[qi * a.k + rank] = step5_id(key);
+      a.out_dist[qi * a.k + rank] = static_cast<int32_t>(key >> 32);
     }
-    a.out_ids[qi * a.k + r] = id;
-    a.out_dist[qi * a.k + r] = dd;
+  }
+  for (int r = n + tid; r < a.k; r += NT) {
+    a.out_ids[qi * a.k + r] = -1;
+    a.out_dist[qi * a.k + r] = kDMax;
   }
 }
 
@@ -711,12 +718,7 @@ cudaError_t scan_dispatch(const v3db_snapshot* s, RotArgs& a, int64_t nq, cudaSt
     case 12: V3DB_ROT(12, kLutW32)
     case 16: V3DB_ROT(16, kLutW32)
     case 24: V3DB_ROT(24, kLutW32)
-    case 32: {
-      const char* var = getenv("V3DB_SCAN_VAR");
-      if (var && var[0] == '1') return launch<32, kLutW32, 1>(a, nq, budget<32, kLutW32, 1>(), st);
-      if (var && var[0] == '2') return launch<32, kLutW32, 2>(a, nq, budget<32, kLutW32, 2>(), st);
-      V3DB_ROT(32, kLutW32)
-    }
+    case 32: V3DB_ROT(32, kLutW32)
     case 48: V3DB_ROT(48, kLutW32)
     case 64: V3DB_ROT(64, kLutW32)
     case 96: V3DB_ROT(96, kLutW32)
