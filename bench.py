@@ -286,6 +286,19 @@ def main():
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     tot_ms = pdist.max_over_ranks(float(np.sum(step_ms)), world, dev)
+
+    # the same step with the witness trace off (qps with the trace on and off)
+    out_off = {key: v for key, v in out.items() if key != "trace_cand_dist"}
+    n_off = max(1, min(args.steps, 5))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_off)]
+    v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out_off, algo=args.algo)
+    for a_, b_ in ev:
+        flush.zero_()
+        a_.record(stream)
+        v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out_off, algo=args.algo)
+        b_.record(stream)
+    torch.cuda.synchronize()
+    off_ms = pdist.max_over_ranks(float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev])), world, dev)
     ms_per_step = tot_ms / args.steps
     qps = cfg.Q * world / (ms_per_step / 1e3)
     coarse_ms = float(np.mean([a for a, _ in kt]))
@@ -306,6 +319,8 @@ def main():
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MiB write); snapshot codes exceed L2",
                    "algo": args.algo, "snapshot_build_s": round(build_s, 3)},
+        "ms_per_step_median": float(np.median(step_ms)), "ms_per_step_best": float(np.min(step_ms)),
+        "value_trace_off": cfg.Q * world / (off_ms / 1e3),
         "scan_gbs": achieved,
         "scan_gbs_padded": ab["padded"] / (scan_ms / 1e3) / 1e9,
         "kernel_ms": {"coarse_steps12": coarse_ms, "scan_steps345": scan_ms},
