@@ -8,6 +8,8 @@ legs may import it.  It shares no code with the CUDA path
 """
 from .v3db_oracle import (  # noqa: F401
     D_MAX,
+    D_MAX_FX,
+    encode_fixed_point,
     Snapshot,
     assign_rebalance,
     build_snapshot,

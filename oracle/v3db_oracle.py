@@ -28,6 +28,19 @@ import numpy as np
 
 # R8: "a public constant d_max that exceeds any attainable d~".
 D_MAX = 2**31 - 1
+# The 16-bit fixed-point variant (NEXT-1) has int64 distances: d_max = 2^63 - 1.
+D_MAX_FX = 2**63 - 1
+FX_SCALE = 2**16 - 1
+
+
+def encode_fixed_point(x, v_max: float):
+    """each coordinate v becomes round((2^16 - 1) * v / v_max), v_max the largest
+    |coordinate| over all involved vectors.  Reading R18: the product and quotient in IEEE double
+    (in that order), round half away from zero.  Returns int32 in [-(2^16-1), 2^16-1]."""
+    y = np.asarray(x, dtype=np.float64) * float(FX_SCALE) / float(v_max)
+    r = np.where(y >= 0, np.floor(y + 0.5), -np.floor(-y + 0.5))
+    assert np.abs(r).max(initial=0) <= FX_SCALE
+    return r.astype(np.int32)
 
 
 def dist(x, y) -> int:
@@ -58,6 +71,12 @@ class Snapshot:
     def Ks(self): return self.codebooks.shape[1]
     @property
     def D(self): return self.centroids.shape[1]
+    @property
+    def fx(self):
+        """16-bit fixed-point variant (NEXT-1): int32 coordinates, int64 distances."""
+        return self.centroids.dtype == np.int32
+    @property
+    def d_max(self): return D_MAX_FX if self.fx else D_MAX
 
 
 # ----------------------------------------------------------------------------------------
@@ -73,7 +92,9 @@ def _rank_keys(x: np.ndarray, mu: np.ndarray) -> np.ndarray:
     gives key directly; it runs in float32 when every partial sum is an integer below 2^24
     (exact), else in float64 (exact below 2^53)."""
     mun = (mu.astype(np.int64) ** 2).sum(1)
-    bound = int(mun.max(initial=0)) + 2 * 128 * 128 * x.shape[1]
+    amax = int(max(np.abs(x).max(initial=0), np.abs(mu).max(initial=0), 1))
+    bound = int(mun.max(initial=0)) + 2 * amax * amax * x.shape[1] + 1
+    assert bound < 2**53
     ft = np.float32 if bound < 2**24 else np.float64
     xa = np.empty((x.shape[0], x.shape[1] + 1), ft)
     xa[:, :-1] = x
@@ -182,15 +203,19 @@ def encode(residuals: np.ndarray, codebooks: np.ndarray, chunk: int = 65536) -> 
 
     N, D = residuals.shape
     M, Ks, d = codebooks.shape
-    assert d * (127 * 127 + 2 * 255 * 127) < 2**24
+    rmax = int(max(np.abs(residuals).max(initial=0), 1))
+    cmax = int(max(np.abs(codebooks).max(initial=0), 1))
+    bound = d * (cmax * cmax + 2 * rmax * cmax)
+    assert bound < 2**53
+    ft = np.float32 if bound < 2**24 else np.float64       # exact either way
     codes = np.empty((N, M), dtype=np.uint8)
 
     def one(m):
-        C = codebooks[m].astype(np.float32)                # [Ks, d]
+        C = codebooks[m].astype(ft)                        # [Ks, d]
         cn = (C * C).sum(1)
         for lo in range(0, N, chunk):
             hi = min(N, lo + chunk)
-            key = cn[None, :] - np.float32(2) * (residuals[lo:hi, m * d:(m + 1) * d].astype(np.float32) @ C.T)
+            key = cn[None, :] - ft(2) * (residuals[lo:hi, m * d:(m + 1) * d].astype(ft) @ C.T)
             codes[lo:hi, m] = np.argmin(key, axis=1)       # lowest c on ties (R6)
 
     with ThreadPoolExecutor(max_workers=min(M, os.cpu_count() or 1)) as ex:
@@ -202,8 +227,11 @@ def build_snapshot(db, nlist: int, L: int, M: int, Ks: int, centroid_rows, codew
                    rule: str = "greedy") -> Snapshot:
     """Index shaping B1-B6.  `rule` selects
     B2: "greedy" (BASELINE.json's streaming overflow rule, R1) or "rebalance" (the paper's Alg. 1,
-    PAPER.md:296-325, on the nearest-centroid assignment)."""
-    db = np.ascontiguousarray(db, dtype=np.int8)
+    PAPER.md:296-325, on the nearest-centroid assignment).  An int8 db is BASELINE.json's int8
+    path; an int32 db is the 16-bit fixed-point variant (NEXT-1), whose
+    codewords are the residual sub-vectors themselves (R19: no saturation; int32)."""
+    fx = np.asarray(db).dtype == np.int32
+    db = np.ascontiguousarray(db, dtype=np.int32 if fx else np.int8)
     N, D = db.shape
     centroid_rows = np.asarray(centroid_rows, dtype=np.int64)
     codeword_rows = np.asarray(codeword_rows, dtype=np.int64).reshape(M, Ks)
@@ -231,13 +259,15 @@ def build_snapshot(db, nlist: int, L: int, M: int, Ks: int, centroid_rows, codew
     else:
         raise ValueError(f"unknown shaping rule {rule!r}")
 
-    # B3: residual r_t = db[t] - mu_{list_of[t]} as int16 in [-255, 255], not clamped (R4, R5)
-    resid = db.astype(np.int16) - mu[list_of].astype(np.int16)
+    # B3: residual r_t = db[t] - mu_{list_of[t]}, not clamped (R4, R5): int16 in [-255, 255] (int8
+    # path) or int64 in [-131070, 131070] (fixed point)
+    resid = db.astype(np.int64 if fx else np.int16) - mu[list_of].astype(np.int64 if fx else np.int16)
 
-    # B4: C_{m,c} = sat_[-127,127]( r_{codeword_rows[m][c]}^{(m)} )  (R5)
-    cb = np.empty((M, Ks, d), dtype=np.int8)
+    # B4: C_{m,c} = sat_[-127,127]( r_{codeword_rows[m][c]}^{(m)} )  (R5); fixed point: no saturation (R19)
+    cb = np.empty((M, Ks, d), dtype=np.int32 if fx else np.int8)
     for m in range(M):
-        cb[m] = np.clip(resid[codeword_rows[m], m * d:(m + 1) * d], -127, 127).astype(np.int8)
+        sub = resid[codeword_rows[m], m * d:(m + 1) * d]
+        cb[m] = sub.astype(np.int32) if fx else np.clip(sub, -127, 127).astype(np.int8)
 
     # B5: PQ codes of the residuals
     code = encode(resid, cb)
@@ -264,7 +294,7 @@ def step1_centroid_distances(q, s: Snapshot) -> np.ndarray:
     """Step 1: d_i := dist(q, mu_i) for i in [n_list]."""
     q = np.asarray(q, dtype=np.int64)
     d = ((q[None, :] - s.centroids.astype(np.int64)) ** 2).sum(axis=1)
-    assert d.max(initial=0) < 2**31
+    assert d.max(initial=0) < (2**47 if s.fx else 2**31)
     return d
 
 
@@ -301,8 +331,8 @@ def step4_candidate_distances(s: Snapshot, probes: np.ndarray, lut: np.ndarray) 
     for rho, i in enumerate(probes):
         f = (s.ids[i] != -1).astype(np.int64)              # validity flag f_{i,j}
         dtil = lut[rho][m_idx, s.codes[i].astype(np.int64)].sum(axis=1)
-        assert (dtil[f == 1] < D_MAX).all(), "d_max must exceed every valid d~ (PAPER.md:398-401)"
-        out[rho] = f * dtil + (1 - f) * D_MAX
+        assert (dtil[f == 1] < s.d_max).all(), "d_max must exceed every valid d~ (PAPER.md:398-401)"
+        out[rho] = np.where(f == 1, dtil, s.d_max)
     return out
 
 
@@ -327,18 +357,19 @@ def query(q, s: Snapshot, nprobe: int, k: int):
 
 
 def query_batch(s: Snapshot, queries, nprobe: int, k: int, rows=None) -> dict:
-    """Run `query` for every row (or the given subset `rows`) of `queries`; int32 outputs in
-    the C-ABI's layouts: out_ids/out_dist [Q][k], trace_lists/trace_list_dist [Q][nprobe],
-    trace_cand_dist [Q][nprobe][L]."""
-    queries = np.asarray(queries, dtype=np.int8)
+    """Run `query` for every row (or the given subset `rows`) of `queries`; outputs in the
+    C-ABI's layouts: out_ids [Q][k], out_dist [Q][k], trace_lists / trace_list_dist [Q][nprobe],
+    trace_cand_dist [Q][nprobe][L] -- int32, distances int64 in the fixed-point variant."""
+    queries = np.asarray(queries, dtype=np.int32 if s.fx else np.int8)
     rows = np.arange(queries.shape[0]) if rows is None else np.asarray(rows)
     nq = len(rows)
+    dt = np.int64 if s.fx else np.int32
     out = {
         "out_ids": np.empty((nq, k), np.int32),
-        "out_dist": np.empty((nq, k), np.int32),
+        "out_dist": np.empty((nq, k), dt),
         "trace_lists": np.empty((nq, nprobe), np.int32),
-        "trace_list_dist": np.empty((nq, nprobe), np.int32),
-        "trace_cand_dist": np.empty((nq, nprobe, s.L), np.int32),
+        "trace_list_dist": np.empty((nq, nprobe), dt),
+        "trace_cand_dist": np.empty((nq, nprobe, s.L), dt),
     }
     for a, r in enumerate(rows):
         ids, dd, p, dp, cand = query(queries[r], s, nprobe, k)

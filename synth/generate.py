@@ -57,6 +57,22 @@ def mixture(gen: str, D: int, cfg_id: int) -> Mixture:
     raise ValueError(f"unknown generator {gen!r}")
 
 
+def _float_rows(mix: Mixture, rng: np.random.Generator, n: int) -> np.ndarray:
+    """The real-valued vectors before BASELINE.json's int8 quantisation (used as they are by the
+    16-bit fixed-point variant, NEXT-1): c0 / sift mixtures clipped to their value range, deep /
+    text rows unit-normalised."""
+    comp = rng.integers(0, mix.centres.shape[0], size=n)
+    noise = rng.standard_normal((n, mix.D), dtype=np.float32)
+    x = mix.centres[comp].astype(np.float32) + np.float32(mix.sigma) * noise
+    if mix.gen == "c0":
+        return np.clip(x, -127, 127)
+    if mix.gen == "sift":
+        return np.clip(x, 0, 255) - np.float32(128)
+    if mix.scale is not None:
+        x *= mix.scale.astype(np.float32)
+    return x / np.linalg.norm(x, axis=1, keepdims=True)
+
+
 def _rows(mix: Mixture, rng: np.random.Generator, n: int) -> np.ndarray:
     comp = rng.integers(0, mix.centres.shape[0], size=n)
     noise = rng.standard_normal((n, mix.D), dtype=np.float32)
@@ -112,3 +128,33 @@ def rank_queries(cfg: Config, rank: int) -> np.ndarray:
     if rank == 0:
         return generate(cfg).queries
     return gen_vectors(cfg, STREAM_Q_RANK + rank, cfg.Q)
+
+
+def gen_float_vectors(cfg: Config, stream: int, n: int) -> np.ndarray:
+    """n float32 rows of the config's mixture (the same draws as gen_vectors, before int8)."""
+    mix = mixture(cfg.gen, cfg.D, cfg.cfg_id)
+    out = np.empty((n, cfg.D), dtype=np.float32)
+    for c, lo in enumerate(range(0, n, CHUNK)):
+        hi = min(n, lo + CHUNK)
+        out[lo:hi] = _float_rows(mix, _rng(cfg.cfg_id, stream, c), hi - lo)
+    return out
+
+
+@dataclass
+class FloatInputs:
+    cfg: Config
+    db: np.ndarray              # float32 [N][D]
+    queries: np.ndarray         # float32 [Q][D]
+    v_max: float                # max |coordinate| over db and queries (the public fixed-point scale input)
+    centroid_rows: np.ndarray
+    codeword_rows: np.ndarray
+
+
+@lru_cache(maxsize=2)
+def generate_float(cfg: Config) -> FloatInputs:
+    """Real-valued inputs for the 16-bit fixed-point variant (NEXT-1)."""
+    db = gen_float_vectors(cfg, STREAM_DB, cfg.N)
+    q = gen_float_vectors(cfg, STREAM_Q, cfg.Q)
+    v_max = float(max(np.abs(db).max(), np.abs(q).max()))
+    cent, code = sample_rows(cfg)
+    return FloatInputs(cfg, db, q, v_max, cent, code)

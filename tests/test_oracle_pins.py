@@ -354,3 +354,62 @@ def test_rebalance_invariants_and_no_op():
         assert (counts0[init[moved]] > L).all()
         if (counts0 <= L).all():
             assert not moved.any()
+
+
+# ---------------------------------------------------------------- 16-bit fixed point (NEXT-1)
+
+def test_fixed_point_encoding_by_hand():
+    """v -> round((2^16 - 1) v / v_max); worked by hand with v_max = 4:
+    4 -> 65535, -4 -> -65535, 1 -> 16383.75 -> 16384, -1 -> -16384, 0 -> 0,
+    2/65535*4... the half case 4 * 0.5 / 65535 -> 0.5 -> 1 (half away from zero, R18)."""
+    x = np.array([4.0, -4.0, 1.0, -1.0, 0.0, 2.0 / 65535.0, -2.0 / 65535.0])
+    got = oracle.encode_fixed_point(x, 4.0)
+    assert got.tolist() == [65535, -65535, 16384, -16384, 0, 1, -1]
+    assert got.dtype == np.int32
+
+
+def test_fixed_point_variant_equals_int8_semantics_when_nothing_saturates():
+    """Special case reducing to the pinned int8 path: on int8-valued data whose residuals never
+    leave [-127, 127] (so R5's saturation is a no-op), the fixed-point oracle (int32 storage, int64
+    distances, unsaturated codewords R19) must return exactly the int8 oracle's snapshot and
+    query results -- only the storage width differs."""
+    rng = np.random.default_rng(41)
+    N, D, nlist, L, M, Ks = 500, 8, 6, 120, 4, 16
+    db8 = rng.integers(-60, 61, size=(N, D)).astype(np.int8)
+    cent = rng.choice(N, nlist, replace=False)
+    code = np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)])
+    s8 = oracle.build_snapshot(db8, nlist, L, M, Ks, cent, code)
+    s32 = oracle.build_snapshot(db8.astype(np.int32), nlist, L, M, Ks, cent, code)
+    assert s32.fx and not s8.fx
+    for name in ("centroids", "codebooks", "ids", "codes", "counts", "list_of"):
+        assert np.array_equal(getattr(s8, name).astype(np.int64), getattr(s32, name).astype(np.int64)), name
+    qs = rng.integers(-60, 61, size=(12, D)).astype(np.int8)
+    r8 = oracle.query_batch(s8, qs, 3, 20)
+    r32 = oracle.query_batch(s32, qs.astype(np.int32), 3, 20)
+    for key in r8:
+        a, b = r8[key].astype(np.int64), r32[key].astype(np.int64)
+        if key == "trace_cand_dist":   # padding: d_max differs (2^31 - 1 vs 2^63 - 1)
+            a = np.where(a == oracle.D_MAX, -1, a)
+            b = np.where(b == oracle.D_MAX_FX, -1, b)
+        assert np.array_equal(a, b), key
+
+
+def test_fixed_point_adc_is_distance_to_reconstruction():
+    """Closed form at 17-bit magnitudes (int64 arithmetic): every valid candidate distance equals
+    dist(q, mu_i + xhat) computed independently with Python integers."""
+    rng = np.random.default_rng(42)
+    x = rng.standard_normal((300, 8))
+    q = rng.standard_normal((4, 8))
+    v_max = float(max(np.abs(x).max(), np.abs(q).max()))
+    db = oracle.encode_fixed_point(x, v_max)
+    qq = oracle.encode_fixed_point(q, v_max)
+    s = oracle.build_snapshot(db, 5, 80, 2, 16, rng.choice(300, 5, replace=False),
+                              np.stack([rng.choice(300, 16, replace=False) for _ in range(2)]))
+    assert s.fx and np.abs(s.codebooks).max() > 127            # genuinely beyond int8
+    for qv in qq:
+        _, _, probes, _, cand = oracle.query(qv, s, 5, 10)
+        for rho, i in enumerate(probes):
+            for j in range(0, s.counts[i], 7):
+                xhat = [int(s.codebooks[m, s.codes[i, j, m], u]) for m in range(2) for u in range(4)]
+                ref = sum((int(qv[u]) - int(s.centroids[i, u]) - xhat[u]) ** 2 for u in range(8))
+                assert cand[rho, j] == ref
