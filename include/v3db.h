@@ -177,6 +177,44 @@ int v3db_witness_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int
                        int32_t* list_order, int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items,
                        int32_t* cand_dist, void* stream);
 
+/* ---- NEXT-1: the paper's 16-bit fixed-point representation ----
+ * "We encode embeddings using 16-bit fixed-point representation ... rounding
+ * round((2^16 - 1) * v / v_max)".  Readings (R18, R19): coordinates become int32 values
+ * in [-65535, 65535] (the sign kept, rounding half away from zero, computed in IEEE double as
+ * (v * 65535) / v_max); every distance is the exact squared L2 in int64 and d_max = 2^63 - 1;
+ * codewords are the residual sub-vectors themselves (int32, no saturation).  The five steps and
+ * the build rules are those of the int8 path with this arithmetic; shaping is the greedy rule. */
+
+/* v3db_encode_fixed_point -- out[i] = round_half_away(x[i] * 65535 / v_max), DEVICE float32 x
+ * [count] -> DEVICE int32 out [count].  Asynchronous on `stream`.  EINVAL: NULL pointer with
+ * count > 0, count < 0, v_max not positive finite.  |x| <= v_max keeps |out| <= 65535. */
+int v3db_encode_fixed_point(const float* x, int64_t count, double v_max, int32_t* out, void* stream);
+
+/* v3db_build_snapshot_fx -- v3db_build_snapshot on an int32 DEVICE database [n][dim] whose
+ * coordinates lie in [-65535, 65535] (EINVAL otherwise).  Same validation, ownership and errors
+ * as v3db_build_snapshot, plus EINVAL when nlist exceeds the composite-key bound at this dim
+ * (2^(64 - bits(dim * 131070^2)), 2^20 at dim 768).  Synchronous. */
+int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap,
+                           int32_t m, int32_t ks, const int32_t* centroid_rows,
+                           const int32_t* codeword_rows, void* stream, v3db_snapshot_t* out);
+
+/* v3db_query_batch_fx -- Steps 1-5 on a fixed-point snapshot: int32 DEVICE queries [nq][dim] in
+ * [-65535, 65535]; out_ids int32 [nq][k]; out_dist, trace_list_dist, trace_cand_dist int64 with
+ * the layouts of v3db_query_batch (padding / missing entries: id -1, distance 2^63 - 1).  EINVAL
+ * as v3db_query_batch, for an int8 snapshot, out-of-range queries, or nprobe * list_cap above the
+ * Step-5 key bound (2^(64 - bits(dim * 262140^2))); ECUDA if more than max(4096, 4k) candidates
+ * tie at the k-th distance of one query.  Synchronous (validation reads back one word). */
+int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, int32_t nprobe,
+                        int32_t k, int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists,
+                        int64_t* trace_list_dist, int64_t* trace_cand_dist, void* stream);
+
+/* v3db_snapshot_kind -- V3DB_KIND_INT8 or V3DB_KIND_FX16 (negative status on a NULL handle).
+ * v3db_query_batch* / v3db_witness_batch reject FX16 snapshots, v3db_query_batch_fx INT8 ones;
+ * v3db_snapshot_export returns int32 CENTROIDS / CODEBOOKS for FX16 snapshots. */
+#define V3DB_KIND_INT8 0
+#define V3DB_KIND_FX16 1
+int v3db_snapshot_kind(v3db_snapshot_t s);
+
 /* v3db_free -- release a snapshot.  NULL-safe.  The caller must not free a snapshot with
  * query work still in flight on any stream. */
 void v3db_free(v3db_snapshot_t s);

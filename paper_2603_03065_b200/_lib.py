@@ -19,6 +19,7 @@ STATUS_NAMES = {0: "V3DB_OK", 1: "V3DB_EINVAL", 2: "V3DB_EINFEASIBLE", 3: "V3DB_
 SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED = 0, 1, 2
 SHAPE_GREEDY, SHAPE_REBALANCE = 0, 1
 FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_IDS, FIELD_CODES, FIELD_COUNTS, FIELD_LIST_OF = range(6)
+KIND_INT8, KIND_FX16 = 0, 1
 
 _c_i8p = ctypes.c_void_p
 _c_i32p = ctypes.c_void_p
@@ -40,6 +41,15 @@ _SIGS = {
                                              ctypes.c_void_p]),
     "v3db_witness_batch": (ctypes.c_int, [ctypes.c_void_p, _c_i8p, ctypes.c_int64, ctypes.c_int32, _c_i32p, _c_i32p,
                                           _c_i32p, _c_i32p, _c_i32p, ctypes.c_void_p]),
+    "v3db_encode_fixed_point": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p,
+                                               ctypes.c_void_p]),
+    "v3db_build_snapshot_fx": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _c_i32p, _c_i32p,
+                                              ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "v3db_query_batch_fx": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                           ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "v3db_snapshot_kind": (ctypes.c_int, [ctypes.c_void_p]),
     "v3db_free": (None, [ctypes.c_void_p]),
     "v3db_snapshot_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "v3db_snapshot_export": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t]),

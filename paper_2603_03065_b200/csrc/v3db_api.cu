@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -67,6 +68,10 @@ void free_snapshot(v3db_snapshot* s) {
   cudaFree(s->codes_rot);
   cudaFree(s->pterm_rot);
   cudaFree(s->cbT);
+  cudaFree(s->centroids32);
+  cudaFree(s->cnorm64);
+  cudaFree(s->codebooks32);
+  cudaFree(s->pterm64);
   delete s;
 }
 
@@ -120,6 +125,56 @@ void keep_pool_memory(int dev) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
+}
+
+// B2, the ordered greedy placement (BASELINE.json configs[0]): every vector, in ascending t, goes
+// to the nearest list with room.  rank(lo, rows, R, d_idx, d_dist) writes each row's R nearest lists
+// (ascending (e, i)) on the GPU; when all R are full, exact(t, e) gives e_t,i for every list.
+template <class RankFn, class ExactFn>
+int place_greedy(int64_t n, int nlist, int L, RankFn rank, ExactFn exact, size_t dist_bytes, cudaStream_t st,
+                 std::vector<int32_t>& list_of, std::vector<int32_t>& flat_pos, std::vector<int32_t>& counts) {
+  const int R = std::min(nlist, 64);
+  const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 18);
+  DevBuf<int32_t> d_rank;
+  DevBuf<uint8_t> d_rdist;
+  HostPinned<int32_t> h_rank;
+  V3DB_CUDA(d_rank.alloc(static_cast<size_t>(chunk) * R));
+  V3DB_CUDA(d_rdist.alloc(static_cast<size_t>(chunk) * R * dist_bytes));
+  V3DB_CUDA(h_rank.alloc(static_cast<size_t>(chunk) * R));
+  std::vector<int64_t> e;
+  for (int64_t lo = 0; lo < n; lo += chunk) {
+    const int64_t rows = std::min(chunk, n - lo);
+    V3DB_CUDA(rank(lo, rows, R, d_rank.p, static_cast<void*>(d_rdist.p)));
+    V3DB_CUDA(cudaMemcpyAsync(h_rank.p, d_rank.p, sizeof(int32_t) * rows * R, cudaMemcpyDeviceToHost, st));
+    V3DB_CUDA(cudaStreamSynchronize(st));
+    for (int64_t r = 0; r < rows; ++r) {
+      const int64_t t = lo + r;
+      int chosen = -1;
+      const int32_t* rk = h_rank.p + r * R;
+      for (int a = 0; a < R; ++a) {
+        if (counts[rk[a]] < L) {
+          chosen = rk[a];
+          break;
+        }
+      }
+      if (chosen < 0) {  // all R nearest lists are full: exact full ranking on the host
+        e.resize(nlist);
+        V3DB_CUDA(exact(t, e));
+        int64_t best = INT64_MAX;
+        for (int i = 0; i < nlist; ++i) {
+          if (counts[i] < L && e[i] < best) {  // strict: lowest index on ties
+            best = e[i];
+            chosen = i;
+          }
+        }
+        if (chosen < 0) return fail(V3DB_EINFEASIBLE, "no list with room (internal)");
+      }
+      list_of[t] = chosen;
+      flat_pos[t] = chosen * L + counts[chosen];  // B6: members in ascending t
+      ++counts[chosen];
+    }
+  }
+  return V3DB_OK;
 }
 
 // Alg. 1 (capacity-constrained rebalancing) on the nearest-centroid assignment;
@@ -248,19 +303,9 @@ const char* v3db_last_error(void) { return g_err.c_str(); }
 
 void v3db_free(v3db_snapshot_t s) { free_snapshot(s); }
 
-int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
-                        int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, void* stream,
-                        v3db_snapshot_t* out) {
-  return v3db_build_snapshot_ex(db, n, dim, nlist, list_cap, m, ks, centroid_rows, codeword_rows, V3DB_SHAPE_GREEDY,
-                                nullptr, stream, out);
-}
-
-int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
-                           int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, int32_t rule,
-                           int64_t* stats, void* stream, v3db_snapshot_t* out) {
-  g_err.clear();
-  if (rule != V3DB_SHAPE_GREEDY && rule != V3DB_SHAPE_REBALANCE) return fail(V3DB_EINVAL, "unknown shaping rule");
-  if (!db || !centroid_rows || !codeword_rows || !out) return fail(V3DB_EINVAL, "NULL required pointer");
+static int validate_build(int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m, int32_t ks,
+                          const int32_t* centroid_rows, const int32_t* codeword_rows, v3db_snapshot_t* out) {
+  if (!centroid_rows || !codeword_rows || !out) return fail(V3DB_EINVAL, "NULL required pointer");
   if (dim < 1 || dim > V3DB_MAX_DIM) return fail(V3DB_EINVAL, "dim out of range [1, V3DB_MAX_DIM]");
   if (m < 1 || dim % m) return fail(V3DB_EINVAL, "dim must be a positive multiple of m (D = Md, PAPER.md:331)");
   if (dim / m > 64) return fail(V3DB_EINVAL, "sub-block dimension d = dim/m > 64 is not supported");
@@ -286,6 +331,24 @@ int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nli
       }
     }
   }
+  return V3DB_OK;
+}
+
+int v3db_build_snapshot(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
+                        int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, void* stream,
+                        v3db_snapshot_t* out) {
+  return v3db_build_snapshot_ex(db, n, dim, nlist, list_cap, m, ks, centroid_rows, codeword_rows, V3DB_SHAPE_GREEDY,
+                                nullptr, stream, out);
+}
+
+int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
+                           int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, int32_t rule,
+                           int64_t* stats, void* stream, v3db_snapshot_t* out) {
+  g_err.clear();
+  if (rule != V3DB_SHAPE_GREEDY && rule != V3DB_SHAPE_REBALANCE) return fail(V3DB_EINVAL, "unknown shaping rule");
+  if (!db) return fail(V3DB_EINVAL, "NULL required pointer");
+  int vrc = validate_build(n, dim, nlist, list_cap, m, ks, centroid_rows, codeword_rows, out);
+  if (vrc != V3DB_OK) return vrc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int d = dim / m;
   const int L = list_cap;
@@ -325,59 +388,33 @@ int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nli
   int64_t moved = 0, rounds = 0;
   if (rule == V3DB_SHAPE_GREEDY) {
     // B2: GPU ranks each vector's R nearest lists by (e, i); host places in ascending t.
-    const int R = std::min(nlist, 64);
-    const int64_t chunk = std::min<int64_t>(n, int64_t(1) << 18);
-    DevBuf<int32_t> d_rank, d_rdist;
-    HostPinned<int32_t> h_rank;
-    V3DB_CUDA(d_rank.alloc(static_cast<size_t>(chunk) * R));
-    V3DB_CUDA(d_rdist.alloc(static_cast<size_t>(chunk) * R));
-    V3DB_CUDA(h_rank.alloc(static_cast<size_t>(chunk) * R));
     std::vector<int8_t> mu_host;
     std::vector<int8_t> row(dim);
-    int64_t fallbacks = 0;
-    for (int64_t lo = 0; lo < n; lo += chunk) {
-      const int64_t rows = std::min(chunk, n - lo);
-      V3DB_CUDA(v3db::coarse_topk(db + lo * dim, rows, dim, s->centroids, s->cnorm, nlist, R, d_rank.p, d_rdist.p, st));
-      V3DB_CUDA(cudaMemcpyAsync(h_rank.p, d_rank.p, sizeof(int32_t) * rows * R, cudaMemcpyDeviceToHost, st));
-      V3DB_CUDA(cudaStreamSynchronize(st));
-      for (int64_t r = 0; r < rows; ++r) {
-        const int64_t t = lo + r;
-        int chosen = -1;
-        const int32_t* rk = h_rank.p + r * R;
-        for (int a = 0; a < R; ++a) {
-          if (counts[rk[a]] < L) {
-            chosen = rk[a];
-            break;
-          }
-        }
-        if (chosen < 0) {  // all R nearest lists are full: exact full ranking on the host
-          ++fallbacks;
+    int rc = place_greedy(
+        n, nlist, L,
+        [&](int64_t lo, int64_t rows, int R, int32_t* d_rank, void* d_rdist) {
+          return v3db::coarse_topk(db + lo * dim, rows, dim, s->centroids, s->cnorm, nlist, R, d_rank,
+                                   static_cast<int32_t*>(d_rdist), st);
+        },
+        [&](int64_t t, std::vector<int64_t>& e) -> cudaError_t {  // exact e_t,i for every list (host)
+          cudaError_t ce = cudaSuccess;
           if (mu_host.empty()) {
             mu_host.resize(static_cast<size_t>(nlist) * dim);
-            V3DB_CUDA(cudaMemcpy(mu_host.data(), s->centroids, mu_host.size(), cudaMemcpyDeviceToHost));
+            ce = cudaMemcpy(mu_host.data(), s->centroids, mu_host.size(), cudaMemcpyDeviceToHost);
           }
-          V3DB_CUDA(cudaMemcpy(row.data(), db + t * dim, dim, cudaMemcpyDeviceToHost));
-          int64_t best = INT64_MAX;
-          for (int i = 0; i < nlist; ++i) {
-            if (counts[i] >= L) continue;
-            int64_t e = 0;
+          if (ce == cudaSuccess) ce = cudaMemcpy(row.data(), db + t * dim, dim, cudaMemcpyDeviceToHost);
+          for (int i = 0; i < nlist && ce == cudaSuccess; ++i) {
+            int64_t acc = 0;
             for (int u = 0; u < dim; ++u) {
               const int64_t df = int64_t(row[u]) - int64_t(mu_host[static_cast<size_t>(i) * dim + u]);
-              e += df * df;
+              acc += df * df;
             }
-            if (e < best) {  // strict: lowest index on ties
-              best = e;
-              chosen = i;
-            }
+            e[i] = acc;
           }
-          if (chosen < 0) return fail(V3DB_EINFEASIBLE, "no list with room (internal)");
-        }
-        list_of[t] = chosen;
-        flat_pos[t] = chosen * L + counts[chosen];  // B6: members in ascending t
-        ++counts[chosen];
-      }
-    }
-    (void)fallbacks;
+          return ce;
+        },
+        sizeof(int32_t), st, list_of, flat_pos, counts);
+    if (rc != V3DB_OK) return rc;
 
   } else {
     int rc = place_rebalance(db, n, dim, nlist, L, s->centroids, s->cnorm, st, list_of, counts, &moved, &rounds);
@@ -445,6 +482,7 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   g_err.clear();
   int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
   if (rc != V3DB_OK) return rc;
+  if (s->fx) return fail(V3DB_EINVAL, "fixed-point snapshot: use v3db_query_batch_fx");
   if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_GENERIC && algo != V3DB_SCAN_ROTATED)
     return fail(V3DB_EINVAL, "unsupported scan algo");
   if (algo == V3DB_SCAN_ROTATED && s->lut_mode == 0)
@@ -492,6 +530,7 @@ int v3db_query_batch_host(v3db_snapshot_t s, const int8_t* queries, int64_t nq, 
   g_err.clear();
   int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
   if (rc != V3DB_OK) return rc;
+  if (s->fx) return fail(V3DB_EINVAL, "fixed-point snapshot: use v3db_query_batch_fx");
   if ((rc = check_device(s)) != V3DB_OK) return rc;
   if (nq == 0) return V3DB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -537,6 +576,7 @@ int v3db_witness_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int
                        int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items, int32_t* cand_dist, void* stream) {
   g_err.clear();
   if (!s) return fail(V3DB_EINVAL, "NULL snapshot");
+  if (s->fx) return fail(V3DB_EINVAL, "the witness API covers int8 snapshots");
   if (nq < 0 || nq > 65535) return fail(V3DB_EINVAL, "nq out of range [0, 65535] (witnesses are per challenged query)");
   if (nq > 0 && !queries) return fail(V3DB_EINVAL, "NULL queries");
   if (nprobe < 1 || nprobe > s->nlist || nprobe > V3DB_MAX_NPROBE)
@@ -548,6 +588,159 @@ int v3db_witness_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int
                                       static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "v3db_witness_batch");
   return V3DB_OK;
+}
+
+// ---- NEXT-1: the 16-bit fixed-point path (fx16.cu) ----
+
+int v3db_encode_fixed_point(const float* x, int64_t count, double v_max, int32_t* out, void* stream) {
+  g_err.clear();
+  if (count < 0) return fail(V3DB_EINVAL, "count < 0");
+  if (count > 0 && (!x || !out)) return fail(V3DB_EINVAL, "NULL pointer");
+  if (!(v_max > 0.0) || !std::isfinite(v_max)) return fail(V3DB_EINVAL, "v_max must be positive and finite");
+  cudaError_t e = v3db::encode_fixed_point(x, count, v_max, out, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "v3db_encode_fixed_point");
+  return V3DB_OK;
+}
+
+// |v| <= 65535 for every coordinate (the 16-bit fixed-point range; the distance bounds of the
+// composite keys and the exactness of the double-precision dot products rest on it).
+static int check_fx_range(const int32_t* x, int64_t count, cudaStream_t st, const char* what) {
+  DevBuf<int> d_m;
+  V3DB_CUDA(d_m.alloc(1));
+  V3DB_CUDA(cudaMemsetAsync(d_m.p, 0, sizeof(int), st));
+  V3DB_CUDA(v3db::abs_max32(x, count, d_m.p, st));
+  int m = 0;
+  V3DB_CUDA(cudaMemcpyAsync(&m, d_m.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  V3DB_CUDA(cudaStreamSynchronize(st));
+  if (m > 65535) return fail(V3DB_EINVAL, std::string(what) + " coordinates outside [-65535, 65535]");
+  return V3DB_OK;
+}
+
+int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nlist, int32_t list_cap, int32_t m,
+                           int32_t ks, const int32_t* centroid_rows, const int32_t* codeword_rows, void* stream,
+                           v3db_snapshot_t* out) {
+  g_err.clear();
+  if (!db) return fail(V3DB_EINVAL, "NULL required pointer");
+  int rc = validate_build(n, dim, nlist, list_cap, m, ks, centroid_rows, codeword_rows, out);
+  if (rc != V3DB_OK) return rc;
+  if (v3db::fx_shift2(dim) < 1 || nlist > (1 << std::min(v3db::fx_shift2(dim), 30)))
+    return fail(V3DB_EINVAL, "nlist too large for the composite Step-2 keys at this dim");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = check_fx_range(db, n * dim, st, "database")) != V3DB_OK) return rc;
+  const int d = dim / m;
+  const int L = list_cap;
+  v3db_snapshot* s = new (std::nothrow) v3db_snapshot();
+  if (!s) return fail(V3DB_ENOMEM, "host allocation failed");
+  struct Guard {
+    v3db_snapshot* s;
+    ~Guard() { free_snapshot(s); }
+  } guard{s};
+  s->n = n;
+  s->dim = dim;
+  s->nlist = nlist;
+  s->L = L;
+  s->M = m;
+  s->Ks = ks;
+  s->d = d;
+  s->fx = 1;
+  V3DB_CUDA(cudaGetDevice(&s->device));
+  keep_pool_memory(s->device);
+  const int64_t slots = static_cast<int64_t>(nlist) * L;
+  V3DB_CUDA(cudaMalloc(&s->centroids32, sizeof(int32_t) * nlist * dim));
+  V3DB_CUDA(cudaMalloc(&s->cnorm64, sizeof(int64_t) * nlist));
+  V3DB_CUDA(cudaMalloc(&s->codebooks32, sizeof(int32_t) * m * ks * d));
+  V3DB_CUDA(cudaMalloc(&s->ids, sizeof(int32_t) * slots));
+  V3DB_CUDA(cudaMalloc(&s->codes, static_cast<size_t>(slots) * m));
+  V3DB_CUDA(cudaMalloc(&s->counts, sizeof(int32_t) * nlist));
+  V3DB_CUDA(cudaMalloc(&s->pterm64, sizeof(int64_t) * slots));
+  V3DB_CUDA(cudaMalloc(&s->list_of, sizeof(int32_t) * n));
+  DevBuf<int32_t> d_rows;
+  V3DB_CUDA(d_rows.alloc(nlist));
+  V3DB_CUDA(cudaMemcpyAsync(d_rows.p, centroid_rows, sizeof(int32_t) * nlist, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(v3db::gather_rows32(db, dim, d_rows.p, nlist, s->centroids32, s->cnorm64, st));  // B1
+
+  std::vector<int32_t> list_of(n), flat_pos(n), counts(nlist, 0);
+  std::vector<int32_t> mu_host, row(dim);
+  rc = place_greedy(
+      n, nlist, L,
+      [&](int64_t lo, int64_t rows, int R, int32_t* d_rank, void* d_rdist) {
+        return v3db::fx_topk(db + lo * dim, rows, dim, s->centroids32, s->cnorm64, nlist, R, d_rank,
+                             static_cast<int64_t*>(d_rdist), st);
+      },
+      [&](int64_t t, std::vector<int64_t>& e) -> cudaError_t {
+        cudaError_t ce = cudaSuccess;
+        if (mu_host.empty()) {
+          mu_host.resize(static_cast<size_t>(nlist) * dim);
+          ce = cudaMemcpy(mu_host.data(), s->centroids32, sizeof(int32_t) * mu_host.size(), cudaMemcpyDeviceToHost);
+        }
+        if (ce == cudaSuccess) ce = cudaMemcpy(row.data(), db + t * dim, sizeof(int32_t) * dim, cudaMemcpyDeviceToHost);
+        for (int i = 0; i < nlist && ce == cudaSuccess; ++i) {
+          int64_t acc = 0;
+          for (int u = 0; u < dim; ++u) {
+            const int64_t df = int64_t(row[u]) - int64_t(mu_host[static_cast<size_t>(i) * dim + u]);
+            acc += df * df;
+          }
+          e[i] = acc;
+        }
+        return ce;
+      },
+      sizeof(int64_t), st, list_of, flat_pos, counts);
+  if (rc != V3DB_OK) return rc;
+  DevBuf<int32_t> d_pos, d_cwrows;
+  V3DB_CUDA(d_pos.alloc(n));
+  V3DB_CUDA(d_cwrows.alloc(static_cast<size_t>(m) * ks));
+  V3DB_CUDA(cudaMemcpyAsync(s->list_of, list_of.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemcpyAsync(d_pos.p, flat_pos.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemcpyAsync(d_cwrows.p, codeword_rows, sizeof(int32_t) * m * ks, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemcpyAsync(s->counts, counts.data(), sizeof(int32_t) * nlist, cudaMemcpyHostToDevice, st));
+  V3DB_CUDA(cudaMemsetAsync(s->ids, 0xff, sizeof(int32_t) * slots, st));
+  V3DB_CUDA(cudaMemsetAsync(s->codes, 0, static_cast<size_t>(slots) * m, st));
+  V3DB_CUDA(v3db::fx_build_tail(db, n, dim, s->centroids32, s->list_of, d_pos.p, m, ks, d_cwrows.p, nlist, L,
+                                s->codebooks32, s->codes, s->ids, s->pterm64, st));  // B3-B6
+  V3DB_CUDA(cudaStreamSynchronize(st));
+  s->total_valid = n;
+  guard.s = nullptr;
+  *out = s;
+  return V3DB_OK;
+}
+
+int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, int32_t nprobe, int32_t k,
+                        int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists, int64_t* trace_list_dist,
+                        int64_t* trace_cand_dist, void* stream) {
+  g_err.clear();
+  int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
+  if (rc != V3DB_OK) return rc;
+  if (!s->fx) return fail(V3DB_EINVAL, "v3db_query_batch_fx needs a snapshot from v3db_build_snapshot_fx");
+  if (static_cast<int64_t>(nprobe) * s->L > (int64_t(1) << std::min(v3db::fx_shift5(s->dim), 31)))
+    return fail(V3DB_EINVAL, "nprobe * list_cap too large for the composite Step-5 keys at this dim");
+  if ((rc = check_device(s)) != V3DB_OK) return rc;
+  if (nq == 0) return V3DB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = check_fx_range(queries, nq * s->dim, st, "query")) != V3DB_OK) return rc;
+  int32_t* lists = trace_lists;
+  int64_t* ldist = trace_list_dist;
+  void* scratch = nullptr;
+  if (!lists || !ldist) {
+    V3DB_CUDA(cudaMallocAsync(&scratch, (sizeof(int32_t) + sizeof(int64_t)) * nq * nprobe, st));
+    if (!ldist) ldist = static_cast<int64_t*>(scratch);
+    if (!lists) lists = reinterpret_cast<int32_t*>(static_cast<int64_t*>(scratch) + nq * nprobe);
+  }
+  prof_record(0, st);
+  cudaError_t e = v3db::fx_topk(queries, nq, s->dim, s->centroids32, s->cnorm64, s->nlist, nprobe, lists, ldist, st);
+  prof_record(1, st);
+  if (e == cudaSuccess) e = v3db::fx_scan(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+  prof_record(2, st);
+  if (scratch) cudaFreeAsync(scratch, st);
+  if (e == cudaErrorNotSupported)
+    return fail(V3DB_ECUDA, "more than 4096 (or 4k) candidates tie at the k-th distance (fx scan buffer)");
+  if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_fx");
+  return V3DB_OK;
+}
+
+int v3db_snapshot_kind(v3db_snapshot_t s) {
+  g_err.clear();
+  if (!s) return fail(V3DB_EINVAL, "NULL snapshot");
+  return s->fx ? V3DB_KIND_FX16 : V3DB_KIND_INT8;
 }
 
 int v3db_snapshot_info(v3db_snapshot_t s, int64_t* out8) {
@@ -565,8 +758,14 @@ int v3db_snapshot_export(v3db_snapshot_t s, int32_t field, void* host_dst, size_
   const void* src = nullptr;
   size_t need = 0;
   switch (field) {
-    case V3DB_FIELD_CENTROIDS: src = s->centroids; need = static_cast<size_t>(s->nlist) * s->dim; break;
-    case V3DB_FIELD_CODEBOOKS: src = s->codebooks; need = static_cast<size_t>(s->M) * s->Ks * s->d; break;
+    case V3DB_FIELD_CENTROIDS:
+      src = s->fx ? static_cast<const void*>(s->centroids32) : s->centroids;
+      need = static_cast<size_t>(s->nlist) * s->dim * (s->fx ? 4 : 1);
+      break;
+    case V3DB_FIELD_CODEBOOKS:
+      src = s->fx ? static_cast<const void*>(s->codebooks32) : s->codebooks;
+      need = static_cast<size_t>(s->M) * s->Ks * s->d * (s->fx ? 4 : 1);
+      break;
     case V3DB_FIELD_IDS: src = s->ids; need = sizeof(int32_t) * slots; break;
     case V3DB_FIELD_CODES: src = s->codes; need = static_cast<size_t>(slots) * s->M; break;
     case V3DB_FIELD_COUNTS: src = s->counts; need = sizeof(int32_t) * s->nlist; break;

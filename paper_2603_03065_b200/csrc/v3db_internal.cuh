@@ -40,6 +40,13 @@ struct v3db_snapshot {
   uint8_t* codes_rot = nullptr;
   int32_t* pterm_rot = nullptr;
   int8_t* cbT = nullptr;
+  // NEXT-1 (fx16.cu): 16-bit fixed-point snapshot.  When fx != 0 the int8
+  // fields centroids / cnorm / codebooks / pterm are unused and these hold the data instead.
+  int fx = 0;
+  int32_t* centroids32 = nullptr;  // [nlist][dim]
+  int64_t* cnorm64 = nullptr;      // [nlist]
+  int32_t* codebooks32 = nullptr;  // [M][Ks][d]
+  int64_t* pterm64 = nullptr;      // [nlist][L]
 };
 
 namespace v3db {
@@ -140,5 +147,22 @@ cudaError_t delta_keys(const int32_t* e_t, const int32_t* e_i, int64_t n, int64_
 cudaError_t witness_batch(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int32_t* list_order,
                           int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items, int32_t* cand_dist,
                           cudaStream_t st);
+
+// NEXT-1, the 16-bit fixed-point path (fx16.cu).
+constexpr int64_t kDMaxFx = 0x7fffffffffffffffLL;  // d_max = 2^63 - 1 (R18)
+int fx_shift2(int dim);  // key shift of Step-2 keys d << sh | i
+int fx_shift5(int dim);  // key shift of Step-5 keys D << sh | slot
+cudaError_t encode_fixed_point(const float* x, int64_t n, double v_max, int32_t* out, cudaStream_t st);
+// max |v| over n int32 values -> *out (device int, pre-zeroed by the caller)
+cudaError_t abs_max32(const int32_t* x, int64_t n, int* out, cudaStream_t st);
+cudaError_t gather_rows32(const int32_t* db, int dim, const int32_t* rows, int nrows, int32_t* out, int64_t* norms,
+                          cudaStream_t st);
+cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, const int64_t* mnorm, int nlist, int R,
+                    int32_t* out_idx, int64_t* out_dist, cudaStream_t st);
+cudaError_t fx_build_tail(const int32_t* db, int64_t n, int dim, const int32_t* mu, const int32_t* list_of,
+                          const int32_t* flat_pos, int M, int Ks, const int32_t* codeword_rows, int nlist, int L,
+                          int32_t* cb, uint8_t* codes, int32_t* ids, int64_t* pterm, cudaStream_t st);
+cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k, const int32_t* lists,
+                    const int64_t* ldist, int32_t* out_ids, int64_t* out_dist, int64_t* trace, cudaStream_t st);
 
 }  // namespace v3db

@@ -6,6 +6,8 @@ device memory and streams only.  Functions mirror the C names without the ``v3db
   query_batch(s, queries, nprobe, k, trace=True, algo=SCAN_AUTO, out=None, stream=None) -> dict
   query_batch_host(s, queries_host, nprobe, k, out) -> None          (end-to-end, host buffers)
   snapshot_info(s) -> dict;  snapshot_export(s, field) -> numpy array;  free(s)
+  NEXT-1, 16-bit fixed point: encode_fixed_point(x, v_max) -> int32 tensor;
+  build_snapshot_fx(db_int32, ...) -> Snapshot;  query_batch_fx(s, queries_int32, nprobe, k) -> dict
 """
 from __future__ import annotations
 
@@ -16,7 +18,7 @@ import torch
 
 from . import _lib
 from ._lib import (FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_CODES, FIELD_COUNTS, FIELD_IDS,  # noqa: F401
-                   FIELD_LIST_OF, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, SHAPE_GREEDY, SHAPE_REBALANCE,
+                   FIELD_LIST_OF, KIND_FX16, KIND_INT8, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, SHAPE_GREEDY, SHAPE_REBALANCE,
                    V3DBError)
 
 
@@ -42,6 +44,7 @@ class Snapshot:
     def __init__(self, handle: ctypes.c_void_p):
         self._h = handle
         self.info = snapshot_info(self)
+        self.kind = int(_lib.load().v3db_snapshot_kind(handle))
 
     @property
     def handle(self) -> ctypes.c_void_p:
@@ -88,6 +91,56 @@ def build_snapshot(db: torch.Tensor, nlist: int, list_cap: int, m: int, ks: int,
     if stats is not None:
         stats.update(moved=int(st[0]), rounds=int(st[1]))
     return Snapshot(h)
+
+
+def encode_fixed_point(x: torch.Tensor, v_max: float, stream=None) -> torch.Tensor:
+    """v3db_encode_fixed_point: round((2^16 - 1) v / v_max) of a CUDA float32 tensor (PAPER.md:781-782,
+    DESIGN.md R18) -> CUDA int32 tensor of the same shape."""
+    lib = _lib.load()
+    if x.dtype != torch.float32 or x.device.type != "cuda" or not x.is_contiguous():
+        raise ValueError("x must be a contiguous CUDA float32 tensor")
+    out = torch.empty(x.shape, dtype=torch.int32, device=x.device)
+    _lib.check(lib.v3db_encode_fixed_point(_ptr(x), x.numel(), float(v_max), _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def build_snapshot_fx(db: torch.Tensor, nlist: int, list_cap: int, m: int, ks: int, centroid_rows, codeword_rows,
+                      stream=None) -> Snapshot:
+    """v3db_build_snapshot_fx: db is a CUDA int32 [n][dim] tensor of 16-bit fixed-point coordinates."""
+    lib = _lib.load()
+    if db.dtype != torch.int32 or db.device.type != "cuda" or db.dim() != 2 or not db.is_contiguous():
+        raise ValueError("db must be a contiguous CUDA int32 [n][dim] tensor")
+    cent = np.ascontiguousarray(np.asarray(centroid_rows, dtype=np.int32).reshape(-1))
+    code = np.ascontiguousarray(np.asarray(codeword_rows, dtype=np.int32).reshape(-1))
+    if cent.size != nlist or code.size != m * ks:
+        raise ValueError("centroid_rows must have nlist entries and codeword_rows m*ks entries")
+    h = ctypes.c_void_p()
+    _lib.check(lib.v3db_build_snapshot_fx(_ptr(db), db.shape[0], db.shape[1], nlist, list_cap, m, ks,
+                                          cent.ctypes.data_as(ctypes.c_void_p), code.ctypes.data_as(ctypes.c_void_p),
+                                          _stream_ptr(stream), ctypes.byref(h)))
+    return Snapshot(h)
+
+
+def query_batch_fx(s: Snapshot, queries: torch.Tensor, nprobe: int, k: int, trace: bool = True,
+                   stream=None) -> dict:
+    """v3db_query_batch_fx: Steps 1-5 on a fixed-point snapshot.  out_ids (int32) / out_dist (int64)
+    [nq][k]; with trace, trace_lists (int32) / trace_list_dist (int64) [nq][nprobe] and
+    trace_cand_dist (int64) [nq][nprobe][L]."""
+    lib = _lib.load()
+    nq = queries.shape[0]
+    _need(queries, torch.int32, "cuda", (nq, s.dim), "queries")
+    dev = queries.device
+    out = {"out_ids": torch.empty((nq, k), dtype=torch.int32, device=dev),
+           "out_dist": torch.empty((nq, k), dtype=torch.int64, device=dev)}
+    if trace:
+        out["trace_lists"] = torch.empty((nq, nprobe), dtype=torch.int32, device=dev)
+        out["trace_list_dist"] = torch.empty((nq, nprobe), dtype=torch.int64, device=dev)
+        out["trace_cand_dist"] = torch.empty((nq, nprobe, s.list_cap), dtype=torch.int64, device=dev)
+    _lib.check(lib.v3db_query_batch_fx(s.handle, _ptr(queries), nq, nprobe, k, _ptr(out["out_ids"]),
+                                       _ptr(out["out_dist"]), _ptr(out.get("trace_lists")),
+                                       _ptr(out.get("trace_list_dist")), _ptr(out.get("trace_cand_dist")),
+                                       _stream_ptr(stream)))
+    return out
 
 
 def alloc_outputs(s: Snapshot, nq: int, nprobe: int, k: int, trace: bool = True, device="cuda", pin=False) -> dict:
@@ -173,9 +226,10 @@ def snapshot_info(s: Snapshot) -> dict:
 def snapshot_export(s: Snapshot, field: int) -> np.ndarray:
     """v3db_snapshot_export: canonical snapshot arrays as numpy (test-only introspection)."""
     i = s.info
+    wide = np.int32 if s.kind == KIND_FX16 else np.int8
     shapes = {
-        FIELD_CENTROIDS: ((i["nlist"], i["dim"]), np.int8),
-        FIELD_CODEBOOKS: ((i["m"], i["ks"], i["d"]), np.int8),
+        FIELD_CENTROIDS: ((i["nlist"], i["dim"]), wide),
+        FIELD_CODEBOOKS: ((i["m"], i["ks"], i["d"]), wide),
         FIELD_IDS: ((i["nlist"], i["list_cap"]), np.int32),
         FIELD_CODES: ((i["nlist"], i["list_cap"], i["m"]), np.uint8),
         FIELD_COUNTS: ((i["nlist"],), np.int32),

@@ -1,0 +1,188 @@
+"""GPU parity of NEXT-1, the paper's 16-bit fixed-point representation (
+DESIGN.md R18/R19): encode -> build -> query through the C ABI (v3db_encode_fixed_point,
+v3db_build_snapshot_fx, v3db_query_batch_fx) vs the oracle's fixed-point variant.  Integer work
+throughout (int32 coordinates, int64 distances): the bar is bit-exact equality of every output.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import generate_float, get_config
+
+from .gpu_util import first_mismatch, oracle_queries
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("centroids", "codebooks", "ids", "codes", "counts", "list_of")
+KEYS = ("out_ids", "out_dist", "trace_lists", "trace_list_dist", "trace_cand_dist")
+
+
+@pytest.fixture(scope="module")
+def v3db():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_03065_b200 import build as libbuild
+    libbuild.build()
+    from paper_2603_03065_b200 import v3db as mod
+    return mod
+
+
+def export_all(v3db, s):
+    f = {"centroids": v3db.FIELD_CENTROIDS, "codebooks": v3db.FIELD_CODEBOOKS, "ids": v3db.FIELD_IDS,
+         "codes": v3db.FIELD_CODES, "counts": v3db.FIELD_COUNTS, "list_of": v3db.FIELD_LIST_OF}
+    return {k: v3db.snapshot_export(s, v) for k, v in f.items()}
+
+
+def check_snapshot(v3db, s, ref_s):
+    assert s.kind == v3db.KIND_FX16
+    got = export_all(v3db, s)
+    for name in FIELDS:
+        exp = getattr(ref_s, name)
+        assert np.array_equal(got[name], exp), f"snapshot {name}: {first_mismatch(got[name], exp)}"
+
+
+def check_query(out, ref, keys=KEYS):
+    for key in keys:
+        got = out[key].cpu().numpy()
+        assert got.dtype == ref[key].dtype, (key, got.dtype, ref[key].dtype)
+        assert np.array_equal(got, ref[key]), f"{key}: {first_mismatch(got, ref[key])}"
+
+
+def run_int32_case(v3db, db, qs, nlist, L, M, Ks, nprobe, k, cent, code):
+    ref_s = oracle.build_snapshot(db, nlist, L, M, Ks, cent, code)
+    ref = oracle_queries(ref_s, qs, nprobe, k)
+    s = v3db.build_snapshot_fx(torch.from_numpy(np.ascontiguousarray(db)).cuda(), nlist, L, M, Ks, cent, code)
+    check_snapshot(v3db, s, ref_s)
+    out = v3db.query_batch_fx(s, torch.from_numpy(np.ascontiguousarray(qs)).cuda(), nprobe, k)
+    check_query(out, ref)
+    return ref_s, ref
+
+
+_CACHE = {}
+
+
+def fx_case(name):
+    """(cfg, float inputs, oracle-encoded db / queries, oracle snapshot, oracle outputs)."""
+    if name not in _CACHE:
+        cfg = get_config(name)
+        f = generate_float(cfg)
+        db = oracle.encode_fixed_point(f.db, f.v_max)
+        qs = oracle.encode_fixed_point(f.queries, f.v_max)
+        ref_s = oracle.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows, f.codeword_rows)
+        ref = oracle_queries(ref_s, qs, cfg.nprobe, cfg.k)
+        _CACHE[name] = (cfg, f, db, qs, ref_s, ref)
+    return _CACHE[name]
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "e2_basic", "e2_lowacc", "e2_large", "c4_mini"])
+def test_fx_end_to_end_parity(v3db, name):
+    """float32 vectors -> GPU encoding -> GPU build -> GPU query, bit-exact against the oracle's
+    encoding, build and query (every snapshot array, top-k and the whole witness trace)."""
+    cfg, f, db, qs, ref_s, ref = fx_case(name)
+    gdb = v3db.encode_fixed_point(torch.from_numpy(f.db).cuda(), f.v_max)
+    gqs = v3db.encode_fixed_point(torch.from_numpy(f.queries).cuda(), f.v_max)
+    assert np.array_equal(gdb.cpu().numpy(), db), first_mismatch(gdb.cpu().numpy(), db)
+    assert np.array_equal(gqs.cpu().numpy(), qs)
+    s = v3db.build_snapshot_fx(gdb, cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows, f.codeword_rows)
+    check_snapshot(v3db, s, ref_s)
+    assert np.abs(v3db.snapshot_export(s, v3db.FIELD_CODEBOOKS)).max() > 127  # genuinely beyond int8
+    out = v3db.query_batch_fx(s, gqs, cfg.nprobe, cfg.k)
+    check_query(out, ref)
+    out2 = v3db.query_batch_fx(s, gqs, cfg.nprobe, cfg.k, trace=False)
+    check_query(out2, ref, keys=("out_ids", "out_dist"))
+
+
+def test_fx_encoding_rounding_cases(v3db):
+    """Hand-worked encodings (the oracle pin's values) and exact halves, on the GPU."""
+    x = np.array([4.0, -4.0, 1.0, -1.0, 0.0, 3.9999], np.float32)
+    got = v3db.encode_fixed_point(torch.from_numpy(x).cuda(), 4.0).cpu().numpy()
+    assert got.tolist() == oracle.encode_fixed_point(x, 4.0).tolist()
+    assert got[:5].tolist() == [65535, -65535, 16384, -16384, 0]
+    # exact halves (v_max = 65535 makes y = v): half away from zero, not to even
+    h = np.array([0.5, -0.5, 1.5, 2.5, -2.5, 65534.5], np.float32)
+    got = v3db.encode_fixed_point(torch.from_numpy(h).cuda(), 65535.0).cpu().numpy()
+    assert got.tolist() == [1, -1, 2, 3, -3, 65535]
+    rng = np.random.default_rng(5)
+    y = (rng.standard_normal(1 << 20) * 3).astype(np.float32)
+    vm = float(np.abs(y).max())
+    g = v3db.encode_fixed_point(torch.from_numpy(y).cuda(), vm).cpu().numpy()
+    assert np.array_equal(g, oracle.encode_fixed_point(y, vm))
+
+
+def test_fx_extreme_magnitudes(v3db):
+    """Coordinates at +-65535 (the range bound): the largest distances the keys must carry."""
+    rng = np.random.default_rng(21)
+    N, D, nlist, L, M, Ks = 600, 32, 12, 80, 8, 16
+    db = rng.choice(np.array([-65535, -65534, 0, 65534, 65535], np.int32), size=(N, D)).astype(np.int32)
+    qs = rng.choice(np.array([-65535, 65535], np.int32), size=(33, D)).astype(np.int32)
+    run_int32_case(v3db, db, qs, nlist, L, M, Ks, 5, 40, rng.choice(N, nlist, replace=False),
+                   np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
+
+
+def test_fx_ties_and_fewer_than_k(v3db):
+    """All vectors identical (every distance ties: the id tie-break orders, R10) and k above the
+    valid count (-1, 2^63 - 1 tail)."""
+    N, D, nlist, L = 300, 8, 4, 100
+    db = np.full((N, D), 40000, np.int32)
+    qs = np.vstack([np.full((1, D), 40000, np.int32), np.full((1, D), -9, np.int32),
+                    (np.arange(D, dtype=np.int32) * 1000)[None]])
+    _, ref = run_int32_case(v3db, db, qs, nlist, L, 4, 4, 3, 50, np.arange(nlist), np.stack([np.arange(4)] * 4))
+    rng = np.random.default_rng(22)
+    db = rng.integers(-65535, 65536, size=(40, 8)).astype(np.int32)
+    qs = rng.integers(-65535, 65536, size=(19, 8)).astype(np.int32)
+    _, ref = run_int32_case(v3db, db, qs, 8, 64, 2, 8, 2, 100, rng.choice(40, 8, replace=False),
+                            np.stack([rng.choice(40, 8, replace=False) for _ in range(2)]))
+    assert (ref["out_ids"] == -1).any() and (ref["out_dist"] == oracle.D_MAX_FX).any()
+
+
+def test_fx_global_table_and_greedy_overflow(v3db):
+    """M * Ks = 16384 (> 96 KiB of int64 table: the per-query table lives in global scratch) and a
+    tight capacity with nlist > 64, so some vectors find all 64 ranked lists full (exact fallback)."""
+    rng = np.random.default_rng(23)
+    N, D, nlist, L, M, Ks = 4000, 128, 80, 52, 64, 256
+    centres = rng.integers(-30000, 30000, size=(3, D))
+    db = (centres[rng.integers(0, 3, N)] + rng.integers(-3000, 3000, size=(N, D))).astype(np.int32)
+    qs = (centres[rng.integers(0, 3, 25)] + rng.integers(-3000, 3000, size=(25, D))).astype(np.int32)
+    run_int32_case(v3db, db, qs, nlist, L, M, Ks, 6, 30, rng.choice(N, nlist, replace=False),
+                   np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
+
+
+@pytest.mark.parametrize("nq", [0, 1, 67])
+def test_fx_ragged_batches(v3db, nq):
+    cfg, f, db, qs, ref_s, ref = fx_case("e2_basic")
+    s = v3db.build_snapshot_fx(torch.from_numpy(db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows,
+                               f.codeword_rows)
+    out = v3db.query_batch_fx(s, torch.from_numpy(np.ascontiguousarray(qs[:nq])).cuda(), cfg.nprobe, cfg.k)
+    for key in KEYS:
+        assert np.array_equal(out[key].cpu().numpy(), ref[key][:nq]), key
+
+
+def test_fx_errors(v3db):
+    cfg, f, db, qs, ref_s, ref = fx_case("c0")
+    gdb = torch.from_numpy(db).cuda()
+    bad = gdb.clone()
+    bad[3, 2] = 65536
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.build_snapshot_fx(bad, cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows, f.codeword_rows)
+    s = v3db.build_snapshot_fx(gdb, cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows, f.codeword_rows)
+    gq = torch.from_numpy(qs).cuda()
+    badq = gq.clone()
+    badq[0, 0] = -65536
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.query_batch_fx(s, badq, cfg.nprobe, cfg.k)
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):   # int8 entry point on a fixed-point snapshot
+        v3db.query_batch(s, gq.to(torch.int8), cfg.nprobe, cfg.k)
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.witness_batch(s, gq.to(torch.int8), cfg.nprobe)
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.query_batch_fx(s, gq, cfg.nprobe, cfg.nprobe * cfg.L + 1)
+    from synth import generate
+    inp = generate(cfg)
+    s8 = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows,
+                             inp.codeword_rows)
+    assert s8.kind == v3db.KIND_INT8
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):   # fixed-point entry point on an int8 snapshot
+        v3db.query_batch_fx(s8, gq, cfg.nprobe, cfg.k)
+    with pytest.raises(v3db.V3DBError, match="EINVAL"):
+        v3db.encode_fixed_point(torch.zeros(4, device="cuda"), 0.0)
