@@ -3,6 +3,7 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--trace on|off]
   python bench.py --impl reference ...      (the CPU oracle on the host cores)
+  python bench.py --precision fx16 ...      (NEXT-1: the paper's 16-bit fixed point)
 
 One step = one v3db_query_batch over the config's whole query batch (Steps 1-5 of
 PAPER.md §4.2, all on the GPU, witness trace on by default), inputs resident in HBM.
@@ -26,7 +27,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth import generate, get_config, rank_queries  # noqa: E402
+from synth import generate, generate_float, get_config, rank_float_queries, rank_queries  # noqa: E402
 
 METRIC = "queries/sec and scan HBM GB/s (fraction of roofline) at nprobe, k, 1 B200"
 FALLBACK_HBM_GBS = 6650.0
@@ -41,6 +42,8 @@ def parse():
     p.add_argument("--config", default="c4")
     p.add_argument("--trace", default="on", choices=["on", "off"])
     p.add_argument("--algo", type=int, default=0, help="V3DB_SCAN_* (0 = auto)")
+    p.add_argument("--precision", default="int8", choices=["int8", "fx16"],
+                   help="int8 (BASELINE.json) or fx16 (the paper's 16-bit fixed point, NEXT-1)")
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -107,18 +110,19 @@ def code_bytes_per_slot(M: int, Ks: int) -> int:
     return math.ceil(M * max(1, math.ceil(math.log2(Ks))) / 8) if Ks > 1 else 0
 
 
-def algorithmic_scan_bytes(cfg, lists: np.ndarray, counts: np.ndarray, trace: bool) -> dict:
+def algorithmic_scan_bytes(cfg, lists: np.ndarray, counts: np.ndarray, trace: bool, fx: bool = False) -> dict:
     """Bytes the scan (Steps 3-5) must move per batch: per query the query
     vector, the codes of the VALID slots of its probed lists, the probed lists' counts, the
     top-k output, and with the trace the masked distance of every probed slot plus the probe
-    list/distance -- no credit for cross-query reuse."""
+    list/distance -- no credit for cross-query reuse.  fx: int32 coordinates, int64 distances."""
     valid = int(counts[lists].sum())
     Q = lists.shape[0]
     cb = code_bytes_per_slot(cfg.M, cfg.Ks)
-    per_batch = Q * cfg.D + valid * cb + Q * 4 * cfg.nprobe + Q * 8 * cfg.k
-    padded = Q * cfg.D + Q * cfg.nprobe * cfg.L * cb + Q * 4 * cfg.nprobe + Q * 8 * cfg.k
+    qb, w = (4, 8) if fx else (1, 4)
+    per_batch = Q * cfg.D * qb + valid * cb + Q * 4 * cfg.nprobe + Q * (4 + w) * cfg.k
+    padded = Q * cfg.D * qb + Q * cfg.nprobe * cfg.L * cb + Q * 4 * cfg.nprobe + Q * (4 + w) * cfg.k
     if trace:
-        tr = Q * (4 * cfg.nprobe * cfg.L + 8 * cfg.nprobe)
+        tr = Q * (w * cfg.nprobe * cfg.L + (4 + w) * cfg.nprobe)
         per_batch += tr
         padded += tr
     return {"valid": per_batch, "padded": padded, "valid_slots": valid}
@@ -189,17 +193,22 @@ def run_reference(args, rank: int, world: int):
         return
     import oracle
     cfg = get_config(args.config)
-    inp = generate(cfg)
+    fx = args.precision == "fx16"
+    inp = generate_float(cfg) if fx else generate(cfg)
     workers = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
-    snap = oracle.build_snapshot(inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    db, queries = inp.db, inp.queries
+    if fx:
+        db = oracle.encode_fixed_point(db, inp.v_max)
+        queries = oracle.encode_fixed_point(queries, inp.v_max)
+    snap = oracle.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
     build_s = time.perf_counter() - t0
     per_step = max(2.0, args.cpu_sample_seconds / max(1, args.steps + args.warmup) * workers)
     for _ in range(args.warmup):
-        time_oracle(snap, inp.queries, cfg, per_step, workers)
+        time_oracle(snap, queries, cfg, per_step, workers)
     tot_q, tot_t = 0, 0.0
     for _ in range(args.steps):
-        _, n, wall = time_oracle(snap, inp.queries, cfg, per_step, workers)
+        _, n, wall = time_oracle(snap, queries, cfg, per_step, workers)
         tot_q += n
         tot_t += wall
     qps = tot_q / tot_t
@@ -208,7 +217,8 @@ def run_reference(args, rank: int, world: int):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "D": cfg.D, "nlist": cfg.nlist, "L": cfg.L,
-                   "M": cfg.M, "Ks": cfg.Ks, "nprobe": cfg.nprobe, "k": cfg.k, "trace": args.trace},
+                   "M": cfg.M, "Ks": cfg.Ks, "nprobe": cfg.nprobe, "k": cfg.k, "trace": args.trace,
+                   "precision": args.precision},
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": workers, "kind": "oracle",
                          "sample": f"{tot_q} queries of the {cfg.name} batch over {args.steps} steps "
                                    f"(oracle snapshot build {build_s:.1f} s, not timed)"},
@@ -241,20 +251,37 @@ def main():
 
     cfg = get_config(args.config)
     trace = args.trace == "on"
-    inp = generate(cfg)
+    fx = args.precision == "fx16"
+    inp = generate_float(cfg) if fx else generate(cfg)
 
     # Snapshot build (offline index shaping; timed separately, not part of a step).
-    db = torch.from_numpy(inp.db).to(dev)
+    if fx:   # NEXT-1: float vectors -> 16-bit fixed point on the GPU (v_max over db and this rank's queries)
+        queries = rank_float_queries(cfg, rank)
+        v_max = float(max(np.abs(inp.db).max(), np.abs(queries).max()))
+        db = v3db.encode_fixed_point(torch.from_numpy(inp.db).to(dev), v_max)
+    else:
+        queries = rank_queries(cfg, rank)    # replicas: an independent batch per rank (weak scaling)
+        db = torch.from_numpy(inp.db).to(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    snap = v3db.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    build = v3db.build_snapshot_fx if fx else v3db.build_snapshot
+    snap = build(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
     build_s = time.perf_counter() - t0
     del db
     counts = v3db.snapshot_export(snap, v3db.FIELD_COUNTS)
 
-    queries = rank_queries(cfg, rank)        # replicas: an independent batch per rank (weak scaling)
-    q = torch.from_numpy(queries).to(dev)
-    out = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=True, device=dev)
+    if fx:
+        q = v3db.encode_fixed_point(torch.from_numpy(queries).to(dev), v_max)
+        out = v3db.alloc_outputs_fx(snap, cfg.Q, cfg.nprobe, cfg.k, trace=True, device=dev)
+
+        def query(o):
+            return v3db.query_batch_fx(snap, q, cfg.nprobe, cfg.k, out=o)
+    else:
+        q = torch.from_numpy(queries).to(dev)
+        out = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=True, device=dev)
+
+        def query(o):
+            return v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=o, algo=args.algo)
     if not trace:
         for key in ("trace_cand_dist",):
             out.pop(key)
@@ -264,7 +291,7 @@ def main():
     v3db.profile_enable(True)
     torch.cuda.cudart().cudaProfilerStart()   # ncu --profile-from-start off sees only the query path
     for _ in range(args.warmup):
-        v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out, algo=args.algo)
+        query(out)
     torch.cuda.synchronize()
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -277,7 +304,7 @@ def main():
         for i in range(args.steps):
             flush.zero_()                                   # L2 flush between timed steps (not timed)
             starts[i].record(stream)
-            v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out, algo=args.algo)
+            query(out)
             ends[i].record(stream)
             kt.append(v3db.profile_read())                  # per-kernel CUDA-event times of this step
         launches = v3db.kernel_launches() - l0
@@ -291,11 +318,11 @@ def main():
     out_off = {key: v for key, v in out.items() if key != "trace_cand_dist"}
     n_off = max(1, min(args.steps, 5))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_off)]
-    v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out_off, algo=args.algo)
+    query(out_off)
     for a_, b_ in ev:
         flush.zero_()
         a_.record(stream)
-        v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out_off, algo=args.algo)
+        query(out_off)
         b_.record(stream)
     torch.cuda.synchronize()
     off_ms = pdist.max_over_ranks(float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev])), world, dev)
@@ -305,18 +332,18 @@ def main():
     scan_ms = float(np.mean([b for _, b in kt]))
 
     lists = out["trace_lists"].cpu().numpy()
-    ab = algorithmic_scan_bytes(cfg, lists, counts, trace)
+    ab = algorithmic_scan_bytes(cfg, lists, counts, trace, fx)
     hbm, peak_src = peaks()
     achieved = ab["valid"] / (scan_ms / 1e3) / 1e9
-    traffic = load_traffic(cfg.name)
+    traffic = load_traffic(cfg.name + ("_fx16" if fx else ""))
 
     result = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "vs_baseline": None, "dtype": "int64" if fx else "int32", "data": "synthetic",
         "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "D": cfg.D, "nlist": cfg.nlist, "L": cfg.L,
                    "M": cfg.M, "Ks": cfg.Ks, "nprobe": cfg.nprobe, "k": cfg.k, "trace": args.trace,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "precision": args.precision, "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MiB write); snapshot codes exceed L2",
                    "algo": args.algo, "snapshot_build_s": round(build_s, 3)},
         "ms_per_step_median": float(np.median(step_ms)), "ms_per_step_best": float(np.min(step_ms)),
@@ -331,7 +358,30 @@ def main():
     }
 
     # End-to-end through the C ABI with HOST buffers (H2D queries, D2H outputs inside).
-    if not args.no_e2e:
+    if not args.no_e2e and fx:
+        # NEXT-1 through the Python binding's public calls: float32 queries H2D, GPU encoding,
+        # v3db_query_batch_fx, outputs D2H into pinned host buffers.
+        qh = torch.from_numpy(queries).pin_memory()
+        oh = v3db.alloc_outputs_fx(snap, cfg.Q, cfg.nprobe, cfg.k, trace=trace, device="cpu", pin=True)
+        od = v3db.alloc_outputs_fx(snap, cfg.Q, cfg.nprobe, cfg.k, trace=trace, device=dev)
+
+        def e2e_step():
+            qd = qh.to(dev, non_blocking=True)
+            v3db.query_batch_fx(snap, v3db.encode_fixed_point(qd, v_max), cfg.nprobe, cfg.k, out=od)
+            for key, v in od.items():
+                oh[key].copy_(v, non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_step()
+        n_e2e = max(1, min(args.steps, 5))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        e2e_s = pdist.max_over_ranks((time.perf_counter() - t0) / n_e2e, world, dev)
+        d2h = sum(v.numel() * v.element_size() for v in oh.values())
+        result["e2e"] = {"value": cfg.Q * world / e2e_s, "unit": "queries/s",
+                         "h2d_bytes_per_step": qh.numel() * 4, "d2h_bytes_per_step": d2h, "steps": n_e2e}
+    elif not args.no_e2e:
         qh = torch.from_numpy(queries).pin_memory()
         oh = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=trace, device="cpu", pin=True)
         v3db.query_batch_host(snap, qh, cfg.nprobe, cfg.k, oh)
@@ -353,8 +403,11 @@ def main():
                "ids": v3db.snapshot_export(snap, v3db.FIELD_IDS),
                "codes": v3db.snapshot_export(snap, v3db.FIELD_CODES), "counts": counts}
         workers = len(os.sched_getaffinity(0))
-        cq, n, wall = time_oracle(oracle_snapshot_from_arrays(arr), inp.queries, cfg, args.cpu_sample_seconds,
-                                  workers)
+        oq = inp.queries
+        if fx:
+            import oracle
+            oq = oracle.encode_fixed_point(queries, v_max)
+        cq, n, wall = time_oracle(oracle_snapshot_from_arrays(arr), oq, cfg, args.cpu_sample_seconds, workers)
         result["cpu_baseline"] = {"value": cq, "unit": "queries/s", "cores": workers, "kind": "oracle",
                                   "sample": f"{n} of {cfg.Q} {cfg.name} queries, Steps 1-5 on this snapshot's "
                                             f"arrays, {wall:.1f} s wall on {workers} processes"}

@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(256) dist_matrix_kernel(const int32_t* __restr
       double a[4], b[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        a[i] = As[kk][ty * 4 + i];
-        b[i] = Bs[kk][tx * 4 + i];
+        a[i] = As[kk][ty + 16 * i];
+        b[i] = Bs[kk][tx + 16 * i];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -107,13 +107,13 @@ __global__ void __launch_bounds__(256) dist_matrix_kernel(const int32_t* __restr
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + ty * 4 + i;
+    const int64_t r = r0 + ty + 16 * i;
     if (r >= n) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int c = c0 + tx * 4 + j;
+      const int c = c0 + tx + 16 * j;
       if (c >= nlist) continue;
-      out[r * nlist + c] = xn_s[ty * 4 + i] + mnorm[c] - 2 * static_cast<long long>(acc[i][j]);
+      out[r * nlist + c] = xn_s[ty + 16 * i] + mnorm[c] - 2 * static_cast<long long>(acc[i][j]);
     }
   }
 }
@@ -133,6 +133,126 @@ __global__ void __launch_bounds__(256) row_topk_kernel(const int64_t* __restrict
     const int i = b + lane;
     top.offer(i < nlist ? (static_cast<uint64_t>(row[i]) << sh) | static_cast<uint32_t>(i) : ~0ull);
   }
+  const uint64_t mask = (uint64_t(1) << sh) - 1;
+  top.store([&](int j, uint64_t key) {
+    out_idx[r * R + j] = static_cast<int32_t>(key & mask);
+    out_dist[r * R + j] = static_cast<int64_t>(key >> sh);
+  });
+}
+
+// Fused Step 1 + Step 2 (and the build ranking): a CTA owns 64 rows of X and sweeps every
+// centroid tile (64 x 64 distances, 4 x 4 per thread, dot products in double -- exact below
+// 2^53), then each warp feeds 8 rows' tile keys (d << sh | i) to those rows' ascending top-R lists
+// in shared memory.  The distance matrix never reaches HBM.  R <= 128.  With a centroid split
+// (gridDim.y = S > 1, small batches) CTA (x, y) sweeps centroid tiles [y * span, (y + 1) * span) and
+// writes its partial lists as keys to part [n][S][R]; fx_merge_kernel selects the final R.
+__global__ void __launch_bounds__(256, 3) fx_coarse_kernel(const int32_t* __restrict__ X, int64_t n, int dim,
+                                                        const int32_t* __restrict__ mu,
+                                                        const int64_t* __restrict__ mnorm, int nlist, int R, int sh,
+                                                        int span, int32_t* __restrict__ out_idx,
+                                                        int64_t* __restrict__ out_dist, uint64_t* __restrict__ part) {
+  __shared__ double AB[2][32][65];  // As [k][row], Bs [k][col]; reused as the key tile [64][65]
+  __shared__ long long xn_s[64];
+  extern __shared__ __align__(16) uint64_t dyn[];
+  auto& As = AB[0];
+  auto& Bs = AB[1];
+  uint64_t* T = dyn;                                   // [64][R]
+  uint64_t* tile = reinterpret_cast<uint64_t*>(&AB[0][0][0]);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4, warp = tid >> 5, lane = tid & 31;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+  for (int e = tid; e < 64 * R; e += 256) T[e] = ~0ull;
+  for (int rr = warp; rr < 64; rr += 8) {  // ||x_r||^2, exact
+    const int64_t r = r0 + rr;
+    long long acc = 0;
+    if (r < n)
+      for (int u = lane; u < dim; u += 32) {
+        const long long v = X[r * dim + u];
+        acc += v * v;
+      }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) xn_s[rr] = acc;
+  }
+  uint64_t thr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) thr[i] = ~0ull;
+  const int c_end = min(nlist, static_cast<int>(blockIdx.y + 1) * span);
+  for (int c0 = blockIdx.y * span; c0 < c_end; c0 += 64) {
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < dim; k0 += 32) {
+      for (int e = tid; e < 64 * 32; e += 256) {
+        const int rr = e >> 5, kk = e & 31;
+        const int64_t r = r0 + rr;
+        const int k = k0 + kk;
+        As[kk][rr] = (r < n && k < dim) ? static_cast<double>(X[r * dim + k]) : 0.0;
+        const int c = c0 + rr;
+        Bs[kk][rr] = (c < nlist && k < dim) ? static_cast<double>(mu[static_cast<int64_t>(c) * dim + k]) : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < 32; ++kk) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // rows ty + 16 i, columns tx + 16 j: conflict-free LDS.64
+          av[i] = As[kk][ty + 16 * i];
+          bv[i] = Bs[kk][tx + 16 * i];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = ty + 16 * i;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + tx + 16 * j;
+        uint64_t key = ~0ull;
+        if (r0 + rr < n && c < nlist) {
+          const long long dd = xn_s[rr] + mnorm[c] - 2 * static_cast<long long>(acc[i][j]);
+          key = (static_cast<uint64_t>(dd) << sh) | static_cast<uint32_t>(c);
+        }
+        tile[rr * 65 + tx + 16 * j] = key;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int rr = warp * 8 + i;
+      thr[i] = warp_offer(T + rr * R, R, thr[i], tile[rr * 65 + lane]);
+      thr[i] = warp_offer(T + rr * R, R, thr[i], tile[rr * 65 + 32 + lane]);
+    }
+    __syncthreads();  // `tile` aliases As / Bs
+  }
+  __syncthreads();
+  const uint64_t mask = (uint64_t(1) << sh) - 1;
+  for (int e = tid; e < 64 * R; e += 256) {
+    const int rr = e / R, j = e - rr * R;
+    const int64_t r = r0 + rr;
+    if (r >= n) continue;
+    if (part) {
+      part[(r * gridDim.y + blockIdx.y) * R + j] = T[e];
+    } else {
+      out_idx[r * R + j] = static_cast<int32_t>(T[e] & mask);
+      out_dist[r * R + j] = static_cast<int64_t>(T[e] >> sh);
+    }
+  }
+}
+
+// The R smallest of each row's S partial lists (warp per row).
+template <int KR>
+__global__ void __launch_bounds__(256) fx_merge_kernel(const uint64_t* __restrict__ part, int64_t n, int S, int R,
+                                                       int sh, int32_t* __restrict__ out_idx,
+                                                       int64_t* __restrict__ out_dist) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (r >= n) return;
+  WarpTopK<KR> top;
+  top.init(R);
+  const uint64_t* row = part + r * S * R;
+  for (int b = 0; b < S * R; b += 32) top.offer(b + lane < S * R ? row[b + lane] : ~0ull);
   const uint64_t mask = (uint64_t(1) << sh) - 1;
   top.store([&](int j, uint64_t key) {
     out_idx[r * R + j] = static_cast<int32_t>(key & mask);
@@ -189,6 +309,20 @@ __global__ void encode32_kernel(const int32_t* __restrict__ db, int64_t n, int d
   }
 }
 
+// codes_rot16 (see slot_dist_rot): byte s of group g of slot j = code of subspace g*16 + ((s + j) mod 16).
+__global__ void rotate16_kernel(const uint8_t* __restrict__ codes, int64_t slots, int L, int M,
+                                uint8_t* __restrict__ out) {
+  const int64_t total = slots * M;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t slot = e / M;
+    const int p = static_cast<int>(e - slot * M);
+    const int j = static_cast<int>(slot % L);
+    const int g = p >> 4, t = p & 15;
+    out[e] = codes[slot * M + g * 16 + ((t + j) & 15)];
+  }
+}
+
 // P_{i,j} = ||xhat||^2 + 2 <mu_i, xhat> (int64); 0 for padding.
 __global__ void slot_terms64_kernel(const int32_t* __restrict__ mu, const int32_t* __restrict__ cb,
                                     const uint8_t* __restrict__ codes, const int32_t* __restrict__ ids, int nlist, int L,
@@ -209,12 +343,96 @@ __global__ void slot_terms64_kernel(const int32_t* __restrict__ mu, const int32_
   }
 }
 
-// Steps 3-5 for one query per CTA (256 threads).
+// Offer one key per lane to the warp's ascending list T[0..R) (warp_offer) and track `mino`, the
+// smallest key that is NOT in the list afterwards: rejected keys and the entry a full list drops
+// on insertion (its old T[R-1] == thr).  Every key is offered exactly once and leaves only
+// through one of those two doors, so at the end min(mino over warps and merge) is the smallest
+// key outside the final top-k.
+__device__ __forceinline__ uint64_t offer_track(uint64_t* T, int R, uint64_t thr, uint64_t key, uint64_t& mino) {
+  if (key >= thr) mino = key < mino ? key : mino;
+  unsigned mask = __ballot_sync(0xffffffffu, key < thr);
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const uint64_t kk = __shfl_sync(0xffffffffu, key, src);
+    if (kk < thr) {
+      mino = thr < mino ? thr : mino;  // the entry the insertion drops
+      thr = warp_insert(T, R, kk);
+    } else {
+      mino = kk < mino ? kk : mino;
+    }
+  }
+  return thr;
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// Four table lookups of one 32-bit code word (subspaces m0..m0+3).
+template <int KS>
+__device__ __forceinline__ long long lut4(const int64_t* A, int Ks, int m0, uint32_t w) {
+  const int ks = KS ? KS : Ks;
+  return A[(m0 + 0) * ks + (w & 0xff)] + A[(m0 + 1) * ks + ((w >> 8) & 0xff)] +
+         A[(m0 + 2) * ks + ((w >> 16) & 0xff)] + A[(m0 + 3) * ks + (w >> 24)];
+}
+
+// D_{i,j} = d_i + P_{i,j} + sum_m A_q[m][c_m] (acc enters as d_i + P_{i,j}); codes read with the
+// widest aligned vector loads M allows.
+template <int MT, int KS>
+__device__ __forceinline__ long long slot_dist(const int64_t* A, const uint8_t* cp, int M, int Ks, long long acc) {
+  if constexpr (MT > 0 && MT % 16 == 0) {
+#pragma unroll
+    for (int v = 0; v < MT / 16; ++v) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(cp) + v);
+      acc += lut4<KS>(A, Ks, 16 * v, w.x) + lut4<KS>(A, Ks, 16 * v + 4, w.y) + lut4<KS>(A, Ks, 16 * v + 8, w.z) +
+             lut4<KS>(A, Ks, 16 * v + 12, w.w);
+    }
+  } else if constexpr (MT > 0 && MT % 8 == 0) {
+#pragma unroll
+    for (int v = 0; v < MT / 8; ++v) {
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(cp) + v);
+      acc += lut4<KS>(A, Ks, 8 * v, w.x) + lut4<KS>(A, Ks, 8 * v + 4, w.y);
+    }
+  } else {
+    for (int m = 0; m < M; ++m) acc += A[m * Ks + cp[m]];
+  }
+  return acc;
+}
+
+// Conflict-free variant (M % 16 == 0, Ks == 256): the table is stored A16[g][c][16] (row c of
+// group g holds the 16 subspaces g*16.. side by side, 8 B each = all 32 banks) and the codes
+// codes_rot16 hold, for slot j, byte s of group g = the code of subspace g*16 + ((s + j) mod 16).
+// Lane l (== j mod 32) at step s then reads column (l + s) mod 16: the 16 lanes of each half-warp
+// hit 16 distinct bank pairs whatever the codes are -- 2 wavefronts per LDS.64, the minimum.
+// rot8[s] = ((lane + s) & 15) * 8.
+template <int MT>
+__device__ __forceinline__ long long slot_dist_rot(const int64_t* A, const uint8_t* cp, const uint32_t (&rot8)[16],
+                                                   long long acc) {
+#pragma unroll
+  for (int g = 0; g < MT / 16; ++g) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(cp) + g);
+    const char* Ab = reinterpret_cast<const char*>(A + g * 256 * 16);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const uint32_t c = (ws[t >> 2] >> (8 * (t & 3))) & 0xffu;
+      acc += *reinterpret_cast<const long long*>(Ab + (c << 7) + rot8[t]);
+    }
+  }
+  return acc;
+}
+
+// Steps 3-5 for one query per CTA (8 warps).
 struct FxScanArgs {
   const int32_t* queries;
-  int dim, M, Ks, L, nprobe, k, sh5, cap;
+  int dim, M, Ks, L, nprobe, k, sh5;
   const int32_t* cb;         // [M][Ks][d]
-  const uint8_t* codes;      // canonical [nlist][L][M]
+  const uint8_t* codes;      // canonical [nlist][L][M] (ROT: codes_rot16, same shape)
   const int64_t* pterm;      // [nlist][L]
   const int32_t* ids;
   const int32_t* counts;
@@ -222,99 +440,176 @@ struct FxScanArgs {
   const int64_t* ldist;      // [nq][nprobe]
   int32_t* out_ids;
   int64_t* out_dist;
-  int64_t* dbuf;             // [nq][nprobe][L]: the trace (or scratch)
+  int64_t* trace;            // [nq][nprobe][L] or null
   int64_t* Ag;               // [nq][M][Ks] when the table does not fit in shared memory, else null
-  int* overflow;             // set when ties exceed the final buffer
 };
 
+// Shared memory: A [M][Ks] int64 (unless GA) | tops [W][k] u64 | resD [k] i64 | resI [k] i32 |
+// q [dim] i32 | wmin [1] u64.
+template <int MT, int KS, bool GA, bool ROT>
 __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int W = 8;
-  const int64_t qi = blockIdx.x;
-  int64_t* A = a.Ag ? a.Ag + qi * a.M * a.Ks : reinterpret_cast<int64_t*>(smem);           // [M][Ks]
-  uint64_t* tops = reinterpret_cast<uint64_t*>(smem + (a.Ag ? 0 : sizeof(int64_t) * a.M * a.Ks));  // [W][k]
-  int64_t* bd = reinterpret_cast<int64_t*>(tops + W * a.k);      // [cap] final candidates: D
-  int32_t* bi = reinterpret_cast<int32_t*>(bd + a.cap);          // [cap] item
-  int* s_cnt = bi + a.cap;
+  const int M = MT ? MT : a.M;
+  const int Ks = KS ? KS : a.Ks;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int d = a.dim / a.M, L = a.L, nprobe = a.nprobe;
+  const int64_t qi = blockIdx.x;
+  const int k = a.k, L = a.L, nprobe = a.nprobe, d = a.dim / M;
+  int64_t* A = GA ? a.Ag + qi * M * Ks : reinterpret_cast<int64_t*>(smem);
+  uint64_t* tops = reinterpret_cast<uint64_t*>(smem + (GA ? 0 : sizeof(int64_t) * M * Ks));
+  long long* resD = reinterpret_cast<long long*>(tops + W * k);
+  int32_t* resI = reinterpret_cast<int32_t*>(resD + k);
+  int32_t* qs = resI + k;
+  uint64_t* wmin = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(qs + a.dim) + 15) & ~uintptr_t(15));
   const int32_t* q = a.queries + qi * a.dim;
-  for (int e = tid; e < a.M * a.Ks; e += 256) {
-    const int m = e / a.Ks;
+  for (int u = tid; u < a.dim; u += 256) qs[u] = q[u];
+  for (int e = tid; e < W * k; e += 256) tops[e] = ~0ull;
+  __syncthreads();
+  // Step 3, factorised: A_q[m][c] = -2 <C_{m,c}, q^{(m)}>
+  for (int e = tid; e < M * Ks; e += 256) {
+    const int m = e / Ks;
     const int32_t* cw = a.cb + static_cast<int64_t>(e) * d;
     long long acc = 0;
-    for (int u = 0; u < d; ++u) acc += static_cast<long long>(cw[u]) * q[m * d + u];
-    A[e] = -2 * acc;
+    for (int u = 0; u < d; ++u) acc += static_cast<long long>(__ldg(cw + u)) * qs[m * d + u];
+    if constexpr (ROT) {
+      const int c = e - m * Ks;
+      A[((m >> 4) * Ks + c) * 16 + (m & 15)] = -2 * acc;
+    } else {
+      A[e] = -2 * acc;
+    }
   }
-  for (int e = tid; e < W * a.k; e += 256) tops[e] = ~0ull;
-  if (tid == 0) *s_cnt = 0;
   __syncthreads();
-  uint64_t* T = tops + warp * a.k;
-  uint64_t thr = ~0ull;
-  int64_t* drow = a.dbuf + qi * nprobe * static_cast<int64_t>(L);
+  // Steps 4-5: every probed slot, per-warp exact top-k on (D << sh5 | slot)
+  const int32_t* qlists = a.lists + qi * nprobe;
+  const int64_t* qld = a.ldist + qi * nprobe;
+  int64_t* trace = a.trace ? a.trace + qi * nprobe * static_cast<int64_t>(L) : nullptr;
+  uint64_t* T = tops + warp * k;
+  uint64_t thr = ~0ull, mino = ~0ull;
+  uint32_t rot8[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) rot8[t] = ((lane + t) & 15) << 3;
+  auto dist = [&](int64_t slot, long long acc) -> long long {
+    if constexpr (ROT) return slot_dist_rot<MT>(A, a.codes + slot * M, rot8, acc);
+    else return slot_dist<MT, KS>(A, a.codes + slot * M, M, Ks, acc);
+  };
   for (int rho = 0; rho < nprobe; ++rho) {
-    const int li = a.lists[qi * nprobe + rho];
-    const long long di = a.ldist[qi * nprobe + rho];
+    const int li = qlists[rho];
+    const long long di = qld[rho];
     const int cnt = a.counts[li];
     const int64_t base = static_cast<int64_t>(li) * L;
-    for (int j0 = warp * 32; j0 < L; j0 += W * 32) {
+    const int lim = trace ? L : cnt;
+    for (int j0 = warp * 32; j0 < lim; j0 += W * 32) {
       const int j = j0 + lane;
       long long D = kDMaxFx;
-      if (j < cnt) {
-        long long acc = di + a.pterm[base + j];
-        const uint8_t* cp = a.codes + (base + j) * a.M;
-        for (int m = 0; m < a.M; ++m) acc += A[m * a.Ks + cp[m]];
-        D = acc;
-      }
-      if (j < L) drow[static_cast<int64_t>(rho) * L + j] = D;
+      if (j < cnt) D = dist(base + j, di + __ldg(a.pterm + base + j));
+      if (trace && j < L) trace[static_cast<int64_t>(rho) * L + j] = D;
       const uint64_t key = j < cnt ? (static_cast<uint64_t>(D) << a.sh5) | static_cast<uint32_t>(rho * L + j) : ~0ull;
-      thr = warp_offer(T, a.k, thr, key);
+      thr = offer_track(T, k, thr, key, mino);
+    }
+  }
+  uint64_t* fin = reinterpret_cast<uint64_t*>(resD);  // the merged list (resD is free until resolved)
+  if (tid == 0) wmin[0] = ~0ull;
+  for (int e = tid; e < k; e += 256) fin[e] = ~0ull;
+  __syncthreads();
+  mino = warp_min_u64(mino);
+  if (lane == 0 && mino != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(wmin), mino);
+  // merge the W sorted lists by rank: the keys are distinct (slot in the low bits), so a key's
+  // final position is the number of smaller keys over all lists (binary search in each)
+  uint64_t lost = ~0ull;
+  for (int e = tid; e < W * k; e += 256) {
+    const uint64_t key = tops[e];
+    if (key == ~0ull) continue;
+    int rank = 0;
+    for (int w = 0; w < W; ++w) {
+      const uint64_t* Lw = tops + w * k;
+      int lo = 0, hi = k;  // first index with Lw[idx] >= key
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (Lw[mid] < key) lo = mid + 1;
+        else hi = mid;
+      }
+      rank += lo;
+    }
+    if (rank < k) fin[rank] = key;
+    else lost = key < lost ? key : lost;
+  }
+  lost = warp_min_u64(lost);
+  if (lane == 0 && lost != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(wmin), lost);
+  __syncthreads();
+  const uint64_t tau = fin[k - 1];
+  const uint64_t smallest_out = wmin[0];
+  const uint64_t slot_mask = (uint64_t(1) << a.sh5) - 1;
+  __syncthreads();  // everyone has read fin[k - 1] before it is resolved in place
+  // resolve the list entries: (D, item), in place (thread e reads fin[e] before writing resD[e])
+  for (int e = tid; e < k; e += 256) {
+    const uint64_t key = fin[e];
+    if (key != ~0ull) {
+      const int slot = static_cast<int>(key & slot_mask);
+      const int rho = slot / L;
+      resD[e] = static_cast<long long>(key >> a.sh5);
+      resI[e] = a.ids[static_cast<int64_t>(qlists[rho]) * L + (slot - rho * L)];
+    } else {
+      resD[e] = kDMaxFx;
+      resI[e] = -1;
+    }
+  }
+  __syncthreads();
+  const long long Dtau = static_cast<long long>(tau >> a.sh5);
+  // ties at the k-th distance that straddle the list boundary need the id order over all of them
+  const bool straddle = tau != ~0ull && smallest_out != ~0ull && (smallest_out >> a.sh5) == (tau >> a.sh5);
+  // list entries placed by their rank among themselves: the valid ones (a prefix of the key-sorted
+  // list) -- or, when ties straddle, those with D < Dtau (also a prefix)
+  int n_keep = 0;
+  for (int e = 0; e < k; ++e)
+    if (resI[e] != -1 && (!straddle || resD[e] < Dtau)) n_keep = e + 1;
+  for (int e = tid; e < n_keep; e += 256) {
+    const long long D = resD[e];
+    const int32_t id = resI[e];
+    int rank = 0;
+    for (int f = 0; f < n_keep; ++f) rank += (resD[f] < D || (resD[f] == D && resI[f] < id)) ? 1 : 0;
+    a.out_ids[qi * k + rank] = id;
+    a.out_dist[qi * k + rank] = D;
+  }
+  if (!straddle) {  // fewer than k valid candidates: (-1, d_max) tail
+    for (int r = n_keep + tid; r < k; r += 256) {
+      a.out_ids[qi * k + r] = -1;
+      a.out_dist[qi * k + r] = kDMaxFx;
+    }
+    return;
+  }
+  // Rare path: the need = k - n_keep smallest items among ALL candidates with D == Dtau
+  // (recomputed; per-warp top-need on item ids, then merged in warp 0).
+  const int need = k - n_keep;
+  __syncthreads();
+  for (int e = tid; e < W * k; e += 256) tops[e] = ~0ull;
+  __syncthreads();
+  thr = ~0ull;
+  uint64_t dummy = ~0ull;
+  for (int rho = 0; rho < nprobe; ++rho) {
+    const int li = qlists[rho];
+    const long long di = qld[rho];
+    const int cnt = a.counts[li];
+    const int64_t base = static_cast<int64_t>(li) * L;
+    for (int j0 = warp * 32; j0 < cnt; j0 += W * 32) {
+      const int j = j0 + lane;
+      uint64_t key = ~0ull;
+      if (j < cnt) {
+        const long long D = dist(base + j, di + __ldg(a.pterm + base + j));
+        if (D == Dtau) key = static_cast<uint32_t>(a.ids[base + j]);
+      }
+      thr = offer_track(T, need, thr, key, dummy);
     }
   }
   __syncthreads();
   if (warp == 0) {
     for (int w = 1; w < W; ++w)
-      for (int b = 0; b < a.k; b += 32) thr = warp_offer(tops, a.k, thr, b + lane < a.k ? tops[w * a.k + b + lane] : ~0ull);
+      for (int b = 0; b < need; b += 32)
+        thr = offer_track(tops, need, thr, b + lane < need ? tops[w * k + b + lane] : ~0ull, dummy);
   }
   __syncthreads();
-  // tau = D of the k-th smallest (D, slot) key: every candidate of the final top-k has D <= tau
-  const uint64_t kth = tops[a.k - 1];
-  const long long tau = kth == ~0ull ? kDMaxFx - 1 : static_cast<long long>(kth >> a.sh5);
-  __syncthreads();
-  // Step 5 in the exact (D, item) order among the candidates with D <= tau (R10)
-  for (int rho = 0; rho < nprobe; ++rho) {
-    const int li = a.lists[qi * nprobe + rho];
-    const int cnt = a.counts[li];
-    for (int j = tid; j < cnt; j += 256) {
-      const long long D = drow[static_cast<int64_t>(rho) * L + j];
-      if (D <= tau) {
-        const int pos = atomicAdd(s_cnt, 1);
-        if (pos < a.cap) {
-          bd[pos] = D;
-          bi[pos] = a.ids[static_cast<int64_t>(li) * L + j];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  const int n = *s_cnt;
-  if (n > a.cap) {
-    if (tid == 0) atomicExch(a.overflow, 1);
-    return;
-  }
-  for (int e = tid; e < n; e += 256) {
-    const long long D = bd[e];
-    const int32_t id = bi[e];
-    int rank = 0;
-    for (int f = 0; f < n; ++f) rank += (bd[f] < D || (bd[f] == D && bi[f] < id)) ? 1 : 0;
-    if (rank < a.k) {
-      a.out_ids[qi * a.k + rank] = id;
-      a.out_dist[qi * a.k + rank] = D;
-    }
-  }
-  for (int r = n + tid; r < a.k; r += 256) {
-    a.out_ids[qi * a.k + r] = -1;
-    a.out_dist[qi * a.k + r] = kDMaxFx;
+  for (int r = tid; r < need; r += 256) {
+    a.out_ids[qi * k + n_keep + r] = static_cast<int32_t>(tops[r]);
+    a.out_dist[qi * k + n_keep + r] = Dtau;
   }
 }
 
@@ -329,6 +624,13 @@ int bits_for(long double v) {
 // Key shifts: Step 2 keys d << sh2 | i need d < 2^(64-sh2); Step 5 keys D << sh5 | slot likewise.
 int fx_shift2(int dim) { return 64 - bits_for(static_cast<long double>(dim) * 131070.0L * 131070.0L); }
 int fx_shift5(int dim) { return 64 - bits_for(static_cast<long double>(dim) * 262140.0L * 262140.0L); }
+
+cudaError_t rotate_codes16(const uint8_t* codes, int64_t slots, int L, int M, uint8_t* out, cudaStream_t st) {
+  rotate16_kernel<<<static_cast<int>(std::min<int64_t>((slots * M + 255) / 256, 148 * 64)), 256, 0, st>>>(codes, slots,
+                                                                                                      L, M, out);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t abs_max32(const int32_t* x, int64_t n, int* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
@@ -360,6 +662,41 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
   if (n <= 0) return cudaSuccess;
   const int sh = fx_shift2(dim);
   if (sh < 1 || nlist > (1 << std::min(sh, 30))) return cudaErrorInvalidValue;
+  if (R <= 128) {
+    const size_t smem = sizeof(uint64_t) * 64 * R;
+    cudaError_t e = cudaFuncSetAttribute(fx_coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int ctiles = (nlist + 63) / 64;
+    for (int64_t lo = 0; lo < n; lo += int64_t(1) << 24) {  // grid.x chunks
+      const int64_t rows = std::min<int64_t>(int64_t(1) << 24, n - lo);
+      const int64_t rtiles = (rows + 63) / 64;
+      // centroid split so that small batches still fill 148 SMs x 2 CTAs (>= 2 tiles per CTA)
+      const int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((4 * 148 + rtiles - 1) / rtiles,
+                                                                             ctiles / 2)));
+      const int span = ((ctiles + S - 1) / S) * 64;
+      const int Sr = (nlist + span - 1) / span;
+      uint64_t* part = nullptr;
+      if (Sr > 1) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(uint64_t) * rows * Sr * R, st);
+        if (e != cudaSuccess) return e;
+      }
+      fx_coarse_kernel<<<dim3(static_cast<unsigned>(rtiles), Sr), 256, smem, st>>>(
+          X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span, out_idx + lo * R, out_dist + lo * R, part);
+      note_launch();
+      if (Sr > 1) {
+        dispatch_kr(R, [&]<int KR>() {
+          fx_merge_kernel<KR><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(part, rows, Sr, R, sh,
+                                                                                   out_idx + lo * R,
+                                                                                   out_dist + lo * R);
+        });
+        note_launch();
+        cudaFreeAsync(part, st);
+      }
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  // R > 128: the [rows x nlist] distance matrix in HBM, then a warp per row
   const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, (int64_t(1) << 30) / nlist));  // <= 8 GB
   int64_t* dm = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dm), sizeof(int64_t) * chunk * nlist, st);
@@ -394,6 +731,24 @@ cudaError_t fx_build_tail(const int32_t* db, int64_t n, int dim, const int32_t* 
   return cudaGetLastError();
 }
 
+template <int MT, int KS, bool GA, bool ROT = false>
+cudaError_t launch_scan_fx(const FxScanArgs& a, int64_t nq, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(scan_fx_kernel<MT, KS, GA, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  scan_fx_kernel<MT, KS, GA, ROT><<<static_cast<unsigned>(nq), 256, smem, st>>>(a);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int MT>
+cudaError_t launch_scan_fx_m(const FxScanArgs& a, int64_t nq, size_t smem, cudaStream_t st, bool rot) {
+  if constexpr (MT % 16 == 0) {
+    if (rot) return launch_scan_fx<MT, 256, false, true>(a, nq, smem, st);
+  }
+  return a.Ks == 256 ? launch_scan_fx<MT, 256, false>(a, nq, smem, st) : launch_scan_fx<MT, 0, false>(a, nq, smem, st);
+}
+
 cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k, const int32_t* lists,
                     const int64_t* ldist, int32_t* out_ids, int64_t* out_dist, int64_t* trace, cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
@@ -406,7 +761,6 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   a.nprobe = nprobe;
   a.k = k;
   a.sh5 = fx_shift5(s->dim);
-  a.cap = std::max(4096, 4 * k);
   a.cb = s->codebooks32;
   a.codes = s->codes;
   a.pterm = s->pterm64;
@@ -416,32 +770,38 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   a.ldist = ldist;
   a.out_ids = out_ids;
   a.out_dist = out_dist;
+  a.trace = trace;
+  a.Ag = nullptr;
   if (a.sh5 < 1 || static_cast<int64_t>(nprobe) * s->L > (int64_t(1) << std::min(a.sh5, 31))) return cudaErrorInvalidValue;
-  // the table A_q stays in shared memory up to 96 KiB (M * Ks <= 12288), else per-query scratch
   const size_t abytes = sizeof(int64_t) * s->M * s->Ks;
-  const bool a_smem = abytes <= 96 * 1024;
-  void* scratch = nullptr;
-  const size_t tb = trace ? 0 : sizeof(int64_t) * nq * nprobe * s->L;
-  const size_t ab = a_smem ? 0 : abytes * nq;
-  cudaError_t e = cudaMallocAsync(&scratch, tb + ab + 256, st);
-  if (e != cudaSuccess) return e;
-  a.overflow = static_cast<int*>(scratch);
-  a.dbuf = trace ? trace : reinterpret_cast<int64_t*>(static_cast<uint8_t*>(scratch) + 256);
-  a.Ag = a_smem ? nullptr : reinterpret_cast<int64_t*>(static_cast<uint8_t*>(scratch) + 256 + tb);
-  e = cudaMemsetAsync(a.overflow, 0, sizeof(int), st);
-  const size_t smem = (a_smem ? abytes : 0) + sizeof(uint64_t) * 8 * k + (8 + 4) * static_cast<size_t>(a.cap) + 16;
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(scan_fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) {
-    scan_fx_kernel<<<static_cast<unsigned>(nq), 256, smem, st>>>(a);
-    note_launch();
-    e = cudaGetLastError();
+  const size_t rest = sizeof(uint64_t) * 8 * k + 12 * static_cast<size_t>(k) + 4 * static_cast<size_t>(s->dim + 4) + 16 + 64;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const bool a_smem = abytes + rest <= static_cast<size_t>(optin);
+  if (!a_smem) {  // the table in per-query global scratch
+    void* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, abytes * nq, st);
+    if (e != cudaSuccess) return e;
+    a.Ag = static_cast<int64_t*>(scratch);
+    e = launch_scan_fx<0, 0, true>(a, nq, rest, st);  // canonical codes
+    cudaFreeAsync(scratch, st);
+    return e;
   }
-  int ovf = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&ovf, a.overflow, sizeof(int), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFreeAsync(scratch, st);
-  if (e == cudaSuccess && ovf) return cudaErrorNotSupported;  // ties beyond the final buffer
-  return e;
+  const size_t smem = abytes + rest;
+  const bool rot = s->codes_rot16 != nullptr;  // M % 16 == 0, Ks == 256 (set at build)
+  if (rot) a.codes = s->codes_rot16;
+  switch (s->M) {
+    case 8: return launch_scan_fx_m<8>(a, nq, smem, st, false);
+    case 16: return launch_scan_fx_m<16>(a, nq, smem, st, rot);
+    case 24: return launch_scan_fx_m<24>(a, nq, smem, st, false);
+    case 32: return launch_scan_fx_m<32>(a, nq, smem, st, rot);
+    case 64: return launch_scan_fx_m<64>(a, nq, smem, st, rot);
+    case 96: return launch_scan_fx_m<96>(a, nq, smem, st, rot);
+    default:
+      a.codes = s->codes;  // the generic loop reads the canonical layout
+      return launch_scan_fx<0, 0, false>(a, nq, smem, st);
+  }
 }
 
 }  // namespace v3db

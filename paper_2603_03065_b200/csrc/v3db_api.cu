@@ -72,6 +72,7 @@ void free_snapshot(v3db_snapshot* s) {
   cudaFree(s->cnorm64);
   cudaFree(s->codebooks32);
   cudaFree(s->pterm64);
+  cudaFree(s->codes_rot16);
   delete s;
 }
 
@@ -697,6 +698,10 @@ int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nl
   V3DB_CUDA(cudaMemsetAsync(s->codes, 0, static_cast<size_t>(slots) * m, st));
   V3DB_CUDA(v3db::fx_build_tail(db, n, dim, s->centroids32, s->list_of, d_pos.p, m, ks, d_cwrows.p, nlist, L,
                                 s->codebooks32, s->codes, s->ids, s->pterm64, st));  // B3-B6
+  if (m % 16 == 0 && ks == 256 && !getenv("V3DB_FX_NOROT")) {  // conflict-free scan layout
+    V3DB_CUDA(cudaMalloc(&s->codes_rot16, static_cast<size_t>(slots) * m));
+    V3DB_CUDA(v3db::rotate_codes16(s->codes, slots, L, m, s->codes_rot16, st));
+  }
   V3DB_CUDA(cudaStreamSynchronize(st));
   s->total_valid = n;
   guard.s = nullptr;

@@ -47,6 +47,7 @@ struct v3db_snapshot {
   int64_t* cnorm64 = nullptr;      // [nlist]
   int32_t* codebooks32 = nullptr;  // [M][Ks][d]
   int64_t* pterm64 = nullptr;      // [nlist][L]
+  uint8_t* codes_rot16 = nullptr;  // [nlist][L][M], per-slot rotated in groups of 16 (M % 16 == 0, Ks == 256)
 };
 
 namespace v3db {
@@ -162,6 +163,7 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
 cudaError_t fx_build_tail(const int32_t* db, int64_t n, int dim, const int32_t* mu, const int32_t* list_of,
                           const int32_t* flat_pos, int M, int Ks, const int32_t* codeword_rows, int nlist, int L,
                           int32_t* cb, uint8_t* codes, int32_t* ids, int64_t* pterm, cudaStream_t st);
+cudaError_t rotate_codes16(const uint8_t* codes, int64_t slots, int L, int M, uint8_t* out, cudaStream_t st);
 cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k, const int32_t* lists,
                     const int64_t* ldist, int32_t* out_ids, int64_t* out_dist, int64_t* trace, cudaStream_t st);
 

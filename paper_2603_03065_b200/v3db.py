@@ -122,24 +122,38 @@ def build_snapshot_fx(db: torch.Tensor, nlist: int, list_cap: int, m: int, ks: i
 
 
 def query_batch_fx(s: Snapshot, queries: torch.Tensor, nprobe: int, k: int, trace: bool = True,
-                   stream=None) -> dict:
+                   out: dict | None = None, stream=None) -> dict:
     """v3db_query_batch_fx: Steps 1-5 on a fixed-point snapshot.  out_ids (int32) / out_dist (int64)
     [nq][k]; with trace, trace_lists (int32) / trace_list_dist (int64) [nq][nprobe] and
     trace_cand_dist (int64) [nq][nprobe][L]."""
     lib = _lib.load()
     nq = queries.shape[0]
     _need(queries, torch.int32, "cuda", (nq, s.dim), "queries")
-    dev = queries.device
-    out = {"out_ids": torch.empty((nq, k), dtype=torch.int32, device=dev),
-           "out_dist": torch.empty((nq, k), dtype=torch.int64, device=dev)}
-    if trace:
-        out["trace_lists"] = torch.empty((nq, nprobe), dtype=torch.int32, device=dev)
-        out["trace_list_dist"] = torch.empty((nq, nprobe), dtype=torch.int64, device=dev)
-        out["trace_cand_dist"] = torch.empty((nq, nprobe, s.list_cap), dtype=torch.int64, device=dev)
+    if out is None:
+        out = alloc_outputs_fx(s, nq, nprobe, k, trace, device=queries.device)
+    _need(out["out_ids"], torch.int32, "cuda", (nq, k), "out_ids")
+    _need(out["out_dist"], torch.int64, "cuda", (nq, k), "out_dist")
+    for key, dt, shape in (("trace_lists", torch.int32, (nq, nprobe)), ("trace_list_dist", torch.int64, (nq, nprobe)),
+                           ("trace_cand_dist", torch.int64, (nq, nprobe, s.list_cap))):
+        if out.get(key) is not None:
+            _need(out[key], dt, "cuda", shape, key)
     _lib.check(lib.v3db_query_batch_fx(s.handle, _ptr(queries), nq, nprobe, k, _ptr(out["out_ids"]),
                                        _ptr(out["out_dist"]), _ptr(out.get("trace_lists")),
                                        _ptr(out.get("trace_list_dist")), _ptr(out.get("trace_cand_dist")),
                                        _stream_ptr(stream)))
+    return out
+
+
+def alloc_outputs_fx(s: Snapshot, nq: int, nprobe: int, k: int, trace: bool = True, device="cuda",
+                     pin=False) -> dict:
+    """Output buffers of query_batch_fx (int32 ids / lists, int64 distances)."""
+    def t(shape, dt):
+        return torch.empty(shape, dtype=dt, device=device, pin_memory=(device == "cpu" and pin))
+    out = {"out_ids": t((nq, k), torch.int32), "out_dist": t((nq, k), torch.int64)}
+    if trace:
+        out["trace_lists"] = t((nq, nprobe), torch.int32)
+        out["trace_list_dist"] = t((nq, nprobe), torch.int64)
+        out["trace_cand_dist"] = t((nq, nprobe, s.list_cap), torch.int64)
     return out
 
 

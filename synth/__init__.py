@@ -8,4 +8,4 @@ indices are passed to both the oracle and the C-ABI, so no RNG is shared across
 languages (SURVEY.md §8(c) reading R3).
 """
 from .configs import CONFIGS, Config, get_config  # noqa: F401
-from .generate import FloatInputs, Inputs, generate, generate_float, rank_queries  # noqa: F401
+from .generate import FloatInputs, Inputs, generate, generate_float, rank_float_queries, rank_queries  # noqa: F401

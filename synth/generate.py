@@ -158,3 +158,11 @@ def generate_float(cfg: Config) -> FloatInputs:
     v_max = float(max(np.abs(db).max(), np.abs(q).max()))
     cent, code = sample_rows(cfg)
     return FloatInputs(cfg, db, q, v_max, cent, code)
+
+
+def rank_float_queries(cfg: Config, rank: int) -> np.ndarray:
+    """Float32 counterpart of rank_queries (NEXT-1 replicas): rank 0 the config's own float queries,
+    rank r > 0 an independent draw (stream 100 + r)."""
+    if rank == 0:
+        return generate_float(cfg).queries
+    return gen_float_vectors(cfg, STREAM_Q_RANK + rank, cfg.Q)

@@ -186,3 +186,33 @@ def test_fx_errors(v3db):
         v3db.query_batch_fx(s8, gq, cfg.nprobe, cfg.k)
     with pytest.raises(v3db.V3DBError, match="EINVAL"):
         v3db.encode_fixed_point(torch.zeros(4, device="cuda"), 0.0)
+
+
+def test_fx_heavy_ties_and_wide_nprobe(v3db):
+    """Binary coordinates scaled to the fixed-point range: distances take few values, so ties at
+    the k-th distance straddle the per-warp lists (the exact id re-selection path); nprobe = 150 >
+    128 also takes the two-kernel Step-1/2 path (distance matrix + per-row top-R)."""
+    rng = np.random.default_rng(24)
+    N, D, nlist, L, M, Ks = 3000, 8, 200, 40, 4, 16
+    db = (rng.integers(0, 2, size=(N, D)) * 65535).astype(np.int32)
+    qs = (rng.integers(0, 2, size=(41, D)) * 65535).astype(np.int32)
+    cent = rng.choice(N, nlist, replace=False)
+    code = np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)])
+    run_int32_case(v3db, db, qs, nlist, L, M, Ks, 3, 25, cent, code)
+    run_int32_case(v3db, db, qs, nlist, L, M, Ks, 150, 333, cent, code)
+
+
+@pytest.mark.parametrize("M,d,Ks", [(24, 4, 256), (48, 2, 256), (16, 8, 256), (32, 4, 64), (96, 8, 256),
+                                    (64, 2, 256), (8, 4, 256)])
+def test_fx_scan_shapes(v3db, M, d, Ks):
+    """Every scan instantiation: M = 8 / 24 (8-byte code loads), 48 (generic loop over the canonical
+    codes although a rotated copy exists), 16 / 64 / 96 (the conflict-free rotated table, M % 16 == 0
+    and Ks = 256), Ks = 64 (runtime table stride, canonical codes)."""
+    rng = np.random.default_rng(25 + M)
+    D = M * d
+    N, nlist, L = 3000, 24, 160
+    centres = rng.integers(-40000, 40000, size=(6, D))
+    db = np.clip(centres[rng.integers(0, 6, N)] + rng.integers(-9000, 9000, size=(N, D)), -65535, 65535).astype(np.int32)
+    qs = np.clip(centres[rng.integers(0, 6, 70)] + rng.integers(-9000, 9000, size=(70, D)), -65535, 65535).astype(np.int32)
+    run_int32_case(v3db, db, qs, nlist, L, M, Ks, 5, 37, rng.choice(N, nlist, replace=False),
+                   np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
