@@ -365,6 +365,81 @@ __device__ __forceinline__ uint64_t offer_track(uint64_t* T, int R, uint64_t thr
   return thr;
 }
 
+// offer_track with a CTA-wide admission bound: *gthr is the smallest k-th key over all warps'
+// lists -- a valid bound for every warp, since the warp owning it holds k smaller keys, so no key
+// at or above it can be in the final top-k.  Keys at or above it are rejected (and tracked like
+// any other rejection); a warp whose own k-th key drops publishes it with atomicMin.
+__device__ __forceinline__ uint64_t offer_shared(uint64_t* T, int R, uint64_t thr, uint64_t key, uint64_t& mino,
+                                                 unsigned long long* gthr) {
+  // lane 0's read, broadcast: lanes not yet reconverged could otherwise read different values
+  uint64_t eff = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile unsigned long long*>(gthr), 0);
+  eff = thr < eff ? thr : eff;
+  if (key >= eff) mino = key < mino ? key : mino;
+  unsigned mask = __ballot_sync(0xffffffffu, key < eff);
+  if (!mask) return thr;
+  const uint64_t old = thr;
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const uint64_t kk = __shfl_sync(0xffffffffu, key, src);
+    if (kk < eff) {
+      mino = thr < mino ? thr : mino;  // the entry the insertion drops
+      thr = warp_insert(T, R, kk);
+      eff = thr < eff ? thr : eff;
+    } else {
+      mino = kk < mino ? kk : mino;
+    }
+  }
+  if (thr < old && (threadIdx.x & 31) == 0) atomicMin(gthr, static_cast<unsigned long long>(thr));
+  return thr;
+}
+
+// Buffered per-warp top-k (k <= 256): keys below the admission bound are appended to the warp's
+// buffer T[0..cap) (ballot + prefix count, no per-key insertion); when fewer than 32 free slots
+// remain, the buffer is sorted (warp bitonic network) and cut back to its k smallest -- the cut
+// keys are tracked like rejections (mino) and T[k-1] becomes the warp's bound.
+__device__ __forceinline__ uint64_t warp_compact(uint64_t* T, int cap, int k, int& bcnt, uint64_t& mino) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  for (int i = bcnt + lane; i < cap; i += 32) T[i] = ~0ull;
+  __syncwarp();
+  for (int size = 2; size <= cap; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < (cap >> 1); i += 32) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const uint64_t x = T[lo], y = T[hi];
+        if ((x > y) == ((lo & size) == 0)) {
+          T[lo] = y;
+          T[hi] = x;
+        }
+      }
+      __syncwarp();
+    }
+  const uint64_t cut = T[k];  // cap > k: the smallest key cut off
+  mino = cut < mino ? cut : mino;
+  bcnt = bcnt < k ? bcnt : k;
+  return bcnt >= k ? T[k - 1] : ~0ull;
+}
+
+__device__ __forceinline__ uint64_t offer_buffered(uint64_t* T, int cap, int k, uint64_t thr, uint64_t key,
+                                                   uint64_t& mino, int& bcnt, unsigned long long* gthr) {
+  uint64_t eff = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile unsigned long long*>(gthr), 0);
+  eff = thr < eff ? thr : eff;
+  const bool pass = key < eff;
+  if (!pass) mino = key < mino ? key : mino;
+  const unsigned bal = __ballot_sync(0xffffffffu, pass);
+  if (!bal) return thr;
+  const int lane = threadIdx.x & 31;
+  if (pass) T[bcnt + __popc(bal & ((1u << lane) - 1))] = key;
+  bcnt += __popc(bal);
+  if (bcnt > cap - 32) {
+    const uint64_t old = thr;
+    thr = warp_compact(T, cap, k, bcnt, mino);
+    if (thr < old && lane == 0) atomicMin(gthr, static_cast<unsigned long long>(thr));
+  }
+  return thr;
+}
+
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
   for (int o = 16; o > 0; o >>= 1) {
     const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
@@ -427,10 +502,11 @@ __device__ __forceinline__ long long slot_dist_rot(const int64_t* A, const uint8
   return acc;
 }
 
-// Steps 3-5 for one query per CTA (8 warps).
+// Steps 3-5 for one query per CTA of NW = 8 warps (16 measured slower: C4 16.7 -> 17.3 ms).
 struct FxScanArgs {
   const int32_t* queries;
   int dim, M, Ks, L, nprobe, k, sh5;
+  int cap;                   // per-warp list stride: the buffer size (k <= 256, buffered) or k
   const int32_t* cb;         // [M][Ks][d]
   const uint8_t* codes;      // canonical [nlist][L][M] (ROT: codes_rot16, same shape)
   const int64_t* pterm;      // [nlist][L]
@@ -446,10 +522,10 @@ struct FxScanArgs {
 
 // Shared memory: A [M][Ks] int64 (unless GA) | tops [W][k] u64 | resD [k] i64 | resI [k] i32 |
 // q [dim] i32 | wmin [1] u64.
-template <int MT, int KS, bool GA, bool ROT>
-__global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
+template <int MT, int KS, bool GA, bool ROT, int NW>
+__global__ void __launch_bounds__(32 * NW) scan_fx_kernel(const FxScanArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int W = 8;
+  constexpr int W = NW, NT = 32 * W;
   const int M = MT ? MT : a.M;
   const int Ks = KS ? KS : a.Ks;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -457,16 +533,19 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
   const int k = a.k, L = a.L, nprobe = a.nprobe, d = a.dim / M;
   int64_t* A = GA ? a.Ag + qi * M * Ks : reinterpret_cast<int64_t*>(smem);
   uint64_t* tops = reinterpret_cast<uint64_t*>(smem + (GA ? 0 : sizeof(int64_t) * M * Ks));
-  long long* resD = reinterpret_cast<long long*>(tops + W * k);
+  const int S = a.cap;  // per-warp list stride
+  const bool buffered = S > k;
+  long long* resD = reinterpret_cast<long long*>(tops + W * S);
   int32_t* resI = reinterpret_cast<int32_t*>(resD + k);
   int32_t* qs = resI + k;
   uint64_t* wmin = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(qs + a.dim) + 15) & ~uintptr_t(15));
   const int32_t* q = a.queries + qi * a.dim;
-  for (int u = tid; u < a.dim; u += 256) qs[u] = q[u];
-  for (int e = tid; e < W * k; e += 256) tops[e] = ~0ull;
+  for (int u = tid; u < a.dim; u += NT) qs[u] = q[u];
+  for (int e = tid; e < W * S; e += NT) tops[e] = ~0ull;
+  if (tid == 0) wmin[1] = ~0ull;  // gthr
   __syncthreads();
   // Step 3, factorised: A_q[m][c] = -2 <C_{m,c}, q^{(m)}>
-  for (int e = tid; e < M * Ks; e += 256) {
+  for (int e = tid; e < M * Ks; e += NT) {
     const int m = e / Ks;
     const int32_t* cw = a.cb + static_cast<int64_t>(e) * d;
     long long acc = 0;
@@ -483,8 +562,9 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
   const int32_t* qlists = a.lists + qi * nprobe;
   const int64_t* qld = a.ldist + qi * nprobe;
   int64_t* trace = a.trace ? a.trace + qi * nprobe * static_cast<int64_t>(L) : nullptr;
-  uint64_t* T = tops + warp * k;
+  uint64_t* T = tops + warp * S;
   uint64_t thr = ~0ull, mino = ~0ull;
+  int bcnt = 0;
   uint32_t rot8[16];
 #pragma unroll
   for (int t = 0; t < 16; ++t) rot8[t] = ((lane + t) & 15) << 3;
@@ -504,24 +584,26 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
       if (j < cnt) D = dist(base + j, di + __ldg(a.pterm + base + j));
       if (trace && j < L) trace[static_cast<int64_t>(rho) * L + j] = D;
       const uint64_t key = j < cnt ? (static_cast<uint64_t>(D) << a.sh5) | static_cast<uint32_t>(rho * L + j) : ~0ull;
-      thr = offer_track(T, k, thr, key, mino);
+      if (buffered) thr = offer_buffered(T, S, k, thr, key, mino, bcnt, reinterpret_cast<unsigned long long*>(wmin + 1));
+      else thr = offer_shared(T, k, thr, key, mino, reinterpret_cast<unsigned long long*>(wmin + 1));
     }
   }
+  if (buffered) warp_compact(T, S, k, bcnt, mino);  // T[0..k): the warp's k smallest, ascending
   uint64_t* fin = reinterpret_cast<uint64_t*>(resD);  // the merged list (resD is free until resolved)
   if (tid == 0) wmin[0] = ~0ull;
-  for (int e = tid; e < k; e += 256) fin[e] = ~0ull;
+  for (int e = tid; e < k; e += NT) fin[e] = ~0ull;
   __syncthreads();
   mino = warp_min_u64(mino);
   if (lane == 0 && mino != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(wmin), mino);
   // merge the W sorted lists by rank: the keys are distinct (slot in the low bits), so a key's
   // final position is the number of smaller keys over all lists (binary search in each)
   uint64_t lost = ~0ull;
-  for (int e = tid; e < W * k; e += 256) {
-    const uint64_t key = tops[e];
+  for (int e = tid; e < W * k; e += NT) {
+    const uint64_t key = tops[(e / k) * S + e % k];
     if (key == ~0ull) continue;
     int rank = 0;
     for (int w = 0; w < W; ++w) {
-      const uint64_t* Lw = tops + w * k;
+      const uint64_t* Lw = tops + w * S;
       int lo = 0, hi = k;  // first index with Lw[idx] >= key
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -541,7 +623,7 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
   const uint64_t slot_mask = (uint64_t(1) << a.sh5) - 1;
   __syncthreads();  // everyone has read fin[k - 1] before it is resolved in place
   // resolve the list entries: (D, item), in place (thread e reads fin[e] before writing resD[e])
-  for (int e = tid; e < k; e += 256) {
+  for (int e = tid; e < k; e += NT) {
     const uint64_t key = fin[e];
     if (key != ~0ull) {
       const int slot = static_cast<int>(key & slot_mask);
@@ -562,7 +644,7 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
   int n_keep = 0;
   for (int e = 0; e < k; ++e)
     if (resI[e] != -1 && (!straddle || resD[e] < Dtau)) n_keep = e + 1;
-  for (int e = tid; e < n_keep; e += 256) {
+  for (int e = tid; e < n_keep; e += NT) {
     const long long D = resD[e];
     const int32_t id = resI[e];
     int rank = 0;
@@ -571,7 +653,7 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
     a.out_dist[qi * k + rank] = D;
   }
   if (!straddle) {  // fewer than k valid candidates: (-1, d_max) tail
-    for (int r = n_keep + tid; r < k; r += 256) {
+    for (int r = n_keep + tid; r < k; r += NT) {
       a.out_ids[qi * k + r] = -1;
       a.out_dist[qi * k + r] = kDMaxFx;
     }
@@ -581,7 +663,7 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
   // (recomputed; per-warp top-need on item ids, then merged in warp 0).
   const int need = k - n_keep;
   __syncthreads();
-  for (int e = tid; e < W * k; e += 256) tops[e] = ~0ull;
+  for (int e = tid; e < W * k; e += NT) tops[e] = ~0ull;
   __syncthreads();
   thr = ~0ull;
   uint64_t dummy = ~0ull;
@@ -597,7 +679,7 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
         const long long D = dist(base + j, di + __ldg(a.pterm + base + j));
         if (D == Dtau) key = static_cast<uint32_t>(a.ids[base + j]);
       }
-      thr = offer_track(T, need, thr, key, dummy);
+      thr = offer_track(tops + warp * k, need, thr, key, dummy);
     }
   }
   __syncthreads();
@@ -607,7 +689,7 @@ __global__ void __launch_bounds__(256) scan_fx_kernel(const FxScanArgs a) {
         thr = offer_track(tops, need, thr, b + lane < need ? tops[w * k + b + lane] : ~0ull, dummy);
   }
   __syncthreads();
-  for (int r = tid; r < need; r += 256) {
+  for (int r = tid; r < need; r += NT) {
     a.out_ids[qi * k + n_keep + r] = static_cast<int32_t>(tops[r]);
     a.out_dist[qi * k + n_keep + r] = Dtau;
   }
@@ -731,12 +813,17 @@ cudaError_t fx_build_tail(const int32_t* db, int64_t n, int dim, const int32_t* 
   return cudaGetLastError();
 }
 
+// smem = table bytes (0 when GA) + fx_rest(8).
+size_t fx_rest(const FxScanArgs& a, int nw) {
+  return sizeof(uint64_t) * nw * a.cap + 12 * static_cast<size_t>(a.k) + 4 * static_cast<size_t>(a.dim + 4) + 16 + 64;
+}
+
 template <int MT, int KS, bool GA, bool ROT = false>
-cudaError_t launch_scan_fx(const FxScanArgs& a, int64_t nq, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(scan_fx_kernel<MT, KS, GA, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+cudaError_t launch_scan_fx(const FxScanArgs& a, int64_t nq, size_t smem8, cudaStream_t st) {
+  auto kern = scan_fx_kernel<MT, KS, GA, ROT, 8>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem8));
   if (e != cudaSuccess) return e;
-  scan_fx_kernel<MT, KS, GA, ROT><<<static_cast<unsigned>(nq), 256, smem, st>>>(a);
+  kern<<<static_cast<unsigned>(nq), 256, smem8, st>>>(a);
   note_launch();
   return cudaGetLastError();
 }
@@ -761,6 +848,11 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   a.nprobe = nprobe;
   a.k = k;
   a.sh5 = fx_shift5(s->dim);
+  a.cap = k;
+  if (k <= 256) {  // buffered per-warp top-k: a power of two >= 2k + 32
+    a.cap = 64;
+    while (a.cap < 2 * k + 32) a.cap <<= 1;
+  }
   a.cb = s->codebooks32;
   a.codes = s->codes;
   a.pterm = s->pterm64;
@@ -774,7 +866,7 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   a.Ag = nullptr;
   if (a.sh5 < 1 || static_cast<int64_t>(nprobe) * s->L > (int64_t(1) << std::min(a.sh5, 31))) return cudaErrorInvalidValue;
   const size_t abytes = sizeof(int64_t) * s->M * s->Ks;
-  const size_t rest = sizeof(uint64_t) * 8 * k + 12 * static_cast<size_t>(k) + 4 * static_cast<size_t>(s->dim + 4) + 16 + 64;
+  const size_t rest = fx_rest(a, 8);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);

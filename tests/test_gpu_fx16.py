@@ -137,10 +137,11 @@ def test_fx_ties_and_fewer_than_k(v3db):
 
 
 def test_fx_global_table_and_greedy_overflow(v3db):
-    """M * Ks = 16384 (> 96 KiB of int64 table: the per-query table lives in global scratch) and a
-    tight capacity with nlist > 64, so some vectors find all 64 ranked lists full (exact fallback)."""
+    """M * Ks = 32768 (a 256 KiB int64 table does not fit in shared memory: the per-query table lives
+    in global scratch) and a tight capacity with nlist > 64, so some vectors find all 64 ranked
+    lists full (exact fallback)."""
     rng = np.random.default_rng(23)
-    N, D, nlist, L, M, Ks = 4000, 128, 80, 52, 64, 256
+    N, D, nlist, L, M, Ks = 4000, 128, 80, 52, 128, 256
     centres = rng.integers(-30000, 30000, size=(3, D))
     db = (centres[rng.integers(0, 3, N)] + rng.integers(-3000, 3000, size=(N, D))).astype(np.int32)
     qs = (centres[rng.integers(0, 3, 25)] + rng.integers(-3000, 3000, size=(25, D))).astype(np.int32)
