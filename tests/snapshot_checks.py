@@ -3,8 +3,9 @@ B1-B6, pins P7/P8) -- test infrastructure, used where the oracle's own build is 
 import numpy as np
 
 
-def check_snapshot(cfg, inp, snap, rng, n_replay=150, n_slots=400):
-    """B1-B6 checked against the rules themselves (not against a second implementation)."""
+def check_snapshot(cfg, inp, snap, rng, n_replay=150, n_slots=400, fx=False):
+    """B1-B6 checked against the rules themselves (not against a second implementation).
+    fx: the 16-bit fixed-point variant (int32 coordinates, unsaturated codewords, R18/R19)."""
     db = inp.db
     N, D = db.shape
     L, M = cfg.L, cfg.M
@@ -27,7 +28,8 @@ def check_snapshot(cfg, inp, snap, rng, n_replay=150, n_slots=400):
     cw = inp.codeword_rows
     for m in range(M):
         r = db[cw[m], m * d:(m + 1) * d].astype(np.int64) - mu[list_of[cw[m]], m * d:(m + 1) * d].astype(np.int64)
-        assert np.array_equal(cb[m], np.clip(r, -127, 127).astype(np.int8)), m
+        exp = r.astype(np.int32) if fx else np.clip(r, -127, 127).astype(np.int8)
+        assert cb.dtype == exp.dtype and np.array_equal(cb[m], exp), m
     # B2 (R1, R2) replayed for sampled vectors: every list ranked before t's list by (e, i) already
     # held L members with id < t, and t's list held fewer than L
     mu64 = mu.astype(np.int64)

@@ -217,3 +217,38 @@ def test_fx_scan_shapes(v3db, M, d, Ks):
     qs = np.clip(centres[rng.integers(0, 6, 70)] + rng.integers(-9000, 9000, size=(70, D)), -65535, 65535).astype(np.int32)
     run_int32_case(v3db, db, qs, nlist, L, M, Ks, 5, 37, rng.choice(N, nlist, replace=False),
                    np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_fx_full_size_sampled_parity(v3db, name):
+    """BASELINE.json's full sizes in bench.py --precision fx16's launch configuration (whole batch,
+    trace on): the GPU encoding equals the oracle's on sampled rows and on every query, the GPU
+    snapshot obeys the build rules (tests/snapshot_checks.py with R18/R19), and the oracle's query
+    on that snapshot reproduces sampled output rows bit for bit."""
+    from types import SimpleNamespace
+
+    from .snapshot_checks import check_snapshot
+    cfg = get_config(name)
+    f = generate_float(cfg)
+    rng = np.random.default_rng(2027)
+    gdb = v3db.encode_fixed_point(torch.from_numpy(f.db).cuda(), f.v_max)
+    rows = np.unique(np.concatenate([rng.choice(cfg.N, 4096, replace=False), [0, cfg.N - 1]]))
+    assert np.array_equal(gdb[torch.from_numpy(rows).cuda()].cpu().numpy(), oracle.encode_fixed_point(f.db[rows], f.v_max))
+    qs = oracle.encode_fixed_point(f.queries, f.v_max)
+    gq = v3db.encode_fixed_point(torch.from_numpy(f.queries).cuda(), f.v_max)
+    assert np.array_equal(gq.cpu().numpy(), qs)
+    s = v3db.build_snapshot_fx(gdb, cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows, f.codeword_rows)
+    snap = export_all(v3db, s)
+    inp = SimpleNamespace(db=gdb.cpu().numpy(), centroid_rows=f.centroid_rows, codeword_rows=f.codeword_rows)
+    del gdb
+    check_snapshot(cfg, inp, snap, rng, n_replay=100, n_slots=300, fx=True)
+    out = v3db.query_batch_fx(s, gq, cfg.nprobe, cfg.k, trace=True)
+    torch.cuda.synchronize()
+    s.free()
+    ref_snap = oracle.Snapshot(snap["centroids"], snap["codebooks"], snap["ids"], snap["codes"], snap["counts"],
+                               snap["list_of"])
+    sample = np.unique(np.concatenate([rng.choice(cfg.Q, 40, replace=False), [0, cfg.Q - 1]]))
+    ref = oracle.query_batch(ref_snap, qs, cfg.nprobe, cfg.k, rows=sample)
+    for key, exp in ref.items():
+        got = out[key][torch.from_numpy(sample).cuda()].cpu().numpy()
+        assert np.array_equal(got, exp), f"{name} {key}: {first_mismatch(got, exp)}"

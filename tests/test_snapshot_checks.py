@@ -64,3 +64,34 @@ def test_rejects_wrong_placement(case):
     bad["list_of"][t] = b
     with pytest.raises(AssertionError):
         check_snapshot(cfg, inp, bad, np.random.default_rng(0), n_replay=inp.db.shape[0], n_slots=10)
+
+
+@pytest.fixture(scope="module")
+def fx_case():
+    """The 16-bit fixed-point variant (NEXT-1): C0's float draws encoded by the oracle."""
+    from types import SimpleNamespace
+    from synth import generate_float
+    cfg = get_config("c0")
+    f = generate_float(cfg)
+    db = oracle.encode_fixed_point(f.db, f.v_max)
+    s = oracle.build_snapshot(db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows, f.codeword_rows)
+    snap = {"centroids": s.centroids, "codebooks": s.codebooks, "ids": s.ids, "codes": s.codes,
+            "counts": s.counts, "list_of": s.list_of}
+    return cfg, SimpleNamespace(db=db, centroid_rows=f.centroid_rows, codeword_rows=f.codeword_rows), snap
+
+
+def test_fx_checker_accepts_and_rejects(fx_case):
+    cfg, inp, snap = fx_case
+    check_snapshot(cfg, inp, snap, np.random.default_rng(0), n_replay=300, n_slots=300, fx=True)
+    with pytest.raises(AssertionError):        # the int8 rules (saturated int8 codewords) do not hold
+        check_snapshot(cfg, inp, snap, np.random.default_rng(0), n_replay=10, n_slots=10, fx=False)
+    bad = {key: v.copy() for key, v in snap.items()}
+    m, c, u = np.argwhere(np.abs(bad["codebooks"]) > 127)[0]
+    bad["codebooks"][m, c, u] = np.clip(bad["codebooks"][m, c, u], -127, 127)   # R5 applied where R19 binds
+    with pytest.raises(AssertionError):
+        check_snapshot(cfg, inp, bad, np.random.default_rng(0), n_replay=10, n_slots=10, fx=True)
+    bad = {key: v.copy() for key, v in snap.items()}
+    i = int(np.argmax(bad["counts"]))
+    bad["codes"][i, 0, 0] = (int(bad["codes"][i, 0, 0]) + 1) % cfg.Ks
+    with pytest.raises(AssertionError):
+        check_snapshot(cfg, inp, bad, np.random.default_rng(0), n_replay=10, n_slots=10**6, fx=True)
