@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(256) row_topk_kernel(const int64_t* __restrict
 // in shared memory.  The distance matrix never reaches HBM.  R <= 128.  With a centroid split
 // (gridDim.y = S > 1, small batches) CTA (x, y) sweeps centroid tiles [y * span, (y + 1) * span) and
 // writes its partial lists as keys to part [n][S][R]; fx_merge_kernel selects the final R.
+template <int KR>
 __global__ void __launch_bounds__(256, 3) fx_coarse_kernel(const int32_t* __restrict__ X, int64_t n, int dim,
                                                         const int32_t* __restrict__ mu,
                                                         const int64_t* __restrict__ mnorm, int nlist, int R, int sh,
@@ -221,8 +222,20 @@ __global__ void __launch_bounds__(256, 3) fx_coarse_kernel(const int32_t* __rest
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int rr = warp * 8 + i;
-      thr[i] = warp_offer(T + rr * R, R, thr[i], tile[rr * 65 + lane]);
-      thr[i] = warp_offer(T + rr * R, R, thr[i], tile[rr * 65 + 32 + lane]);
+      const uint64_t k0 = tile[rr * 65 + lane], k1 = tile[rr * 65 + 32 + lane];
+      if (!__any_sync(0xffffffffu, k0 < thr[i] || k1 < thr[i])) continue;
+      // the row's list into registers (WarpTopK: insertion by ballots + shuffles), back to smem
+      WarpTopK<KR> top;
+      top.k = R;
+      top.thr = thr[i];
+#pragma unroll
+      for (int r = 0; r < KR; ++r) top.v[r] = r * 32 + lane < R ? T[rr * R + r * 32 + lane] : ~0ull;
+      top.offer(k0);
+      top.offer(k1);
+#pragma unroll
+      for (int r = 0; r < KR; ++r)
+        if (r * 32 + lane < R) T[rr * R + r * 32 + lane] = top.v[r];
+      thr[i] = top.thr;
     }
     __syncthreads();  // `tile` aliases As / Bs
   }
@@ -502,6 +515,23 @@ __device__ __forceinline__ long long slot_dist_rot(const int64_t* A, const uint8
   return acc;
 }
 
+// slot_dist_rot on code words already in registers (the software-pipelined scan loop).
+template <int MT>
+__device__ __forceinline__ long long slot_dist_rot_w(const int64_t* A, const uint4 (&wv)[MT / 16],
+                                                     const uint32_t (&rot8)[16], long long acc) {
+#pragma unroll
+  for (int g = 0; g < MT / 16; ++g) {
+    const char* Ab = reinterpret_cast<const char*>(A + g * 256 * 16);
+    const uint32_t ws[4] = {wv[g].x, wv[g].y, wv[g].z, wv[g].w};
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const uint32_t c = (ws[t >> 2] >> (8 * (t & 3))) & 0xffu;
+      acc += *reinterpret_cast<const long long*>(Ab + (c << 7) + rot8[t]);
+    }
+  }
+  return acc;
+}
+
 // Steps 3-5 for one query per CTA of NW = 8 warps (16 measured slower: C4 16.7 -> 17.3 ms).
 struct FxScanArgs {
   const int32_t* queries;
@@ -572,6 +602,51 @@ __global__ void __launch_bounds__(32 * NW) scan_fx_kernel(const FxScanArgs a) {
     if constexpr (ROT) return slot_dist_rot<MT>(A, a.codes + slot * M, rot8, acc);
     else return slot_dist<MT, KS>(A, a.codes + slot * M, M, Ks, acc);
   };
+  if constexpr (ROT) {
+    // software-pipelined: the codes and P term of the warp's next 32-slot chunk are loaded while
+    // the current chunk is scanned (the chunk sequence runs over (probe rank, slot) like below)
+    constexpr int G = MT / 16;
+    auto lim_of = [&](int r) { return trace ? L : a.counts[qlists[r]]; };
+    auto load = [&](int r, int jj, uint4 (&w)[G], long long& p) {
+      const int li = qlists[r];
+      const int j = jj + lane;
+      if (j < a.counts[li]) {
+        const int64_t slot = static_cast<int64_t>(li) * L + j;
+        const uint4* src = reinterpret_cast<const uint4*>(a.codes + slot * MT);
+#pragma unroll
+        for (int g = 0; g < G; ++g) w[g] = __ldg(src + g);
+        p = __ldg(a.pterm + slot);
+      }
+    };
+    int rho = 0, j0 = warp * 32;
+    while (rho < nprobe && j0 >= lim_of(rho)) ++rho;
+    uint4 cw[G];
+    long long cp = 0;
+    if (rho < nprobe) load(rho, j0, cw, cp);
+    while (rho < nprobe) {
+      int nrho = rho, nj0 = j0 + W * 32;
+      while (nrho < nprobe && nj0 >= lim_of(nrho)) {
+        ++nrho;
+        nj0 = warp * 32;
+      }
+      uint4 nw[G];
+      long long np = 0;
+      if (nrho < nprobe) load(nrho, nj0, nw, np);
+      const int cnt = a.counts[qlists[rho]];
+      const int j = j0 + lane;
+      long long D = kDMaxFx;
+      if (j < cnt) D = slot_dist_rot_w<MT>(A, cw, rot8, qld[rho] + cp);
+      if (trace && j < L) trace[static_cast<int64_t>(rho) * L + j] = D;
+      const uint64_t key = j < cnt ? (static_cast<uint64_t>(D) << a.sh5) | static_cast<uint32_t>(rho * L + j) : ~0ull;
+      if (buffered) thr = offer_buffered(T, S, k, thr, key, mino, bcnt, reinterpret_cast<unsigned long long*>(wmin + 1));
+      else thr = offer_shared(T, k, thr, key, mino, reinterpret_cast<unsigned long long*>(wmin + 1));
+      rho = nrho;
+      j0 = nj0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) cw[g] = nw[g];
+      cp = np;
+    }
+  } else
   for (int rho = 0; rho < nprobe; ++rho) {
     const int li = qlists[rho];
     const long long di = qld[rho];
@@ -746,7 +821,11 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
   if (sh < 1 || nlist > (1 << std::min(sh, 30))) return cudaErrorInvalidValue;
   if (R <= 128) {
     const size_t smem = sizeof(uint64_t) * 64 * R;
-    cudaError_t e = cudaFuncSetAttribute(fx_coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(fx_coarse_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fx_coarse_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fx_coarse_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ctiles = (nlist + 63) / 64;
     for (int64_t lo = 0; lo < n; lo += int64_t(1) << 24) {  // grid.x chunks
@@ -762,8 +841,16 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
         e = cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(uint64_t) * rows * Sr * R, st);
         if (e != cudaSuccess) return e;
       }
-      fx_coarse_kernel<<<dim3(static_cast<unsigned>(rtiles), Sr), 256, smem, st>>>(
-          X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span, out_idx + lo * R, out_dist + lo * R, part);
+      const dim3 grid(static_cast<unsigned>(rtiles), Sr);
+      if (R <= 32)
+        fx_coarse_kernel<1><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
+                                                     out_idx + lo * R, out_dist + lo * R, part);
+      else if (R <= 64)
+        fx_coarse_kernel<2><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
+                                                     out_idx + lo * R, out_dist + lo * R, part);
+      else
+        fx_coarse_kernel<4><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
+                                                     out_idx + lo * R, out_dist + lo * R, part);
       note_launch();
       if (Sr > 1) {
         dispatch_kr(R, [&]<int KR>() {
