@@ -105,6 +105,34 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def contraction_peak(kind: str, n: int = 8192, reps: int = 5) -> float:
+    """Measured dense peak of the coarse step's contraction on this GPU: int8
+    via torch._int_mm (cuBLASLt), fp64 via torch.mm (cuBLAS DGEMM) at n^3, best of `reps`, TOP/s or
+    TFLOP/s.  Run after the timed region."""
+    import torch
+    if kind == "int8":
+        a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda").t().contiguous().t()
+        fn = lambda: torch._int_mm(a, b)  # noqa: E731
+    else:
+        n = 4096
+        a = torch.rand((n, n), dtype=torch.float64, device="cuda")
+        b = torch.rand((n, n), dtype=torch.float64, device="cuda")
+        fn = lambda: torch.mm(a, b)  # noqa: E731
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record()
+        fn()
+        e_.record()
+        torch.cuda.synchronize()
+        best = min(best, s_.elapsed_time(e_))
+    return 2.0 * n ** 3 / (best / 1e3) / 1e12
+
+
 def code_bytes_per_slot(M: int, Ks: int) -> int:
     """ceil(M * log2(Ks) / 8): the information content of one PQ code."""
     return math.ceil(M * max(1, math.ceil(math.log2(Ks))) / 8) if Ks > 1 else 0
@@ -396,6 +424,18 @@ def main():
                          "d2h_bytes_per_step": d2h, "steps": n_e2e}
 
     result["clocks"] = clk.summary()
+
+    # the coarse step's contraction against the measured peak of its arithmetic (int8 tensor
+    # cores; fp64 for the fixed-point path): 2 Q nlist D ops per batch
+    try:
+        cpk = contraction_peak("fp64" if fx else "int8")
+        cops = 2.0 * cfg.Q * cfg.nlist * cfg.D / (coarse_ms / 1e3) / 1e12
+        result["coarse_roofline"] = {
+            "bound": "fp64" if fx else "tensor", "achieved": cops, "peak": cpk, "unit": "TOP/s",
+            "frac": cops / cpk, "kernel": "coarse (Steps 1-2, fused top-nprobe)",
+            "peak_source": "measured now: torch.mm float64 4096^3" if fx else "measured now: torch._int_mm 8192^3"}
+    except Exception as exc:  # never fail the bench line on the auxiliary peak
+        result["coarse_roofline"] = {"error": str(exc)[:200]}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         arr = {"centroids": v3db.snapshot_export(snap, v3db.FIELD_CENTROIDS),
