@@ -146,19 +146,22 @@ __global__ void __launch_bounds__(256) row_topk_kernel(const int64_t* __restrict
 // in shared memory.  The distance matrix never reaches HBM.  R <= 128.  With a centroid split
 // (gridDim.y = S > 1, small batches) CTA (x, y) sweeps centroid tiles [y * span, (y + 1) * span) and
 // writes its partial lists as keys to part [n][S][R]; fx_merge_kernel selects the final R.
-template <int KR>
-__global__ void __launch_bounds__(256, 3) fx_coarse_kernel(const int32_t* __restrict__ X, int64_t n, int dim,
+template <int KR, int NJ>
+__global__ void __launch_bounds__(256, 2) fx_coarse_kernel(const int32_t* __restrict__ X, int64_t n, int dim,
                                                         const int32_t* __restrict__ mu,
                                                         const int64_t* __restrict__ mnorm, int nlist, int R, int sh,
                                                         int span, int32_t* __restrict__ out_idx,
                                                         int64_t* __restrict__ out_dist, uint64_t* __restrict__ part) {
-  __shared__ double AB[2][32][65];  // As [k][row], Bs [k][col]; reused as the key tile [64][65]
+  constexpr int CW = 16 * NJ;       // centroids per tile: 4 rows x NJ columns per thread
+  // dynamic: As [32][65] (k, row) | Bs [32][CW + 1] (k, col) -- reused as the key tile [64][65],
+  // 64 columns at a time -- | T [64][R]
   __shared__ long long xn_s[64];
   extern __shared__ __align__(16) uint64_t dyn[];
-  auto& As = AB[0];
-  auto& Bs = AB[1];
-  uint64_t* T = dyn;                                   // [64][R]
-  uint64_t* tile = reinterpret_cast<uint64_t*>(&AB[0][0][0]);
+  auto As = reinterpret_cast<double (*)[65]>(dyn);
+  auto Bs = reinterpret_cast<double (*)[CW + 1]>(dyn + 32 * 65);
+  uint64_t* T = dyn + 32 * 65 + 32 * (CW + 1);
+  uint64_t* tile = dyn;
+  static_assert(32 * 65 + 32 * (CW + 1) >= 64 * 65, "key tile alias");
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4, warp = tid >> 5, lane = tid & 31;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
   for (int e = tid; e < 64 * R; e += 256) T[e] = ~0ull;
@@ -177,67 +180,72 @@ __global__ void __launch_bounds__(256, 3) fx_coarse_kernel(const int32_t* __rest
 #pragma unroll
   for (int i = 0; i < 8; ++i) thr[i] = ~0ull;
   const int c_end = min(nlist, static_cast<int>(blockIdx.y + 1) * span);
-  for (int c0 = blockIdx.y * span; c0 < c_end; c0 += 64) {
-    double acc[4][4] = {};
+  for (int c0 = blockIdx.y * span; c0 < c_end; c0 += CW) {
+    double acc[4][NJ] = {};
     for (int k0 = 0; k0 < dim; k0 += 32) {
       for (int e = tid; e < 64 * 32; e += 256) {
         const int rr = e >> 5, kk = e & 31;
         const int64_t r = r0 + rr;
         const int k = k0 + kk;
         As[kk][rr] = (r < n && k < dim) ? static_cast<double>(X[r * dim + k]) : 0.0;
-        const int c = c0 + rr;
-        Bs[kk][rr] = (c < nlist && k < dim) ? static_cast<double>(mu[static_cast<int64_t>(c) * dim + k]) : 0.0;
+      }
+      for (int e = tid; e < CW * 32; e += 256) {
+        const int cc = e >> 5, kk = e & 31;
+        const int c = c0 + cc, k = k0 + kk;
+        Bs[kk][cc] = (c < nlist && k < dim) ? static_cast<double>(mu[static_cast<int64_t>(c) * dim + k]) : 0.0;
       }
       __syncthreads();
-#pragma unroll 8
+#pragma unroll 4
       for (int kk = 0; kk < 32; ++kk) {
-        double av[4], bv[4];
+        double av[4], bv[NJ];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {  // rows ty + 16 i, columns tx + 16 j: conflict-free LDS.64
-          av[i] = As[kk][ty + 16 * i];
-          bv[i] = Bs[kk][tx + 16 * i];
-        }
+        for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];  // rows ty + 16 i: broadcast
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) bv[j] = Bs[kk][tx + 16 * j];  // columns tx + 16 j: conflict-free
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+          for (int j = 0; j < NJ; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int rr = ty + 16 * i;
+    for (int h = 0; h < NJ / 4; ++h) {  // 64 columns at a time through the key tile
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c = c0 + tx + 16 * j;
-        uint64_t key = ~0ull;
-        if (r0 + rr < n && c < nlist) {
-          const long long dd = xn_s[rr] + mnorm[c] - 2 * static_cast<long long>(acc[i][j]);
-          key = (static_cast<uint64_t>(dd) << sh) | static_cast<uint32_t>(c);
+      for (int i = 0; i < 4; ++i) {
+        const int rr = ty + 16 * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = c0 + 64 * h + tx + 16 * j;
+          uint64_t key = ~0ull;
+          if (r0 + rr < n && c < nlist) {
+            const long long dd = xn_s[rr] + mnorm[c] - 2 * static_cast<long long>(acc[i][4 * h + j]);
+            key = (static_cast<uint64_t>(dd) << sh) | static_cast<uint32_t>(c);
+          }
+          tile[rr * 65 + tx + 16 * j] = key;
         }
-        tile[rr * 65 + tx + 16 * j] = key;
       }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = warp * 8 + i;
+        const uint64_t k0 = tile[rr * 65 + lane], k1 = tile[rr * 65 + 32 + lane];
+        if (!__any_sync(0xffffffffu, k0 < thr[i] || k1 < thr[i])) continue;
+        // the row's list into registers (WarpTopK: insertion by ballots + shuffles), back to smem
+        WarpTopK<KR> top;
+        top.k = R;
+        top.thr = thr[i];
+#pragma unroll
+        for (int r = 0; r < KR; ++r) top.v[r] = r * 32 + lane < R ? T[rr * R + r * 32 + lane] : ~0ull;
+        top.offer(k0);
+        top.offer(k1);
+#pragma unroll
+        for (int r = 0; r < KR; ++r)
+          if (r * 32 + lane < R) T[rr * R + r * 32 + lane] = top.v[r];
+        thr[i] = top.thr;
+      }
+      __syncthreads();  // `tile` aliases As / Bs
     }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int rr = warp * 8 + i;
-      const uint64_t k0 = tile[rr * 65 + lane], k1 = tile[rr * 65 + 32 + lane];
-      if (!__any_sync(0xffffffffu, k0 < thr[i] || k1 < thr[i])) continue;
-      // the row's list into registers (WarpTopK: insertion by ballots + shuffles), back to smem
-      WarpTopK<KR> top;
-      top.k = R;
-      top.thr = thr[i];
-#pragma unroll
-      for (int r = 0; r < KR; ++r) top.v[r] = r * 32 + lane < R ? T[rr * R + r * 32 + lane] : ~0ull;
-      top.offer(k0);
-      top.offer(k1);
-#pragma unroll
-      for (int r = 0; r < KR; ++r)
-        if (r * 32 + lane < R) T[rr * R + r * 32 + lane] = top.v[r];
-      thr[i] = top.thr;
-    }
-    __syncthreads();  // `tile` aliases As / Bs
   }
   __syncthreads();
   const uint64_t mask = (uint64_t(1) << sh) - 1;
@@ -820,21 +828,22 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
   const int sh = fx_shift2(dim);
   if (sh < 1 || nlist > (1 << std::min(sh, 30))) return cudaErrorInvalidValue;
   if (R <= 128) {
-    const size_t smem = sizeof(uint64_t) * 64 * R;
-    cudaError_t e = cudaFuncSetAttribute(fx_coarse_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    constexpr int NJ = 8, CW = 16 * NJ;
+    const size_t smem = sizeof(uint64_t) * (32 * 65 + 32 * (CW + 1) + 64 * R);
+    cudaError_t e = cudaFuncSetAttribute(fx_coarse_kernel<1, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fx_coarse_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = cudaFuncSetAttribute(fx_coarse_kernel<2, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fx_coarse_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = cudaFuncSetAttribute(fx_coarse_kernel<4, NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int ctiles = (nlist + 63) / 64;
+    const int ctiles = (nlist + CW - 1) / CW;
     for (int64_t lo = 0; lo < n; lo += int64_t(1) << 24) {  // grid.x chunks
       const int64_t rows = std::min<int64_t>(int64_t(1) << 24, n - lo);
       const int64_t rtiles = (rows + 63) / 64;
       // centroid split so that small batches still fill 148 SMs x 2 CTAs (>= 2 tiles per CTA)
       const int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((4 * 148 + rtiles - 1) / rtiles,
                                                                              ctiles / 2)));
-      const int span = ((ctiles + S - 1) / S) * 64;
+      const int span = ((ctiles + S - 1) / S) * CW;
       const int Sr = (nlist + span - 1) / span;
       uint64_t* part = nullptr;
       if (Sr > 1) {
@@ -843,13 +852,13 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
       }
       const dim3 grid(static_cast<unsigned>(rtiles), Sr);
       if (R <= 32)
-        fx_coarse_kernel<1><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
+        fx_coarse_kernel<1, NJ><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
                                                      out_idx + lo * R, out_dist + lo * R, part);
       else if (R <= 64)
-        fx_coarse_kernel<2><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
+        fx_coarse_kernel<2, NJ><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
                                                      out_idx + lo * R, out_dist + lo * R, part);
       else
-        fx_coarse_kernel<4><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
+        fx_coarse_kernel<4, NJ><<<grid, 256, smem, st>>>(X + lo * dim, rows, dim, mu, mnorm, nlist, R, sh, span,
                                                      out_idx + lo * R, out_dist + lo * R, part);
       note_launch();
       if (Sr > 1) {
