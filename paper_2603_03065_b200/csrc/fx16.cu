@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "topk.cuh"
@@ -556,6 +557,7 @@ struct FxScanArgs {
   int64_t* out_dist;
   int64_t* trace;            // [nq][nprobe][L] or null
   int64_t* Ag;               // [nq][M][Ks] when the table does not fit in shared memory, else null
+  const int32_t* order;      // L2-aware query order (minhash_order) or null
 };
 
 // Shared memory: A [M][Ks] int64 (unless GA) | tops [W][k] u64 | resD [k] i64 | resI [k] i32 |
@@ -567,9 +569,9 @@ __global__ void __launch_bounds__(32 * NW) scan_fx_kernel(const FxScanArgs a) {
   const int M = MT ? MT : a.M;
   const int Ks = KS ? KS : a.Ks;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t qi = blockIdx.x;
+  const int64_t qi = a.order ? a.order[blockIdx.x] : blockIdx.x;
   const int k = a.k, L = a.L, nprobe = a.nprobe, d = a.dim / M;
-  int64_t* A = GA ? a.Ag + qi * M * Ks : reinterpret_cast<int64_t*>(smem);
+  int64_t* A = GA ? a.Ag + static_cast<int64_t>(blockIdx.x) * M * Ks : reinterpret_cast<int64_t*>(smem);
   uint64_t* tops = reinterpret_cast<uint64_t*>(smem + (GA ? 0 : sizeof(int64_t) * M * Ks));
   const int S = a.cap;  // per-warp list stride
   const bool buffered = S > k;
@@ -932,6 +934,8 @@ cudaError_t launch_scan_fx_m(const FxScanArgs& a, int64_t nq, size_t smem, cudaS
   return a.Ks == 256 ? launch_scan_fx<MT, 256, false>(a, nq, smem, st) : launch_scan_fx<MT, 0, false>(a, nq, smem, st);
 }
 
+static cudaError_t fx_scan_launch(const v3db_snapshot* s, FxScanArgs& a, int64_t nq, size_t smem, cudaStream_t st);
+
 cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k, const int32_t* lists,
                     const int64_t* ldist, int32_t* out_ids, int64_t* out_dist, int64_t* trace, cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
@@ -960,6 +964,7 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   a.out_dist = out_dist;
   a.trace = trace;
   a.Ag = nullptr;
+  a.order = nullptr;
   if (a.sh5 < 1 || static_cast<int64_t>(nprobe) * s->L > (int64_t(1) << std::min(a.sh5, 31))) return cudaErrorInvalidValue;
   const size_t abytes = sizeof(int64_t) * s->M * s->Ks;
   const size_t rest = fx_rest(a, 8);
@@ -977,6 +982,26 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
     return e;
   }
   const size_t smem = abytes + rest;
+  // the int8 scan's L2-aware query order, under the same condition (snapshot codes beyond L2)
+  const char* sched = getenv("V3DB_SCHED");
+  const bool want = sched ? sched[0] == '1'
+                          : (nq >= 2048 && static_cast<int64_t>(s->nlist) * s->L * s->M > (int64_t(64) << 20));
+  if (want) {
+    void* sbuf = nullptr;
+    cudaError_t e = cudaMallocAsync(&sbuf, sizeof(int32_t) * (2 * nq + s->nlist), st);
+    if (e != cudaSuccess) return e;
+    e = minhash_order(lists, nq, nprobe, s->nlist, static_cast<int32_t*>(sbuf), st);
+    if (e == cudaSuccess) {
+      a.order = static_cast<int32_t*>(sbuf) + nq;
+      e = fx_scan_launch(s, a, nq, smem, st);
+    }
+    cudaFreeAsync(sbuf, st);
+    return e;
+  }
+  return fx_scan_launch(s, a, nq, smem, st);
+}
+
+static cudaError_t fx_scan_launch(const v3db_snapshot* s, FxScanArgs& a, int64_t nq, size_t smem, cudaStream_t st) {
   const bool rot = s->codes_rot16 != nullptr;  // M % 16 == 0, Ks == 256 (set at build)
   if (rot) a.codes = s->codes_rot16;
   switch (s->M) {

@@ -731,6 +731,22 @@ cudaError_t scan_dispatch(const v3db_snapshot* s, RotArgs& a, int64_t nq, cudaSt
 
 }  // namespace
 
+// The L2-aware query order (see minhash_kernel): scratch [2 nq + nlist] int32; the order is
+// written to scratch + nq.
+cudaError_t minhash_order(const int32_t* lists, int64_t nq, int nprobe, int nlist, int32_t* scratch, cudaStream_t st) {
+  int32_t* key = scratch;
+  int32_t* order = key + nq;
+  int* hist = order + nq;
+  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int) * nlist, st);
+  if (e != cudaSuccess) return e;
+  const unsigned g = static_cast<unsigned>((nq + 255) / 256);
+  minhash_kernel<<<g, 256, 0, st>>>(lists, nq, nprobe, key, hist);
+  scan_hist_kernel<<<1, 1024, 0, st>>>(hist, nlist);
+  scatter_kernel<<<g, 256, 0, st>>>(key, nq, hist, order);
+  note_launch(3);
+  return cudaGetLastError();
+}
+
 cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
                          const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
                          int32_t* trace, cudaStream_t st) {
@@ -764,23 +780,12 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
   if (want) {
     cudaError_t e = cudaMallocAsync(&sbuf, sizeof(int32_t) * (2 * nq + s->nlist), st);
     if (e != cudaSuccess) return e;
-    int32_t* key = static_cast<int32_t*>(sbuf);
-    int32_t* order = key + nq;
-    int* hist = order + nq;
-    e = cudaMemsetAsync(hist, 0, sizeof(int) * s->nlist, st);
-    if (e == cudaSuccess) {
-      const unsigned g = static_cast<unsigned>((nq + 255) / 256);
-      minhash_kernel<<<g, 256, 0, st>>>(lists, nq, nprobe, key, hist);
-      scan_hist_kernel<<<1, 1024, 0, st>>>(hist, s->nlist);
-      scatter_kernel<<<g, 256, 0, st>>>(key, nq, hist, order);
-      note_launch(3);
-      e = cudaGetLastError();
-    }
+    e = minhash_order(lists, nq, nprobe, s->nlist, static_cast<int32_t*>(sbuf), st);
     if (e != cudaSuccess) {
       cudaFreeAsync(sbuf, st);
       return e;
     }
-    a.order = order;
+    a.order = static_cast<int32_t*>(sbuf) + nq;
   }
   cudaError_t res = scan_dispatch(s, a, nq, st);
   if (sbuf) cudaFreeAsync(sbuf, st);

@@ -163,6 +163,9 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
 cudaError_t fx_build_tail(const int32_t* db, int64_t n, int dim, const int32_t* mu, const int32_t* list_of,
                           const int32_t* flat_pos, int M, int Ks, const int32_t* codeword_rows, int nlist, int L,
                           int32_t* cb, uint8_t* codes, int32_t* ids, int64_t* pterm, cudaStream_t st);
+// L2-aware query order (scan_rot.cu): queries grouped by the MinHash min(probe list ids);
+// scratch [2 nq + nlist] int32, the order lands in scratch + nq.
+cudaError_t minhash_order(const int32_t* lists, int64_t nq, int nprobe, int nlist, int32_t* scratch, cudaStream_t st);
 cudaError_t rotate_codes16(const uint8_t* codes, int64_t slots, int L, int M, uint8_t* out, cudaStream_t st);
 cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k, const int32_t* lists,
                     const int64_t* ldist, int32_t* out_ids, int64_t* out_dist, int64_t* trace, cudaStream_t st);
