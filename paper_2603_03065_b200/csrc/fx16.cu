@@ -331,17 +331,19 @@ __global__ void encode32_kernel(const int32_t* __restrict__ db, int64_t n, int d
   }
 }
 
-// codes_rot16 (see slot_dist_rot): byte s of group g of slot j = code of subspace g*16 + ((s + j) mod 16).
+// codes_rot16 (see slot_dist_rot_w): byte s of group g of slot j = code of subspace
+// off_g + ((s + j) mod gs), groups of gs = 16 and a trailing group of 8 when M % 16 == 8.
 __global__ void rotate16_kernel(const uint8_t* __restrict__ codes, int64_t slots, int L, int M,
                                 uint8_t* __restrict__ out) {
   const int64_t total = slots * M;
+  const int m16 = M & ~15;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t slot = e / M;
     const int p = static_cast<int>(e - slot * M);
     const int j = static_cast<int>(slot % L);
-    const int g = p >> 4, t = p & 15;
-    out[e] = codes[slot * M + g * 16 + ((t + j) & 15)];
+    const int off = p < m16 ? (p & ~15) : m16, gs = p < m16 ? 16 : 8;
+    out[e] = codes[slot * M + off + ((p - off + j) & (gs - 1))];
   }
 }
 
@@ -501,44 +503,65 @@ __device__ __forceinline__ long long slot_dist(const int64_t* A, const uint8_t* 
   return acc;
 }
 
-// Conflict-free variant (M % 16 == 0, Ks == 256): the table is stored A16[g][c][16] (row c of
-// group g holds the 16 subspaces g*16.. side by side, 8 B each = all 32 banks) and the codes
-// codes_rot16 hold, for slot j, byte s of group g = the code of subspace g*16 + ((s + j) mod 16).
-// Lane l (== j mod 32) at step s then reads column (l + s) mod 16: the 16 lanes of each half-warp
-// hit 16 distinct bank pairs whatever the codes are -- 2 wavefronts per LDS.64, the minimum.
-// rot8[s] = ((lane + s) & 15) * 8.
+// Conflict-free variant (M % 8 == 0, Ks == 256): subspaces in groups of 16 (and a trailing
+// group of 8 when M % 16 == 8).  Group g's table is stored [c][gs] (row c holds the gs subspaces
+// side by side, 8 B each: 128 B = all 32 banks for gs = 16) and the codes codes_rot16 hold, for
+// slot j, byte s of group g = the code of subspace off_g + ((s + j) mod gs).  Lane l (== j mod 32)
+// at step s then reads column (l + s) mod gs: for gs = 16 the 16 lanes of each half-warp hit 16
+// distinct bank pairs whatever the codes are -- 2 wavefronts per LDS.64, the minimum; for gs = 8
+// lanes l and l + 8 share a column and collide only when their rows have the same parity.
+// rot8[s] = ((lane + s) & 15) * 8.  w = the slot's M code bytes as 32-bit words.
 template <int MT>
-__device__ __forceinline__ long long slot_dist_rot(const int64_t* A, const uint8_t* cp, const uint32_t (&rot8)[16],
-                                                   long long acc) {
+__device__ __forceinline__ void load_code_words(const uint8_t* p, uint32_t (&w)[MT / 4]) {
+  if constexpr (MT % 16 == 0) {
 #pragma unroll
-  for (int g = 0; g < MT / 16; ++g) {
-    const uint4 w = __ldg(reinterpret_cast<const uint4*>(cp) + g);
+    for (int g = 0; g < MT / 16; ++g) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(p) + g);
+      w[4 * g] = x.x;
+      w[4 * g + 1] = x.y;
+      w[4 * g + 2] = x.z;
+      w[4 * g + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int g = 0; g < MT / 8; ++g) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p) + g);
+      w[2 * g] = x.x;
+      w[2 * g + 1] = x.y;
+    }
+  }
+}
+
+template <int MT>
+__device__ __forceinline__ long long slot_dist_rot_w(const int64_t* A, const uint32_t (&w)[MT / 4],
+                                                     const uint32_t (&rot8)[16], long long acc) {
+  constexpr int G16 = MT / 16;
+#pragma unroll
+  for (int g = 0; g < G16; ++g) {
     const char* Ab = reinterpret_cast<const char*>(A + g * 256 * 16);
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-      const uint32_t c = (ws[t >> 2] >> (8 * (t & 3))) & 0xffu;
+      const uint32_t c = (w[4 * g + (t >> 2)] >> (8 * (t & 3))) & 0xffu;
       acc += *reinterpret_cast<const long long*>(Ab + (c << 7) + rot8[t]);
+    }
+  }
+  if constexpr (MT % 16 == 8) {
+    const char* Ab = reinterpret_cast<const char*>(A + G16 * 256 * 16);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t c = (w[4 * G16 + (t >> 2)] >> (8 * (t & 3))) & 0xffu;
+      acc += *reinterpret_cast<const long long*>(Ab + (c << 6) + (rot8[t] & 0x38u));
     }
   }
   return acc;
 }
 
-// slot_dist_rot on code words already in registers (the software-pipelined scan loop).
 template <int MT>
-__device__ __forceinline__ long long slot_dist_rot_w(const int64_t* A, const uint4 (&wv)[MT / 16],
-                                                     const uint32_t (&rot8)[16], long long acc) {
-#pragma unroll
-  for (int g = 0; g < MT / 16; ++g) {
-    const char* Ab = reinterpret_cast<const char*>(A + g * 256 * 16);
-    const uint32_t ws[4] = {wv[g].x, wv[g].y, wv[g].z, wv[g].w};
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const uint32_t c = (ws[t >> 2] >> (8 * (t & 3))) & 0xffu;
-      acc += *reinterpret_cast<const long long*>(Ab + (c << 7) + rot8[t]);
-    }
-  }
-  return acc;
+__device__ __forceinline__ long long slot_dist_rot(const int64_t* A, const uint8_t* cp, const uint32_t (&rot8)[16],
+                                                   long long acc) {
+  uint32_t w[MT / 4];
+  load_code_words<MT>(cp, w);
+  return slot_dist_rot_w<MT>(A, w, rot8, acc);
 }
 
 // Steps 3-5 for one query per CTA of NW = 8 warps (16 measured slower: C4 16.7 -> 17.3 ms).
@@ -592,7 +615,9 @@ __global__ void __launch_bounds__(32 * NW) scan_fx_kernel(const FxScanArgs a) {
     for (int u = 0; u < d; ++u) acc += static_cast<long long>(__ldg(cw + u)) * qs[m * d + u];
     if constexpr (ROT) {
       const int c = e - m * Ks;
-      A[((m >> 4) * Ks + c) * 16 + (m & 15)] = -2 * acc;
+      constexpr int G16 = MT / 16;
+      if (m < 16 * G16) A[((m >> 4) * Ks + c) * 16 + (m & 15)] = -2 * acc;
+      else A[G16 * Ks * 16 + c * 8 + (m - 16 * G16)] = -2 * acc;  // trailing group of 8
     } else {
       A[e] = -2 * acc;
     }
@@ -615,22 +640,20 @@ __global__ void __launch_bounds__(32 * NW) scan_fx_kernel(const FxScanArgs a) {
   if constexpr (ROT) {
     // software-pipelined: the codes and P term of the warp's next 32-slot chunk are loaded while
     // the current chunk is scanned (the chunk sequence runs over (probe rank, slot) like below)
-    constexpr int G = MT / 16;
+    constexpr int NWD = MT / 4;
     auto lim_of = [&](int r) { return trace ? L : a.counts[qlists[r]]; };
-    auto load = [&](int r, int jj, uint4 (&w)[G], long long& p) {
+    auto load = [&](int r, int jj, uint32_t (&w)[NWD], long long& p) {
       const int li = qlists[r];
       const int j = jj + lane;
       if (j < a.counts[li]) {
         const int64_t slot = static_cast<int64_t>(li) * L + j;
-        const uint4* src = reinterpret_cast<const uint4*>(a.codes + slot * MT);
-#pragma unroll
-        for (int g = 0; g < G; ++g) w[g] = __ldg(src + g);
+        load_code_words<MT>(a.codes + slot * MT, w);
         p = __ldg(a.pterm + slot);
       }
     };
     int rho = 0, j0 = warp * 32;
     while (rho < nprobe && j0 >= lim_of(rho)) ++rho;
-    uint4 cw[G];
+    uint32_t cw[NWD];
     long long cp = 0;
     if (rho < nprobe) load(rho, j0, cw, cp);
     while (rho < nprobe) {
@@ -639,7 +662,7 @@ __global__ void __launch_bounds__(32 * NW) scan_fx_kernel(const FxScanArgs a) {
         ++nrho;
         nj0 = warp * 32;
       }
-      uint4 nw[G];
+      uint32_t nw[NWD];
       long long np = 0;
       if (nrho < nprobe) load(nrho, nj0, nw, np);
       const int cnt = a.counts[qlists[rho]];
@@ -653,7 +676,7 @@ __global__ void __launch_bounds__(32 * NW) scan_fx_kernel(const FxScanArgs a) {
       rho = nrho;
       j0 = nj0;
 #pragma unroll
-      for (int g = 0; g < G; ++g) cw[g] = nw[g];
+      for (int g = 0; g < NWD; ++g) cw[g] = nw[g];
       cp = np;
     }
   } else
@@ -928,7 +951,7 @@ cudaError_t launch_scan_fx(const FxScanArgs& a, int64_t nq, size_t smem8, cudaSt
 
 template <int MT>
 cudaError_t launch_scan_fx_m(const FxScanArgs& a, int64_t nq, size_t smem, cudaStream_t st, bool rot) {
-  if constexpr (MT % 16 == 0) {
+  if constexpr (MT % 8 == 0) {
     if (rot) return launch_scan_fx<MT, 256, false, true>(a, nq, smem, st);
   }
   return a.Ks == 256 ? launch_scan_fx<MT, 256, false>(a, nq, smem, st) : launch_scan_fx<MT, 0, false>(a, nq, smem, st);
@@ -1005,9 +1028,9 @@ static cudaError_t fx_scan_launch(const v3db_snapshot* s, FxScanArgs& a, int64_t
   const bool rot = s->codes_rot16 != nullptr;  // M % 16 == 0, Ks == 256 (set at build)
   if (rot) a.codes = s->codes_rot16;
   switch (s->M) {
-    case 8: return launch_scan_fx_m<8>(a, nq, smem, st, false);
+    case 8: return launch_scan_fx_m<8>(a, nq, smem, st, rot);
     case 16: return launch_scan_fx_m<16>(a, nq, smem, st, rot);
-    case 24: return launch_scan_fx_m<24>(a, nq, smem, st, false);
+    case 24: return launch_scan_fx_m<24>(a, nq, smem, st, rot);
     case 32: return launch_scan_fx_m<32>(a, nq, smem, st, rot);
     case 64: return launch_scan_fx_m<64>(a, nq, smem, st, rot);
     case 96: return launch_scan_fx_m<96>(a, nq, smem, st, rot);

@@ -698,7 +698,7 @@ int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nl
   V3DB_CUDA(cudaMemsetAsync(s->codes, 0, static_cast<size_t>(slots) * m, st));
   V3DB_CUDA(v3db::fx_build_tail(db, n, dim, s->centroids32, s->list_of, d_pos.p, m, ks, d_cwrows.p, nlist, L,
                                 s->codebooks32, s->codes, s->ids, s->pterm64, st));  // B3-B6
-  if (m % 16 == 0 && ks == 256 && !getenv("V3DB_FX_NOROT")) {  // conflict-free scan layout
+  if (m % 8 == 0 && ks == 256 && !getenv("V3DB_FX_NOROT")) {  // conflict-free scan layout
     V3DB_CUDA(cudaMalloc(&s->codes_rot16, static_cast<size_t>(slots) * m));
     V3DB_CUDA(v3db::rotate_codes16(s->codes, slots, L, m, s->codes_rot16, st));
   }

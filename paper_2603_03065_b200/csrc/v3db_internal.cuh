@@ -47,7 +47,7 @@ struct v3db_snapshot {
   int64_t* cnorm64 = nullptr;      // [nlist]
   int32_t* codebooks32 = nullptr;  // [M][Ks][d]
   int64_t* pterm64 = nullptr;      // [nlist][L]
-  uint8_t* codes_rot16 = nullptr;  // [nlist][L][M], per-slot rotated in groups of 16 (M % 16 == 0, Ks == 256)
+  uint8_t* codes_rot16 = nullptr;  // [nlist][L][M], per-slot rotated in groups of 16 (+ 8) (M % 8 == 0, Ks == 256)
 };
 
 namespace v3db {

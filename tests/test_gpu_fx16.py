@@ -206,9 +206,9 @@ def test_fx_heavy_ties_and_wide_nprobe(v3db):
 @pytest.mark.parametrize("M,d,Ks", [(24, 4, 256), (48, 2, 256), (16, 8, 256), (32, 4, 64), (96, 8, 256),
                                     (64, 2, 256), (8, 4, 256)])
 def test_fx_scan_shapes(v3db, M, d, Ks):
-    """Every scan instantiation: M = 8 / 24 (8-byte code loads), 48 (generic loop over the canonical
-    codes although a rotated copy exists), 16 / 64 / 96 (the conflict-free rotated table, M % 16 == 0
-    and Ks = 256), Ks = 64 (runtime table stride, canonical codes)."""
+    """Every scan instantiation: the rotated table (Ks = 256) with groups of 16 only (M = 16, 64, 96),
+    16 + a trailing group of 8 (M = 24) and 8 only (M = 8); M = 48 (generic loop over the canonical
+    codes although a rotated copy exists); Ks = 64 (runtime table stride, canonical codes)."""
     rng = np.random.default_rng(25 + M)
     D = M * d
     N, nlist, L = 3000, 24, 160
