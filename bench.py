@@ -387,18 +387,13 @@ def main():
 
     # End-to-end through the C ABI with HOST buffers (H2D queries, D2H outputs inside).
     if not args.no_e2e and fx:
-        # NEXT-1 through the Python binding's public calls: float32 queries H2D, GPU encoding,
-        # v3db_query_batch_fx, outputs D2H into pinned host buffers.
+        # NEXT-1 through v3db_query_batch_fx_host: pinned float32 queries H2D, GPU encoding, Steps
+        # 1-5, outputs D2H into pinned host buffers, all inside the C-ABI call.
         qh = torch.from_numpy(queries).pin_memory()
         oh = v3db.alloc_outputs_fx(snap, cfg.Q, cfg.nprobe, cfg.k, trace=trace, device="cpu", pin=True)
-        od = v3db.alloc_outputs_fx(snap, cfg.Q, cfg.nprobe, cfg.k, trace=trace, device=dev)
 
         def e2e_step():
-            qd = qh.to(dev, non_blocking=True)
-            v3db.query_batch_fx(snap, v3db.encode_fixed_point(qd, v_max), cfg.nprobe, cfg.k, out=od)
-            for key, v in od.items():
-                oh[key].copy_(v, non_blocking=True)
-            torch.cuda.synchronize()
+            v3db.query_batch_fx_host(snap, qh, v_max, cfg.nprobe, cfg.k, oh)
         e2e_step()
         n_e2e = max(1, min(args.steps, 5))
         barrier()

@@ -208,6 +208,17 @@ int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, i
                         int32_t k, int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists,
                         int64_t* trace_list_dist, int64_t* trace_cand_dist, void* stream);
 
+/* v3db_query_batch_fx_host -- the end-to-end fixed-point entry: HOST float32 queries [nq][dim]
+ * copied host->device, encoded with v_max (v3db_encode_fixed_point), v3db_query_batch_fx with
+ * library-owned device buffers, the requested outputs copied device->host (layouts and types of
+ * v3db_query_batch_fx, HOST memory; pinned memory makes the copies asynchronous DMA); synchronizes
+ * `stream` before returning.  trace pointers may be NULL.  Errors as v3db_query_batch_fx, plus
+ * EINVAL for v_max not positive finite. */
+int v3db_query_batch_fx_host(v3db_snapshot_t s, const float* queries, int64_t nq, double v_max,
+                             int32_t nprobe, int32_t k, int32_t* out_ids, int64_t* out_dist,
+                             int32_t* trace_lists, int64_t* trace_list_dist, int64_t* trace_cand_dist,
+                             void* stream);
+
 /* v3db_snapshot_kind -- V3DB_KIND_INT8 or V3DB_KIND_FX16 (negative status on a NULL handle).
  * v3db_query_batch* / v3db_witness_batch reject FX16 snapshots, v3db_query_batch_fx INT8 ones;
  * v3db_snapshot_export returns int32 CENTROIDS / CODEBOOKS for FX16 snapshots. */

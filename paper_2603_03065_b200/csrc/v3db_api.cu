@@ -742,6 +742,57 @@ int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, i
   return V3DB_OK;
 }
 
+int v3db_query_batch_fx_host(v3db_snapshot_t s, const float* queries, int64_t nq, double v_max, int32_t nprobe,
+                             int32_t k, int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists,
+                             int64_t* trace_list_dist, int64_t* trace_cand_dist, void* stream) {
+  g_err.clear();
+  int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
+  if (rc != V3DB_OK) return rc;
+  if (!s->fx) return fail(V3DB_EINVAL, "v3db_query_batch_fx_host needs a snapshot from v3db_build_snapshot_fx");
+  if (!(v_max > 0.0) || !std::isfinite(v_max)) return fail(V3DB_EINVAL, "v_max must be positive and finite");
+  if ((rc = check_device(s)) != V3DB_OK) return rc;
+  if (nq == 0) return V3DB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t fb = sizeof(float) * static_cast<size_t>(nq) * s->dim;
+  const size_t qb = sizeof(int32_t) * static_cast<size_t>(nq) * s->dim;
+  const size_t ib = sizeof(int32_t) * static_cast<size_t>(nq) * k, db = sizeof(int64_t) * static_cast<size_t>(nq) * k;
+  const size_t lb = sizeof(int32_t) * static_cast<size_t>(nq) * nprobe, ldb = 2 * lb;
+  const size_t tb = trace_cand_dist ? sizeof(int64_t) * static_cast<size_t>(nq) * nprobe * s->L : 0;
+  uint8_t* buf = nullptr;
+  V3DB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), fb + qb + ib + db + lb + ldb + tb + 2048, st));
+  uint8_t* p = buf;
+  auto take = [&](size_t bytes) {
+    uint8_t* r = p;
+    p += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  float* dx = reinterpret_cast<float*>(take(fb));
+  int32_t* dq = reinterpret_cast<int32_t*>(take(qb));
+  int32_t* dids = reinterpret_cast<int32_t*>(take(ib));
+  int64_t* ddist = reinterpret_cast<int64_t*>(take(db));
+  int32_t* dl = reinterpret_cast<int32_t*>(take(lb));
+  int64_t* dld = reinterpret_cast<int64_t*>(take(ldb));
+  int64_t* dtr = tb ? reinterpret_cast<int64_t*>(take(tb)) : nullptr;
+  cudaError_t e = cudaMemcpyAsync(dx, queries, fb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = v3db::encode_fixed_point(dx, nq * s->dim, v_max, dq, st);
+  if (e == cudaSuccess) {
+    rc = v3db_query_batch_fx(s, dq, nq, nprobe, k, dids, ddist, dl, dld, dtr, stream);
+    if (rc != V3DB_OK) {
+      cudaFreeAsync(buf, st);
+      return rc;
+    }
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_ids, dids, ib, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_dist, ddist, db, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && trace_lists) e = cudaMemcpyAsync(trace_lists, dl, lb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && trace_list_dist) e = cudaMemcpyAsync(trace_list_dist, dld, ldb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && dtr) e = cudaMemcpyAsync(trace_cand_dist, dtr, tb, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(buf, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_fx_host");
+  return V3DB_OK;
+}
+
 int v3db_snapshot_kind(v3db_snapshot_t s) {
   g_err.clear();
   if (!s) return fail(V3DB_EINVAL, "NULL snapshot");

@@ -144,6 +144,22 @@ def query_batch_fx(s: Snapshot, queries: torch.Tensor, nprobe: int, k: int, trac
     return out
 
 
+def query_batch_fx_host(s: Snapshot, queries: torch.Tensor, v_max: float, nprobe: int, k: int, out: dict,
+                        stream=None) -> dict:
+    """v3db_query_batch_fx_host: HOST float32 queries and HOST output buffers (alloc_outputs_fx with
+    device="cpu", pin=True); the call copies in, encodes, runs Steps 1-5, copies out, synchronizes."""
+    lib = _lib.load()
+    nq = queries.shape[0]
+    _need(queries, torch.float32, "cpu", (nq, s.dim), "queries")
+    _need(out["out_ids"], torch.int32, "cpu", (nq, k), "out_ids")
+    _need(out["out_dist"], torch.int64, "cpu", (nq, k), "out_dist")
+    tl, tld, tcd = out.get("trace_lists"), out.get("trace_list_dist"), out.get("trace_cand_dist")
+    _lib.check(lib.v3db_query_batch_fx_host(s.handle, _ptr(queries), nq, float(v_max), nprobe, k, _ptr(out["out_ids"]),
+                                            _ptr(out["out_dist"]), _ptr(tl), _ptr(tld), _ptr(tcd),
+                                            _stream_ptr(stream)))
+    return out
+
+
 def alloc_outputs_fx(s: Snapshot, nq: int, nprobe: int, k: int, trace: bool = True, device="cuda",
                      pin=False) -> dict:
     """Output buffers of query_batch_fx (int32 ids / lists, int64 distances)."""

@@ -252,3 +252,16 @@ def test_fx_full_size_sampled_parity(v3db, name):
     for key, exp in ref.items():
         got = out[key][torch.from_numpy(sample).cuda()].cpu().numpy()
         assert np.array_equal(got, exp), f"{name} {key}: {first_mismatch(got, exp)}"
+
+
+def test_fx_host_entry(v3db):
+    """v3db_query_batch_fx_host (HOST float32 queries, encoding inside the call) equals the oracle."""
+    cfg, f, db, qs, ref_s, ref = fx_case("e2_large")
+    s = v3db.build_snapshot_fx(torch.from_numpy(db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows,
+                               f.codeword_rows)
+    oh = v3db.alloc_outputs_fx(s, cfg.Q, cfg.nprobe, cfg.k, trace=True, device="cpu", pin=True)
+    v3db.query_batch_fx_host(s, torch.from_numpy(f.queries), f.v_max, cfg.nprobe, cfg.k, oh)
+    check_query(oh, ref)
+    oh2 = v3db.alloc_outputs_fx(s, cfg.Q, cfg.nprobe, cfg.k, trace=False, device="cpu")
+    v3db.query_batch_fx_host(s, torch.from_numpy(f.queries), f.v_max, cfg.nprobe, cfg.k, oh2)
+    check_query(oh2, ref, keys=("out_ids", "out_dist"))
