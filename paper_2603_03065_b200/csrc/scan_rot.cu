@@ -404,6 +404,10 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
       if constexpr (MODE == kLutP64) {
 #pragma unroll
         for (int col = m; col < 64; col += M) T[cc * 64 + col] = A;
+      } else if constexpr (M % 32 == 0) {  // groups of 32: one column per subspace
+        int32_t* Tg = T + (m >> 5) * (kW32GroupBytes / 4);
+        Tg[cc * 32 + (m & 31)] = A;
+        if (cc == 0) Tg[256 * 32 + (m & 31)] = A;  // row 256 duplicates row 0 (wrap of code 0)
       } else {
         // the group of subspace m by compile-time selects (rot_goff / rot_gsize of a runtime group
         // index are evaluated as loops at run time: ~25 % of C3's instructions)
