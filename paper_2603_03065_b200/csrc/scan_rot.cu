@@ -181,25 +181,35 @@ __device__ int compact(uint64_t* buf, int* hist, int* s_int, const int4* probe, 
   for (int r = 0; r < CAPM; ++r) kv[r] = tid + r * NT < n ? buf[tid + r * NT] : ~0ull;
   int kept = n;
   if (n > a.k) {
-    // 4-pass radix select (8-bit digits) of the k-th smallest D.
+    // Radix select (8-bit digits) of the k-th smallest D.  Every buffered D is <= *tau once tau is
+    // set, so the leading digits above tau's top bit are 0 for all entries: those passes are
+    // skipped.  Two histograms alternate (warp 0 scans one while the others clear the next), so a
+    // pass costs two barriers.
     uint32_t prefix = 0;
     int kk = a.k;
+    const uint32_t bound = *tau;  // kTauInit (all ones) before the first compaction
+    const int top = 32 - __clz(bound | 1u);
+    const int pass0 = 3 - (top - 1) / 8;
+    for (int b = tid; b < 256; b += NT) hist[b] = 0;
+    bar_c<NT>();
 #pragma unroll 1
-    for (int pass = 0; pass < 4; ++pass) {
-      const int shift = 24 - 8 * pass;
-      for (int b = tid; b < 256; b += NT) hist[b] = 0;
-      bar_c<NT>();
+    for (int pass = pass0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass, par = (pass - pass0) & 1;
+      int* H = hist + 256 * par;
 #pragma unroll
       for (int r = 0; r < CAPM; ++r) {
         const uint32_t D = static_cast<uint32_t>(kv[r] >> 32);
-        if (tid + r * NT < n && (pass == 0 || (D >> (shift + 8)) == prefix)) atomicAdd(&hist[(D >> shift) & 255], 1);
+        if (tid + r * NT < n && (pass == 0 || (D >> (shift + 8)) == prefix)) atomicAdd(&H[(D >> shift) & 255], 1);
       }
       bar_c<NT>();
-      if (warp == 0) {
+      if (warp != 0) {
+        int* Hn = hist + 256 * (par ^ 1);  // the next pass's histogram (last read one pass ago)
+        for (int b = tid - 32; b < 256; b += NT - 32) Hn[b] = 0;
+      } else {
         int h[8], sum = 0;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
-          h[b] = hist[lane * 8 + b];
+          h[b] = H[lane * 8 + b];
           sum += h[b];
         }
         int incl = sum;
@@ -217,29 +227,29 @@ __device__ int compact(uint64_t* buf, int* hist, int* s_int, const int4* probe, 
             cum += h[b];
             ++bin;
           }
-          s_int[8] = bin;
-          s_int[9] = kk - cum;
+          s_int[8 + 2 * par] = bin;
+          s_int[9 + 2 * par] = kk - cum;
         }
       }
       bar_c<NT>();
-      prefix = (prefix << 8) | static_cast<uint32_t>(s_int[8]);
-      kk = s_int[9];
-      bar_c<NT>();  // s_int[8..9] reused next pass
+      prefix = (prefix << 8) | static_cast<uint32_t>(s_int[8 + 2 * par]);
+      kk = s_int[9 + 2 * par];
+      // no barrier: the next pass writes the other histogram and the other s_int pair
     }
     *tau = prefix;  // exact k-th smallest D
-    if (tid == 0) s_int[10] = 0;
+    if (tid == 0) s_int[12] = 0;
     bar_c<NT>();
 #pragma unroll
     for (int r = 0; r < CAPM; ++r) {
       const bool keep = tid + r * NT < n && static_cast<uint32_t>(kv[r] >> 32) <= prefix;
       const uint32_t bal = __ballot_sync(kFull, keep);
       int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&s_int[10], __popc(bal));
+      if (lane == 0 && bal) base = atomicAdd(&s_int[12], __popc(bal));
       base = __shfl_sync(kFull, base, 0);
       if (keep) buf[base + __popc(bal & ((1u << lane) - 1u))] = kv[r];
     }
     bar_c<NT>();
-    kept = s_int[10];
+    kept = s_int[12];
   }
   if (final) {  // resolve: the caller orders the survivors by (D, id) (rank_scatter)
     for (int e = tid; e < kept; e += NT) buf[e] = resolve_key(buf[e], probe, a);
@@ -303,7 +313,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
   int* hist = reinterpret_cast<int*>(smem + a.off_hist);
   int4* probe = reinterpret_cast<int4*>(smem + a.off_probe);  // (list, d_i, count, 0)
   int8_t* qs = reinterpret_cast<int8_t*>(smem + a.off_q);
-  int* s_int = reinterpret_cast<int*>(smem + a.off_int);     // [0] count [1] request [2] done, [8..10] scratch
+  int* s_int = reinterpret_cast<int*>(smem + a.off_int);     // [0] count [1] request [2] done, [8..12] scratch
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* empty = full + a.NS;
 
@@ -635,7 +645,7 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
     int cp = e_cap ? atoi(e_cap) : c[2];
     while (cp < a.k + head) cp *= 2;
     const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) + 16u * ns * seg +
-                        8u * cp + 256 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
+                        8u * cp + 512 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
     SEG = seg;
     NS = ns;
     cap = cp;
@@ -657,7 +667,7 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
   a.off_buf = o;
   o += 8u * cap;
   a.off_hist = o;
-  o += 256 * 4;
+  o += 512 * 4;  // two alternating radix histograms
   a.off_probe = o;
   o += 16u * a.nprobe;
   a.off_q = o;
