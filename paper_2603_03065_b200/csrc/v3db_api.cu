@@ -554,21 +554,54 @@ int v3db_query_batch_host(v3db_snapshot_t s, const int8_t* queries, int64_t nq, 
   int32_t* dl = reinterpret_cast<int32_t*>(take(lb));
   int32_t* dld = reinterpret_cast<int32_t*>(take(lb));
   int32_t* dtr = tb ? reinterpret_cast<int32_t*>(take(tb)) : nullptr;
-  cudaError_t e = cudaMemcpyAsync(dq, queries, qb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) {
-    rc = v3db_query_batch_ex(s, dq, nq, nprobe, k, dids, ddist, dl, dld, dtr, V3DB_SCAN_AUTO, stream);
-    if (rc != V3DB_OK) {
-      cudaFreeAsync(buf, st);
-      return rc;
-    }
+  // With the witness trace requested the call is bound by the device->host copy of the trace;
+  // the batch then runs in sub-batches whose outputs are copied on a second stream while the next
+  // sub-batch computes (results do not depend on the split: queries are independent).
+  const int nchunk = (tb && nq >= 8192) ? 4 : 1;
+  const int64_t qc = (nq + nchunk - 1) / nchunk;
+  cudaStream_t cs = st;
+  cudaEvent_t ev[5] = {};
+  cudaError_t e = cudaSuccess;
+  if (nchunk > 1) {
+    e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int c = 0; c <= nchunk && e == cudaSuccess; ++c) e = cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming);
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out_ids, dids, ob, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out_dist, ddist, ob, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && trace_lists) e = cudaMemcpyAsync(trace_lists, dl, lb, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && trace_list_dist) e = cudaMemcpyAsync(trace_list_dist, dld, lb, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && dtr) e = cudaMemcpyAsync(trace_cand_dist, dtr, tb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dq, queries, qb, cudaMemcpyHostToDevice, st);
+  for (int c = 0; c < nchunk && e == cudaSuccess; ++c) {
+    const int64_t q0 = c * qc, n = std::min(qc, nq - q0);
+    if (n <= 0) break;
+    rc = v3db_query_batch_ex(s, dq + q0 * s->dim, n, nprobe, k, dids + q0 * k, ddist + q0 * k, dl + q0 * nprobe,
+                             dld + q0 * nprobe, dtr ? dtr + q0 * nprobe * s->L : nullptr, V3DB_SCAN_AUTO, stream);
+    if (rc != V3DB_OK) break;
+    if (nchunk > 1) {
+      e = cudaEventRecord(ev[c], st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[c], 0);
+    }
+    const size_t ob_c = sizeof(int32_t) * static_cast<size_t>(n) * k, lb_c = sizeof(int32_t) * static_cast<size_t>(n) * nprobe;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_ids + q0 * k, dids + q0 * k, ob_c, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_dist + q0 * k, ddist + q0 * k, ob_c, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && trace_lists)
+      e = cudaMemcpyAsync(trace_lists + q0 * nprobe, dl + q0 * nprobe, lb_c, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && trace_list_dist)
+      e = cudaMemcpyAsync(trace_list_dist + q0 * nprobe, dld + q0 * nprobe, lb_c, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && dtr)
+      e = cudaMemcpyAsync(trace_cand_dist + q0 * nprobe * s->L, dtr + q0 * nprobe * s->L, lb_c * s->L,
+                          cudaMemcpyDeviceToHost, cs);
+  }
+  if (nchunk > 1) {  // the buffer is freed on `st` after the copies on `cs`
+    cudaError_t e2 = cudaEventRecord(ev[nchunk], cs);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, ev[nchunk], 0);
+    if (e == cudaSuccess) e = e2;
+  }
   cudaFreeAsync(buf, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaError_t es = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = es;
+  if (nchunk > 1) {
+    for (auto& x : ev)
+      if (x) cudaEventDestroy(x);
+    cudaStreamDestroy(cs);
+  }
+  if (rc != V3DB_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_host");
   return V3DB_OK;
 }

@@ -207,9 +207,17 @@ def test_empty_batch_and_trace_off_and_host_api(v3db):
     # host-buffer entry point (end-to-end path of bench.py)
     qh = torch.from_numpy(inp.queries).pin_memory()
     oh = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=True, device="cpu", pin=True)
-    v3db.query_batch_host(s, qh, cfg.nprobe, cfg.k, oh)
+    v3db.query_batch_host(s, qh, cfg.nprobe, cfg.k, oh)   # Q = 10 000: pipelined in 4 sub-batches
     for key, exp in ref.items():
         assert np.array_equal(oh[key].numpy(), exp), key
+    n = 9001                                                 # ragged sub-batches
+    oh = v3db.alloc_outputs(s, n, cfg.nprobe, cfg.k, trace=True, device="cpu", pin=True)
+    v3db.query_batch_host(s, qh[:n].contiguous(), cfg.nprobe, cfg.k, oh)
+    for key, exp in ref.items():
+        assert np.array_equal(oh[key].numpy(), exp[:n]), key
+    oh = v3db.alloc_outputs(s, cfg.Q, cfg.nprobe, cfg.k, trace=False, device="cpu", pin=True)
+    v3db.query_batch_host(s, qh, cfg.nprobe, cfg.k, oh)   # no trace: one batch
+    assert_query_equal(oh, ref, keys=("out_ids", "out_dist"))
     s.free()
 
 
