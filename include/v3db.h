@@ -202,8 +202,9 @@ int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nl
  * [-65535, 65535]; out_ids int32 [nq][k]; out_dist, trace_list_dist, trace_cand_dist int64 with
  * the layouts of v3db_query_batch (padding / missing entries: id -1, distance 2^63 - 1).  EINVAL
  * as v3db_query_batch, for an int8 snapshot, out-of-range queries, or nprobe * list_cap above the
- * Step-5 key bound (2^(64 - bits(dim * 262140^2))); ECUDA if more than max(4096, 4k) candidates
- * tie at the k-th distance of one query.  Synchronous (validation reads back one word). */
+ * Step-5 key bound (2^(64 - bits(dim * 262140^2))); ENOMEM, ECUDA.  Ties at the k-th distance are
+ * resolved exactly by item id however many there are.  The range check of the queries reads one
+ * word back, so the call returns after that check (the kernels stay asynchronous on `stream`). */
 int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, int32_t nprobe,
                         int32_t k, int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists,
                         int64_t* trace_list_dist, int64_t* trace_cand_dist, void* stream);

@@ -742,19 +742,11 @@ int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nl
   return V3DB_OK;
 }
 
-int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, int32_t nprobe, int32_t k,
-                        int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists, int64_t* trace_list_dist,
-                        int64_t* trace_cand_dist, void* stream) {
-  g_err.clear();
-  int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
-  if (rc != V3DB_OK) return rc;
-  if (!s->fx) return fail(V3DB_EINVAL, "v3db_query_batch_fx needs a snapshot from v3db_build_snapshot_fx");
-  if (static_cast<int64_t>(nprobe) * s->L > (int64_t(1) << std::min(v3db::fx_shift5(s->dim), 31)))
-    return fail(V3DB_EINVAL, "nprobe * list_cap too large for the composite Step-5 keys at this dim");
-  if ((rc = check_device(s)) != V3DB_OK) return rc;
-  if (nq == 0) return V3DB_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((rc = check_fx_range(queries, nq * s->dim, st, "query")) != V3DB_OK) return rc;
+// Steps 1-5 on a validated fixed-point query batch already range-checked (stream-ordered, no host
+// synchronization).
+static int fx_query_impl(v3db_snapshot_t s, const int32_t* queries, int64_t nq, int32_t nprobe, int32_t k,
+                         int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists, int64_t* trace_list_dist,
+                         int64_t* trace_cand_dist, cudaStream_t st) {
   int32_t* lists = trace_lists;
   int64_t* ldist = trace_list_dist;
   void* scratch = nullptr;
@@ -769,21 +761,40 @@ int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, i
   if (e == cudaSuccess) e = v3db::fx_scan(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
   prof_record(2, st);
   if (scratch) cudaFreeAsync(scratch, st);
-  if (e == cudaErrorNotSupported)
-    return fail(V3DB_ECUDA, "more than 4096 (or 4k) candidates tie at the k-th distance (fx scan buffer)");
   if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_fx");
   return V3DB_OK;
+}
+
+static int validate_fx_query(v3db_snapshot_t s, const void* queries, int64_t nq, int32_t nprobe, int32_t k,
+                             const void* out_ids, const void* out_dist) {
+  int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
+  if (rc != V3DB_OK) return rc;
+  if (!s->fx) return fail(V3DB_EINVAL, "the fixed-point query entry points need a snapshot from v3db_build_snapshot_fx");
+  if (static_cast<int64_t>(nprobe) * s->L > (int64_t(1) << std::min(v3db::fx_shift5(s->dim), 31)))
+    return fail(V3DB_EINVAL, "nprobe * list_cap too large for the composite Step-5 keys at this dim");
+  return check_device(s);
+}
+
+int v3db_query_batch_fx(v3db_snapshot_t s, const int32_t* queries, int64_t nq, int32_t nprobe, int32_t k,
+                        int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists, int64_t* trace_list_dist,
+                        int64_t* trace_cand_dist, void* stream) {
+  g_err.clear();
+  int rc = validate_fx_query(s, queries, nq, nprobe, k, out_ids, out_dist);
+  if (rc != V3DB_OK) return rc;
+  if (nq == 0) return V3DB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = check_fx_range(queries, nq * s->dim, st, "query")) != V3DB_OK) return rc;
+  return fx_query_impl(s, queries, nq, nprobe, k, out_ids, out_dist, trace_lists, trace_list_dist, trace_cand_dist,
+                       st);
 }
 
 int v3db_query_batch_fx_host(v3db_snapshot_t s, const float* queries, int64_t nq, double v_max, int32_t nprobe,
                              int32_t k, int32_t* out_ids, int64_t* out_dist, int32_t* trace_lists,
                              int64_t* trace_list_dist, int64_t* trace_cand_dist, void* stream) {
   g_err.clear();
-  int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
+  int rc = validate_fx_query(s, queries, nq, nprobe, k, out_ids, out_dist);
   if (rc != V3DB_OK) return rc;
-  if (!s->fx) return fail(V3DB_EINVAL, "v3db_query_batch_fx_host needs a snapshot from v3db_build_snapshot_fx");
   if (!(v_max > 0.0) || !std::isfinite(v_max)) return fail(V3DB_EINVAL, "v_max must be positive and finite");
-  if ((rc = check_device(s)) != V3DB_OK) return rc;
   if (nq == 0) return V3DB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t fb = sizeof(float) * static_cast<size_t>(nq) * s->dim;
@@ -806,22 +817,62 @@ int v3db_query_batch_fx_host(v3db_snapshot_t s, const float* queries, int64_t nq
   int32_t* dl = reinterpret_cast<int32_t*>(take(lb));
   int64_t* dld = reinterpret_cast<int64_t*>(take(ldb));
   int64_t* dtr = tb ? reinterpret_cast<int64_t*>(take(tb)) : nullptr;
-  cudaError_t e = cudaMemcpyAsync(dx, queries, fb, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = v3db::encode_fixed_point(dx, nq * s->dim, v_max, dq, st);
-  if (e == cudaSuccess) {
-    rc = v3db_query_batch_fx(s, dq, nq, nprobe, k, dids, ddist, dl, dld, dtr, stream);
-    if (rc != V3DB_OK) {
-      cudaFreeAsync(buf, st);
-      return rc;
-    }
+  // sub-batches with the outputs copied on a second stream, as in v3db_query_batch_host
+  const int nchunk = (tb && nq >= 8192) ? 4 : 1;
+  const int64_t qc = (nq + nchunk - 1) / nchunk;
+  cudaStream_t cs = st;
+  cudaEvent_t ev[5] = {};
+  cudaError_t e = cudaSuccess;
+  if (nchunk > 1) {
+    e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int c = 0; c <= nchunk && e == cudaSuccess; ++c) e = cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming);
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out_ids, dids, ib, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out_dist, ddist, db, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && trace_lists) e = cudaMemcpyAsync(trace_lists, dl, lb, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && trace_list_dist) e = cudaMemcpyAsync(trace_list_dist, dld, ldb, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && dtr) e = cudaMemcpyAsync(trace_cand_dist, dtr, tb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dx, queries, fb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = v3db::encode_fixed_point(dx, nq * s->dim, v_max, dq, st);
+  // one range check of the whole encoded batch, before any output copy is queued
+  if (e == cudaSuccess && (rc = check_fx_range(dq, nq * s->dim, st, "query")) != V3DB_OK) {
+    cudaFreeAsync(buf, st);
+    if (nchunk > 1) {
+      for (auto& x : ev)
+        if (x) cudaEventDestroy(x);
+      cudaStreamDestroy(cs);
+    }
+    return rc;
+  }
+  const int64_t Lq = static_cast<int64_t>(nprobe) * s->L;
+  for (int c = 0; c < nchunk && e == cudaSuccess; ++c) {
+    const int64_t q0 = c * qc, n = std::min(qc, nq - q0);
+    if (n <= 0) break;
+    rc = fx_query_impl(s, dq + q0 * s->dim, n, nprobe, k, dids + q0 * k, ddist + q0 * k, dl + q0 * nprobe,
+                       dld + q0 * nprobe, dtr ? dtr + q0 * Lq : nullptr, st);
+    if (rc != V3DB_OK) break;
+    if (nchunk > 1) {
+      e = cudaEventRecord(ev[c], st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[c], 0);
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_ids + q0 * k, dids + q0 * k, 4 * n * k, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_dist + q0 * k, ddist + q0 * k, 8 * n * k, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && trace_lists)
+      e = cudaMemcpyAsync(trace_lists + q0 * nprobe, dl + q0 * nprobe, 4 * n * nprobe, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && trace_list_dist)
+      e = cudaMemcpyAsync(trace_list_dist + q0 * nprobe, dld + q0 * nprobe, 8 * n * nprobe, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess && dtr)
+      e = cudaMemcpyAsync(trace_cand_dist + q0 * Lq, dtr + q0 * Lq, 8 * n * Lq, cudaMemcpyDeviceToHost, cs);
+  }
+  if (nchunk > 1) {
+    cudaError_t e2 = cudaEventRecord(ev[nchunk], cs);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, ev[nchunk], 0);
+    if (e == cudaSuccess) e = e2;
+  }
   cudaFreeAsync(buf, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaError_t es = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = es;
+  if (nchunk > 1) {
+    for (auto& x : ev)
+      if (x) cudaEventDestroy(x);
+    cudaStreamDestroy(cs);
+  }
+  if (rc != V3DB_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_fx_host");
   return V3DB_OK;
 }
