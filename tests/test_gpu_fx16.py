@@ -262,6 +262,12 @@ def test_fx_host_entry(v3db):
     oh = v3db.alloc_outputs_fx(s, cfg.Q, cfg.nprobe, cfg.k, trace=True, device="cpu", pin=True)
     v3db.query_batch_fx_host(s, torch.from_numpy(f.queries), f.v_max, cfg.nprobe, cfg.k, oh)
     check_query(oh, ref)
+    cfg1, f1, db1, qs1, ref_s1, ref1 = fx_case("c1")          # Q = 10 000: pipelined sub-batches
+    s1 = v3db.build_snapshot_fx(torch.from_numpy(db1).cuda(), cfg1.nlist, cfg1.L, cfg1.M, cfg1.Ks, f1.centroid_rows,
+                                f1.codeword_rows)
+    oh1 = v3db.alloc_outputs_fx(s1, cfg1.Q, cfg1.nprobe, cfg1.k, trace=True, device="cpu", pin=True)
+    v3db.query_batch_fx_host(s1, torch.from_numpy(f1.queries), f1.v_max, cfg1.nprobe, cfg1.k, oh1)
+    check_query(oh1, ref1)
     oh2 = v3db.alloc_outputs_fx(s, cfg.Q, cfg.nprobe, cfg.k, trace=False, device="cpu")
     v3db.query_batch_fx_host(s, torch.from_numpy(f.queries), f.v_max, cfg.nprobe, cfg.k, oh2)
     check_query(oh2, ref, keys=("out_ids", "out_dist"))
