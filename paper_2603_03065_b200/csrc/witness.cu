@@ -59,6 +59,34 @@ __global__ void bitonic_step_kernel(uint64_t* __restrict__ keys, int64_t pairs, 
   }
 }
 
+// The steps of a bitonic sort whose stride is below the tile, in shared memory: one CTA per
+// tile of `tile` keys (a power of two dividing P, so a tile never straddles a segment).  The
+// direction of a compare-exchange depends on the key's index within its segment, exactly as in
+// bitonic_step_kernel.  size_lo..size_hi: the merge sizes to run (strides size/2 .. 1 each, only
+// those below the tile).
+__global__ void __launch_bounds__(512) bitonic_tile_kernel(uint64_t* __restrict__ keys, int P, int tile, int size_lo,
+                                                           int size_hi) {
+  extern __shared__ uint64_t sk[];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * tile;
+  const int off = static_cast<int>(base % P);
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) sk[e] = keys[base + e];
+  __syncthreads();
+  for (int size = size_lo; size <= size_hi; size <<= 1) {
+    for (int stride = min(size, tile) >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (tile >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+        const uint64_t a = sk[lo], b = sk[hi];
+        if ((a > b) == (((off + lo) & size) == 0)) {
+          sk[lo] = b;
+          sk[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) keys[base + e] = sk[e];
+}
+
 // Per (query, probe rank): the literal Step-3 table LUT_{i,m,c} = dist(C_{m,c}, (q - mu_i)^{(m)})
 // in shared memory, then for every slot j the selected entries l^{(m)}_{i,j} (Step 4 witness) and
 // the Step-5 key of the masked candidate distance D_{i,j}.
@@ -134,15 +162,30 @@ int pow2_at_least(int64_t n) {
 
 }  // namespace
 
-// Ascending sort of every P-key segment (P a power of two): bitonic network, one launch per step.
+// Ascending sort of every P-key segment (P a power of two): bitonic network.  Steps whose stride
+// is below the 4096-key tile run in shared memory (bitonic_tile_kernel: all sizes up to the tile
+// in one launch, then one launch per larger size); only the larger strides are global passes
+// (one launch each) -- 15 launches instead of 136 for a 2^16-key segment.
 cudaError_t segmented_sort(uint64_t* keys, int64_t nseg, int P, cudaStream_t st) {
   const int64_t pairs = nseg * (P / 2);
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>((pairs + 255) / 256, 148 * 16));
-  for (int size = 2; size <= P; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+  const int tile = std::min(P, 4096);
+  const int64_t tiles = nseg * (P / tile);
+  const size_t smem = sizeof(uint64_t) * tile;
+  if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(bitonic_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  bitonic_tile_kernel<<<static_cast<unsigned>(tiles), 512, smem, st>>>(keys, P, tile, 2, tile);
+  note_launch();
+  for (int size = 2 * tile; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride >= tile; stride >>= 1) {
       bitonic_step_kernel<<<grid, 256, 0, st>>>(keys, pairs, P, size, stride);
       note_launch();
     }
+    bitonic_tile_kernel<<<static_cast<unsigned>(tiles), 512, smem, st>>>(keys, P, tile, size, size);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 
