@@ -184,16 +184,50 @@ __global__ void __launch_bounds__(256, 2) fx_coarse_kernel(const int32_t* __rest
   for (int c0 = blockIdx.y * span; c0 < c_end; c0 += CW) {
     double acc[4][NJ] = {};
     for (int k0 = 0; k0 < dim; k0 += 32) {
-      for (int e = tid; e < 64 * 32; e += 256) {
-        const int rr = e >> 5, kk = e & 31;
-        const int64_t r = r0 + rr;
-        const int k = k0 + kk;
-        As[kk][rr] = (r < n && k < dim) ? static_cast<double>(X[r * dim + k]) : 0.0;
-      }
-      for (int e = tid; e < CW * 32; e += 256) {
-        const int cc = e >> 5, kk = e & 31;
-        const int c = c0 + cc, k = k0 + kk;
-        Bs[kk][cc] = (c < nlist && k < dim) ? static_cast<double>(mu[static_cast<int64_t>(c) * dim + k]) : 0.0;
+      if (dim % 32 == 0) {  // 16-byte loads, all issued before the conversions and stores
+        constexpr int NA = 64 * 8 / 256, NB = CW * 8 / 256;
+        int4 va[NA], vb[NB];
+#pragma unroll
+        for (int x = 0; x < NA; ++x) {
+          const int e = tid + x * 256, rr = e >> 3, kq = (e & 7) * 4;
+          const int64_t r = r0 + rr;
+          va[x] = r < n ? __ldg(reinterpret_cast<const int4*>(X + r * dim + k0 + kq)) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int x = 0; x < NB; ++x) {
+          const int e = tid + x * 256, cc = e >> 3, kq = (e & 7) * 4;
+          const int c = c0 + cc;
+          vb[x] = c < nlist ? __ldg(reinterpret_cast<const int4*>(mu + static_cast<int64_t>(c) * dim + k0 + kq))
+                            : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int x = 0; x < NA; ++x) {
+          const int e = tid + x * 256, rr = e >> 3, kq = (e & 7) * 4;
+          As[kq][rr] = va[x].x;
+          As[kq + 1][rr] = va[x].y;
+          As[kq + 2][rr] = va[x].z;
+          As[kq + 3][rr] = va[x].w;
+        }
+#pragma unroll
+        for (int x = 0; x < NB; ++x) {
+          const int e = tid + x * 256, cc = e >> 3, kq = (e & 7) * 4;
+          Bs[kq][cc] = vb[x].x;
+          Bs[kq + 1][cc] = vb[x].y;
+          Bs[kq + 2][cc] = vb[x].z;
+          Bs[kq + 3][cc] = vb[x].w;
+        }
+      } else {
+        for (int e = tid; e < 64 * 32; e += 256) {
+          const int rr = e >> 5, kk = e & 31;
+          const int64_t r = r0 + rr;
+          const int k = k0 + kk;
+          As[kk][rr] = (r < n && k < dim) ? static_cast<double>(X[r * dim + k]) : 0.0;
+        }
+        for (int e = tid; e < CW * 32; e += 256) {
+          const int cc = e >> 5, kk = e & 31;
+          const int c = c0 + cc, k = k0 + kk;
+          Bs[kk][cc] = (c < nlist && k < dim) ? static_cast<double>(mu[static_cast<int64_t>(c) * dim + k]) : 0.0;
+        }
       }
       __syncthreads();
 #pragma unroll 4
