@@ -1,34 +1,60 @@
 """Build libv3db.so in-tree with nvcc for sm_100a (no JIT cache, so the .so travels with
-the repo snapshot to the GPU box).  Usage: python -m paper_2603_03065_b200.build"""
+the repo snapshot to the GPU box).  Usage: python -m paper_2603_03065_b200.build
+
+Each csrc/*.cu compiles to its own object (in parallel, only when it or a header changed), then
+one nvcc link makes the shared library."""
 from __future__ import annotations
 
 import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libv3db.so")
+OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3"]
 
 
 def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "v3db.h")]
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in deps):
-        return OUT
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-I" + os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *sources()]
+def headers() -> list[str]:
+    return glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "v3db.h")]
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+
+
+def _compile(src: str, verbose: bool) -> str:
+    obj = _obj(src)
+    cmd = [NVCC, *FLAGS, "-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(obj + ".tmp", obj)
+    return obj
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    hdr = max(os.path.getmtime(p) for p in headers())
+    stale = [s for s in sources()
+             if force or not os.path.exists(_obj(s)) or os.path.getmtime(_obj(s)) < max(os.path.getmtime(s), hdr)]
+    if stale:
+        with ThreadPoolExecutor(max_workers=min(len(stale), os.cpu_count() or 4)) as ex:
+            list(ex.map(lambda s: _compile(s, verbose), stale))
+    objs = [_obj(s) for s in sources()]
+    if stale or not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
+        subprocess.run([NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs], check=True)
+        os.replace(OUT + ".tmp", OUT)
     return OUT
 
 
