@@ -24,6 +24,12 @@ KEYS = [
     "smsp__warp_issue_stalled_mio_throttle_per_warp_active.pct",
     "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
     "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    # tensor pipe (tcgen05 kind::i8: the coarse kernels)
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
 ]
 
 
@@ -35,9 +41,9 @@ def rep(path):
     for v in rows[2:]:
         name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
         print(f"## {name[:140]}\n\n| metric | value | unit |\n|---|---|---|")
-        for k in KEYS:
-            if k in h:
-                i = h.index(k)
+        for k in KEYS:  # raw column names may carry a section prefix ("TPC.TriageCompute.")
+            i = next((j for j, col in enumerate(h) if col == k or col.endswith("." + k)), None)
+            if i is not None and v[i] not in ("", "n/a"):
                 print(f"| {k} | {v[i]} | {units[i]} |")
         print()
 
