@@ -1,15 +1,17 @@
 // fx16.cu -- NEXT-1: the five-step semantics on the paper's own 16-bit
 // fixed-point representation: coordinates round((2^16-1) v / v_max) in
 // [-65535, 65535] (int32), all distances exact in int64 (d_max = 2^63 - 1), codewords the residual
-// sub-vectors themselves (R19).  Same steps and readings as the int8 path; different arithmetic:
-//   * Step 1 (and the build ranking): <x, mu> via IEEE-double FMAs -- exact, every partial sum is
-//     an integer below dim * 65535^2 < 2^53 -- in a tiled kernel that writes the [rows x nlist]
-//     int64 distance matrix; a warp per row then keeps the R smallest (d, i) as 64-bit composite
-//     keys (d << sh | i, sh from the distance bound);
-//   * Steps 3-5: one CTA per query, the factorised table A_q[m][c] = -2 <C_{m,c}, q^{(m)}> in int64
-//     (shared memory), D = d_i + P_{i,j} + sum_m A_q[m][c_m] per slot, every D to the trace, per-warp
-//     threshold top-k on (D << sh5 | slot) keys for the k-th D, then the exact (D, item) order of
-//     the candidates with D <= that value (ties resolved by item id, R10).
+// sub-vectors themselves (R19).  Same steps and readings as the int8 path; different arithmetic
+// (DESIGN.md §6.6):
+//   * Step 1-2 (and the build ranking), fx_coarse_kernel: <x, mu> via IEEE-double FMAs -- exact,
+//     every partial sum is an integer below dim * 65535^2 < 2^53 -- in 64 x 128 tiles whose keys
+//     (d << sh | i, sh from the distance bound) update each row's top-R list in shared memory; the
+//     distance matrix never reaches HBM (a materialised matrix + warp top-R only for R > 128);
+//   * Steps 3-5, scan_fx_kernel: one CTA per query, the factorised table
+//     A_q[m][c] = -2 <C_{m,c}, q^{(m)}> in int64 (conflict-free rotated layout for M % 8 == 0,
+//     Ks = 256), D = d_i + P_{i,j} + sum_m A_q[m][c_m] per slot, every D to the trace, buffered
+//     per-warp top-k on (D << sh5 | slot) keys with a CTA-wide admission bound, a rank merge, and
+//     an exact re-selection by item id when ties at the k-th distance straddle the lists (R10).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
