@@ -49,7 +49,9 @@ int plan_lut(int M, int Ks, int d, int* G) {
   if (M < 4 || M % 4 != 0 || M > 128 || d % 4 != 0 || Ks < 1 || Ks > 256) return 0;
   const char* force = getenv("V3DB_LUT_MODE");  // test/bench hook: "w32" forces W32 where P64 applies
   const bool want_w32 = force && force[0] == 'w';
-  const bool p64_ok = M == 4 || M == 8 || M == 16 || M == 32;
+  // P64: one rotation group of all M <= 32 subspaces; lane l reads column l + s < 64 at step s,
+  // which holds subspace (l + s) mod M (columns m, m + M, ... replicate subspace m)
+  const bool p64_ok = M <= 32 && (M == 4 || M == 8 || M == 12 || M == 16 || M == 20 || M == 24 || M == 28 || M == 32);
   const bool w32_ok = M == 8 || M == 12 || M == 16 || M == 24 || M == 32 || M == 48 || M == 64 || M == 96 || M == 128;
   // default: P64 (1 ALU op per lookup) wherever it applies; W32 (2 ALU ops, half the table) for
   // the other shapes.  Measured with 256-codeword tables (P64: 64 KB table, 2 stages of 16 chunks;
@@ -741,7 +743,11 @@ cudaError_t scan_dispatch(const v3db_snapshot* s, RotArgs& a, int64_t nq, cudaSt
     switch (s->M) {
       case 4: V3DB_ROT(4, kLutP64)
       case 8: V3DB_ROT(8, kLutP64)
+      case 12: V3DB_ROT(12, kLutP64)
       case 16: V3DB_ROT(16, kLutP64)
+      case 20: V3DB_ROT(20, kLutP64)
+      case 24: V3DB_ROT(24, kLutP64)
+      case 28: V3DB_ROT(28, kLutP64)
       case 32: V3DB_ROT(32, kLutP64)
       default: return cudaErrorInvalidValue;
     }

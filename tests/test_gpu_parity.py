@@ -167,10 +167,15 @@ def test_rotated_w32_geometry(v3db, name, monkeypatch):
     s.free()
 
 
-@pytest.mark.parametrize("M,d,k", [(12, 4, 10), (24, 4, 10), (48, 2 * 4, 100), (96, 8, 100), (128, 4, 37)])
-def test_rotated_group_decompositions(v3db, M, d, k):
-    """W32 rotation groups of every size mix: 12 = 8+4, 24 = 16+8, 48 = 32+16, 96 = 3x32 (512
-    consumer threads), 128 = 4x32; ragged list fill and a ragged last chunk (L % 32 != 0)."""
+@pytest.mark.parametrize("M,d,k,geo", [(12, 4, 10, "w32"), (24, 4, 10, "w32"), (48, 2 * 4, 100, None),
+                                       (96, 8, 100, None), (128, 4, 37, None), (12, 4, 10, None),
+                                       (20, 4, 10, None), (24, 4, 10, None), (28, 4, 19, None)])
+def test_rotated_group_decompositions(v3db, M, d, k, geo, monkeypatch):
+    """W32 rotation groups of every size mix: 12 = 8+4, 24 = 16+8 (forced), 48 = 32+16, 96 = 3x32
+    (512 consumer threads), 128 = 4x32; the P64 geometry with M not dividing 64 (12, 20, 24, 28:
+    columns l + s hold subspace (l + s) mod M); ragged list fill and a ragged last chunk."""
+    if geo:
+        monkeypatch.setenv("V3DB_LUT_MODE", geo)
     rng = np.random.default_rng(100 + M)
     N, D, nlist, L, Ks = 3000, M * d, 12, 300, 256
     db = rng.integers(-100, 100, size=(N, D)).astype(np.int8)
