@@ -19,8 +19,11 @@ def _init(s, q):
 
 
 def _work(args):
-    rows, nprobe, k = args
-    return oracle.query_batch(_S, _Q, nprobe, k, rows=rows)
+    rows, nprobe, k = args[:3]
+    out = oracle.query_batch(_S, _Q, nprobe, k, rows=rows)
+    if len(args) > 3 and not args[3]:       # the candidate trace is not wanted for this shard
+        out["trace_cand_dist"] = out["trace_cand_dist"][:0]
+    return out
 
 
 def oracle_queries(s, queries, nprobe, k, rows=None, workers=None):
@@ -35,6 +38,35 @@ def oracle_queries(s, queries, nprobe, k, rows=None, workers=None):
                              initargs=(s, queries)) as ex:
         parts = list(ex.map(_work, [(sh, nprobe, k) for sh in shards if len(sh)]))
     return {key: np.concatenate([p[key] for p in parts]) for key in parts[0]}
+
+
+def oracle_queries_all(s, queries, nprobe, k, trace_rows, workers=None):
+    """oracle.query_batch over EVERY row of `queries` (process pool); trace_cand_dist is kept only
+    for the rows in `trace_rows` (sorted), to bound the host memory and the pickling at C4 sizes.
+    Returns (outputs without the trace for all rows, trace_cand_dist for trace_rows)."""
+    import multiprocessing as mp
+    workers = workers or min(32, len(os.sched_getaffinity(0)))
+    rows = np.arange(queries.shape[0])
+    shards = [sh for sh in np.array_split(rows, workers * 4) if len(sh)]
+    want = set(int(r) for r in trace_rows)
+    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork"), initializer=_init,
+                             initargs=(s, queries)) as ex:
+        jobs = []
+        for sh in shards:   # split every shard into its traced and untraced rows
+            tr = np.array([r for r in sh if int(r) in want], dtype=np.int64)
+            nt = np.array([r for r in sh if int(r) not in want], dtype=np.int64)
+            if len(tr):
+                jobs.append((tr, True))
+            if len(nt):
+                jobs.append((nt, False))
+        parts = list(ex.map(_work, [(r, nprobe, k, t) for r, t in jobs]))
+    order = np.concatenate([r for r, _ in jobs])
+    inv = np.argsort(order)
+    full = {key: np.concatenate([p[key] for p in parts])[inv] for key in parts[0] if key != "trace_cand_dist"}
+    tr_rows = np.concatenate([r for r, t in jobs if t]) if any(t for _, t in jobs) else np.zeros(0, np.int64)
+    tr_vals = np.concatenate([p["trace_cand_dist"] for p, (_, t) in zip(parts, jobs) if t])
+    o = np.argsort(tr_rows)
+    return full, tr_rows[o], tr_vals[o]
 
 
 def first_mismatch(a: np.ndarray, b: np.ndarray) -> str:

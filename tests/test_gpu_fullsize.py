@@ -1,14 +1,14 @@
 """GPU parity at BASELINE.json's full sizes (C1-C4), in the launch configuration bench.py times
-(the whole query batch, V3DB_SCAN_AUTO, trace on), on sampled outputs the oracle computes one by
-one.
+(the whole query batch, V3DB_SCAN_AUTO, trace on): every query row of the batch (the candidate
+trace of every row for C1-C3, of 2048 sampled rows for C4), the oracle run on a process pool.
 
 At these sizes the oracle's own build is too slow to run in a test (C4: 2.1e13 MACs to rank), so
 the GPU-built snapshot is verified directly against the build rules instead (SURVEY.md §8(c)
 B1-B6, pins P7/P8): exact structure, every centroid and codeword, the greedy placement replayed
 for sampled vectors, the PQ codes of sampled slots by brute force.  The oracle's query (Steps
-1-5) then runs on that verified snapshot for sampled queries and every output
-row -- top-k ids and distances, probed lists, their distances and the full candidate trace -- must
-equal the GPU's bit for bit.
+1-5) then runs on that verified snapshot for every query and every output --
+top-k ids and distances, probed lists, their distances and the candidate trace -- must equal the
+GPU's bit for bit.
 """
 import numpy as np
 import pytest
@@ -16,7 +16,7 @@ import pytest
 import oracle
 from synth import generate, get_config
 
-from .gpu_util import first_mismatch
+from .gpu_util import first_mismatch, oracle_queries_all
 from .snapshot_checks import check_snapshot
 
 torch = pytest.importorskip("torch")
@@ -57,11 +57,18 @@ def test_full_size_sampled_parity(v3db, name):
     s.free()
     ref_snap = oracle.Snapshot(snap["centroids"], snap["codebooks"], snap["ids"], snap["codes"], snap["counts"],
                                snap["list_of"])
-    sample = np.unique(np.concatenate([rng.choice(cfg.Q, 40, replace=False), [0, cfg.Q - 1]]))
-    ref = oracle.query_batch(ref_snap, inp.queries, cfg.nprobe, cfg.k, rows=sample)
-    for key, exp in ref.items():
-        got = out[key][torch.from_numpy(sample).cuda()].cpu().numpy()
+    # EVERY query row: top-k ids and distances, probed lists and their distances; the candidate
+    # trace for every row up to 2^28 entries (C1-C3), else for 2048 sampled rows (C4: 3.2 GB)
+    if cfg.Q * cfg.nprobe * cfg.L <= (1 << 28):
+        trace_rows = np.arange(cfg.Q)
+    else:
+        trace_rows = np.unique(np.concatenate([rng.choice(cfg.Q, 2046, replace=False), [0, cfg.Q - 1]]))
+    full, tr_rows, tr_vals = oracle_queries_all(ref_snap, inp.queries, cfg.nprobe, cfg.k, trace_rows)
+    for key, exp in full.items():
+        got = out[key].cpu().numpy()
         assert np.array_equal(got, exp), f"{name} {key}: {first_mismatch(got, exp)}"
+    got = out["trace_cand_dist"][torch.from_numpy(tr_rows).cuda()].cpu().numpy()
+    assert np.array_equal(got, tr_vals), f"{name} trace_cand_dist: {first_mismatch(got, tr_vals)}"
     for a, qi in enumerate(wq):
         exp = oracle.witness(inp.queries[qi], ref_snap, cfg.nprobe)
         for key, e in zip(("list_order", "list_dist", "lut_sel", "cand_items", "cand_dist"), exp):
