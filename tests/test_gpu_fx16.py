@@ -9,7 +9,7 @@ import pytest
 import oracle
 from synth import generate_float, get_config
 
-from .gpu_util import first_mismatch, oracle_queries
+from .gpu_util import first_mismatch, oracle_queries, oracle_queries_all
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -224,7 +224,8 @@ def test_fx_full_size_sampled_parity(v3db, name):
     """BASELINE.json's full sizes in bench.py --precision fx16's launch configuration (whole batch,
     trace on): the GPU encoding equals the oracle's on sampled rows and on every query, the GPU
     snapshot obeys the build rules (tests/snapshot_checks.py with R18/R19), and the oracle's query
-    on that snapshot reproduces sampled output rows bit for bit."""
+    on that snapshot reproduces every query row bit for bit (the candidate trace of every row, or
+    of 2048 rows where it exceeds 2^27 entries)."""
     from types import SimpleNamespace
 
     from .snapshot_checks import check_snapshot
@@ -247,11 +248,17 @@ def test_fx_full_size_sampled_parity(v3db, name):
     s.free()
     ref_snap = oracle.Snapshot(snap["centroids"], snap["codebooks"], snap["ids"], snap["codes"], snap["counts"],
                                snap["list_of"])
-    sample = np.unique(np.concatenate([rng.choice(cfg.Q, 40, replace=False), [0, cfg.Q - 1]]))
-    ref = oracle.query_batch(ref_snap, qs, cfg.nprobe, cfg.k, rows=sample)
-    for key, exp in ref.items():
-        got = out[key][torch.from_numpy(sample).cuda()].cpu().numpy()
+    # every query row; the int64 candidate trace of every row up to 2^27 entries, else 2048 rows
+    if cfg.Q * cfg.nprobe * cfg.L <= (1 << 27):
+        trace_rows = np.arange(cfg.Q)
+    else:
+        trace_rows = np.unique(np.concatenate([rng.choice(cfg.Q, 2046, replace=False), [0, cfg.Q - 1]]))
+    full, tr_rows, tr_vals = oracle_queries_all(ref_snap, qs, cfg.nprobe, cfg.k, trace_rows)
+    for key, exp in full.items():
+        got = out[key].cpu().numpy()
         assert np.array_equal(got, exp), f"{name} {key}: {first_mismatch(got, exp)}"
+    got = out["trace_cand_dist"][torch.from_numpy(tr_rows).cuda()].cpu().numpy()
+    assert np.array_equal(got, tr_vals), f"{name} trace_cand_dist: {first_mismatch(got, tr_vals)}"
 
 
 def test_fx_host_entry(v3db):
