@@ -977,6 +977,23 @@ size_t fx_rest(const FxScanArgs& a, int nw) {
 
 template <int MT, int KS, bool GA, bool ROT = false>
 cudaError_t launch_scan_fx(const FxScanArgs& a, int64_t nq, size_t smem8, cudaStream_t st) {
+  // A table too large for two CTAs per SM leaves one CTA of 8 warps per SM: then 12 warps when
+  // their per-warp lists still fit (experiment hook V3DB_FX_W12=0/1)
+  if constexpr (MT == 96 && ROT) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t smem12 = smem8 - fx_rest(a, 8) + fx_rest(a, 12);
+    const char* w = getenv("V3DB_FX_W12");
+    if (smem8 > 114 * 1024 && smem12 <= static_cast<size_t>(optin) && !(w && w[0] == '0')) {
+      auto kern = scan_fx_kernel<MT, KS, GA, ROT, 12>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem12));
+      if (e != cudaSuccess) return e;
+      kern<<<static_cast<unsigned>(nq), 384, smem12, st>>>(a);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   auto kern = scan_fx_kernel<MT, KS, GA, ROT, 8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem8));
   if (e != cudaSuccess) return e;
