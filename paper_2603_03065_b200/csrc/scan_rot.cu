@@ -111,6 +111,7 @@ struct RotArgs {
   const int8_t* queries;
   int dim, d, Ks, L, Lp, nprobe, k, cap, NS, SEG;
   int first_mult;         // first compaction at first_mult * k buffered candidates (capped by hw)
+  int direct_max;         // final selection by direct ranking when at most this many are buffered
   uint32_t off_stage, off_desc, off_vc, off_buf, off_hist, off_probe, off_q, off_int, off_bar, stage_bytes;
   const int8_t* cbT;
   const uint8_t* codes;   // codes_rot [nlist][Lp/32][unit][lane][U]
@@ -600,8 +601,16 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
 
   // Final Step 5: the k smallest (D, item) keys, (d_max, -1) past the valid candidates (R11).
   // The survivors (resolved, distinct keys) are placed by rank: one pass, one barrier.
-  uint32_t t2 = tau;
-  const int n = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, a.k, true, &t2);
+  // Few survivors: resolve them all and place by rank directly (no radix select, no barriers
+  // beyond one); many: cut to the k smallest D (ties kept) first.
+  int n = n_base;
+  if (n_base <= a.direct_max) {
+    for (int e = tid; e < n_base; e += NT) buf[e] = resolve_key(buf[e], probe, a);
+    bar_c<NT>();
+  } else {
+    uint32_t t2 = tau;
+    n = compact<NT, CAPM>(buf, hist, s_int, probe, a, n_base, a.k, true, &t2);
+  }
   for (int e = tid; e < n; e += NT) {
     const uint64_t key = buf[e];
     int rank = 0;
@@ -814,6 +823,8 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
   {
     const char* f = getenv("V3DB_FIRST");  // experiments
     a.first_mult = f ? atoi(f) : 16;  // measured: 16 vs 4 -0.8 % at C4, -1.8 % at C3, flat at C1/C2
+    const char* dm = getenv("V3DB_DIRECT");  // experiments
+    a.direct_max = dm ? atoi(dm) : 256;  // measured: C1 scan -10 %, C2/C3 -2 %, C4 flat (1024: C4 +5 %)
   }
   // L2-aware schedule when the probed lists do not fit in L2 anyway and the batch is large
   const char* sched = getenv("V3DB_SCHED");
