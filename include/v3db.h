@@ -135,12 +135,20 @@ int v3db_query_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32
                      int32_t* trace_list_dist, int32_t* trace_cand_dist, void* stream);
 
 /* Scan-kernel selection for v3db_query_batch_ex (results are bit-identical for all). */
-#define V3DB_SCAN_AUTO 0    /* ROTATED when the snapshot's shape supports it, else GENERIC   */
-#define V3DB_SCAN_GENERIC 1 /* per-query LUT [M][Ks] in shared memory, any shape            */
-#define V3DB_SCAN_ROTATED 2 /* conflict-free rotated LUT (M % 4 == 0, d % 4 == 0, M <= 128) */
+#define V3DB_SCAN_AUTO 0       /* LIST_MAJOR where supported, else ROTATED, else GENERIC          */
+#define V3DB_SCAN_GENERIC 1    /* per-query LUT [M][Ks] in shared memory, any shape               */
+#define V3DB_SCAN_ROTATED 2    /* conflict-free rotated LUT (M % 4 == 0, d % 4 == 0, M <= 128)    */
+#define V3DB_SCAN_LIST_MAJOR 3 /* Steps 3-4 as the exact identity d_i + P_ij - 2 <q, xhat_ij>:   */
+                               /* tcgen05 int8 tiles per (list, probing queries) (dim % 16 == 0) */
 
 /* v3db_query_batch_ex -- v3db_query_batch with an explicit scan kernel (`algo`, one of
- * V3DB_SCAN_*).  EINVAL for an unknown algo, or ROTATED on a snapshot it does not support. */
+ * V3DB_SCAN_*).  EINVAL for an unknown algo, or a kernel the snapshot's shape does not
+ * support.  LIST_MAJOR computes every D_{i,j} of Step 4 from the identity
+ *   sum_m LUT_{i,m,code_m} = dist(q - mu_i, xhat_ij) = d_i + P_ij - 2 <q, xhat_ij>
+ * (xhat_ij the slot's reconstruction; P_ij = ||xhat||^2 + 2 <mu_i, xhat>), exact
+ * in int32, so every output equals the literal Steps 3-4 bit for bit; with
+ * trace_cand_dist NULL it writes the candidate distances to library scratch
+ * (4 * nq * nprobe * L bytes) because its Step 5 reads them back. */
 int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32_t nprobe,
                         int32_t k, int32_t* out_ids, int32_t* out_dist, int32_t* trace_lists,
                         int32_t* trace_list_dist, int32_t* trace_cand_dist, int32_t algo,
@@ -250,13 +258,46 @@ int v3db_snapshot_export(v3db_snapshot_t s, int32_t field, void* host_dst, size_
 /* Profiling hooks (used by bench.py; off by default, never change results).
  * v3db_profile_enable(1) makes every v3db_query_batch* call record CUDA events on its
  * stream around each kernel; v3db_profile_read waits for the most recent call's events and
- * writes up to n elapsed times in milliseconds: [0] Steps 1-2 (coarse top-nprobe kernel),
- * [1] Steps 3-5 (scan kernel(s) incl. any grouping pass).  Not thread-safe: profile one
+ * writes up to n (<= 5) elapsed times in milliseconds: [0] Steps 1-2 (coarse top-nprobe
+ * kernels), [1] Steps 3-5 (everything after Steps 1-2), [2] the scan's main kernel alone (the
+ * list-major contraction / the rotated or generic scan), [3] the scan's prologue (pair grouping or
+ * L2-aware query order), [4] the scan's epilogue (list-major Step-5 selection; 0 for the
+ * query-major scans, whose kernel includes Step 5).  Not thread-safe: profile one
  * stream at a time.  v3db_kernel_launches returns the number of kernels this library has
  * launched since load (all entry points). */
 int v3db_profile_enable(int32_t on);
 int v3db_profile_read(float* out_ms, int32_t n);
 int64_t v3db_kernel_launches(void);
+
+/* v3db_set_option / v3db_get_option -- process-wide implementation choices (never change a
+ * result: every choice is exact; tests use them to reach every code path, bench/tools to
+ * measure alternatives).  0 is the default everywhere.  Set them between calls, not while
+ * work is being enqueued from another thread.  EINVAL for an unknown key.
+ *   V3DB_OPT_LUT_W32      1: the W32 rotated table even where P64 applies (read at build)
+ *   V3DB_OPT_COARSE_SIMT  1: Steps 1-2 / build ranking on the mma.sync kernel (not tcgen05)
+ *   V3DB_OPT_SCHED        L2-aware query order of the query-major scans: 0 auto, 1 on, 2 off
+ *   V3DB_OPT_FX_NOROT     1: no rotated fixed-point code copy (read at fx16 build)
+ *   V3DB_OPT_FX_W12       fx16 scan warps per CTA (0 = auto)
+ *   V3DB_OPT_SCAN_SEG / _NS / _CAP / _FIRST / _DIRECT   rotated-LUT scan geometry (0 = auto)
+ *   V3DB_OPT_LM_NT        list-major scan: (query, rank) pairs per work item, 32/64/128/256
+ *                         (0 = auto: the largest whose B operand fits)
+ *   V3DB_OPT_AUTO_SCAN    the kernel V3DB_SCAN_AUTO picks where several apply (0 = list-major,
+ *                         else one of the V3DB_SCAN_* values) */
+#define V3DB_OPT_LUT_W32 0
+#define V3DB_OPT_COARSE_SIMT 1
+#define V3DB_OPT_SCHED 2
+#define V3DB_OPT_FX_NOROT 3
+#define V3DB_OPT_FX_W12 4
+#define V3DB_OPT_SCAN_SEG 5
+#define V3DB_OPT_SCAN_NS 6
+#define V3DB_OPT_SCAN_CAP 7
+#define V3DB_OPT_SCAN_FIRST 8
+#define V3DB_OPT_SCAN_DIRECT 9
+#define V3DB_OPT_LM_NT 10
+#define V3DB_OPT_AUTO_SCAN 11
+#define V3DB_OPT_COUNT 12
+int v3db_set_option(int32_t key, int64_t value);
+int64_t v3db_get_option(int32_t key);
 
 /* v3db_last_error -- thread-local message for the last non-OK status on this thread
  * ("" if none).  The pointer stays valid until the next call on the same thread. */

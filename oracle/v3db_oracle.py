@@ -38,7 +38,12 @@ def encode_fixed_point(x, v_max: float):
     |coordinate| over all involved vectors.  Reading R18: the product and quotient in IEEE double
     (in that order), round half away from zero.  Returns int32 in [-(2^16-1), 2^16-1]."""
     y = np.asarray(x, dtype=np.float64) * float(FX_SCALE) / float(v_max)
-    r = np.where(y >= 0, np.floor(y + 0.5), -np.floor(-y + 0.5))
+    # round half away from zero on |y|: floor(|y|) plus one when the fractional part is >= 1/2.
+    # |y| - floor(|y|) is exact in IEEE double, so the comparison is the mathematical one
+    # (floor(|y| + 0.5) would round y = nextafter(0.5, 0) up: the addition rounds to 1.0).
+    a = np.abs(y)
+    f = np.floor(a)
+    r = np.sign(y) * (f + (a - f >= 0.5))
     assert np.abs(r).max(initial=0) <= FX_SCALE
     return r.astype(np.int32)
 

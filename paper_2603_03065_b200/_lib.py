@@ -11,15 +11,18 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libv3db.so")
+# V3DB_LIB=debug loads the debug build (device-side invariant traps, identical results)
+LIB_PATH = os.path.join(HERE, "libv3db_debug.so" if os.environ.get("V3DB_LIB") == "debug" else "libv3db.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "v3db.h")
 
 V3DB_OK, V3DB_EINVAL, V3DB_EINFEASIBLE, V3DB_ENOMEM, V3DB_ECUDA = range(5)
 STATUS_NAMES = {0: "V3DB_OK", 1: "V3DB_EINVAL", 2: "V3DB_EINFEASIBLE", 3: "V3DB_ENOMEM", 4: "V3DB_ECUDA"}
-SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED = 0, 1, 2
+SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, SCAN_LIST_MAJOR = 0, 1, 2, 3
 SHAPE_GREEDY, SHAPE_REBALANCE = 0, 1
 FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_IDS, FIELD_CODES, FIELD_COUNTS, FIELD_LIST_OF = range(6)
 KIND_INT8, KIND_FX16 = 0, 1
+(OPT_LUT_W32, OPT_COARSE_SIMT, OPT_SCHED, OPT_FX_NOROT, OPT_FX_W12, OPT_SCAN_SEG, OPT_SCAN_NS, OPT_SCAN_CAP,
+ OPT_SCAN_FIRST, OPT_SCAN_DIRECT, OPT_LM_NT, OPT_AUTO_SCAN) = range(12)
 
 _c_i8p = ctypes.c_void_p
 _c_i32p = ctypes.c_void_p
@@ -60,6 +63,8 @@ _SIGS = {
     "v3db_profile_enable": (ctypes.c_int, [ctypes.c_int32]),
     "v3db_profile_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_float), ctypes.c_int32]),
     "v3db_kernel_launches": (ctypes.c_int64, []),
+    "v3db_set_option": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64]),
+    "v3db_get_option": (ctypes.c_int64, [ctypes.c_int32]),
 }
 
 _lib = None

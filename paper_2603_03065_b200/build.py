@@ -13,8 +13,13 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-OUT = os.path.join(HERE, "libv3db.so")
-OBJ = os.path.join(HERE, "build")
+# variant -> (library, object directory, extra flags).  "debug" adds the device-side invariant
+# traps (V3DB_DCHECK) and the V3DB_SYNC_CHECK launch checks; results are identical.
+VARIANTS = {
+    "release": ("libv3db.so", "build", []),
+    "debug": ("libv3db_debug.so", "build_debug", ["-DV3DB_DEBUG"]),
+}
+OUT = os.path.join(HERE, VARIANTS["release"][0])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3"]
@@ -28,13 +33,17 @@ def headers() -> list[str]:
     return glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "v3db.h")]
 
 
-def _obj(src: str) -> str:
-    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def lib_path(variant: str = "release") -> str:
+    return os.path.join(HERE, VARIANTS[variant][0])
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = _obj(src)
-    cmd = [NVCC, *FLAGS, "-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj + ".tmp"]
+def _obj(src: str, variant: str = "release") -> str:
+    return os.path.join(HERE, VARIANTS[variant][1], os.path.basename(src)[:-3] + ".o")
+
+
+def _compile(src: str, verbose: bool, variant: str = "release") -> str:
+    obj = _obj(src, variant)
+    cmd = [NVCC, *FLAGS, *VARIANTS[variant][2], "-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -43,20 +52,23 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, variant: str = "release") -> str:
+    out = lib_path(variant)
+    os.makedirs(os.path.join(HERE, VARIANTS[variant][1]), exist_ok=True)
     hdr = max(os.path.getmtime(p) for p in headers())
     stale = [s for s in sources()
-             if force or not os.path.exists(_obj(s)) or os.path.getmtime(_obj(s)) < max(os.path.getmtime(s), hdr)]
+             if force or not os.path.exists(_obj(s, variant))
+             or os.path.getmtime(_obj(s, variant)) < max(os.path.getmtime(s), hdr)]
     if stale:
         with ThreadPoolExecutor(max_workers=min(len(stale), os.cpu_count() or 4)) as ex:
-            list(ex.map(lambda s: _compile(s, verbose), stale))
-    objs = [_obj(s) for s in sources()]
-    if stale or not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
-        subprocess.run([NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *objs], check=True)
-        os.replace(OUT + ".tmp", OUT)
-    return OUT
+            list(ex.map(lambda s: _compile(s, verbose, variant), stale))
+    objs = [_obj(s, variant) for s in sources()]
+    if stale or not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(o) for o in objs):
+        subprocess.run([NVCC, *ARCH, "-shared", "-o", out + ".tmp", *objs], check=True)
+        os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force=True))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv,
+                variant="debug" if "--debug" in sys.argv else "release"))

@@ -156,6 +156,33 @@ __global__ void rotate_kernel(const uint8_t* __restrict__ codes, const int32_t* 
   }
 }
 
+// xhat[i][jp][u] = C_{m, code_{i,jp,m}}[u - m d] (m = u / d): the reconstruction of slot (i, jp)
+// (concatenated codewords) for valid slots, 0 for padding slots and jp >= L.
+// 16 bytes per thread (dim % 16 == 0).
+__global__ void xhat_kernel(const uint8_t* __restrict__ codes, const int32_t* __restrict__ counts,
+                            const int8_t* __restrict__ cb, int nlist, int L, int Lp, int dim, int M, int Ks,
+                            int8_t* __restrict__ out) {
+  const int d = dim / M, cpr = dim / 16;
+  const int64_t total = static_cast<int64_t>(nlist) * Lp * cpr;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t sp = e / cpr;
+    const int c = static_cast<int>(e - sp * cpr);
+    const int i = static_cast<int>(sp / Lp), jp = static_cast<int>(sp - static_cast<int64_t>(i) * Lp);
+    alignas(16) int8_t v[16];
+    if (jp < __ldg(counts + i)) {
+      const uint8_t* cd = codes + (static_cast<int64_t>(i) * L + jp) * M;
+      for (int b = 0; b < 16; ++b) {
+        const int u = c * 16 + b, m = u / d;
+        v[b] = cb[(static_cast<int64_t>(m) * Ks + cd[m]) * d + (u - m * d)];
+      }
+    } else {
+      for (int b = 0; b < 16; ++b) v[b] = 0;
+    }
+    *reinterpret_cast<int4*>(out + sp * dim + c * 16) = *reinterpret_cast<const int4*>(v);
+  }
+}
+
 __global__ void transpose_cb_kernel(const int8_t* __restrict__ cb, int M, int Ks, int d, int8_t* __restrict__ cbT) {
   const int total = M * Ks * d;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -217,6 +244,16 @@ cudaError_t rotate_codes(const uint8_t* codes, const int32_t* pterm, int nlist, 
   const int64_t total = static_cast<int64_t>(nlist) * Lp * M;
   const int blocks = static_cast<int>((total + 255) / 256 < 16384 ? (total + 255) / 256 : 16384);
   rotate_kernel<<<blocks, 256, 0, st>>>(codes, pterm, nlist, L, Lp, M, mode, G, rot_unit(M), codes_rot, pterm_rot);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t make_xhat(const uint8_t* codes, const int32_t* counts, const int8_t* cb, int nlist, int L, int Lp,
+                      int dim, int M, int Ks, int8_t* xhat, cudaStream_t st) {
+  if (dim % 16 != 0) return cudaErrorInvalidValue;
+  const int64_t total = static_cast<int64_t>(nlist) * Lp * (dim / 16);
+  const int blocks = static_cast<int>((total + 255) / 256 < 32768 ? (total + 255) / 256 : 32768);
+  xhat_kernel<<<blocks, 256, 0, st>>>(codes, counts, cb, nlist, L, Lp, dim, M, Ks, xhat);
   note_launch();
   return cudaGetLastError();
 }

@@ -448,10 +448,12 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   if (n <= 0) return cudaSuccess;
   const int kp = (dim + kPanel - 1) / kPanel;
   const size_t fixed = 1024 + static_cast<size_t>(kp) * kAPanelBytes + kEpiWarps * 64 * 4 + 64 * 8;
-  const int stages = static_cast<int>(std::min<size_t>(6, (227 * 1024 - fixed) / kBStageBytes));
-  const char* force = getenv("V3DB_FORCE_COARSE_MMA");
+  // (A tiles of more than ~12 K panels leave no room for two B stages: the mma.sync kernel then)
+  const int stages = fixed + 2 * kBStageBytes > 227 * 1024
+                         ? 0
+                         : static_cast<int>(std::min<size_t>(6, (227 * 1024 - fixed) / kBStageBytes));
   const bool tc_ok = dim % 16 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
-                     reinterpret_cast<uintptr_t>(mu) % 16 == 0 && stages >= 2 && !(force && force[0] == '1');
+                     reinterpret_cast<uintptr_t>(mu) % 16 == 0 && stages >= 2 && !opt(V3DB_OPT_COARSE_SIMT);
   CUtensorMap tmX, tmMu;
   if (!tc_ok || !make_tmap_i8(&tmX, X, n, dim, kRows, kPanel) || !make_tmap_i8(&tmMu, mu, nlist, dim, kChunk, kPanel))
     return coarse_topk_mma(X, n, dim, mu, cnorm, nlist, R, out_idx, out_dist, st);
@@ -474,7 +476,7 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   const size_t b_g = align256(sizeof(int32_t) * n * ngroups), b_t = align256(sizeof(int32_t) * n),
                b_c = align256(sizeof(uint64_t) * n * capc), b_n = align256(sizeof(int) * n);
   uint8_t* base = nullptr;
-  e = cudaMallocAsync(reinterpret_cast<void**>(&base), b_g + b_t + b_c + 2 * b_n, st);
+  e = scratch_alloc(reinterpret_cast<void**>(&base), b_g + b_t + b_c + 2 * b_n, st);
   if (e != cudaSuccess) return e;
   CoarseArgs a;
   a.n = n;

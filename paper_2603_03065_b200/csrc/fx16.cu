@@ -41,8 +41,11 @@ __global__ void encode_fp_kernel(const float* __restrict__ x, int64_t n, double 
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double y = __ddiv_rn(__dmul_rn(static_cast<double>(x[i]), 65535.0), v_max);
-    const double r = y >= 0.0 ? floor(__dadd_rn(y, 0.5)) : -floor(__dadd_rn(-y, 0.5));  // half away from zero (R18)
-    out[i] = static_cast<int32_t>(r);
+    // half away from zero (R18) on |y|: floor plus one when the fractional part (exact in IEEE
+    // double) is >= 1/2 -- floor(|y| + 0.5) would round the double just below 0.5 up
+    const double a = fabs(y), f = floor(a);
+    const int32_t r = static_cast<int32_t>(f) + (__dsub_rn(a, f) >= 0.5 ? 1 : 0);
+    out[i] = y < 0.0 ? -r : r;
   }
 }
 
@@ -490,6 +493,7 @@ __device__ __forceinline__ uint64_t offer_buffered(uint64_t* T, int cap, int k, 
   const unsigned bal = __ballot_sync(0xffffffffu, pass);
   if (!bal) return thr;
   const int lane = threadIdx.x & 31;
+  V3DB_DCHECK(bcnt + __popc(bal) <= cap);
   if (pass) T[bcnt + __popc(bal & ((1u << lane) - 1))] = key;
   bcnt += __popc(bal);
   if (bcnt > cap - 32) {
@@ -908,7 +912,7 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
       const int Sr = (nlist + span - 1) / span;
       uint64_t* part = nullptr;
       if (Sr > 1) {
-        e = cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(uint64_t) * rows * Sr * R, st);
+        e = scratch_alloc(reinterpret_cast<void**>(&part), sizeof(uint64_t) * rows * Sr * R, st);
         if (e != cudaSuccess) return e;
       }
       const dim3 grid(static_cast<unsigned>(rtiles), Sr);
@@ -938,7 +942,7 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
   // R > 128: the [rows x nlist] distance matrix in HBM, then a warp per row
   const int64_t chunk = std::max<int64_t>(64, std::min<int64_t>(n, (int64_t(1) << 30) / nlist));  // <= 8 GB
   int64_t* dm = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dm), sizeof(int64_t) * chunk * nlist, st);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&dm), sizeof(int64_t) * chunk * nlist, st);
   if (e != cudaSuccess) return e;
   for (int64_t lo = 0; lo < n && e == cudaSuccess; lo += chunk) {
     const int64_t rows = std::min(chunk, n - lo);
@@ -978,14 +982,13 @@ size_t fx_rest(const FxScanArgs& a, int nw) {
 template <int MT, int KS, bool GA, bool ROT = false>
 cudaError_t launch_scan_fx(const FxScanArgs& a, int64_t nq, size_t smem8, cudaStream_t st) {
   // A table too large for two CTAs per SM leaves one CTA of 8 warps per SM: then 12 warps when
-  // their per-warp lists still fit (experiment hook V3DB_FX_W12=0/1)
+  // their per-warp lists still fit (option V3DB_OPT_FX_W12 = 8 forces 8 warps)
   if constexpr (MT == 96 && ROT) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const size_t smem12 = smem8 - fx_rest(a, 8) + fx_rest(a, 12);
-    const char* w = getenv("V3DB_FX_W12");
-    if (smem8 > 114 * 1024 && smem12 <= static_cast<size_t>(optin) && !(w && w[0] == '0')) {
+    if (smem8 > 114 * 1024 && smem12 <= static_cast<size_t>(optin) && opt(V3DB_OPT_FX_W12) != 8) {
       auto kern = scan_fx_kernel<MT, KS, GA, ROT, 12>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem12));
       if (e != cudaSuccess) return e;
@@ -1050,7 +1053,7 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   const bool a_smem = abytes + rest <= static_cast<size_t>(optin);
   if (!a_smem) {  // the table in per-query global scratch
     void* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, abytes * nq, st);
+    cudaError_t e = scratch_alloc(&scratch, abytes * nq, st);
     if (e != cudaSuccess) return e;
     a.Ag = static_cast<int64_t*>(scratch);
     e = launch_scan_fx<0, 0, true>(a, nq, rest, st);  // canonical codes
@@ -1059,12 +1062,12 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   }
   const size_t smem = abytes + rest;
   // the int8 scan's L2-aware query order, under the same condition (snapshot codes beyond L2)
-  const char* sched = getenv("V3DB_SCHED");
-  const bool want = sched ? sched[0] == '1'
+  const int64_t sched = opt(V3DB_OPT_SCHED);
+  const bool want = sched ? sched == 1
                           : (nq >= 2048 && static_cast<int64_t>(s->nlist) * s->L * s->M > (int64_t(64) << 20));
   if (want) {
     void* sbuf = nullptr;
-    cudaError_t e = cudaMallocAsync(&sbuf, sizeof(int32_t) * (2 * nq + s->nlist), st);
+    cudaError_t e = scratch_alloc(&sbuf, sizeof(int32_t) * (2 * nq + s->nlist), st);
     if (e != cudaSuccess) return e;
     e = minhash_order(lists, nq, nprobe, s->nlist, static_cast<int32_t*>(sbuf), st);
     if (e == cudaSuccess) {
@@ -1077,8 +1080,12 @@ cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, 
   return fx_scan_launch(s, a, nq, smem, st);
 }
 
+bool fx_rot_supported(int M, int Ks) {
+  return Ks == 256 && (M == 8 || M == 16 || M == 24 || M == 32 || M == 64 || M == 96);
+}
+
 static cudaError_t fx_scan_launch(const v3db_snapshot* s, FxScanArgs& a, int64_t nq, size_t smem, cudaStream_t st) {
-  const bool rot = s->codes_rot16 != nullptr;  // M % 16 == 0, Ks == 256 (set at build)
+  const bool rot = s->codes_rot16 != nullptr && fx_rot_supported(s->M, s->Ks);  // built iff supported
   if (rot) a.codes = s->codes_rot16;
   switch (s->M) {
     case 8: return launch_scan_fx_m<8>(a, nq, smem, st, rot);

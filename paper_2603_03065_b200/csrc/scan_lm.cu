@@ -1,0 +1,668 @@
+// scan_lm.cu -- Steps 3-5 of PAPER.md §4.2, list-major, on the 5th-gen tensor cores.
+//
+// Step 3 builds LUT_{i,m,c} = dist(C_{m,c}, (q - mu_i)^{(m)}) and Step 4 sums
+// the entries a slot's codes select.  With xhat_{i,j} the slot's reconstruction
+// (its codewords concatenated) that sum is the exact integer identity
+//     d~_{i,j} = sum_m LUT_{i,m,code_m} = dist(q - mu_i, xhat) = d_i + P_{i,j} - 2 <q, xhat_{i,j}>
+// with P_{i,j} = ||xhat||^2 + 2 <mu_i, xhat> (per slot, built once) -- every term an integer below
+// 2^31, so the result equals the literal Steps 3-4 bit for bit.
+// Grouped by list, the per-query terms <q, xhat> of all the queries probing list i form a dense
+// int8 contraction  [128 slots x D] . [D x n_i queries] -> int32, issued as tcgen05.mma.kind::i8
+// (M = 128 slots, N = the probing queries, K = 32) with the slots' xhat brought in by TMA and the
+// gathered query rows by cp.async; the accumulators live in TMEM.  Each list tile is read once per
+// batch for all the queries that probe it instead of once per query.
+//
+// Work item = (list i, up to NT of the (query, rank) pairs probing it).  Warp roles (persistent
+// CTA, one per SM, static round-robin over the items):
+//   warp 0      one lane: TMA loads of the xhat tiles (128 slots x 128-byte K panel) into a ring;
+//   warp 1      one lane: the MMAs (double-buffered B operand, NACC TMEM accumulators);
+//   warps 2-3   gather the item's query rows into the 128B-swizzled K-major B operand (cp.async)
+//               and the per-pair metadata (trace row, d_i, group-minimum row);
+//   warps 4-11  epilogue: tcgen05.ld (lane = slot, column = pair), D = d_i + P - 2 acc, padding
+//               slots d_max, the whole trace row segment with coalesced stores
+//               (32 lanes = 32 consecutive slots), and the minimum D of every 32-slot group.
+// Step 5, lm_select_kernel, one CTA per query: tau = the k-th smallest group
+// minimum (>= the k-th smallest D: k distinct candidates reach it), then an exact radix selection
+// of the k smallest (D, item) keys among the slots of the groups whose minimum is <= tau (read
+// back from the trace), ties at the k-th distance resolved by item id (R10).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "tc_common.cuh"
+#include "topk.cuh"
+#include "v3db_internal.cuh"
+
+namespace v3db {
+namespace {
+
+constexpr int kTile = 128;                              // slots per tile (UMMA M) = TMEM lanes
+constexpr int kPanel = 128;                             // bytes of K per swizzled panel
+constexpr uint32_t kAStageBytes = kTile * kPanel;       // 16 KB
+constexpr int kEpiWarps = 8;
+constexpr int kWarpTma = 0, kWarpMma = 1, kWarpGat = 2, kNGat = 2, kWarpEpi = 4;
+constexpr int kThreads = 32 * (kWarpEpi + kEpiWarps);  // 384
+constexpr uint32_t kFull = 0xffffffffu;
+
+struct LmArgs {
+  int nprobe, L, Lp, dim, kp, NT, nacc, S, ngroups;
+  const int8_t* queries;
+  const int32_t* pairs;   // pair ids (q * nprobe + rho) grouped by list
+  const int4* items;      // (list, first pair, pairs, 0)
+  const int* n_items;
+  const int32_t* ldist;   // [nq * nprobe] d_i of each pair
+  const int32_t* counts;  // [nlist]
+  const int32_t* pterm;   // [nlist][L]
+  int32_t* trace;         // [nq][nprobe][L]
+  int32_t* gmin;          // [nq][nprobe][ngroups]
+  uint32_t off_b, off_meta, off_bar, b_bytes;
+};
+
+struct PairMeta {  // 16 B, read by the epilogue as one broadcast LDS.128
+  int trow_lo, trow_hi;  // trace element offset of the pair's row: pair * L
+  int d;                 // d_i
+  int goff;              // pair * ngroups
+};
+
+
+// ----------------------------------------------------------------------------------------------
+// The contraction + epilogue kernel.
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__ CUtensorMap tmX, const LmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                         // [S][128 x 128 B]
+  uint8_t* sB = smem + a.off_b;                               // [2][kp][NT x 128 B]
+  PairMeta* meta = reinterpret_cast<PairMeta*>(smem + a.off_meta);  // [2][NT]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  uint64_t* afull = bars;                  // [S]
+  uint64_t* aempty = afull + a.S;          // [S]
+  uint64_t* bfull = aempty + a.S;          // [2]
+  uint64_t* bempty = bfull + 2;            // [2]
+  uint64_t* accf = bempty + 2;             // [nacc]
+  uint64_t* acce = accf + a.nacc;          // [nacc]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + a.nacc);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_items = *a.n_items;
+  const int NT = a.NT, L = a.L;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.S; ++s) {
+      tc::mbar_init(afull + s, 1);
+      tc::mbar_init(aempty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(bfull + b, kNGat);
+      tc::mbar_init(bempty + b, 1 + kEpiWarps);
+    }
+    for (int c = 0; c < a.nacc; ++c) {
+      tc::mbar_init(accf + c, 1);
+      tc::mbar_init(acce + c, kEpiWarps);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == kWarpMma) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kWarpTma) {
+    // ------------------------------------------------------------ xhat tiles (TMA)
+    if (lane == 0) {
+      tc::tma_prefetch(&tmX);
+      int s = 0, u = 0;
+      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
+        const int4 it = a.items[j];
+        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+        for (int t = 0; t < nvt; ++t) {
+          for (int p = 0; p < a.kp; ++p) {
+            if (u > 0) tc::mbar_wait(aempty + s, (u - 1) & 1);
+            tc::mbar_expect_tx(afull + s, kAStageBytes);
+            tc::tma_load_2d(sA + s * kAStageBytes, &tmX, afull + s, p * kPanel, it.x * a.Lp + t * kTile);
+            if (++s == a.S) {
+              s = 0;
+              ++u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int s = 0, u = 0, n = 0, tcount = 0;
+      for (int j = blockIdx.x; j < n_items; j += gridDim.x, ++n) {
+        const int4 it = a.items[j];
+        const int b = n & 1;
+        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+        const int N = (it.z + 15) & ~15;  // UMMA N for M = 128: multiple of 16
+        const uint32_t idesc = tc::idesc_s8(kTile, N);
+        tc::mbar_wait(bfull + b, (n >> 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t b_addr = tc::smem_u32(sB + b * a.b_bytes);
+        for (int t = 0; t < nvt; ++t, ++tcount) {
+          const int acc = tcount % a.nacc, ua = tcount / a.nacc;
+          if (ua > 0) {
+            tc::mbar_wait(acce + acc, (ua - 1) & 1);
+            tc::fence_after_sync();
+          }
+          for (int p = 0; p < a.kp; ++p) {
+            tc::mbar_wait(afull + s, u & 1);
+            tc::fence_after_sync();
+            const int nk = min(4, (a.dim - p * kPanel + 31) / 32);
+            const uint32_t a_addr = tc::smem_u32(sA + s * kAStageBytes);
+            const uint32_t bp = b_addr + p * NT * kPanel;
+            for (int kk = 0; kk < nk; ++kk)
+              tc::mma_s8(tmem + acc * NT, tc::desc_sw128(a_addr + kk * 32), tc::desc_sw128(bp + kk * 32), idesc,
+                         (p | kk) != 0);
+            tc::mma_commit(aempty + s);
+            if (++s == a.S) {
+              s = 0;
+              ++u;
+            }
+          }
+          tc::mma_commit(accf + acc);
+        }
+        tc::mma_commit(bempty + b);  // the B buffer is free once this item's MMAs completed
+      }
+    }
+  } else if (warp < kWarpEpi) {
+    // ------------------------------------------------------------ gather: B operand + metadata
+    const int gt = tid - kWarpGat * 32;  // 0 .. 63
+    const int cpr = a.dim >> 4;          // 16-byte chunks per query row
+    int n = 0;
+    for (int j = blockIdx.x; j < n_items; j += gridDim.x, ++n) {
+      const int4 it = a.items[j];
+      const int b = n & 1;
+      if (n >= 2) tc::mbar_wait(bempty + b, ((n >> 1) - 1) & 1);
+      uint8_t* dst = sB + b * a.b_bytes;
+      PairMeta* mt = meta + b * NT;
+      for (int r = gt; r < it.z; r += 32 * kNGat) {
+        const int pr = __ldg(a.pairs + it.y + r);
+        const int64_t trow = static_cast<int64_t>(pr) * L;
+        mt[r] = PairMeta{static_cast<int>(trow & 0xffffffff), static_cast<int>(trow >> 32), __ldg(a.ldist + pr),
+                         pr * a.ngroups};
+      }
+      for (int e = gt; e < it.z * cpr; e += 32 * kNGat) {
+        const int r = e / cpr, c = e - r * cpr;
+        const int q = __ldg(a.pairs + it.y + r) / a.nprobe;
+        uint8_t* d = dst + (c >> 3) * NT * kPanel + tc::sw128_offset(r, c & 7);
+        tc::cp_async16(d, a.queries + static_cast<int64_t>(q) * a.dim + c * 16, 16);
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bfull + b);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int e = warp - kWarpEpi, qd = warp & 3, cg = e >> 2;
+    constexpr int NCG = kEpiWarps / 4;
+    int n = 0, tcount = 0;
+    for (int j = blockIdx.x; j < n_items; j += gridDim.x, ++n) {
+      const int4 it = a.items[j];
+      const int b = n & 1, np = it.z;
+      const int cnt = __ldg(a.counts + it.x);
+      const int nvt = (cnt + kTile - 1) / kTile, ntl = (L + kTile - 1) / kTile;
+      const PairMeta* mt = meta + b * NT;
+      tc::mbar_wait(bfull + b, (n >> 1) & 1);
+      for (int t = 0; t < ntl; ++t) {
+        const int slot = t * kTile + qd * 32 + lane;
+        const bool inL = slot < L, valid = slot < cnt;
+        if (t < nvt) {
+          const int acc = tcount % a.nacc, ua = tcount / a.nacc;
+          ++tcount;
+          const int32_t P = valid ? __ldg(a.pterm + static_cast<int64_t>(it.x) * L + slot) : 0;
+          tc::mbar_wait(accf + acc, ua & 1);
+          tc::fence_after_sync();
+          const bool gvalid = t * kTile + qd * 32 < cnt;  // this warp's 32-slot group holds a valid slot
+          for (int jc = cg; jc * 32 < np; jc += NCG) {
+            uint32_t v[32];
+            tc::tmem_ld32(tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT + jc * 32, v);
+            tc::tmem_ld_wait();
+            int gm = kDMax;
+            const int ncol = min(32, np - jc * 32);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              if (c >= ncol) break;  // warp-uniform
+              const PairMeta m = mt[jc * 32 + c];
+              const int32_t D = valid ? m.d + P - 2 * static_cast<int32_t>(v[c]) : kDMax;
+              const int64_t trow = (static_cast<int64_t>(m.trow_hi) << 32) | static_cast<uint32_t>(m.trow_lo);
+              if (inL) __stcs(a.trace + trow + slot, D);
+              const int mn = __reduce_min_sync(kFull, D);
+              gm = lane == c ? mn : gm;
+            }
+            if (gvalid && lane < ncol) a.gmin[mt[jc * 32 + lane].goff + t * 4 + qd] = gm;
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(acce + acc);
+        } else {
+          // a tile of padding only: D = d_max, nothing read
+          for (int c = cg; c < np; c += NCG) {
+            const PairMeta m = mt[c];
+            const int64_t trow = (static_cast<int64_t>(m.trow_hi) << 32) | static_cast<uint32_t>(m.trow_lo);
+            if (inL) __stcs(a.trace + trow + slot, kDMax);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bempty + b);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == kWarpMma) tc::tmem_dealloc(tmem, 512);
+}
+
+// ----------------------------------------------------------------------------------------------
+// Grouping: the (query, rank) pairs by probed list, and the work items.
+// ----------------------------------------------------------------------------------------------
+__global__ void pair_hist_kernel(const int32_t* __restrict__ lists, int64_t npairs, int* __restrict__ hist) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npairs;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(hist + __ldg(lists + p), 1);
+}
+
+// One CTA of 1024 threads: off[i] = exclusive prefix of hist (pairs per list), iof[i] = exclusive
+// prefix of ceil(hist[i] / NT) (items per list); *n_items = the total.
+__global__ void __launch_bounds__(1024) lm_scan_kernel(const int* __restrict__ hist, int nlist, int NT,
+                                                       int* __restrict__ off, int* __restrict__ iof,
+                                                       int* __restrict__ n_items) {
+  __shared__ int part[1024], ipart[1024];
+  const int per = (nlist + 1023) / 1024, b = threadIdx.x * per, e = min(nlist, b + per);
+  int sum = 0, isum = 0;
+  for (int i = b; i < e; ++i) {
+    sum += hist[i];
+    isum += (hist[i] + NT - 1) / NT;
+  }
+  part[threadIdx.x] = sum;
+  ipart[threadIdx.x] = isum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    const int w = threadIdx.x >= o ? ipart[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    ipart[threadIdx.x] += w;
+    __syncthreads();
+  }
+  int run = part[threadIdx.x] - sum, irun = ipart[threadIdx.x] - isum;
+  for (int i = b; i < e; ++i) {
+    off[i] = run;
+    iof[i] = irun;
+    run += hist[i];
+    irun += (hist[i] + NT - 1) / NT;
+  }
+  if (threadIdx.x == 1023) *n_items = ipart[1023];
+}
+
+__global__ void pair_scatter_kernel(const int32_t* __restrict__ lists, int64_t npairs, int* __restrict__ cur,
+                                    int32_t* __restrict__ pairs) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npairs;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    pairs[atomicAdd(cur + __ldg(lists + p), 1)] = static_cast<int32_t>(p);
+}
+
+// items of list i: (i, off[i] + r * NT, min(NT, hist[i] - r * NT)); off[] here is the list's first
+// pair (the scatter advanced its copy `cur`, so the start is recomputed as cur - hist).
+__global__ void items_kernel(const int* __restrict__ hist, const int* __restrict__ cur, const int* __restrict__ iof,
+                             int nlist, int NT, int4* __restrict__ items) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nlist; i += gridDim.x * blockDim.x) {
+    const int h = hist[i];
+    const int p0 = cur[i] - h;
+    for (int r = 0; r * NT < h; ++r) items[iof[i] + r] = make_int4(i, p0 + r * NT, min(NT, h - r * NT), 0);
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Step 5: exact per-query selection from the group minima and the trace.
+// ----------------------------------------------------------------------------------------------
+constexpr int kSelThreads = 256;
+constexpr int kSelGroups = 4096;  // selected-group list capacity (more: every valid group is scanned)
+
+struct SelArgs {
+  int nprobe, L, ngroups, k;
+  const int32_t* lists;
+  const int32_t* counts;
+  const int32_t* ids;
+  const int32_t* trace;
+  const int32_t* gmin;
+  int32_t* out_ids;
+  int32_t* out_dist;
+};
+
+// CTA-wide radix selection (8-bit digits) of the kk-th smallest (1-based) 32-bit value among those
+// `gen(i, &v)` yields for i in [0, n); every value is known to be <= bound, so the leading digits
+// above bound's top bit are skipped.  Returns the value; *below = how many yielded values are smaller.
+template <class Gen>
+__device__ uint32_t cta_radix_select(int n, int kk, uint32_t bound, Gen gen, int* hist, int* sc, int* below) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int top = 32 - __clz(bound | 1u);
+  const int pass0 = 3 - (top - 1) / 8;
+  uint32_t prefix = 0;
+  const int k0 = kk;
+  for (int pass = pass0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kSelThreads) {
+      uint32_t v;
+      if (gen(i, v) && (pass == pass0 || (v >> (shift + 8)) == prefix)) atomicAdd(hist + ((v >> shift) & 255), 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int h[8], sum = 0;
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        h[x] = hist[lane * 8 + x];
+        sum += h[x];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int w = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += w;
+      }
+      int cum = incl - sum;
+      if (cum < kk && kk <= incl) {
+        int bin = lane * 8;
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          if (cum + h[x] >= kk) break;
+          cum += h[x];
+          ++bin;
+        }
+        sc[0] = bin;
+        sc[1] = kk - cum;
+      }
+    }
+    __syncthreads();
+    prefix = (prefix << 8) | static_cast<uint32_t>(sc[0]);
+    kk = sc[1];
+    __syncthreads();
+  }
+  *below = k0 - kk;
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kSelThreads) lm_select_kernel(const SelArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  int* pl = reinterpret_cast<int*>(sm);            // [nprobe] probed list
+  int* pc = pl + a.nprobe;                         // [nprobe] its count
+  int* hist = pc + a.nprobe;                       // [256]
+  int* sc = hist + 256;                            // [16] scratch
+  int* sel = sc + 16;                              // [kSelGroups] selected groups (rho << 16 | g)
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sel + kSelGroups);  // [k]
+  const int tid = threadIdx.x;
+  const int64_t q = blockIdx.x;
+  const int nprobe = a.nprobe, L = a.L, NG = a.ngroups, k = a.k;
+  for (int r = tid; r < nprobe; r += kSelThreads) {
+    const int li = a.lists[q * nprobe + r];
+    pl[r] = li;
+    pc[r] = __ldg(a.counts + li);
+  }
+  if (tid < 16) sc[tid] = 0;
+  __syncthreads();
+  const int32_t* gq = a.gmin + q * nprobe * NG;
+  const int32_t* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
+  // valid groups: (rho, g) with 32 g < count_rho
+  auto gen_g = [&](int i, uint32_t& v) {
+    const int rho = i / NG, g = i - rho * NG;
+    if (32 * g >= pc[rho]) return false;
+    v = static_cast<uint32_t>(gq[i]);
+    return true;
+  };
+  {
+    int nvalid_g = 0;
+    for (int r = tid; r < nprobe; r += kSelThreads) nvalid_g += (pc[r] + 31) >> 5;
+    if (nvalid_g) atomicAdd(sc + 2, nvalid_g);
+  }
+  __syncthreads();
+  const int V = sc[2];
+  int below = 0;
+  // tau = the k-th smallest group minimum (each is a real candidate's D), or "everything" if fewer
+  // than k valid groups exist
+  const uint32_t tau = V >= k ? cta_radix_select(nprobe * NG, k, 0x7ffffffeu, gen_g, hist, sc, &below) : 0x7ffffffeu;
+  // the selected groups (minimum <= tau) and how many valid slots they hold
+  if (tid == 0) {
+    sc[3] = 0;
+    sc[4] = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nprobe * NG; i += kSelThreads) {
+    uint32_t v;
+    if (gen_g(i, v) && v <= tau) {
+      const int rho = i / NG, g = i - rho * NG;
+      const int pos = atomicAdd(sc + 3, 1);
+      if (pos < kSelGroups) sel[pos] = (rho << 16) | g;
+      atomicAdd(sc + 4, min(32, pc[rho] - 32 * g));
+    }
+  }
+  __syncthreads();
+  const int nsel = sc[3];
+  const bool all = nsel > kSelGroups || nprobe > 65535 || NG > 65535;  // fall back to every valid group
+  const int total_slots = all ? nprobe * NG * 32 : nsel * 32;
+  // candidate i: slot lane (i & 31) of selected group i >> 5 (or of group i >> 5 of the query)
+  auto slot_of = [&](int i, int& rho, int& j) {
+    const int gi = i >> 5;
+    int g;
+    if (all) {
+      rho = gi / NG;
+      g = gi - rho * NG;
+    } else {
+      const int sg = sel[gi];
+      rho = sg >> 16;
+      g = sg & 0xffff;
+    }
+    j = 32 * g + (i & 31);
+    return j < pc[rho];
+  };
+  auto gen_d = [&](int i, uint32_t& v) {
+    int rho, j;
+    if (!slot_of(i, rho, j)) return false;
+    v = static_cast<uint32_t>(tq[rho * static_cast<int64_t>(L) + j]);
+    return v <= tau;
+  };
+  // how many candidates (valid, D <= tau) exist
+  if (tid == 0) sc[5] = 0;
+  __syncthreads();
+  {
+    int c = 0;
+    for (int i = tid; i < total_slots; i += kSelThreads) {
+      uint32_t v;
+      c += gen_d(i, v) ? 1 : 0;
+    }
+    atomicAdd(sc + 5, c);
+  }
+  __syncthreads();
+  const int ncand = sc[5];
+  const int kk = min(k, ncand);
+  uint32_t dk = 0xffffffffu, idk = 0xffffffffu;
+  if (ncand > k) {
+    // the k-th smallest D; then, if the ties at it do not all fit, the (k - below)-th smallest item
+    // key among them (R10: (D, id) order, id as signed int32 -> key id ^ 0x80000000)
+    dk = cta_radix_select(total_slots, k, tau, gen_d, hist, sc, &below);
+    const int need = k - below;
+    if (tid == 0) sc[6] = 0;
+    __syncthreads();
+    {
+      int c = 0;
+      for (int i = tid; i < total_slots; i += kSelThreads) {
+        uint32_t v;
+        c += (gen_d(i, v) && v == dk) ? 1 : 0;
+      }
+      atomicAdd(sc + 6, c);
+    }
+    __syncthreads();
+    if (sc[6] > need) {
+      auto gen_id = [&](int i, uint32_t& v) {
+        int rho, j;
+        if (!slot_of(i, rho, j)) return false;
+        if (static_cast<uint32_t>(tq[rho * static_cast<int64_t>(L) + j]) != dk) return false;
+        v = static_cast<uint32_t>(__ldg(a.ids + static_cast<int64_t>(pl[rho]) * L + j)) ^ 0x80000000u;
+        return true;
+      };
+      int b2 = 0;
+      idk = cta_radix_select(total_slots, need, 0xffffffffu, gen_id, hist, sc, &b2);
+    }
+  }
+  // collect the min(k, ncand) winners as resolved (D, item) keys, then place them by rank
+  if (tid == 0) sc[7] = 0;
+  __syncthreads();
+  for (int i = tid; i < total_slots; i += kSelThreads) {
+    uint32_t v;
+    if (!gen_d(i, v) || v > dk) continue;
+    int rho, j;
+    slot_of(i, rho, j);
+    const int32_t id = __ldg(a.ids + static_cast<int64_t>(pl[rho]) * L + j);
+    if (v == dk && (static_cast<uint32_t>(id) ^ 0x80000000u) > idk) continue;
+    const int pos = atomicAdd(sc + 7, 1);
+    V3DB_DCHECK(pos < kk);
+    keys[pos] = step5_key(static_cast<int32_t>(v), id);
+  }
+  __syncthreads();
+  const int m = sc[7];
+  for (int e2 = tid; e2 < m; e2 += kSelThreads) {
+    const uint64_t key = keys[e2];
+    int rank = 0;
+    for (int f = 0; f < m; ++f) rank += keys[f] < key ? 1 : 0;
+    a.out_ids[q * k + rank] = step5_id(key);
+    a.out_dist[q * k + rank] = static_cast<int32_t>(key >> 32);
+  }
+  for (int r = m + tid; r < k; r += kSelThreads) {  // fewer than k valid candidates (R11)
+    a.out_ids[q * k + r] = -1;
+    a.out_dist[q * k + r] = kDMax;
+  }
+}
+
+size_t al(size_t x, size_t b) { return (x + b - 1) / b * b; }
+
+}  // namespace
+
+cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
+                            const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
+                            int32_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t)) {
+  if (nq <= 0) return cudaSuccess;
+  if (!s->xhat || s->dim % 16 != 0) return cudaErrorInvalidValue;
+  const int64_t npairs = nq * nprobe;
+  const int L = s->L, ngroups = (L + 31) / 32, kp = (s->dim + kPanel - 1) / kPanel;
+  if (npairs >= (int64_t(1) << 31) || npairs * ngroups >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  // NT: pairs per item, the largest of 256 / 128 / 64 / 32 whose double-buffered B operand fits 128 KB
+  int NT = 256;
+  const int64_t nt_opt = opt(V3DB_OPT_LM_NT);
+  if (nt_opt == 32 || nt_opt == 64 || nt_opt == 128 || nt_opt == 256) NT = static_cast<int>(nt_opt);
+  while (NT > 32 && 2u * kp * NT * kPanel > 128u * 1024) NT >>= 1;
+  const int nacc = std::min(4, 512 / NT);
+  const uint32_t b_bytes = static_cast<uint32_t>(kp) * NT * kPanel;
+  int S = 6;
+  auto smem_of = [&](int stages) {
+    return 1024 + static_cast<size_t>(stages) * kAStageBytes + 2 * b_bytes + 2 * sizeof(PairMeta) * NT +
+           8 * (2 * stages + 4 + 2 * nacc) + 16;
+  };
+  while (S > 2 && smem_of(S) > 227 * 1024) --S;
+  if (smem_of(S) > 227 * 1024) return cudaErrorInvalidConfiguration;
+
+  CUtensorMap tmX;
+  if (!make_tmap_i8(&tmX, s->xhat, static_cast<uint64_t>(s->nlist) * s->lm_Lp, s->dim, kTile, kPanel))
+    return cudaErrorInvalidValue;
+
+  // scratch: hist, off/cur, iof, n_items, pairs, items, gmin (+ trace when the caller passes none)
+  const int nlist = s->nlist;
+  const int64_t max_items = nlist + npairs / NT + 1;
+  const size_t b_hist = al(sizeof(int) * nlist, 256), b_pairs = al(sizeof(int32_t) * npairs, 256),
+               b_items = al(sizeof(int4) * max_items, 256), b_gmin = al(sizeof(int32_t) * npairs * ngroups, 256),
+               b_trace = trace_cand ? 0 : al(sizeof(int32_t) * npairs * L, 256);
+  uint8_t* base = nullptr;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&base), 3 * b_hist + 256 + b_pairs + b_items + b_gmin + b_trace, st);
+  if (e != cudaSuccess) return e;
+  int* hist = reinterpret_cast<int*>(base);
+  int* cur = reinterpret_cast<int*>(base + b_hist);
+  int* iof = reinterpret_cast<int*>(base + 2 * b_hist);
+  int* n_items = reinterpret_cast<int*>(base + 3 * b_hist);
+  int32_t* pairs = reinterpret_cast<int32_t*>(base + 3 * b_hist + 256);
+  int4* items = reinterpret_cast<int4*>(base + 3 * b_hist + 256 + b_pairs);
+  int32_t* gmin = reinterpret_cast<int32_t*>(base + 3 * b_hist + 256 + b_pairs + b_items);
+  int32_t* trace = trace_cand ? trace_cand : reinterpret_cast<int32_t*>(base + 3 * b_hist + 256 + b_pairs + b_items + b_gmin);
+
+  int dev = 0, sms = 148;
+  e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, sizeof(int) * nlist, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(base, st);
+    return e;
+  }
+  const unsigned pg = static_cast<unsigned>(std::min<int64_t>((npairs + 255) / 256, 4 * sms));
+  pair_hist_kernel<<<pg, 256, 0, st>>>(lists, npairs, hist);
+  lm_scan_kernel<<<1, 1024, 0, st>>>(hist, nlist, NT, cur, iof, n_items);
+  pair_scatter_kernel<<<pg, 256, 0, st>>>(lists, npairs, cur, pairs);
+  items_kernel<<<(nlist + 255) / 256, 256, 0, st>>>(hist, cur, iof, nlist, NT, items);
+  note_launch(4);
+  if (prof) prof(2, st);
+
+  LmArgs a;
+  a.nprobe = nprobe;
+  a.L = L;
+  a.Lp = s->lm_Lp;
+  a.dim = s->dim;
+  a.kp = kp;
+  a.NT = NT;
+  a.nacc = nacc;
+  a.S = S;
+  a.ngroups = ngroups;
+  a.queries = queries;
+  a.pairs = pairs;
+  a.items = items;
+  a.n_items = n_items;
+  a.ldist = ldist;
+  a.counts = s->counts;
+  a.pterm = s->pterm;
+  a.trace = trace;
+  a.gmin = gmin;
+  a.off_b = S * kAStageBytes;
+  a.off_meta = a.off_b + 2 * b_bytes;
+  a.off_bar = static_cast<uint32_t>(al(a.off_meta + 2 * sizeof(PairMeta) * NT, 8));
+  a.b_bytes = b_bytes;
+  const size_t smem = smem_of(S);
+  e = cudaFuncSetAttribute(lm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) {
+    const int64_t grid = std::min<int64_t>(sms, max_items);
+    lm_kernel<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(tmX, a);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = debug_sync(st, "lm_kernel");
+  if (prof) prof(3, st);
+  if (e == cudaSuccess) {
+    SelArgs sa;
+    sa.nprobe = nprobe;
+    sa.L = L;
+    sa.ngroups = ngroups;
+    sa.k = k;
+    sa.lists = lists;
+    sa.counts = s->counts;
+    sa.ids = s->ids;
+    sa.trace = trace;
+    sa.gmin = gmin;
+    sa.out_ids = out_ids;
+    sa.out_dist = out_dist;
+    const size_t ssm = sizeof(int) * (2 * nprobe + 256 + 16 + kSelGroups) + 16 + sizeof(uint64_t) * k;
+    e = cudaFuncSetAttribute(lm_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm));
+    if (e == cudaSuccess) {
+      lm_select_kernel<<<static_cast<unsigned>(nq), kSelThreads, ssm, st>>>(sa);
+      note_launch();
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess) e = debug_sync(st, "lm_select_kernel");
+  cudaFreeAsync(base, st);
+  return e;
+}
+
+}  // namespace v3db

@@ -22,9 +22,10 @@
 //
 // Streaming.  A producer warp (one lane) walks the probed lists'
 // VALID 32-slot chunks in probe order and packs them into CTA-wide stages of SEG chunks; each
-// stage is filled by one cp.async.bulk (TMA bulk copy) of codes and one of P terms per list piece
-// (~1-2 pieces per stage), completion on the stage's `full` mbarrier; the consumer warps split the
-// stage's chunks and release it on its `empty` mbarrier.  codes_rot stores each chunk
+// stage is filled by one cp.async.bulk (TMA bulk copy) of codes per list piece (~1-2 pieces per
+// stage) plus per-chunk descriptors, completion on the stage's `full` mbarrier (expect-tx, copies,
+// descriptors, then the producer's arrival); the consumer warps split the stage's chunks, read each
+// chunk's P terms from global memory (__ldg, L2) and release the stage on its `empty` mbarrier.  codes_rot stores each chunk
 // unit-transposed ([unit][lane][U bytes]) so the lanes' stage reads are conflict-free LDS.128/64/32.
 // Chunks holding only padding are never read: their trace entries (d_max) are written up front.
 //
@@ -47,8 +48,7 @@ namespace v3db {
 int plan_lut(int M, int Ks, int d, int* G) {
   *G = 0;
   if (M < 4 || M % 4 != 0 || M > 128 || d % 4 != 0 || Ks < 1 || Ks > 256) return 0;
-  const char* force = getenv("V3DB_LUT_MODE");  // test/bench hook: "w32" forces W32 where P64 applies
-  const bool want_w32 = force && force[0] == 'w';
+  const bool want_w32 = opt(V3DB_OPT_LUT_W32) != 0;  // test/bench option: W32 where P64 applies
   // P64: one rotation group of all M <= 32 subspaces; lane l reads column l + s < 64 at step s,
   // which holds subspace (l + s) mod M (columns m, m + M, ... replicate subspace m)
   const bool p64_ok = M <= 32 && (M == 4 || M == 8 || M == 12 || M == 16 || M == 20 || M == 24 || M == 28 || M == 32);
@@ -371,7 +371,10 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
         if (t >= NS) mbar_wait_sleep(empty + s, eph);  // consumers released the previous fill
         uint8_t* st = stages + static_cast<uint32_t>(s) * a.stage_bytes;
         const int g0 = t * SEG, g1 = min(TV, g0 + SEG);
-        tc::mbar_expect_tx(full + s, static_cast<uint32_t>(g1 - g0) * 32u * M);
+        // expect the stage's bytes (no arrival yet), issue the copies and write the chunk
+        // descriptors, THEN arrive: the arrival's release orders the descriptor stores before any
+        // consumer's acquire of the completed phase (the copies' complete_tx alone would not)
+        tc::mbar_expect_tx_only(full + s, static_cast<uint32_t>(g1 - g0) * 32u * M);
         // one codes copy per piece (a run of valid chunks of one list)
         for (int g = g0; g < g1;) {
           while (vcoff[rho + 1] <= g) ++rho;
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
           const uint32_t i = static_cast<uint32_t>(g - g0);
           // per-chunk descriptors: (d_i, rho*L + 32*jc (trace / flat offset), valid slots | slots << 8,
           // P-term offset list*Lp + 32*jc)
+          V3DB_DCHECK(i + m <= static_cast<uint32_t>(SEG) && (i + m) * 32u * M <= a.stage_bytes);
           for (int x = 0; x < m; ++x)
             dsc[s * SEG + i + x] = make_int4(pr.y, rho * L + (jc + x) * 32,
                                              min(32, pr.z - (jc + x) * 32) | (min(32, L - (jc + x) * 32) << 8),
@@ -389,6 +393,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
           bulk_g2s(st + i * 32u * M, a.codes + slot0 * M, static_cast<uint32_t>(m) * 32u * M, full + s);
           g += m;
         }
+        tc::mbar_arrive(full + s);
         if (++s == NS) {
           s = 0;
           if (t + 1 > NS) eph ^= 1u;
@@ -539,6 +544,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
       if (lane == 0) {
         const int cnt = __popc(bal);
         base = atomicAdd(&s_int[0], cnt);
+        V3DB_DCHECK(base + cnt <= a.cap);  // headroom argument above (hw)
         if (base + cnt > (tau == kTauInit ? first : hw)) vs[1] = 1;
       }
       base = __shfl_sync(kFull, base, 0);
@@ -649,14 +655,14 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
                                 {8, 2, 1024}};
   int SEG = 8, NS = 2, cap = 1024;
   size_t smem = 0;
-  const char* e_seg = getenv("V3DB_SEG");  // experiments: force (SEG, NS, cap)
-  const char* e_ns = getenv("V3DB_NS");
-  const char* e_cap = getenv("V3DB_CAP");
+  const int e_seg = static_cast<int>(opt(V3DB_OPT_SCAN_SEG));  // experiments: force (SEG, NS, cap)
+  const int e_ns = static_cast<int>(opt(V3DB_OPT_SCAN_NS));
+  const int e_cap = static_cast<int>(opt(V3DB_OPT_SCAN_CAP));
   for (const auto& c : cand) {
-    const int seg = e_seg ? atoi(e_seg) : c[0], ns = e_ns ? atoi(e_ns) : c[1];
+    const int seg = e_seg > 0 ? e_seg : c[0], ns = e_ns > 0 ? e_ns : c[1];
     // headroom: one stage share of every consumer warp above the high-water mark, which must be >= k
     const int head = (NT / 32) * ((seg + NT / 32 - 1) / (NT / 32)) * 32;
-    int cp = e_cap ? atoi(e_cap) : c[2];
+    int cp = e_cap > 0 ? e_cap : c[2];
     while (cp < a.k + head) cp *= 2;
     const size_t need = al(lut, 128) + static_cast<size_t>(ns) * al(seg * chunk, 128) + al(4u * (a.nprobe + 1), 16) + 16u * ns * seg +
                         8u * cp + 512 * 4 + 16u * a.nprobe + al(a.dim, 16) + 256 + 16u * ns;
@@ -664,7 +670,7 @@ cudaError_t launch(RotArgs a, int64_t nq, int smem_budget, cudaStream_t st) {
     NS = ns;
     cap = cp;
     smem = need;
-    if (need <= static_cast<size_t>(smem_budget) || (e_seg && e_ns)) break;
+    if (need <= static_cast<size_t>(smem_budget) || (e_seg > 0 && e_ns > 0)) break;
   }
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   a.SEG = SEG;
@@ -821,18 +827,18 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
   a.trace = trace;
   a.order = nullptr;
   {
-    const char* f = getenv("V3DB_FIRST");  // experiments
-    a.first_mult = f ? atoi(f) : 16;  // measured: 16 vs 4 -0.8 % at C4, -1.8 % at C3, flat at C1/C2
-    const char* dm = getenv("V3DB_DIRECT");  // experiments
-    a.direct_max = dm ? atoi(dm) : 256;  // measured: C1 scan -10 %, C2/C3 -2 %, C4 flat (1024: C4 +5 %)
+    const int64_t f = opt(V3DB_OPT_SCAN_FIRST);  // experiments
+    a.first_mult = f > 0 ? static_cast<int>(f) : 16;  // measured: 16 vs 4 -0.8 % at C4, -1.8 % at C3, flat at C1/C2
+    const int64_t dm = opt(V3DB_OPT_SCAN_DIRECT);  // experiments (-1 = never rank directly)
+    a.direct_max = dm > 0 ? static_cast<int>(dm) : dm < 0 ? 0 : 256;  // measured: C1 scan -10 %, C2/C3 -2 %, C4 flat
   }
   // L2-aware schedule when the probed lists do not fit in L2 anyway and the batch is large
-  const char* sched = getenv("V3DB_SCHED");
-  const bool want = sched ? sched[0] == '1'
+  const int64_t sched = opt(V3DB_OPT_SCHED);
+  const bool want = sched ? sched == 1
                           : (nq >= 2048 && static_cast<int64_t>(s->nlist) * s->L * s->M > (int64_t(64) << 20));
   void* sbuf = nullptr;
   if (want) {
-    cudaError_t e = cudaMallocAsync(&sbuf, sizeof(int32_t) * (2 * nq + s->nlist), st);
+    cudaError_t e = scratch_alloc(&sbuf, sizeof(int32_t) * (2 * nq + s->nlist), st);
     if (e != cudaSuccess) return e;
     e = minhash_order(lists, nq, nprobe, s->nlist, static_cast<int32_t*>(sbuf), st);
     if (e != cudaSuccess) {

@@ -73,6 +73,7 @@ void free_snapshot(v3db_snapshot* s) {
   cudaFree(s->codebooks32);
   cudaFree(s->pterm64);
   cudaFree(s->codes_rot16);
+  cudaFree(s->xhat);
   delete s;
 }
 
@@ -85,26 +86,47 @@ int check_device(const v3db_snapshot* s) {
 }
 
 // Profiling state (v3db_profile_*): events around each query kernel on the call's stream.
+// Marks: 0 call start, 1 after Steps 1-2, 2 after the scan's prologue (grouping / query order),
+// 3 after the scan's main kernel, 4 call end (after the selection).
 struct Profiler {
   std::mutex mu;
   bool on = false;
   bool created = false;
   bool recorded = false;
-  cudaEvent_t ev[3];
+  int marked = 0;  // bit i: mark i recorded in the current call
+  cudaEvent_t ev[5];
 };
 Profiler g_prof;
 std::atomic<int64_t> g_launches{0};
 
 void prof_record(int i, cudaStream_t st) {
   if (!g_prof.on) return;
+  if (i == 0) g_prof.marked = 0;
   cudaEventRecord(g_prof.ev[i], st);
-  if (i == 2) g_prof.recorded = true;
+  g_prof.marked |= 1 << i;
+  if (i == 4) g_prof.recorded = true;
+}
+// around a scan implementation that may record marks 2 and 3 itself
+void prof_scan_begin(cudaStream_t st) {
+  prof_record(1, st);
+  prof_record(2, st);
+}
+void prof_scan_end(cudaStream_t st) {
+  if (g_prof.on && !(g_prof.marked & 8)) prof_record(3, st);
+  prof_record(4, st);
 }
 
 }  // namespace
 
 namespace v3db {
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+std::atomic<int64_t> g_opts[V3DB_OPT_COUNT];
+int64_t opt(int key) { return g_opts[key].load(std::memory_order_relaxed); }
+
+#ifdef V3DB_DEBUG
+// Debug build only (libv3db_debug.so): V3DB_SYNC_CHECK=1 synchronizes after each launch group
+// and reports the first error tagged with the kernel name.
 cudaError_t debug_sync(cudaStream_t st, const char* what) {
   static const bool on = [] {
     const char* e = getenv("V3DB_SYNC_CHECK");
@@ -116,16 +138,53 @@ cudaError_t debug_sync(cudaStream_t st, const char* what) {
   if (e != cudaSuccess) g_err = std::string("after ") + what + ": " + cudaGetErrorString(e);
   return e;
 }
+#else
+cudaError_t debug_sync(cudaStream_t, const char*) { return cudaSuccess; }
+#endif
+
+// The library's own stream-ordered pool per device (query scratch): freed blocks stay in it
+// instead of going back to the driver at every synchronization, without touching the device's
+// default pool that the application (torch) may configure.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) {
+        pools[dev] = nullptr;
+        return e;
+      }
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool = pools[dev];
+  }
+  return cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, st);
+}
 }  // namespace v3db
 
-// Keep freed stream-ordered scratch in the device's default pool instead of returning it to
-// the driver at every synchronization (the list-major scan allocates ~0.5 GB per C4 call).
-void keep_pool_memory(int dev) {
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
+int v3db_set_option(int32_t key, int64_t value) {
+  g_err.clear();
+  if (key < 0 || key >= V3DB_OPT_COUNT) return fail(V3DB_EINVAL, "unknown option key");
+  v3db::g_opts[key].store(value, std::memory_order_relaxed);
+  return V3DB_OK;
+}
+
+int64_t v3db_get_option(int32_t key) {
+  if (key < 0 || key >= V3DB_OPT_COUNT) return 0;
+  return v3db::opt(key);
 }
 
 // B2, the ordered greedy placement (BASELINE.json configs[0]): every vector, in ascending t, goes
@@ -228,6 +287,7 @@ int place_rebalance(const int8_t* db, int64_t n, int dim, int nlist, int L, cons
     }
     int64_t P = 1;
     while (P < mm) P <<= 1;
+    if (P > (int64_t(1) << 30)) return fail(V3DB_EINVAL, "Alg. 1: more than 2^30 candidate moves in one round");
     DevBuf<int32_t> d_F, d_cnF, d_vs, d_src, d_tpos, d_et, d_ei;
     DevBuf<int8_t> d_muF, d_X;
     DevBuf<uint64_t> d_keys;
@@ -290,11 +350,9 @@ int v3db_profile_read(float* out_ms, int32_t n) {
   g_err.clear();
   if (!out_ms || n < 0) return fail(V3DB_EINVAL, "NULL pointer");
   if (!g_prof.recorded) return fail(V3DB_EINVAL, "no profiled query call recorded");
-  V3DB_CUDA(cudaEventSynchronize(g_prof.ev[2]));
-  float t[2];
-  V3DB_CUDA(cudaEventElapsedTime(&t[0], g_prof.ev[0], g_prof.ev[1]));
-  V3DB_CUDA(cudaEventElapsedTime(&t[1], g_prof.ev[1], g_prof.ev[2]));
-  for (int i = 0; i < n && i < 2; ++i) out_ms[i] = t[i];
+  V3DB_CUDA(cudaEventSynchronize(g_prof.ev[4]));
+  static const int span[5][2] = {{0, 1}, {1, 4}, {2, 3}, {1, 2}, {3, 4}};
+  for (int i = 0; i < n && i < 5; ++i) V3DB_CUDA(cudaEventElapsedTime(&out_ms[i], g_prof.ev[span[i][0]], g_prof.ev[span[i][1]]));
   return V3DB_OK;
 }
 
@@ -368,7 +426,6 @@ int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nli
   s->Ks = ks;
   s->d = d;
   V3DB_CUDA(cudaGetDevice(&s->device));
-  keep_pool_memory(s->device);
   const int64_t slots = static_cast<int64_t>(nlist) * L;
   V3DB_CUDA(cudaMalloc(&s->centroids, static_cast<size_t>(nlist) * dim));
   V3DB_CUDA(cudaMalloc(&s->cnorm, sizeof(int32_t) * nlist));
@@ -458,6 +515,12 @@ int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nli
                                  st));
     V3DB_CUDA(v3db::transpose_codebooks(s->codebooks, m, ks, d, s->cbT, st));
   }
+  // reconstruction of every slot for the list-major tensor-core scan (dim % 16 == 0)
+  if (dim % 16 == 0) {
+    s->lm_Lp = (L + 127) & ~127;
+    V3DB_CUDA(cudaMalloc(&s->xhat, static_cast<size_t>(nlist) * s->lm_Lp * dim));
+    V3DB_CUDA(v3db::make_xhat(s->codes, s->counts, s->codebooks, nlist, L, s->lm_Lp, dim, m, ks, s->xhat, st));
+  }
   V3DB_CUDA(cudaStreamSynchronize(st));
   s->total_valid = n;
   guard.s = nullptr;
@@ -484,11 +547,19 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   int rc = validate_query(s, queries, nq, nprobe, k, out_ids, out_dist);
   if (rc != V3DB_OK) return rc;
   if (s->fx) return fail(V3DB_EINVAL, "fixed-point snapshot: use v3db_query_batch_fx");
-  if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_GENERIC && algo != V3DB_SCAN_ROTATED)
+  if (algo != V3DB_SCAN_AUTO && algo != V3DB_SCAN_GENERIC && algo != V3DB_SCAN_ROTATED && algo != V3DB_SCAN_LIST_MAJOR)
     return fail(V3DB_EINVAL, "unsupported scan algo");
   if (algo == V3DB_SCAN_ROTATED && s->lut_mode == 0)
     return fail(V3DB_EINVAL, "V3DB_SCAN_ROTATED does not support this snapshot's (M, Ks, d)");
-  if (algo == V3DB_SCAN_AUTO) algo = s->lut_mode != 0 ? V3DB_SCAN_ROTATED : V3DB_SCAN_GENERIC;
+  if (algo == V3DB_SCAN_LIST_MAJOR && !s->xhat)
+    return fail(V3DB_EINVAL, "V3DB_SCAN_LIST_MAJOR needs dim % 16 == 0");
+  if (algo == V3DB_SCAN_AUTO) {
+    const int64_t pref = v3db::opt(V3DB_OPT_AUTO_SCAN);
+    if (pref == V3DB_SCAN_GENERIC || (pref == V3DB_SCAN_ROTATED && s->lut_mode != 0))
+      algo = static_cast<int32_t>(pref);
+    else
+      algo = s->xhat ? V3DB_SCAN_LIST_MAJOR : s->lut_mode != 0 ? V3DB_SCAN_ROTATED : V3DB_SCAN_GENERIC;
+  }
   if ((rc = check_device(s)) != V3DB_OK) return rc;
   if (nq == 0) return V3DB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -496,20 +567,23 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   int32_t* ldist = trace_list_dist;
   void* scratch = nullptr;
   if (!lists || !ldist) {
-    V3DB_CUDA(cudaMallocAsync(&scratch, sizeof(int32_t) * 2 * nq * nprobe, st));
+    V3DB_CUDA(v3db::scratch_alloc(&scratch, sizeof(int32_t) * 2 * nq * nprobe, st));
     if (!lists) lists = static_cast<int32_t*>(scratch);
     if (!ldist) ldist = static_cast<int32_t*>(scratch) + nq * nprobe;
   }
   prof_record(0, st);
   cudaError_t e = v3db::coarse_topk(queries, nq, s->dim, s->centroids, s->cnorm, s->nlist, nprobe, lists, ldist, st);
-  prof_record(1, st);
+  prof_scan_begin(st);
   if (e == cudaSuccess) {
-    if (algo == V3DB_SCAN_ROTATED)
+    if (algo == V3DB_SCAN_LIST_MAJOR)
+      e = v3db::scan_list_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st,
+                                g_prof.on ? prof_record : nullptr);
+    else if (algo == V3DB_SCAN_ROTATED)
       e = v3db::scan_rotated(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
     else
       e = v3db::scan_generic(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
   }
-  prof_record(2, st);
+  prof_scan_end(st);
   if (scratch) cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) {
     if (g_err.empty()) return cuda_fail(e, "query kernels");
@@ -541,7 +615,7 @@ int v3db_query_batch_host(v3db_snapshot_t s, const int8_t* queries, int64_t nq, 
   const size_t tb = trace_cand_dist ? sizeof(int32_t) * static_cast<size_t>(nq) * nprobe * s->L : 0;
   const size_t total = ((qb + 255) & ~size_t(255)) + 2 * ob + 2 * lb + tb + 1024;
   uint8_t* buf = nullptr;
-  V3DB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), total, st));
+  V3DB_CUDA(v3db::scratch_alloc(reinterpret_cast<void**>(&buf), total, st));
   uint8_t* p = buf;
   auto take = [&](size_t bytes) {
     uint8_t* r = p;
@@ -618,6 +692,8 @@ int v3db_witness_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int
   int rc = check_device(s);
   if (rc != V3DB_OK) return rc;
   if (nq == 0) return V3DB_OK;
+  if (static_cast<int64_t>(nprobe) * s->L > (int64_t(1) << 30))
+    return fail(V3DB_EINVAL, "nprobe * list_cap > 2^30: the witness sort segment is too long");
   cudaError_t e = v3db::witness_batch(s, queries, nq, nprobe, list_order, list_dist, lut_sel, cand_items, cand_dist,
                                       static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "v3db_witness_batch");
@@ -678,7 +754,6 @@ int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nl
   s->d = d;
   s->fx = 1;
   V3DB_CUDA(cudaGetDevice(&s->device));
-  keep_pool_memory(s->device);
   const int64_t slots = static_cast<int64_t>(nlist) * L;
   V3DB_CUDA(cudaMalloc(&s->centroids32, sizeof(int32_t) * nlist * dim));
   V3DB_CUDA(cudaMalloc(&s->cnorm64, sizeof(int64_t) * nlist));
@@ -731,7 +806,7 @@ int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nl
   V3DB_CUDA(cudaMemsetAsync(s->codes, 0, static_cast<size_t>(slots) * m, st));
   V3DB_CUDA(v3db::fx_build_tail(db, n, dim, s->centroids32, s->list_of, d_pos.p, m, ks, d_cwrows.p, nlist, L,
                                 s->codebooks32, s->codes, s->ids, s->pterm64, st));  // B3-B6
-  if (m % 8 == 0 && ks == 256 && !getenv("V3DB_FX_NOROT")) {  // conflict-free scan layout
+  if (v3db::fx_rot_supported(m, ks) && !v3db::opt(V3DB_OPT_FX_NOROT)) {  // conflict-free scan layout
     V3DB_CUDA(cudaMalloc(&s->codes_rot16, static_cast<size_t>(slots) * m));
     V3DB_CUDA(v3db::rotate_codes16(s->codes, slots, L, m, s->codes_rot16, st));
   }
@@ -751,15 +826,15 @@ static int fx_query_impl(v3db_snapshot_t s, const int32_t* queries, int64_t nq, 
   int64_t* ldist = trace_list_dist;
   void* scratch = nullptr;
   if (!lists || !ldist) {
-    V3DB_CUDA(cudaMallocAsync(&scratch, (sizeof(int32_t) + sizeof(int64_t)) * nq * nprobe, st));
+    V3DB_CUDA(v3db::scratch_alloc(&scratch, (sizeof(int32_t) + sizeof(int64_t)) * nq * nprobe, st));
     if (!ldist) ldist = static_cast<int64_t*>(scratch);
     if (!lists) lists = reinterpret_cast<int32_t*>(static_cast<int64_t*>(scratch) + nq * nprobe);
   }
   prof_record(0, st);
   cudaError_t e = v3db::fx_topk(queries, nq, s->dim, s->centroids32, s->cnorm64, s->nlist, nprobe, lists, ldist, st);
-  prof_record(1, st);
+  prof_scan_begin(st);
   if (e == cudaSuccess) e = v3db::fx_scan(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
-  prof_record(2, st);
+  prof_scan_end(st);
   if (scratch) cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_fx");
   return V3DB_OK;
@@ -803,7 +878,7 @@ int v3db_query_batch_fx_host(v3db_snapshot_t s, const float* queries, int64_t nq
   const size_t lb = sizeof(int32_t) * static_cast<size_t>(nq) * nprobe, ldb = 2 * lb;
   const size_t tb = trace_cand_dist ? sizeof(int64_t) * static_cast<size_t>(nq) * nprobe * s->L : 0;
   uint8_t* buf = nullptr;
-  V3DB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), fb + qb + ib + db + lb + ldb + tb + 2048, st));
+  V3DB_CUDA(v3db::scratch_alloc(reinterpret_cast<void**>(&buf), fb + qb + ib + db + lb + ldb + tb + 2048, st));
   uint8_t* p = buf;
   auto take = [&](size_t bytes) {
     uint8_t* r = p;

@@ -40,6 +40,11 @@ struct v3db_snapshot {
   uint8_t* codes_rot = nullptr;
   int32_t* pterm_rot = nullptr;
   int8_t* cbT = nullptr;
+  // list-major tensor-core scan (scan_lm.cu): xhat [nlist][lm_Lp][dim] int8 = the reconstruction
+  // of every slot (0 for padding), lm_Lp = L rounded up to 128 (one UMMA tile of slots); null when
+  // the shape is not supported (dim % 16 != 0).
+  int8_t* xhat = nullptr;
+  int lm_Lp = 0;
   // NEXT-1 (fx16.cu): 16-bit fixed-point snapshot.  When fx != 0 the int8
   // fields centroids / cnorm / codebooks / pterm are unused and these hold the data instead.
   int fx = 0;
@@ -50,12 +55,31 @@ struct v3db_snapshot {
   uint8_t* codes_rot16 = nullptr;  // [nlist][L][M], per-slot rotated in groups of 16 (+ 8) (M % 8 == 0, Ks == 256)
 };
 
+// Device-side invariant checks: traps in the debug build (libv3db_debug.so, -DV3DB_DEBUG), no
+// code in the release build.  Used on every shared-memory buffer append / stage write whose bound
+// rests on a protocol argument rather than on a per-write guard.
+#ifdef V3DB_DEBUG
+#define V3DB_DCHECK(cond)  \
+  do {                     \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define V3DB_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace v3db {
 
 // Counts every kernel launch of the library (v3db_kernel_launches).
 void note_launch(int n = 1);
-// Debugging aid (env V3DB_SYNC_CHECK=1): synchronize the stream after a launch and return the
-// first error tagged with the kernel name (through v3db_last_error).  No-op otherwise.
+// Process-wide implementation options (v3db_set_option; V3DB_OPT_* keys, 0 = default).
+int64_t opt(int key);
+// Stream-ordered scratch from the library's own device memory pool (free with cudaFreeAsync).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+// Debugging aid (debug build libv3db_debug.so only, env V3DB_SYNC_CHECK=1): synchronize the
+// stream after a launch and return the first error tagged with the kernel name (through
+// v3db_last_error).  No-op in the release build.
 cudaError_t debug_sync(cudaStream_t st, const char* what);
 
 constexpr int32_t kDMax = 0x7fffffff;  // d_max = 2^31 - 1 (reading R8)
@@ -121,6 +145,8 @@ __host__ __device__ constexpr int rot_goff(int M, int g) {
 // Build: codes_rot / pterm_rot from the canonical codes / pterm, and cbT.
 cudaError_t rotate_codes(const uint8_t* codes, const int32_t* pterm, int nlist, int L, int M, int mode, int G,
                          uint8_t* codes_rot, int32_t* pterm_rot, cudaStream_t st);
+cudaError_t make_xhat(const uint8_t* codes, const int32_t* counts, const int8_t* cb, int nlist, int L, int Lp,
+                      int dim, int M, int Ks, int8_t* xhat, cudaStream_t st);
 cudaError_t transpose_codebooks(const int8_t* cb, int M, int Ks, int d, int8_t* cbT, cudaStream_t st);
 
 // Steps 3-5, generic query-major scan (scan_lut.cu): any shape, per-query LUT [M][Ks] in shared
@@ -134,6 +160,15 @@ cudaError_t scan_generic(const v3db_snapshot* s, const int8_t* queries, int64_t 
 cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
                          const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
                          int32_t* trace_cand, cudaStream_t st);
+
+// Steps 3-5, list-major tensor-core scan (scan_lm.cu): D_{i,j} = d_i + P_{i,j} - 2 <q, xhat_{i,j}> as
+// tcgen05 kind::i8 tiles per (list, 128 slots, <= NT probing queries), every D to the trace (a
+// library scratch trace when the caller passes none), 32-slot group minima, then an exact per-query
+// selection.  Requires s->xhat.  prof(i) records profiling marks 2 (after grouping) and 3 (after
+// the contraction kernel).
+cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
+                            const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
+                            int32_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t));
 
 // Ascending sort of nseg segments of P (a power of two) 64-bit keys (witness.cu).
 cudaError_t segmented_sort(uint64_t* keys, int64_t nseg, int P, cudaStream_t st);
@@ -166,6 +201,8 @@ cudaError_t fx_build_tail(const int32_t* db, int64_t n, int dim, const int32_t* 
 // L2-aware query order (scan_rot.cu): queries grouped by the MinHash min(probe list ids);
 // scratch [2 nq + nlist] int32, the order lands in scratch + nq.
 cudaError_t minhash_order(const int32_t* lists, int64_t nq, int nprobe, int nlist, int32_t* scratch, cudaStream_t st);
+// The fx16 scan instantiations that read the rotated code copy (codes_rot16 is built only for these).
+bool fx_rot_supported(int M, int Ks);
 cudaError_t rotate_codes16(const uint8_t* codes, int64_t slots, int L, int M, uint8_t* out, cudaStream_t st);
 cudaError_t fx_scan(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k, const int32_t* lists,
                     const int64_t* ldist, int32_t* out_ids, int64_t* out_dist, int64_t* trace, cudaStream_t st);

@@ -154,8 +154,8 @@ __global__ void unpack_kernel(const uint64_t* __restrict__ keys, int64_t nq, int
   }
 }
 
-int pow2_at_least(int64_t n) {
-  int p = 1;
+int64_t pow2_at_least(int64_t n) {
+  int64_t p = 1;
   while (p < n) p <<= 1;
   return p;
 }
@@ -193,11 +193,14 @@ cudaError_t witness_batch(const v3db_snapshot* s, const int8_t* queries, int64_t
                           int32_t* list_dist, int32_t* lut_sel, int32_t* cand_items, int32_t* cand_dist,
                           cudaStream_t st) {
   if (nq <= 0) return cudaSuccess;
-  const int P1 = pow2_at_least(s->nlist);
   const int64_t nsel = static_cast<int64_t>(nprobe) * s->L;
-  const int P2 = pow2_at_least(nsel);
+  // segments of up to 2^30 keys (segmented_sort's int segment length; larger ones are refused)
+  if (pow2_at_least(s->nlist) > (int64_t(1) << 30) || pow2_at_least(nsel) > (int64_t(1) << 30))
+    return cudaErrorInvalidValue;
+  const int P1 = static_cast<int>(pow2_at_least(s->nlist));
+  const int P2 = static_cast<int>(pow2_at_least(nsel));
   uint64_t* keys1 = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&keys1), sizeof(uint64_t) * (nq * P1 + nq * P2), st);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&keys1), sizeof(uint64_t) * (nq * P1 + nq * P2), st);
   if (e != cudaSuccess) return e;
   uint64_t* keys2 = keys1 + nq * P1;
   const unsigned g = 148 * 8;

@@ -18,8 +18,9 @@ import torch
 
 from . import _lib
 from ._lib import (FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_CODES, FIELD_COUNTS, FIELD_IDS,  # noqa: F401
-                   FIELD_LIST_OF, KIND_FX16, KIND_INT8, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, SHAPE_GREEDY, SHAPE_REBALANCE,
-                   V3DBError)
+                   FIELD_LIST_OF, KIND_FX16, KIND_INT8, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, SCAN_LIST_MAJOR, SHAPE_GREEDY, SHAPE_REBALANCE,
+                   V3DBError, OPT_LUT_W32, OPT_COARSE_SIMT, OPT_SCHED, OPT_FX_NOROT, OPT_FX_W12,
+                   OPT_SCAN_SEG, OPT_SCAN_NS, OPT_SCAN_CAP, OPT_SCAN_FIRST, OPT_SCAN_DIRECT, OPT_LM_NT, OPT_AUTO_SCAN)
 
 
 def _stream_ptr(stream) -> ctypes.c_void_p:
@@ -154,6 +155,12 @@ def query_batch_fx_host(s: Snapshot, queries: torch.Tensor, v_max: float, nprobe
     _need(out["out_ids"], torch.int32, "cpu", (nq, k), "out_ids")
     _need(out["out_dist"], torch.int64, "cpu", (nq, k), "out_dist")
     tl, tld, tcd = out.get("trace_lists"), out.get("trace_list_dist"), out.get("trace_cand_dist")
+    if tl is not None:
+        _need(tl, torch.int32, "cpu", (nq, nprobe), "trace_lists")
+    if tld is not None:
+        _need(tld, torch.int64, "cpu", (nq, nprobe), "trace_list_dist")
+    if tcd is not None:
+        _need(tcd, torch.int64, "cpu", (nq, nprobe, s.list_cap), "trace_cand_dist")
     _lib.check(lib.v3db_query_batch_fx_host(s.handle, _ptr(queries), nq, float(v_max), nprobe, k, _ptr(out["out_ids"]),
                                             _ptr(out["out_dist"]), _ptr(tl), _ptr(tld), _ptr(tcd),
                                             _stream_ptr(stream)))
@@ -219,6 +226,12 @@ def query_batch_host(s: Snapshot, queries: torch.Tensor, nprobe: int, k: int, ou
     for name in ("out_ids", "out_dist"):
         _need(out[name], torch.int32, "cpu", (nq, k), name)
     tl, tld, tcd = out.get("trace_lists"), out.get("trace_list_dist"), out.get("trace_cand_dist")
+    if tl is not None:
+        _need(tl, torch.int32, "cpu", (nq, nprobe), "trace_lists")
+    if tld is not None:
+        _need(tld, torch.int32, "cpu", (nq, nprobe), "trace_list_dist")
+    if tcd is not None:
+        _need(tcd, torch.int32, "cpu", (nq, nprobe, s.list_cap), "trace_cand_dist")
     _lib.check(lib.v3db_query_batch_host(s.handle, _ptr(queries), nq, nprobe, k, _ptr(out["out_ids"]),
                                          _ptr(out["out_dist"]), _ptr(tl), _ptr(tld), _ptr(tcd),
                                          _stream_ptr(stream)))
@@ -280,13 +293,37 @@ def profile_enable(on: bool = True) -> None:
     _lib.check(_lib.load().v3db_profile_enable(1 if on else 0))
 
 
-def profile_read() -> tuple[float, float]:
-    """v3db_profile_read: (coarse ms, scan ms) of the most recent profiled query call."""
-    buf = (ctypes.c_float * 2)()
-    _lib.check(_lib.load().v3db_profile_read(buf, 2))
-    return float(buf[0]), float(buf[1])
+def profile_read(detail: bool = False) -> tuple:
+    """v3db_profile_read: (coarse ms, scan ms) of the most recent profiled query call; with
+    detail=True (coarse, scan, scan main kernel, scan prologue, scan epilogue) in ms."""
+    buf = (ctypes.c_float * 5)()
+    _lib.check(_lib.load().v3db_profile_read(buf, 5))
+    return tuple(float(x) for x in buf) if detail else (float(buf[0]), float(buf[1]))
 
 
 def kernel_launches() -> int:
     """v3db_kernel_launches: kernels launched by libv3db since load."""
     return int(_lib.load().v3db_kernel_launches())
+
+
+def set_option(key: int, value: int) -> int:
+    """v3db_set_option (V3DB_OPT_* keys, 0 = default); returns the previous value."""
+    lib = _lib.load()
+    prev = int(lib.v3db_get_option(key))
+    _lib.check(lib.v3db_set_option(key, int(value)))
+    return prev
+
+
+class option:
+    """Context manager: `with v3db.option(v3db.OPT_LUT_W32, 1): ...` restores the old value."""
+
+    def __init__(self, key: int, value: int):
+        self.key, self.value, self.prev = key, value, None
+
+    def __enter__(self):
+        self.prev = set_option(self.key, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.key, self.prev)
+        return False

@@ -103,6 +103,12 @@ def test_fx_encoding_rounding_cases(v3db):
     h = np.array([0.5, -0.5, 1.5, 2.5, -2.5, 65534.5], np.float32)
     got = v3db.encode_fixed_point(torch.from_numpy(h).cuda(), 65535.0).cpu().numpy()
     assert got.tolist() == [1, -1, 2, 3, -3, 65535]
+    # the float32 neighbours of the halves: just below 1/2 rounds to 0 (floor(y + 0.5) would give 1)
+    b = np.nextafter(np.float32(0.5), np.float32(0))
+    n = np.array([b, -b, np.nextafter(np.float32(0.5), np.float32(1)), np.nextafter(np.float32(2.5), np.float32(0)),
+                  np.nextafter(np.float32(1.5), np.float32(2))], np.float32)
+    got = v3db.encode_fixed_point(torch.from_numpy(n).cuda(), 65535.0).cpu().numpy()
+    assert got.tolist() == [0, 0, 1, 2, 2] == oracle.encode_fixed_point(n, 65535.0).tolist()
     rng = np.random.default_rng(5)
     y = (rng.standard_normal(1 << 20) * 3).astype(np.float32)
     vm = float(np.abs(y).max())

@@ -2,8 +2,9 @@
 
 All arithmetic is integer, so the bar is bit-exact equality of every output: the snapshot
 arrays (centroids, codebooks, ids, codes, counts, list_of), out_ids, out_dist,
-trace_lists, trace_list_dist and trace_cand_dist.  Both scan kernels (the generic
-query-major LUT scan and the rotated conflict-free LUT scan) are checked.
+trace_lists, trace_list_dist and trace_cand_dist.  Every scan kernel (the generic
+query-major LUT scan, the rotated conflict-free LUT scan and the list-major tensor-core scan) is
+checked.
 """
 import numpy as np
 import pytest
@@ -17,7 +18,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 FIELDS = ("centroids", "codebooks", "ids", "codes", "counts", "list_of")
-ALGOS = {"auto": 0, "gen": 1, "rot": 2}
+ALGOS = {"auto": 0, "gen": 1, "rot": 2, "lm": 3}
 
 
 @pytest.fixture(scope="module")
@@ -72,7 +73,7 @@ def config_case(name):
     return _CACHE[name]
 
 
-@pytest.mark.parametrize("algo", ["gen", "rot"])
+@pytest.mark.parametrize("algo", ["gen", "rot", "lm"])
 @pytest.mark.parametrize("name", ["c0", "c1", "e2_basic", "e2_lowacc", "e2_large", "c4_mini"])
 def test_full_parity_small_configs(v3db, name, algo):
     """Full snapshot + full query batch, bit-exact (C0, C1 and the paper's E2 shapes)."""
@@ -148,7 +149,7 @@ def test_ragged_batch_sizes(v3db, nq):
     qs = np.vstack([inp.queries] * 3)[:nq]
     want = oracle.query_batch(ref_s, qs, cfg.nprobe, cfg.k)
     q = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
-    for algo in (1, 2):
+    for algo in (1, 2, 3):
         out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, algo=algo)
         torch.cuda.synchronize()
         assert_query_equal(out, want)
@@ -158,9 +159,9 @@ def test_ragged_batch_sizes(v3db, nq):
 @pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_basic"])
 def test_rotated_w32_geometry(v3db, name, monkeypatch):
     """The wrap geometry (kLutW32) on shapes where AUTO picks the 64-column one: same bits."""
-    monkeypatch.setenv("V3DB_LUT_MODE", "w32")
     cfg, inp, ref_s, ref = config_case(name)
-    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    with v3db.option(v3db.OPT_LUT_W32, 1):
+        s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
     out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k, algo=ALGOS["rot"])
     torch.cuda.synchronize()
     assert_query_equal(out, ref)
@@ -174,14 +175,13 @@ def test_rotated_group_decompositions(v3db, M, d, k, geo, monkeypatch):
     """W32 rotation groups of every size mix: 12 = 8+4, 24 = 16+8 (forced), 48 = 32+16, 96 = 3x32
     (512 consumer threads), 128 = 4x32; the P64 geometry with M not dividing 64 (12, 20, 24, 28:
     columns l + s hold subspace (l + s) mod M); ragged list fill and a ragged last chunk."""
-    if geo:
-        monkeypatch.setenv("V3DB_LUT_MODE", geo)
     rng = np.random.default_rng(100 + M)
     N, D, nlist, L, Ks = 3000, M * d, 12, 300, 256
     db = rng.integers(-100, 100, size=(N, D)).astype(np.int8)
     qs = rng.integers(-100, 100, size=(41, D)).astype(np.int8)
-    run_case(v3db, db, qs, nlist, L, M, Ks, 5, k, rng.choice(N, nlist, replace=False),
-             np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
+    with v3db.option(v3db.OPT_LUT_W32, 1 if geo == "w32" else 0):
+        run_case(v3db, db, qs, nlist, L, M, Ks, 5, k, rng.choice(N, nlist, replace=False),
+                 np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
 
 
 @pytest.mark.parametrize("k", [1, 7, 100, 333, 1024])
@@ -205,7 +205,7 @@ def test_empty_batch_and_trace_off_and_host_api(v3db):
     # nq = 0 is a no-op
     v3db.query_batch(s, q[:0], cfg.nprobe, cfg.k)
     # trace off: same top-k
-    for algo in (1, 2):
+    for algo in (1, 2, 3):
         out = v3db.query_batch(s, q, cfg.nprobe, cfg.k, trace=False, algo=algo)
         torch.cuda.synchronize()
         assert_query_equal(out, ref, keys=("out_ids", "out_dist"))
@@ -275,12 +275,12 @@ def test_rotated_rejected_for_unsupported_shape(v3db):
 def test_coarse_mma_fallback_path(v3db, name, monkeypatch):
     """The mma.sync coarse kernel (used when the TMA/tcgen05 path does not apply) gives the
     same bit-exact snapshot and query results."""
-    monkeypatch.setenv("V3DB_FORCE_COARSE_MMA", "1")
     cfg, inp, ref_s, ref = config_case(name)
-    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
-    assert_snapshot_equal(v3db, s, ref_s)
-    out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k)
-    torch.cuda.synchronize()
+    with v3db.option(v3db.OPT_COARSE_SIMT, 1):
+        s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+        assert_snapshot_equal(v3db, s, ref_s)
+        out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k)
+        torch.cuda.synchronize()
     assert_query_equal(out, ref)
     s.free()
 
@@ -354,4 +354,80 @@ def test_rebalance_parity(v3db, name):
     out = v3db.query_batch(s, torch.from_numpy(np.ascontiguousarray(qs)).cuda(), cfg.nprobe, cfg.k)
     torch.cuda.synchronize()
     assert_query_equal(out, want)
+    s.free()
+
+
+# ---------------------------------------------------------------- list-major tensor-core scan
+
+def test_lm_edge_all_identical_vectors(v3db):
+    """Every D ties: tau (k-th smallest group minimum) equals every group's minimum, so every group
+    is selected; the k winners come from the item-id radix pass among the ties (R10)."""
+    N, D, nlist, L = 600, 32, 4, 200
+    db = np.full((N, D), 7, np.int8)
+    qs = np.vstack([np.full((1, D), 7, np.int8), np.full((1, D), -9, np.int8), np.arange(D, dtype=np.int8)[None]])
+    run_case(v3db, db, qs, nlist, L, 4, 4, 3, 50, np.arange(nlist), np.stack([np.arange(4)] * 4),
+             algos=("lm", "gen"))
+
+
+def test_lm_edge_fewer_than_k_valid(v3db):
+    """Fewer valid candidates than k (fewer valid groups than k): everything valid is returned,
+    then (-1, d_max) (R11); lists shorter than one 32-slot group, tiles of padding only."""
+    rng = np.random.default_rng(12)
+    N, D, nlist, L = 40, 16, 8, 300
+    db = rng.integers(-100, 100, size=(N, D)).astype(np.int8)
+    qs = rng.integers(-100, 100, size=(19, D)).astype(np.int8)
+    ref_s, ref = run_case(v3db, db, qs, nlist, L, 2, 8, 2, 100, rng.choice(N, nlist, replace=False),
+                          np.stack([rng.choice(N, 8, replace=False) for _ in range(2)]), algos=("lm",))
+    assert (ref["out_ids"] == -1).any()
+
+
+def test_lm_edge_outlier_list(v3db):
+    """A query whose nearest list holds a single vector (one valid group of one slot)."""
+    rng = np.random.default_rng(13)
+    N, D, nlist, L = 3000, 16, 3, 2000
+    db = rng.integers(-20, 20, size=(N, D)).astype(np.int8)
+    db[0] = 120
+    qs = np.vstack([np.full((4, D), 118, np.int8), rng.integers(-20, 20, size=(5, D)).astype(np.int8)])
+    run_case(v3db, db, qs, nlist, L, 4, 32, 3, 10, [0, 1, 2], np.stack([rng.choice(N, 32, replace=False)] * 4),
+             algos=("lm",))
+
+
+@pytest.mark.parametrize("D,M,L,nq", [(16, 4, 130, 300), (48, 12, 257, 70), (96, 24, 384, 41), (256, 32, 100, 33),
+                                      (768, 96, 320, 20), (2048, 128, 64, 9)])
+def test_lm_shapes(v3db, D, M, L, nq):
+    """Dims below one 32-byte K step, ragged K panels (48, 96), several panels (256, 768, 2048 =
+    the largest dim: 16 panels, NT = 32 pairs per item), L not a multiple of 128 (partial tiles,
+    tiles of padding only), many queries per list (items split at NT)."""
+    rng = np.random.default_rng(D + L)
+    nlist = 12
+    N = min(900, nlist * L * 9 // 10)
+    db = rng.integers(-90, 90, size=(N, D)).astype(np.int8)
+    qs = rng.integers(-90, 90, size=(nq, D)).astype(np.int8)
+    run_case(v3db, db, qs, nlist, L, M, 16, 4, 37, rng.choice(N, nlist, replace=False),
+             np.stack([rng.choice(N, 16, replace=False) for _ in range(M)]), algos=("lm",))
+
+
+@pytest.mark.parametrize("nt", [32, 64, 128, 256])
+def test_lm_items_per_pair_count(v3db, nt):
+    """Every NT (pairs per work item: items split lists probed by more queries), same bits."""
+    cfg, inp, ref_s, ref = config_case("c1")
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    with v3db.option(v3db.OPT_LM_NT, nt):
+        out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k, algo=ALGOS["lm"])
+        torch.cuda.synchronize()
+    assert_query_equal(out, ref)
+    s.free()
+
+
+@pytest.mark.parametrize("k", [1, 7, 100, 333, 1024])
+def test_lm_topk_sizes(v3db, k):
+    """The list-major Step-5 selection for k from 1 to V3DB_MAX_K (C4's list shape)."""
+    cfg, inp, ref_s, _ = config_case("c4_mini")
+    qs = inp.queries[:48]
+    want = oracle.query_batch(ref_s, qs, cfg.nprobe, k)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    for trace in (True, False):
+        out = v3db.query_batch(s, torch.from_numpy(qs).cuda(), cfg.nprobe, k, trace=trace, algo=ALGOS["lm"])
+        torch.cuda.synchronize()
+        assert_query_equal(out, want, keys=None if trace else ("out_ids", "out_dist"))
     s.free()

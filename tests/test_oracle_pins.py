@@ -368,6 +368,23 @@ def test_fixed_point_encoding_by_hand():
     assert got.dtype == np.int32
 
 
+def test_fixed_point_rounding_just_below_half():
+    """PAPER.md:781-782's rounding at the representable neighbours of the half-integers (R18:
+    half away from zero).  With v_max = 65535 the scaled value is y = v exactly, so v = the largest
+    double below 0.5 must round to 0 (an implementation computing floor(y + 0.5) returns 1: the
+    sum rounds to 1.0), the smallest double above 0.5 to 1, 2.5 to 3, nextafter(2.5, 0) to 2,
+    and every case mirrored for negative v."""
+    below, above = np.nextafter(0.5, 0.0), np.nextafter(0.5, 1.0)
+    v = np.array([below, above, 0.5, 2.5, np.nextafter(2.5, 0.0), np.nextafter(1.5, 2.0), 1.0, 0.0])
+    exp = [0, 1, 1, 3, 2, 2, 1, 0]
+    assert oracle.encode_fixed_point(v, 65535.0).tolist() == exp
+    assert oracle.encode_fixed_point(-v, 65535.0).tolist() == [-e for e in exp]
+    # the same through float32 input (the C ABI takes float32): 0.5 - 2^-25 is a float32 value
+    x32 = np.array([np.nextafter(np.float32(0.5), np.float32(0))], dtype=np.float32)
+    assert oracle.encode_fixed_point(x32, 65535.0).tolist() == [0]
+    assert oracle.encode_fixed_point(-x32, 65535.0).tolist() == [0]
+
+
 def test_fixed_point_variant_equals_int8_semantics_when_nothing_saturates():
     """Special case reducing to the pinned int8 path: on int8-valued data whose residuals never
     leave [-127, 127] (so R5's saturation is a no-op), the fixed-point oracle (int32 storage, int64
