@@ -69,7 +69,9 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
                                                                 const __grid_constant__ CUtensorMap tmMu,
                                                                 const CoarseArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the shared array (an integer round trip would
+  // make every access through `smem` a generic-address LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                   // kp panels of [128][128]
   uint8_t* sB = smem + a.kp * kAPanelBytes;             // stages of [256][128]
   int* sCn = reinterpret_cast<int*>(sB + a.stages * kBStageBytes);  // [kEpiWarps][64] ||mu||^2

@@ -18,10 +18,10 @@
 //   warp 1      one lane: the MMAs (double-buffered B operand, NACC TMEM accumulators);
 //   warps 2-3   gather the item's query rows into the 128B-swizzled K-major B operand (cp.async)
 //               and the per-pair metadata (trace row, d_i, group-minimum row);
-//   warps 4-11  epilogue: tcgen05.ld (lane = slot, column = pair), D = d_i + P - 2 acc, padding
+//   warps 4-19  epilogue: tcgen05.ld (lane = slot, column = pair), D = d_i + P - 2 acc, padding
 //               slots d_max, the whole trace row segment with coalesced stores
 //               (32 lanes = 32 consecutive slots), and the minimum D of every 32-slot group.
-// Step 5, lm_select_kernel, one CTA per query: tau = the k-th smallest group
+// Step 5, lm_select_fast_kernel, one CTA per query: tau = the k-th smallest group
 // minimum (>= the k-th smallest D: k distinct candidates reach it), then an exact radix selection
 // of the k smallest (D, item) keys among the slots of the groups whose minimum is <= tau (read
 // back from the trace), ties at the k-th distance resolved by item id (R10).
@@ -41,13 +41,15 @@ namespace {
 constexpr int kTile = 128;                              // slots per tile (UMMA M) = TMEM lanes
 constexpr int kPanel = 128;                             // bytes of K per swizzled panel
 constexpr uint32_t kAStageBytes = kTile * kPanel;       // 16 KB
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;                           // 4 per TMEM lane quadrant
+constexpr int kChunk = 16;                              // accumulator columns per tcgen05.ld
+constexpr int kNB = 3;                                  // B operand (query rows) buffers
 constexpr int kWarpTma = 0, kWarpMma = 1, kWarpGat = 2, kNGat = 2, kWarpEpi = 4;
-constexpr int kThreads = 32 * (kWarpEpi + kEpiWarps);  // 384
+constexpr int kThreads = 32 * (kWarpEpi + kEpiWarps);  // 640
 constexpr uint32_t kFull = 0xffffffffu;
 
 struct LmArgs {
-  int nprobe, L, Lp, dim, kp, NT, nacc, S, ngroups;
+  int nprobe, L, Lp, dim, kp, NT, nacc, lg_nacc, S, nb, ngroups;
   const int8_t* queries;
   const int32_t* pairs;   // pair ids (q * nprobe + rho) grouped by list
   const int4* items;      // (list, first pair, pairs, 0)
@@ -57,31 +59,33 @@ struct LmArgs {
   const int32_t* pterm;   // [nlist][L]
   int32_t* trace;         // [nq][nprobe][L]
   int32_t* gmin;          // [nq][nprobe][ngroups]
-  uint32_t off_b, off_meta, off_bar, b_bytes;
+  uint32_t off_b, off_meta, off_wmin, off_bar, b_bytes;
 };
 
-struct PairMeta {  // 16 B, read by the epilogue as one broadcast LDS.128
-  int trow_lo, trow_hi;  // trace element offset of the pair's row: pair * L
-  int d;                 // d_i
-  int goff;              // pair * ngroups
+struct PairMeta {     // 16 B, read by the epilogue as one broadcast LDS.128
+  uint64_t row;       // address of the pair's trace row: trace + pair * L
+  int d;              // d_i
+  int goff;           // pair * ngroups
 };
-
 
 // ----------------------------------------------------------------------------------------------
 // The contraction + epilogue kernel.
 // ----------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__ CUtensorMap tmX, const LmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the shared array (an integer round trip would
+  // make every access through `smem` a generic-address LD/ST instead of LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                         // [S][128 x 128 B]
-  uint8_t* sB = smem + a.off_b;                               // [2][kp][NT x 128 B]
-  PairMeta* meta = reinterpret_cast<PairMeta*>(smem + a.off_meta);  // [2][NT]
+  uint8_t* sB = smem + a.off_b;                               // [nb][kp][NT x 128 B]
+  PairMeta* meta = reinterpret_cast<PairMeta*>(smem + a.off_meta);  // [nb][NT]
+  int* wmin = reinterpret_cast<int*>(smem + a.off_wmin);     // [kEpiWarps][kChunk] column minima
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* afull = bars;                  // [S]
   uint64_t* aempty = afull + a.S;          // [S]
-  uint64_t* bfull = aempty + a.S;          // [2]
-  uint64_t* bempty = bfull + 2;            // [2]
-  uint64_t* accf = bempty + 2;             // [nacc]
+  uint64_t* bfull = aempty + a.S;          // [kNB]
+  uint64_t* bempty = bfull + kNB;          // [kNB]
+  uint64_t* accf = bempty + kNB;           // [nacc]
   uint64_t* acce = accf + a.nacc;          // [nacc]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + a.nacc);
 
@@ -94,13 +98,13 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
       tc::mbar_init(afull + s, 1);
       tc::mbar_init(aempty + s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kNB; ++b) {
       tc::mbar_init(bfull + b, kNGat);
       tc::mbar_init(bempty + b, 1 + kEpiWarps);
     }
     for (int c = 0; c < a.nacc; ++c) {
       tc::mbar_init(accf + c, 1);
-      tc::mbar_init(acce + c, kEpiWarps);
+      tc::mbar_init(acce + c, kEpiWarps / 2);  // one epilogue group drains an accumulator
     }
     tc::mbar_fence_init();
   }
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
         const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
         for (int t = 0; t < nvt; ++t) {
           for (int p = 0; p < a.kp; ++p) {
-            if (u > 0) tc::mbar_wait(aempty + s, (u - 1) & 1);
+            if (u > 0) tc::mbar_wait_sleep(aempty + s, (u - 1) & 1);
             tc::mbar_expect_tx(afull + s, kAStageBytes);
             tc::tma_load_2d(sA + s * kAStageBytes, &tmX, afull + s, p * kPanel, it.x * a.Lp + t * kTile);
             if (++s == a.S) {
@@ -134,24 +138,23 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
   } else if (warp == kWarpMma) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      int s = 0, u = 0, n = 0, tcount = 0;
-      for (int j = blockIdx.x; j < n_items; j += gridDim.x, ++n) {
+      int s = 0, u = 0, b = 0, bph = 0, tcount = 0;
+      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
         const int4 it = a.items[j];
-        const int b = n & 1;
         const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
         const int N = (it.z + 15) & ~15;  // UMMA N for M = 128: multiple of 16
         const uint32_t idesc = tc::idesc_s8(kTile, N);
-        tc::mbar_wait(bfull + b, (n >> 1) & 1);
+        tc::mbar_wait_sleep(bfull + b, bph);
         tc::fence_after_sync();
         const uint32_t b_addr = tc::smem_u32(sB + b * a.b_bytes);
         for (int t = 0; t < nvt; ++t, ++tcount) {
-          const int acc = tcount % a.nacc, ua = tcount / a.nacc;
+          const int acc = tcount & (a.nacc - 1), ua = tcount >> a.lg_nacc;
           if (ua > 0) {
-            tc::mbar_wait(acce + acc, (ua - 1) & 1);
+            tc::mbar_wait_sleep(acce + acc, (ua - 1) & 1);
             tc::fence_after_sync();
           }
           for (int p = 0; p < a.kp; ++p) {
-            tc::mbar_wait(afull + s, u & 1);
+            tc::mbar_wait_sleep(afull + s, u & 1);
             tc::fence_after_sync();
             const int nk = min(4, (a.dim - p * kPanel + 31) / 32);
             const uint32_t a_addr = tc::smem_u32(sA + s * kAStageBytes);
@@ -168,23 +171,25 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
           tc::mma_commit(accf + acc);
         }
         tc::mma_commit(bempty + b);  // the B buffer is free once this item's MMAs completed
+        if (++b == a.nb) {
+          b = 0;
+          bph ^= 1;
+        }
       }
     }
   } else if (warp < kWarpEpi) {
     // ------------------------------------------------------------ gather: B operand + metadata
     const int gt = tid - kWarpGat * 32;  // 0 .. 63
     const int cpr = a.dim >> 4;          // 16-byte chunks per query row
-    int n = 0;
-    for (int j = blockIdx.x; j < n_items; j += gridDim.x, ++n) {
+    int b = 0, use = 0;  // buffer, times the ring wrapped
+    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
       const int4 it = a.items[j];
-      const int b = n & 1;
-      if (n >= 2) tc::mbar_wait(bempty + b, ((n >> 1) - 1) & 1);
+      if (use > 0) tc::mbar_wait_sleep(bempty + b, (use - 1) & 1);
       uint8_t* dst = sB + b * a.b_bytes;
       PairMeta* mt = meta + b * NT;
       for (int r = gt; r < it.z; r += 32 * kNGat) {
         const int pr = __ldg(a.pairs + it.y + r);
-        const int64_t trow = static_cast<int64_t>(pr) * L;
-        mt[r] = PairMeta{static_cast<int>(trow & 0xffffffff), static_cast<int>(trow >> 32), __ldg(a.ldist + pr),
+        mt[r] = PairMeta{reinterpret_cast<uint64_t>(a.trace + static_cast<int64_t>(pr) * L), __ldg(a.ldist + pr),
                          pr * a.ngroups};
       }
       for (int e = gt; e < it.z * cpr; e += 32 * kNGat) {
@@ -198,61 +203,87 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
       tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(bfull + b);
+      if (++b == a.nb) {
+        b = 0;
+        ++use;
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int e = warp - kWarpEpi, qd = warp & 3, cg = e >> 2;
-    constexpr int NCG = kEpiWarps / 4;
-    int n = 0, tcount = 0;
-    for (int j = blockIdx.x; j < n_items; j += gridDim.x, ++n) {
+    // Two groups of 8 warps take alternate tiles (two tiles drain at once).  Within a group, warp:
+    // TMEM lane quadrant qd (its 32 slots of the tile) and column group cg (chunks of 16 columns
+    // cg, cg + 2, ...).  Thread = one slot; per column (pair): D to the trace (the 32 lanes store
+    // 128 consecutive bytes) and the group minimum over the 32 lanes (REDUX).
+    const int e = warp - kWarpEpi, qd = warp & 3, grp = e >> 3, cg = (e >> 2) & 1;
+    constexpr int NCG = 2;
+    int* wm = wmin + e * kChunk;
+    int b = 0, bph = 0, tcount = 0, tall = 0;
+    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
       const int4 it = a.items[j];
-      const int b = n & 1, np = it.z;
+      const int np = it.z;
       const int cnt = __ldg(a.counts + it.x);
       const int nvt = (cnt + kTile - 1) / kTile, ntl = (L + kTile - 1) / kTile;
       const PairMeta* mt = meta + b * NT;
-      tc::mbar_wait(bfull + b, (n >> 1) & 1);
-      for (int t = 0; t < ntl; ++t) {
-        const int slot = t * kTile + qd * 32 + lane;
-        const bool inL = slot < L, valid = slot < cnt;
+      const int32_t* prow = a.pterm + static_cast<int64_t>(it.x) * L;
+      tc::mbar_wait_sleep(bfull + b, bph);
+      for (int t = 0; t < ntl; ++t, ++tall) {
+        const bool mine = (tall & 1) == grp;
+        const int sbase = t * kTile + qd * 32, slot = sbase + lane;
+        const uint64_t toff = 4ull * static_cast<uint32_t>(slot);
         if (t < nvt) {
-          const int acc = tcount % a.nacc, ua = tcount / a.nacc;
+          const int acc = tcount & (a.nacc - 1), ua = tcount >> a.lg_nacc;
           ++tcount;
-          const int32_t P = valid ? __ldg(a.pterm + static_cast<int64_t>(it.x) * L + slot) : 0;
-          tc::mbar_wait(accf + acc, ua & 1);
+          if (!mine) continue;
+          const bool valid = slot < cnt;
+          const int32_t P = valid ? __ldg(prow + slot) : 0;   // issued before the wait
+          const bool full = sbase + 32 <= cnt;                // warp-uniform: every slot valid (< L)
+          tc::mbar_wait_sleep(accf + acc, ua & 1);
           tc::fence_after_sync();
-          const bool gvalid = t * kTile + qd * 32 < cnt;  // this warp's 32-slot group holds a valid slot
-          for (int jc = cg; jc * 32 < np; jc += NCG) {
-            uint32_t v[32];
-            tc::tmem_ld32(tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT + jc * 32, v);
+          for (int jc = cg; jc * kChunk < np; jc += NCG) {
+            uint32_t v[kChunk];
+            tc::tmem_ld16(tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT + jc * kChunk, v);
             tc::tmem_ld_wait();
-            int gm = kDMax;
-            const int ncol = min(32, np - jc * 32);
+            const PairMeta* mc = mt + jc * kChunk;
+            const int ncol = min(kChunk, np - jc * kChunk);
+            if (full && ncol == kChunk) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              if (c >= ncol) break;  // warp-uniform
-              const PairMeta m = mt[jc * 32 + c];
-              const int32_t D = valid ? m.d + P - 2 * static_cast<int32_t>(v[c]) : kDMax;
-              const int64_t trow = (static_cast<int64_t>(m.trow_hi) << 32) | static_cast<uint32_t>(m.trow_lo);
-              if (inL) __stcs(a.trace + trow + slot, D);
-              const int mn = __reduce_min_sync(kFull, D);
-              gm = lane == c ? mn : gm;
+              for (int c = 0; c < kChunk; ++c) {
+                const PairMeta m = mc[c];
+                const int32_t D = m.d + P - 2 * static_cast<int32_t>(v[c]);
+                __stcs(reinterpret_cast<int32_t*>(m.row + toff), D);
+                const int mn = __reduce_min_sync(kFull, D);
+                if (lane == 0) wm[c] = mn;
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < kChunk; ++c) {
+                if (c < ncol) {  // warp-uniform
+                  const PairMeta m = mc[c];
+                  const int32_t D = valid ? m.d + P - 2 * static_cast<int32_t>(v[c]) : kDMax;
+                  if (slot < L) __stcs(reinterpret_cast<int32_t*>(m.row + toff), D);
+                  const int mn = __reduce_min_sync(kFull, D);
+                  if (lane == 0) wm[c] = mn;
+                }
+              }
             }
-            if (gvalid && lane < ncol) a.gmin[mt[jc * 32 + lane].goff + t * 4 + qd] = gm;
+            __syncwarp();
+            if (sbase < cnt && lane < ncol) a.gmin[mc[lane].goff + t * 4 + qd] = wm[lane];
+            __syncwarp();
           }
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(acce + acc);
-        } else {
+        } else if (mine && slot < L) {
           // a tile of padding only: D = d_max, nothing read
-          for (int c = cg; c < np; c += NCG) {
-            const PairMeta m = mt[c];
-            const int64_t trow = (static_cast<int64_t>(m.trow_hi) << 32) | static_cast<uint32_t>(m.trow_lo);
-            if (inL) __stcs(a.trace + trow + slot, kDMax);
-          }
+          for (int c = cg; c < np; c += NCG) __stcs(reinterpret_cast<int32_t*>(mt[c].row + toff), kDMax);
         }
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(bempty + b);
+      if (++b == a.nb) {
+        b = 0;
+        bph ^= 1;
+      }
     }
   }
   tc::fence_before_sync();
@@ -324,6 +355,7 @@ __global__ void items_kernel(const int* __restrict__ hist, const int* __restrict
 // Step 5: exact per-query selection from the group minima and the trace.
 // ----------------------------------------------------------------------------------------------
 constexpr int kSelThreads = 256;
+constexpr int kWarpProbeCap = 128;  // largest nprobe of the cached selection path
 constexpr int kSelGroups = 4096;  // selected-group list capacity (more: every valid group is scanned)
 
 struct SelArgs {
@@ -391,8 +423,9 @@ __device__ uint32_t cta_radix_select(int n, int kk, uint32_t bound, Gen gen, int
   return prefix;
 }
 
-__global__ void __launch_bounds__(kSelThreads) lm_select_kernel(const SelArgs a) {
-  extern __shared__ __align__(16) uint8_t sm[];
+// Streaming selection (no per-query capacity limit): every pass re-reads the group minima and the
+// candidates' distances from global memory.  Used for the queries the cached path cannot hold.
+__device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
   int* pl = reinterpret_cast<int*>(sm);            // [nprobe] probed list
   int* pc = pl + a.nprobe;                         // [nprobe] its count
   int* hist = pc + a.nprobe;                       // [256]
@@ -400,8 +433,8 @@ __global__ void __launch_bounds__(kSelThreads) lm_select_kernel(const SelArgs a)
   int* sel = sc + 16;                              // [kSelGroups] selected groups (rho << 16 | g)
   uint64_t* keys = reinterpret_cast<uint64_t*>(sel + kSelGroups);  // [k]
   const int tid = threadIdx.x;
-  const int64_t q = blockIdx.x;
   const int nprobe = a.nprobe, L = a.L, NG = a.ngroups, k = a.k;
+  __syncthreads();  // the caller may have used the same shared memory
   for (int r = tid; r < nprobe; r += kSelThreads) {
     const int li = a.lists[q * nprobe + r];
     pl[r] = li;
@@ -541,6 +574,278 @@ __global__ void __launch_bounds__(kSelThreads) lm_select_kernel(const SelArgs a)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Step 5, one CTA per query, small shared footprint (8 CTAs per SM): the valid group minima are
+// cached in shared memory; tau = the upper edge of a histogram bin holding the k-th smallest one
+// (>= it, hence >= the k-th smallest D); the candidates -- the valid slots with D <= tau of the
+// groups whose minimum is <= tau -- are re-read from the trace (L2) in each pass.  The k smallest
+// (D, item) keys are exact: 256-bin histograms of D - dmin over a shrinking window; candidates
+// below the window's target bin win outright, the target bin is refined until it holds
+// <= kBinCap entries, which are ranked on their full (D, item) keys (R10).  Queries beyond the
+// caches (or kBinCap candidates tied at one distance) take the streaming path.
+// ---------------------------------------------------------------------------------------------
+constexpr int kSelGcap = 2048;     // cached group minima per query
+constexpr int kSelKmax = 256;      // largest k of the cached path
+constexpr int kBinCap = 256;       // entries of the final histogram bin ranked pairwise
+
+struct SelSmem {
+  uint32_t gv[kSelGcap];           // valid group minima - dmin
+  int gid[kSelGcap];               // rho << 16 | g, compacted to the selected groups
+  int hist[256];
+  int pl[kWarpProbeCap];           // probed lists
+  int pc[kWarpProbeCap];           // their counts
+  int pg[kWarpProbeCap + 1];       // valid-group prefix
+  uint64_t keys[kSelKmax];         // winners
+  uint64_t bin[kBinCap];           // final-bin entries
+  int sc[40];
+};
+
+// Block-wide: the bin of hist[0, 256) holding rank kk (1-based); *before = entries below it,
+// *inbin = its population.  256 threads; ends with a barrier.
+__device__ __forceinline__ int cta_bin_of(SelSmem& S, int kk, int* before, int* inbin) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = S.hist[tid];
+  int incl = h;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int w = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += w;
+  }
+  if (lane == 31) S.sc[24 + warp] = incl;
+  __syncthreads();
+  int base = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) base += w < warp ? S.sc[24 + w] : 0;
+  const int excl = base + incl - h;
+  if (excl < kk && kk <= excl + h) {
+    S.sc[0] = tid;
+    S.sc[1] = excl;
+    S.sc[2] = h;
+  }
+  __syncthreads();
+  *before = S.sc[1];
+  *inbin = S.sc[2];
+  return S.sc[0];
+}
+
+__global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const SelArgs a, int* __restrict__ flags) {
+  __shared__ SelSmem S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t q = blockIdx.x;
+  const int nprobe = a.nprobe, L = a.L, NG = a.ngroups, k = a.k;
+  const int32_t* gq = a.gmin + q * nprobe * NG;
+  const int32_t* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
+  for (int r = tid; r < nprobe; r += kSelThreads) {
+    const int li = a.lists[q * nprobe + r];
+    S.pl[r] = li;
+    S.pc[r] = __ldg(a.counts + li);
+  }
+  if (tid < 40) S.sc[tid] = tid == 3 ? 0x7fffffff : 0;
+  __syncthreads();
+  if (warp == 0) {  // prefix sums of the valid groups per probe
+    int carry = 0;
+    for (int r0 = 0; r0 < nprobe; r0 += 32) {
+      const int r = r0 + lane;
+      const int c = r < nprobe ? (S.pc[r] + 31) >> 5 : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int w = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += w;
+      }
+      if (r < nprobe) S.pg[r] = carry + incl - c;
+      carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) S.pg[nprobe] = carry;
+  }
+  __syncthreads();
+  const int V = S.pg[nprobe];
+  if (V > kSelGcap) {
+    if (tid == 0) flags[q] = 1;
+    return;
+  }
+  // the valid group minima (8 loads in flight per thread), their minimum and maximum
+  int mn = 0x7fffffff, mx = 0;
+  {
+    const int tot = nprobe * NG;
+    for (int i0 = tid; i0 < tot; i0 += 8 * kSelThreads) {
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kSelThreads;
+        v[u] = i < tot ? gq[i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kSelThreads;
+        if (i < tot) {
+          const int r = i / NG, g = i - r * NG;
+          if (32 * g < S.pc[r]) {
+            const int pos = S.pg[r] + g;
+            S.gv[pos] = static_cast<uint32_t>(v[u]);
+            S.gid[pos] = (r << 16) | g;
+            mn = min(mn, v[u]);
+            mx = max(mx, v[u]);
+          }
+        }
+      }
+    }
+  }
+  mn = __reduce_min_sync(kFull, mn);
+  mx = __reduce_max_sync(kFull, mx);
+  if (lane == 0) {
+    atomicMin(S.sc + 3, mn);
+    atomicMax(S.sc + 4, mx);
+  }
+  __syncthreads();
+  const uint32_t dmin = static_cast<uint32_t>(S.sc[3]);
+  uint32_t tau = 0x7ffffffeu - dmin;  // relative
+  if (V >= k) {
+    uint32_t w0 = 0, span = static_cast<uint32_t>(S.sc[4]) - dmin + 1u;
+    int need = k;
+    for (;;) {
+      const int bits = 32 - __clz((span - 1u) | 1u);
+      const int sh = bits > 8 ? bits - 8 : 0;
+      S.hist[tid] = 0;
+      __syncthreads();
+      for (int i = tid; i < V; i += kSelThreads) {
+        const uint32_t rel = S.gv[i] - dmin;
+        if (rel >= w0 && rel - w0 < span) atomicAdd(S.hist + ((rel - w0) >> sh), 1);
+      }
+      __syncthreads();
+      int before, inbin;
+      const int b = cta_bin_of(S, need, &before, &inbin);
+      w0 += static_cast<uint32_t>(b) << sh;
+      span = 1u << sh;
+      need -= before;
+      if (sh == 0 || inbin <= 64) break;  // a bin of <= 64 group minima: tight enough
+    }
+    tau = w0 + span - 1u;
+    if (dmin + tau > 0x7ffffffeu) tau = 0x7ffffffeu - dmin;
+  }
+  // compact the selected groups (minimum <= tau) into gid[0, nsel)
+  if (tid == 0) S.sc[5] = 0;
+  __syncthreads();
+  int mine[8], nm = 0;  // a thread's selected groups (V <= 2048: at most 8 per thread)
+  for (int i = tid; i < V; i += kSelThreads)
+    if (S.gv[i] - dmin <= tau) mine[nm++] = S.gid[i];
+  __syncthreads();
+  {
+    int base = nm ? atomicAdd(S.sc + 5, nm) : 0;
+    for (int x = 0; x < nm; ++x) S.gid[base + x] = mine[x];
+  }
+  __syncthreads();
+  const int nsel = S.sc[5];
+  const int nslot = nsel * 32;
+  // candidate f in [0, nslot): slot (f & 31) of selected group f >> 5; relative D or ~0
+  auto load_rel = [&](int f, int& r, int& j) {
+    const int id = S.gid[f >> 5];
+    r = id >> 16;
+    j = 32 * (id & 0xffff) + (f & 31);
+    const uint32_t D = j < S.pc[r] ? static_cast<uint32_t>(tq[r * static_cast<int64_t>(L) + j]) : 0xffffffffu;
+    const uint32_t rel = D - dmin;
+    return rel <= tau ? rel : 0xffffffffu;
+  };
+  auto item_of = [&](int r, int j) { return __ldg(a.ids + static_cast<int64_t>(S.pl[r]) * L + j); };
+  // window [w0, w0 + span) of D - dmin holding the k-th smallest candidate; `need` = its rank in it
+  uint32_t w0 = 0, span = tau + 1u;
+  int need = k, ntot = -1;
+  for (;;) {
+    const int bits = 32 - __clz((span - 1u) | 1u);
+    const int sh = bits > 8 ? bits - 8 : 0;
+    S.hist[tid] = 0;
+    __syncthreads();
+    int c = 0;
+    for (int f0 = tid; f0 < nslot; f0 += 4 * kSelThreads) {
+      uint32_t rel[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int r, j;
+        const int f = f0 + u * kSelThreads;
+        rel[u] = f < nslot ? load_rel(f, r, j) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (rel[u] == 0xffffffffu) continue;
+        ++c;
+        if (rel[u] >= w0 && rel[u] - w0 < span) atomicAdd(S.hist + ((rel[u] - w0) >> sh), 1);
+      }
+    }
+    if (ntot < 0) {
+      c = __reduce_add_sync(kFull, c);
+      if (lane == 0) atomicAdd(S.sc + 6, c);
+    }
+    __syncthreads();
+    if (ntot < 0) {
+      ntot = S.sc[6];
+      if (ntot <= k) break;  // every candidate wins
+    }
+    int before, inbin;
+    const int b = cta_bin_of(S, need, &before, &inbin);
+    const uint32_t hi = w0 + (static_cast<uint32_t>(b) << sh);
+    const bool last = sh == 0 || inbin <= kBinCap;
+    if (last && inbin > kBinCap) {  // more than kBinCap candidates tied at one distance
+      if (tid == 0) flags[q] = 1;
+      return;
+    }
+    // candidates below the target bin win; on the last pass the bin's entries are gathered too
+    for (int f = tid; f < nslot; f += kSelThreads) {
+      int r, j;
+      const uint32_t rel = load_rel(f, r, j);
+      if (rel == 0xffffffffu || rel < w0) continue;
+      if (rel < hi) {
+        S.keys[atomicAdd(S.sc + 7, 1)] = step5_key(static_cast<int32_t>(rel + dmin), item_of(r, j));
+      } else if (last && rel - hi < (1u << sh)) {
+        S.bin[atomicAdd(S.sc + 8, 1)] = step5_key(static_cast<int32_t>(rel + dmin), item_of(r, j));
+      }
+    }
+    w0 = hi;
+    span = 1u << sh;
+    need -= before;
+    __syncthreads();
+    if (last) {
+      const int nb = S.sc[8], nlo = S.sc[7];
+      V3DB_DCHECK(nb == inbin && nlo + need == k);
+      for (int e2 = tid; e2 < nb; e2 += kSelThreads) {  // the `need` smallest keys of the bin
+        const uint64_t key = S.bin[e2];
+        int rank = 0;
+        for (int f = 0; f < nb; ++f) rank += S.bin[f] < key ? 1 : 0;
+        if (rank < need) S.keys[nlo + rank] = key;
+      }
+      break;
+    }
+  }
+  int m = k;
+  if (ntot <= k) {  // every candidate wins (fewer than k valid: (-1, d_max) tail, R11)
+    for (int f = tid; f < nslot; f += kSelThreads) {
+      int r, j;
+      const uint32_t rel = load_rel(f, r, j);
+      if (rel != 0xffffffffu) S.keys[atomicAdd(S.sc + 7, 1)] = step5_key(static_cast<int32_t>(rel + dmin), item_of(r, j));
+    }
+    m = ntot;
+  }
+  __syncthreads();
+  for (int e2 = tid; e2 < m; e2 += kSelThreads) {
+    const uint64_t key = S.keys[e2];
+    int rank = 0;
+    for (int f = 0; f < m; ++f) rank += S.keys[f] < key ? 1 : 0;
+    a.out_ids[q * k + rank] = step5_id(key);
+    a.out_dist[q * k + rank] = static_cast<int32_t>(key >> 32);
+  }
+  for (int r = m + tid; r < k; r += kSelThreads) {
+    a.out_ids[q * k + r] = -1;
+    a.out_dist[q * k + r] = kDMax;
+  }
+}
+
+// The queries the per-warp path flagged (or every query when it does not apply): one CTA each.
+__global__ void __launch_bounds__(kSelThreads) lm_select_cta_kernel(const SelArgs a, const int* __restrict__ flags) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int64_t q = blockIdx.x;
+  if (flags && flags[q] == 0) return;
+  select_streaming(a, q, sm);
+}
+
 size_t al(size_t x, size_t b) { return (x + b - 1) / b * b; }
 
 }  // namespace
@@ -554,16 +859,19 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   const int L = s->L, ngroups = (L + 31) / 32, kp = (s->dim + kPanel - 1) / kPanel;
   if (npairs >= (int64_t(1) << 31) || npairs * ngroups >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   // NT: pairs per item, the largest of 256 / 128 / 64 / 32 whose double-buffered B operand fits 128 KB
-  int NT = 256;
+  int NT = 128;
   const int64_t nt_opt = opt(V3DB_OPT_LM_NT);
   if (nt_opt == 32 || nt_opt == 64 || nt_opt == 128 || nt_opt == 256) NT = static_cast<int>(nt_opt);
-  while (NT > 32 && 2u * kp * NT * kPanel > 128u * 1024) NT >>= 1;
-  const int nacc = std::min(4, 512 / NT);
+  int nb = kNB;  // B buffers: 3, or 2 when three of the smallest NT do not fit (dim near 2048)
+  while (NT > 32 && static_cast<uint32_t>(nb) * kp * NT * kPanel > 128u * 1024) NT >>= 1;
+  if (static_cast<uint32_t>(nb) * kp * NT * kPanel > 128u * 1024) nb = 2;
+  const int nacc = std::min(4, 512 / NT);  // a power of two
+  const int lg_nacc = nacc == 4 ? 2 : nacc == 2 ? 1 : 0;
   const uint32_t b_bytes = static_cast<uint32_t>(kp) * NT * kPanel;
   int S = 6;
   auto smem_of = [&](int stages) {
-    return 1024 + static_cast<size_t>(stages) * kAStageBytes + 2 * b_bytes + 2 * sizeof(PairMeta) * NT +
-           8 * (2 * stages + 4 + 2 * nacc) + 16;
+    return 1024 + static_cast<size_t>(stages) * kAStageBytes + nb * b_bytes + nb * sizeof(PairMeta) * NT +
+           4 * kEpiWarps * kChunk + 8 * (2 * stages + 2 * kNB + 2 * nacc) + 16;
   };
   while (S > 2 && smem_of(S) > 227 * 1024) --S;
   if (smem_of(S) > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -576,7 +884,8 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   const int nlist = s->nlist;
   const int64_t max_items = nlist + npairs / NT + 1;
   const size_t b_hist = al(sizeof(int) * nlist, 256), b_pairs = al(sizeof(int32_t) * npairs, 256),
-               b_items = al(sizeof(int4) * max_items, 256), b_gmin = al(sizeof(int32_t) * npairs * ngroups, 256),
+               b_items = al(sizeof(int4) * max_items, 256),
+               b_gmin = al(sizeof(int32_t) * npairs * ngroups, 256) + al(sizeof(int) * nq, 256),  // + flags
                b_trace = trace_cand ? 0 : al(sizeof(int32_t) * npairs * L, 256);
   uint8_t* base = nullptr;
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&base), 3 * b_hist + 256 + b_pairs + b_items + b_gmin + b_trace, st);
@@ -626,8 +935,11 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   a.trace = trace;
   a.gmin = gmin;
   a.off_b = S * kAStageBytes;
-  a.off_meta = a.off_b + 2 * b_bytes;
-  a.off_bar = static_cast<uint32_t>(al(a.off_meta + 2 * sizeof(PairMeta) * NT, 8));
+  a.lg_nacc = lg_nacc;
+  a.nb = nb;
+  a.off_meta = a.off_b + nb * b_bytes;  // PairMeta is 16 B: 16-byte aligned (b_bytes is a multiple of 128)
+  a.off_wmin = a.off_meta + nb * sizeof(PairMeta) * NT;
+  a.off_bar = static_cast<uint32_t>(al(a.off_wmin + 4 * kEpiWarps * kChunk, 8));
   a.b_bytes = b_bytes;
   const size_t smem = smem_of(S);
   e = cudaFuncSetAttribute(lm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -653,14 +965,26 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
     sa.out_ids = out_ids;
     sa.out_dist = out_dist;
     const size_t ssm = sizeof(int) * (2 * nprobe + 256 + 16 + kSelGroups) + 16 + sizeof(uint64_t) * k;
-    e = cudaFuncSetAttribute(lm_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm));
+    const bool fast = k <= kSelKmax && nprobe <= kWarpProbeCap && ngroups <= 65535;
+    int* flags = nullptr;
+    if (fast) {  // cached selection; the flagged queries then take the streaming one
+      flags = reinterpret_cast<int*>(gmin + npairs * ngroups);
+      e = cudaMemsetAsync(flags, 0, sizeof(int) * nq, st);
+      if (e == cudaSuccess) {
+        lm_select_fast_kernel<<<static_cast<unsigned>(nq), kSelThreads, 0, st>>>(sa, flags);
+        note_launch();
+        e = cudaGetLastError();
+      }
+    }
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lm_select_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm));
     if (e == cudaSuccess) {
-      lm_select_kernel<<<static_cast<unsigned>(nq), kSelThreads, ssm, st>>>(sa);
+      lm_select_cta_kernel<<<static_cast<unsigned>(nq), kSelThreads, ssm, st>>>(sa, flags);
       note_launch();
       e = cudaGetLastError();
     }
   }
-  if (e == cudaSuccess) e = debug_sync(st, "lm_select_kernel");
+  if (e == cudaSuccess) e = debug_sync(st, "lm_select kernels");
   cudaFreeAsync(base, st);
   return e;
 }

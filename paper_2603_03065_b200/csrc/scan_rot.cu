@@ -77,19 +77,6 @@ constexpr uint32_t kFull = 0xffffffffu;
 // checked at kernel entry.
 constexpr uint32_t kSmemLo = 0x400;
 
-// mbarrier phase wait that lets the hardware suspend the warp (instead of spinning) until the
-// phase completes or the hint expires.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n"
-        : "=r"(ok)
-        : "r"(tc::smem_u32(bar)), "r"(parity), "r"(1000000u)
-        : "memory");
-  } while (!ok);
-}
-
 __device__ __forceinline__ int32_t lds32(uint32_t addr) {
   int32_t v;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -368,7 +355,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
       int rho = 0, s = 0;
       uint32_t eph = 0;  // parity of the empty-barrier phase to wait for (per ring pass)
       for (int t = 0; t < NSTG; ++t) {
-        if (t >= NS) mbar_wait_sleep(empty + s, eph);  // consumers released the previous fill
+        if (t >= NS) tc::mbar_wait_sleep(empty + s, eph);  // consumers released the previous fill
         uint8_t* st = stages + static_cast<uint32_t>(s) * a.stage_bytes;
         const int g0 = t * SEG, g1 = min(TV, g0 + SEG);
         // expect the stage's bytes (no arrival yet), issue the copies and write the chunk
@@ -554,7 +541,7 @@ __global__ void __launch_bounds__(Geo<M, MODE, VAR>::NTOT, Geo<M, MODE, VAR>::MI
     }
   };
   for (int t = 0, s = 0; t < NSTG; ++t) {
-    mbar_wait_sleep(full + s, fph);
+    tc::mbar_wait_sleep(full + s, fph);
     const uint8_t* st = stages + static_cast<uint32_t>(s) * a.stage_bytes;
     const int4* ds = dsc + s * SEG;
     const int n = min(TV, t * SEG + SEG) - t * SEG;
