@@ -153,7 +153,43 @@ def algorithmic_scan_bytes(cfg, lists: np.ndarray, counts: np.ndarray, trace: bo
         tr = Q * (w * cfg.nprobe * cfg.L + (4 + w) * cfg.nprobe)
         per_batch += tr
         padded += tr
-    return {"valid": per_batch, "padded": padded, "valid_slots": valid}
+    return {"valid": per_batch, "padded": padded, "valid_slots": valid, "topk_out": Q * (4 + w) * cfg.k}
+
+
+def resolved_algo(v3db, snap, algo: int, fx: bool) -> str:
+    """The scan kernel V3DB_SCAN_AUTO (or the explicit algo) runs for this snapshot."""
+    if fx:
+        return "fx16"
+    names = {1: "generic", 2: "rotated", 3: "list_major"}
+    if algo:
+        return names[algo]
+    return "list_major" if snap.dim % 16 == 0 else "rotated"
+
+
+def algo_used_pre(algo: int, snap) -> str:
+    return {1: "generic", 2: "rotated", 3: "list_major"}.get(algo) or ("list_major" if snap.dim % 16 == 0 else "rotated")
+
+
+def main_kernel_name(algo: str) -> str:
+    return {"list_major": "lm_kernel (Steps 3-4 + trace, tcgen05 int8 tiles per list)",
+            "rotated": "scan_rot_kernel (Steps 3-5)", "generic": "scan_lut (Steps 3-5)",
+            "fx16": "scan_fx_kernel (Steps 3-5)"}[algo]
+
+
+def roofline_key(name: str, fx: bool, algo: str, trace: bool) -> str:
+    return name + ("_fx16" if fx else "") + ("" if algo in ("list_major", "fx16") else "_" + algo) + \
+        ("" if trace else "_traceoff")
+
+
+def l2_label(cfg, algo: str, codes_mb: float) -> str:
+    """What the 256 MiB write between timed steps leaves for the next step to fetch from HBM."""
+    lm_mb = cfg.nlist * (-(-cfg.L // 128) * 128) * cfg.D / 1e6   # the list-major kernel's xhat
+    data_mb = lm_mb if algo == "list_major" else codes_mb
+    what = "xhat" if algo == "list_major" else "codes"
+    if data_mb > 126:
+        return f"flushed between timed steps (256 MiB write); the snapshot's {what} ({data_mb:.0f} MB) exceed L2"
+    return (f"flushed between timed steps (256 MiB write); the snapshot's {what} ({data_mb:.0f} MB) fit in L2, "
+            f"so within a step they are re-read from L2 after the first touch")
 
 
 def load_traffic(cfg_name: str):
@@ -334,7 +370,7 @@ def main():
             starts[i].record(stream)
             query(out)
             ends[i].record(stream)
-            kt.append(v3db.profile_read())                  # per-kernel CUDA-event times of this step
+            kt.append(v3db.profile_read(detail=True))       # per-kernel CUDA-event times of this step
         launches = v3db.kernel_launches() - l0
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStop()
@@ -354,16 +390,45 @@ def main():
         b_.record(stream)
     torch.cuda.synchronize()
     off_ms = pdist.max_over_ranks(float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev])), world, dev)
+    # the literal-LUT alternative (V3DB_SCAN_ROTATED: per-query Step-3 table + Step-4 lookups), same
+    # launch, timed beside the default for the record (int8 only)
+    rot = None
+    if not fx and algo_used_pre(args.algo, snap) == "list_major":
+        try:
+            ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+            v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out, algo=v3db.SCAN_ROTATED)
+            kr = []
+            for a_, b_ in ev2:
+                flush.zero_()
+                a_.record(stream)
+                v3db.query_batch(snap, q, cfg.nprobe, cfg.k, out=out, algo=v3db.SCAN_ROTATED)
+                b_.record(stream)
+                kr.append(v3db.profile_read(detail=True))
+            torch.cuda.synchronize()
+            rms = float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev2]))
+            rot = {"ms_per_step": rms, "value": cfg.Q / (rms / 1e3),
+                   "scan_kernel_ms": float(np.mean([t[2] for t in kr])), "kernel": "scan_rot_kernel"}
+        except Exception as exc:  # shapes the rotated scan does not support
+            rot = {"error": str(exc)[:160]}
     ms_per_step = tot_ms / args.steps
     qps = cfg.Q * world / (ms_per_step / 1e3)
-    coarse_ms = float(np.mean([a for a, _ in kt]))
-    scan_ms = float(np.mean([b for _, b in kt]))
+    coarse_ms = float(np.mean([t[0] for t in kt]))
+    scan_ms = float(np.mean([t[1] for t in kt]))
+    main_ms = float(np.mean([t[2] for t in kt]))      # the scan's main kernel alone
+    pro_ms = float(np.mean([t[3] for t in kt]))
+    sel_ms = float(np.mean([t[4] for t in kt]))
+    algo_used = resolved_algo(v3db, snap, args.algo, fx)
 
     lists = out["trace_lists"].cpu().numpy()
     ab = algorithmic_scan_bytes(cfg, lists, counts, trace, fx)
     hbm, peak_src = peaks()
-    achieved = ab["valid"] / (scan_ms / 1e3) / 1e9
-    traffic = load_traffic(cfg.name + ("_fx16" if fx else ""))
+    traffic = load_traffic(roofline_key(cfg.name, fx, algo_used, trace))
+    # dominant kernel: the scan's main kernel (list-major: Steps 3-4 + trace; query-major: Steps
+    # 3-5).  Its algorithmic bytes: SURVEY.md §8(d) per query (no credit for cross-query reuse),
+    # less the top-k output the list-major selection kernel writes.
+    main_bytes = ab["valid"] - (ab["topk_out"] if algo_used == "list_major" else 0)
+    achieved = main_bytes / (main_ms / 1e3) / 1e9
+    codes_mb = cfg.nlist * cfg.L * cfg.M / 1e6
 
     result = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -372,18 +437,31 @@ def main():
         "config": {"workload": cfg.name, "Q": cfg.Q, "N": cfg.N, "D": cfg.D, "nlist": cfg.nlist, "L": cfg.L,
                    "M": cfg.M, "Ks": cfg.Ks, "nprobe": cfg.nprobe, "k": cfg.k, "trace": args.trace,
                    "precision": args.precision, "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "flushed between timed steps (256 MiB write); snapshot codes exceed L2",
-                   "algo": args.algo, "snapshot_build_s": round(build_s, 3)},
+                   "l2": l2_label(cfg, algo_used, codes_mb),
+                   "algo": algo_used, "snapshot_build_s": round(build_s, 3)},
         "ms_per_step_median": float(np.median(step_ms)), "ms_per_step_best": float(np.min(step_ms)),
         "value_trace_off": cfg.Q * world / (off_ms / 1e3),
-        "scan_gbs": achieved,
+        "scan_gbs": ab["valid"] / (scan_ms / 1e3) / 1e9,
         "scan_gbs_padded": ab["padded"] / (scan_ms / 1e3) / 1e9,
-        "kernel_ms": {"coarse_steps12": coarse_ms, "scan_steps345": scan_ms},
+        "kernel_ms": {"coarse_steps12": coarse_ms, "scan_steps345": scan_ms, "scan_main_kernel": main_ms,
+                      "scan_prologue": pro_ms, "scan_select": sel_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "scan (Steps 3-5)", "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": ab["valid"]},
+                     "traffic": traffic, "kernel": main_kernel_name(algo_used), "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": main_bytes,
+                     "accounting": "SURVEY.md §8(d): per query its probed lists' valid codes, no credit for "
+                                   "cross-query reuse" + (
+                                       "; the list-major kernel reads each probed list ONCE per batch for all "
+                                       "its queries (DRAM traffic = `traffic`), so frac > 1 is that reuse, "
+                                       "see dram_roofline" if algo_used == "list_major" else "")},
         "gpu_launches": int(launches),
     }
+    if rot is not None:
+        result["rotated_lut_scan"] = rot
+    if traffic:
+        dram = traffic / (main_ms / 1e3) / 1e9
+        result["dram_roofline"] = {"bound": "hbm", "achieved": dram, "peak": hbm, "unit": "GB/s", "frac": dram / hbm,
+                                   "bytes_per_launch": traffic, "source": "ncu dram__bytes_read.sum + "
+                                   "dram__bytes_write.sum of the same kernel (profiles/ncu_traffic.json)"}
 
     # End-to-end through the C ABI with HOST buffers (H2D queries, D2H outputs inside).
     if not args.no_e2e and fx:
@@ -417,6 +495,17 @@ def main():
         d2h = sum(v.numel() * 4 for v in oh.values())
         result["e2e"] = {"value": cfg.Q * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": qh.numel(),
                          "d2h_bytes_per_step": d2h, "steps": n_e2e}
+        if trace:   # the same end-to-end call without the witness trace (top-k + probe lists only)
+            oh2 = v3db.alloc_outputs(snap, cfg.Q, cfg.nprobe, cfg.k, trace=False, device="cpu", pin=True)
+            v3db.query_batch_host(snap, qh, cfg.nprobe, cfg.k, oh2)
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                v3db.query_batch_host(snap, qh, cfg.nprobe, cfg.k, oh2)
+            e2 = pdist.max_over_ranks((time.perf_counter() - t0) / n_e2e, world, dev)
+            result["e2e_trace_off"] = {"value": cfg.Q * world / e2, "unit": "queries/s",
+                                       "h2d_bytes_per_step": qh.numel(),
+                                       "d2h_bytes_per_step": sum(v.numel() * 4 for v in oh2.values()), "steps": n_e2e}
 
     result["clocks"] = clk.summary()
 

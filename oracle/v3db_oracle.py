@@ -116,41 +116,88 @@ def assign_greedy(db: np.ndarray, mu: np.ndarray, L: int, chunk: int = 4096) -> 
     For t = 0, 1, ..., N-1 in order: rank the lists by (e_{t,i} = dist(db[t], mu_i), i)
     ascending and append t to the FIRST list in that ranking whose current count is < L.
     The first list in the (e, i) ranking that has room is exactly the lowest-index
-    minimiser of e over the lists that have room, which is what is computed below
-    (np.argmin returns the first, i.e. lowest-index, minimum).  The ranking keys of a
-    chunk of vectors do not depend on the placement, so a thread pool computes them a few
-    chunks ahead; the placement itself runs strictly in ascending t.
+    minimiser of e over the lists that have room (np.argmin returns the first minimum).
+
+    Evaluation order (the same result as the vector-by-vector loop, pinned against it in
+    tests/test_oracle_pins.py): within a chunk of vectors every vector first takes the minimiser
+    over the lists that have room at the chunk's start.  That is the sequential choice for every
+    vector up to the first one whose chosen list its predecessors in the chunk have filled (a list
+    that fills up is never the choice of a vector before that point, so removing it from the lists
+    with room changes no earlier choice).  The vectors before that point are placed at once, the
+    lists that became full are closed, the choices that pointed at them are recomputed over the
+    remaining lists, and the walk resumes at that vector.  A thread pool computes the ranking keys
+    and first choices of chunks ahead, against the lists that had room when it started: a list
+    only ever fills up, so such a choice is still the minimiser over the lists with room at
+    placement time unless it has filled meanwhile -- and those choices are recomputed.
     """
     from concurrent.futures import ThreadPoolExecutor
 
     N = db.shape[0]
     nlist = mu.shape[0]
     list_of = np.empty(N, dtype=np.int32)
-    counts = [0] * nlist
-    room = np.zeros(nlist, dtype=np.float64)          # 0 where the list has room, +inf when full
+    counts = np.zeros(nlist, dtype=np.int64)
+    closed = np.zeros(nlist, dtype=bool)               # lists that are full
 
-    def rank(lo):
-        e = _rank_keys(db[lo:min(N, lo + chunk)], mu)  # [chunk, nlist] e_{t,i} - ||x_t||^2
-        return e, np.argmin(e, axis=1).tolist()        # nearest list, lowest index on ties
+    def rank(lo, closed_then):
+        e = _rank_keys(db[lo:min(N, lo + chunk)], mu)    # [chunk, nlist] e_{t,i} - ||x_t||^2
+        e += np.where(closed_then, np.inf, 0).astype(e.dtype)   # only lists with room (as of closed_then)
+        return e, np.argmin(e, axis=1)                 # nearest list with room, lowest index on ties
 
     starts = list(range(0, N, chunk))
-    with ThreadPoolExecutor(max_workers=3) as ex:
-        futs = [ex.submit(rank, lo) for lo in starts[:3]]
+    ahead = max(2, min(16, (os.cpu_count() or 4)))
+    with ThreadPoolExecutor(max_workers=ahead) as ex:
+        futs = [ex.submit(rank, lo, closed.copy()) for lo in starts[:ahead]]
         for c, lo in enumerate(starts):
-            e, first = futs[c].result()
+            e, choice = futs[c].result()
             futs[c] = None
-            if c + 3 < len(starts):
-                futs.append(ex.submit(rank, starts[c + 3]))
-            for r in range(len(first)):
-                i = first[r]
-                if counts[i] >= L:                       # overflow: next-nearest list with room
-                    i = int(np.argmin(e[r] + room))
-                    assert counts[i] < L, "N > nlist * L (infeasible)"
-                list_of[lo + r] = i
-                counts[i] += 1
-                if counts[i] == L:
-                    room[i] = np.inf
+            room = np.where(closed, np.inf, 0).astype(e.dtype)
+            n = e.shape[0]
+            redo = np.flatnonzero(closed[choice])       # choices that filled since the worker started
+            if len(redo):
+                choice[redo] = np.argmin(e[redo] + room, axis=1)
+            pos = 0
+            while pos < n:
+                ch = choice[pos:]
+                # ordinal of each vector among the vectors of ch that chose the same list
+                order = np.argsort(ch, kind="stable")
+                srt = ch[order]
+                first = np.r_[0, np.flatnonzero(srt[1:] != srt[:-1]) + 1]
+                run = np.diff(np.r_[first, len(srt)])
+                ordinal = np.empty(len(ch), dtype=np.int64)
+                ordinal[order] = np.arange(len(srt)) - np.repeat(first, run)
+                over = counts[ch] + ordinal >= L            # its list is full when its turn comes
+                b = int(np.argmax(over)) if over.any() else len(ch)
+                list_of[lo + pos:lo + pos + b] = ch[:b]
+                counts += np.bincount(ch[:b], minlength=nlist)
+                pos += b
+                if pos == n:
+                    break
+                closed |= counts >= L                       # close the lists that filled up
+                room[closed] = np.inf
+                redo = np.flatnonzero(closed[choice[pos:]]) + pos
+                choice[redo] = np.argmin(e[redo] + room, axis=1)
+                assert not closed[choice[pos]], "N > nlist * L (infeasible)"
+            closed |= counts >= L
+            if c + ahead < len(starts):
+                futs.append(ex.submit(rank, starts[c + ahead], closed.copy()))
     return list_of
+
+
+def _assign_greedy_rowwise(db: np.ndarray, mu: np.ndarray, L: int) -> np.ndarray:
+    """B2 vector by vector (the definition's loop), for the pins of assign_greedy."""
+    N, nlist = db.shape[0], mu.shape[0]
+    e = _rank_keys(db, mu)
+    counts = np.zeros(nlist, dtype=np.int64)
+    room = np.zeros(nlist, dtype=e.dtype)
+    out = np.empty(N, dtype=np.int32)
+    for t in range(N):
+        i = int(np.argmin(e[t] + room))
+        assert counts[i] < L, "N > nlist * L (infeasible)"
+        out[t] = i
+        counts[i] += 1
+        if counts[i] == L:
+            room[i] = np.inf
+    return out
 
 
 def nearest_lists(db: np.ndarray, mu: np.ndarray, chunk: int = 4096) -> np.ndarray:

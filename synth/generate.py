@@ -87,13 +87,28 @@ def _rows(mix: Mixture, rng: np.random.Generator, n: int) -> np.ndarray:
     return np.clip(np.rint(127.0 * x), -127, 127).astype(np.int8)
 
 
+def _chunked(fill, n: int) -> None:
+    """fill(c, lo, hi) for every chunk [lo, hi) of CHUNK rows; chunks are independently seeded, so
+    a thread pool (numpy's generators and arithmetic release the GIL) gives the same bytes."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    spans = [(c, lo, min(n, lo + CHUNK)) for c, lo in enumerate(range(0, n, CHUNK))]
+    if len(spans) <= 1:
+        for sp in spans:
+            fill(*sp)
+        return
+    with ThreadPoolExecutor(max_workers=min(len(spans), os.cpu_count() or 4)) as ex:
+        list(ex.map(lambda sp: fill(*sp), spans))
+
+
 def gen_vectors(cfg: Config, stream: int, n: int) -> np.ndarray:
     """n int8 rows of dimension cfg.D from the config's mixture, chunk-seeded."""
     mix = mixture(cfg.gen, cfg.D, cfg.cfg_id)
     out = np.empty((n, cfg.D), dtype=np.int8)
-    for c, lo in enumerate(range(0, n, CHUNK)):
-        hi = min(n, lo + CHUNK)
+
+    def fill(c, lo, hi):
         out[lo:hi] = _rows(mix, _rng(cfg.cfg_id, stream, c), hi - lo)
+    _chunked(fill, n)
     return out
 
 
@@ -134,9 +149,10 @@ def gen_float_vectors(cfg: Config, stream: int, n: int) -> np.ndarray:
     """n float32 rows of the config's mixture (the same draws as gen_vectors, before int8)."""
     mix = mixture(cfg.gen, cfg.D, cfg.cfg_id)
     out = np.empty((n, cfg.D), dtype=np.float32)
-    for c, lo in enumerate(range(0, n, CHUNK)):
-        hi = min(n, lo + CHUNK)
+
+    def fill(c, lo, hi):
         out[lo:hi] = _float_rows(mix, _rng(cfg.cfg_id, stream, c), hi - lo)
+    _chunked(fill, n)
     return out
 
 

@@ -40,6 +40,40 @@ def oracle_queries(s, queries, nprobe, k, rows=None, workers=None):
     return {key: np.concatenate([p[key] for p in parts]) for key in parts[0]}
 
 
+_G = None
+
+
+def _init_check(s, q, got):
+    global _S, _Q, _G
+    _S, _Q, _G = s, q, got
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+
+def _check(args):
+    pos, rows, nprobe, k = args   # pos: positions of `rows` inside the GPU arrays
+    out = oracle.query_batch(_S, _Q, nprobe, k, rows=rows)
+    bad = []
+    for key, exp in out.items():
+        got = _G[key][pos]
+        if not np.array_equal(got, exp):
+            bad.append(f"{key} rows {int(rows[0])}..{int(rows[-1])}: {first_mismatch(got, exp)}")
+    return bad
+
+
+def oracle_check(s, queries, nprobe, k, got: dict, rows=None, workers=None) -> list:
+    """Compare GPU outputs `got` (host arrays whose first axis is `rows`, default every query) with
+    oracle.query_batch on s, row by row, in a process pool whose workers compare in place (fork:
+    the GPU arrays are shared, nothing large is pickled).  Returns the mismatch descriptions."""
+    import multiprocessing as mp
+    rows = np.arange(queries.shape[0]) if rows is None else np.asarray(rows)
+    workers = workers or min(32, len(os.sched_getaffinity(0)))
+    pos = np.arange(len(rows))
+    jobs = [(p, rows[p], nprobe, k) for p in np.array_split(pos, max(1, workers * 4)) if len(p)]
+    with ProcessPoolExecutor(workers, mp_context=mp.get_context("fork"), initializer=_init_check,
+                             initargs=(s, queries, got)) as ex:
+        return [b for part in ex.map(_check, jobs) for b in part]
+
+
 def oracle_queries_all(s, queries, nprobe, k, trace_rows, workers=None):
     """oracle.query_batch over EVERY row of `queries` (process pool); trace_cand_dist is kept only
     for the rows in `trace_rows` (sorted), to bound the host memory and the pickling at C4 sizes.

@@ -215,6 +215,34 @@ def test_greedy_matches_bruteforce_tiny(seed):
     assert vo.assign_greedy(db, mu, L, chunk=7).tolist() == _greedy_bruteforce(db, mu, L)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_greedy_rowwise_matches_bruteforce_tiny(seed):
+    """The vector-by-vector reference loop itself against the literal (e, i) ranking."""
+    rng = np.random.default_rng(200 + seed)
+    N, D, nlist = 70, 2, 6
+    L = int(np.ceil(N / nlist)) + seed % 2
+    db = rng.integers(-2, 3, size=(N, D)).astype(np.int8)
+    mu = db[rng.choice(N, nlist, replace=False)]
+    assert vo._assign_greedy_rowwise(db, mu, L).tolist() == _greedy_bruteforce(db, mu, L)
+
+
+@pytest.mark.parametrize("chunk", [1, 64, 777, 4096])
+@pytest.mark.parametrize("slack", [0, 3, 50])
+def test_greedy_blocked_matches_rowwise(chunk, slack):
+    """The chunked evaluation of B2 (lists closing mid-chunk, stale choices of the look-ahead
+    workers) equals the vector-by-vector loop, with heavy overflow (slack 0: every list fills),
+    many ties (a 5-value alphabet) and chunk boundaries everywhere."""
+    rng = np.random.default_rng(chunk + 7 * slack)
+    N, D, nlist = 6000, 3, 37
+    L = int(np.ceil(N / nlist)) + slack
+    db = rng.integers(-2, 3, size=(N, D)).astype(np.int8)
+    db[: N // 3] = rng.integers(-60, 60, size=(N // 3, D))
+    mu = db[rng.choice(N, nlist, replace=False)]
+    got = vo.assign_greedy(db, mu, L, chunk=chunk)
+    assert np.array_equal(got, vo._assign_greedy_rowwise(db, mu, L))
+    assert np.bincount(got, minlength=nlist).max() <= L
+
+
 def greedy_replay_violations(db, s, sample=None):
     """P7 replay check that does not re-run the algorithm: for vector t in list i, every
     list ranked before i by (e, i) already held L members with id < t, and list i held
