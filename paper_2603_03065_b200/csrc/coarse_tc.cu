@@ -358,7 +358,8 @@ __global__ void __launch_bounds__(256) tau_kernel(int64_t n, int ngroups, int R,
 template <int KR>
 __global__ void __launch_bounds__(256) select_kernel(int64_t n, int R, int capc, const uint64_t* __restrict__ cand,
                                                     const int* __restrict__ ccnt, int32_t* __restrict__ out_idx,
-                                                    int32_t* __restrict__ out_dist, int* __restrict__ flags) {
+                                                    int32_t* __restrict__ out_dist, int* __restrict__ flags,
+                                                    int* __restrict__ hist) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
   if (row >= n) return;
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(256) select_kernel(int64_t n, int R, int capc,
   top.store([&](int j, uint64_t key) {
     out_idx[row * R + j] = static_cast<int32_t>(key & 0xffffffffu);
     out_dist[row * R + j] = static_cast<int32_t>(key >> 32);
+    if (hist) atomicAdd(hist + static_cast<uint32_t>(key), 1);
   });
 }
 
@@ -383,7 +385,7 @@ template <int KR>
 __global__ void __launch_bounds__(256) fallback_kernel(const int8_t* __restrict__ X, int64_t n, int dim,
                                                       const int8_t* __restrict__ mu, int nlist, int R,
                                                       const int* __restrict__ flags, int32_t* __restrict__ out_idx,
-                                                      int32_t* __restrict__ out_dist) {
+                                                      int32_t* __restrict__ out_dist, int* __restrict__ hist) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
   if (row >= n || flags[row] == 0) return;
@@ -407,7 +409,14 @@ __global__ void __launch_bounds__(256) fallback_kernel(const int8_t* __restrict_
   top.store([&](int j, uint64_t key) {
     out_idx[row * R + j] = static_cast<int32_t>(key & 0xffffffffu);
     out_dist[row * R + j] = static_cast<int32_t>(key >> 32);
+    if (hist) atomicAdd(hist + static_cast<uint32_t>(key), 1);
   });
+}
+
+__global__ void list_hist_kernel(const int32_t* __restrict__ idx, int64_t n, int* __restrict__ hist) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(hist + __ldg(idx + p), 1);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -446,7 +455,7 @@ bool make_tmap_i8(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 }
 
 cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, const int32_t* cnorm, int nlist,
-                        int R, int32_t* out_idx, int32_t* out_dist, cudaStream_t st) {
+                        int R, int32_t* out_idx, int32_t* out_dist, cudaStream_t st, int* list_hist) {
   if (n <= 0) return cudaSuccess;
   const int kp = (dim + kPanel - 1) / kPanel;
   const size_t fixed = 1024 + static_cast<size_t>(kp) * kAPanelBytes + kEpiWarps * 64 * 4 + 64 * 8;
@@ -457,8 +466,16 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   const bool tc_ok = dim % 16 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(mu) % 16 == 0 && stages >= 2 && !opt(V3DB_OPT_COARSE_SIMT);
   CUtensorMap tmX, tmMu;
-  if (!tc_ok || !make_tmap_i8(&tmX, X, n, dim, kRows, kPanel) || !make_tmap_i8(&tmMu, mu, nlist, dim, kChunk, kPanel))
-    return coarse_topk_mma(X, n, dim, mu, cnorm, nlist, R, out_idx, out_dist, st);
+  if (!tc_ok || !make_tmap_i8(&tmX, X, n, dim, kRows, kPanel) || !make_tmap_i8(&tmMu, mu, nlist, dim, kChunk, kPanel)) {
+    cudaError_t em = coarse_topk_mma(X, n, dim, mu, cnorm, nlist, R, out_idx, out_dist, st);
+    if (em == cudaSuccess && list_hist) {
+      list_hist_kernel<<<static_cast<unsigned>(std::min<int64_t>((n * R + 255) / 256, 1184)), 256, 0, st>>>(out_idx, n * R,
+                                                                                                       list_hist);
+      note_launch();
+      em = cudaGetLastError();
+    }
+    return em;
+  }
 
   // group size G: a power of two <= 32 with >= 2R groups when nlist allows
   int G = 1;
@@ -524,8 +541,8 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
     tau_kernel<<<rb, 256, 0, st>>>(n, ngroups, R, a.gmin, const_cast<int32_t*>(a.tau), a.ccnt);
     coarse_tc_kernel<2, 0><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
     dispatch_kr(R, [&]<int KR>() {
-      select_kernel<KR><<<rb, 256, 0, st>>>(n, R, capc, a.cand, a.ccnt, out_idx, out_dist, flags);
-      fallback_kernel<KR><<<rb, 256, 0, st>>>(X, n, dim, mu, nlist, R, flags, out_idx, out_dist);
+      select_kernel<KR><<<rb, 256, 0, st>>>(n, R, capc, a.cand, a.ccnt, out_idx, out_dist, flags, list_hist);
+      fallback_kernel<KR><<<rb, 256, 0, st>>>(X, n, dim, mu, nlist, R, flags, out_idx, out_dist, list_hist);
     });
     note_launch(5);
     e = cudaGetLastError();

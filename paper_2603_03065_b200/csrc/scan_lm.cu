@@ -300,17 +300,27 @@ __global__ void pair_hist_kernel(const int32_t* __restrict__ lists, int64_t npai
     atomicAdd(hist + __ldg(lists + p), 1);
 }
 
-// One CTA of 1024 threads: off[i] = exclusive prefix of hist (pairs per list), iof[i] = exclusive
-// prefix of ceil(hist[i] / NT) (items per list); *n_items = the total.
-__global__ void __launch_bounds__(1024) lm_scan_kernel(const int* __restrict__ hist, int nlist, int NT,
-                                                       int* __restrict__ off, int* __restrict__ iof,
-                                                       int* __restrict__ n_items) {
+// One CTA of 1024 threads: cur[i] = exclusive prefix of hist (the list's first pair in list order,
+// advanced by pair_scatter_kernel), the work items (list, first pair, pairs <= NT) of every list in
+// list order, and *n_items.  Each thread owns a contiguous run of lists, read with 16-byte loads.
+__global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restrict__ hist, int nlist, int NT,
+                                                             int* __restrict__ cur, int4* __restrict__ items,
+                                                             int* __restrict__ n_items) {
   __shared__ int part[1024], ipart[1024];
-  const int per = (nlist + 1023) / 1024, b = threadIdx.x * per, e = min(nlist, b + per);
+  const int per = (((nlist + 1023) / 1024) + 3) & ~3, b = threadIdx.x * per, e = min(nlist, b + per);
   int sum = 0, isum = 0;
-  for (int i = b; i < e; ++i) {
-    sum += hist[i];
-    isum += (hist[i] + NT - 1) / NT;
+  for (int x = b; x < e; x += 4) {  // 16-byte loads (b is a multiple of 4; hist is 256-byte aligned)
+    int4 v;
+    if (x + 3 < e) {
+      v = *reinterpret_cast<const int4*>(hist + x);
+    } else {
+      v.x = hist[x];
+      v.y = x + 1 < e ? hist[x + 1] : 0;
+      v.z = x + 2 < e ? hist[x + 2] : 0;
+      v.w = x + 3 < e ? hist[x + 3] : 0;
+    }
+    sum += v.x + v.y + v.z + v.w;
+    isum += (v.x + NT - 1) / NT + (v.y + NT - 1) / NT + (v.z + NT - 1) / NT + (v.w + NT - 1) / NT;
   }
   part[threadIdx.x] = sum;
   ipart[threadIdx.x] = isum;
@@ -325,10 +335,10 @@ __global__ void __launch_bounds__(1024) lm_scan_kernel(const int* __restrict__ h
   }
   int run = part[threadIdx.x] - sum, irun = ipart[threadIdx.x] - isum;
   for (int i = b; i < e; ++i) {
-    off[i] = run;
-    iof[i] = irun;
-    run += hist[i];
-    irun += (hist[i] + NT - 1) / NT;
+    const int hi = hist[i];
+    cur[i] = run;
+    for (int r = 0; r * NT < hi; ++r) items[irun++] = make_int4(i, run + r * NT, min(NT, hi - r * NT), 0);
+    run += hi;
   }
   if (threadIdx.x == 1023) *n_items = ipart[1023];
 }
@@ -338,17 +348,6 @@ __global__ void pair_scatter_kernel(const int32_t* __restrict__ lists, int64_t n
   for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npairs;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x)
     pairs[atomicAdd(cur + __ldg(lists + p), 1)] = static_cast<int32_t>(p);
-}
-
-// items of list i: (i, off[i] + r * NT, min(NT, hist[i] - r * NT)); off[] here is the list's first
-// pair (the scatter advanced its copy `cur`, so the start is recomputed as cur - hist).
-__global__ void items_kernel(const int* __restrict__ hist, const int* __restrict__ cur, const int* __restrict__ iof,
-                             int nlist, int NT, int4* __restrict__ items) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nlist; i += gridDim.x * blockDim.x) {
-    const int h = hist[i];
-    const int p0 = cur[i] - h;
-    for (int r = 0; r * NT < h; ++r) items[iof[i] + r] = make_int4(i, p0 + r * NT, min(NT, h - r * NT), 0);
-  }
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -718,7 +717,7 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
       w0 += static_cast<uint32_t>(b) << sh;
       span = 1u << sh;
       need -= before;
-      if (sh == 0 || inbin <= 64) break;  // a bin of <= 64 group minima: tight enough
+      if (sh == 0 || inbin <= 8) break;  // a bin of <= 8 group minima: tight enough
     }
     tau = w0 + span - 1u;
     if (dmin + tau > 0x7ffffffeu) tau = 0x7ffffffeu - dmin;
@@ -852,7 +851,8 @@ size_t al(size_t x, size_t b) { return (x + b - 1) / b * b; }
 
 cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
                             const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
-                            int32_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t)) {
+                            int32_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t),
+                            const int* list_hist) {
   if (nq <= 0) return cudaSuccess;
   if (!s->xhat || s->dim % 16 != 0) return cudaErrorInvalidValue;
   const int64_t npairs = nq * nprobe;
@@ -880,7 +880,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   if (!make_tmap_i8(&tmX, s->xhat, static_cast<uint64_t>(s->nlist) * s->lm_Lp, s->dim, kTile, kPanel))
     return cudaErrorInvalidValue;
 
-  // scratch: hist, off/cur, iof, n_items, pairs, items, gmin (+ trace when the caller passes none)
+  // scratch: hist, cur, (unused), n_items, pairs, items, gmin + flags (+ trace when the caller passes none)
   const int nlist = s->nlist;
   const int64_t max_items = nlist + npairs / NT + 1;
   const size_t b_hist = al(sizeof(int) * nlist, 256), b_pairs = al(sizeof(int32_t) * npairs, 256),
@@ -892,7 +892,6 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   if (e != cudaSuccess) return e;
   int* hist = reinterpret_cast<int*>(base);
   int* cur = reinterpret_cast<int*>(base + b_hist);
-  int* iof = reinterpret_cast<int*>(base + 2 * b_hist);
   int* n_items = reinterpret_cast<int*>(base + 3 * b_hist);
   int32_t* pairs = reinterpret_cast<int32_t*>(base + 3 * b_hist + 256);
   int4* items = reinterpret_cast<int4*>(base + 3 * b_hist + 256 + b_pairs);
@@ -902,17 +901,20 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   int dev = 0, sms = 148;
   e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, sizeof(int) * nlist, st);
+  if (e == cudaSuccess && !list_hist) e = cudaMemsetAsync(hist, 0, sizeof(int) * nlist, st);
   if (e != cudaSuccess) {
     cudaFreeAsync(base, st);
     return e;
   }
   const unsigned pg = static_cast<unsigned>(std::min<int64_t>((npairs + 255) / 256, 4 * sms));
-  pair_hist_kernel<<<pg, 256, 0, st>>>(lists, npairs, hist);
-  lm_scan_kernel<<<1, 1024, 0, st>>>(hist, nlist, NT, cur, iof, n_items);
+  if (!list_hist) {
+    pair_hist_kernel<<<pg, 256, 0, st>>>(lists, npairs, hist);
+    note_launch();
+  }
+  const int* hsrc = list_hist ? list_hist : hist;
+  lm_scan_items_kernel<<<1, 1024, 0, st>>>(hsrc, nlist, NT, cur, items, n_items);
   pair_scatter_kernel<<<pg, 256, 0, st>>>(lists, npairs, cur, pairs);
-  items_kernel<<<(nlist + 255) / 256, 256, 0, st>>>(hist, cur, iof, nlist, NT, items);
-  note_launch(4);
+  note_launch(2);
   if (prof) prof(2, st);
 
   LmArgs a;

@@ -571,13 +571,24 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
     if (!lists) lists = static_cast<int32_t*>(scratch);
     if (!ldist) ldist = static_cast<int32_t*>(scratch) + nq * nprobe;
   }
+  // list-major scan: Steps 1-2 also count the (query, rank) pairs per list for its grouping
+  int* list_hist = nullptr;
+  if (algo == V3DB_SCAN_LIST_MAJOR) {
+    cudaError_t eh = v3db::scratch_alloc(reinterpret_cast<void**>(&list_hist), sizeof(int) * s->nlist, st);
+    if (eh == cudaSuccess) eh = cudaMemsetAsync(list_hist, 0, sizeof(int) * s->nlist, st);
+    if (eh != cudaSuccess) {
+      if (scratch) cudaFreeAsync(scratch, st);
+      return cuda_fail(eh, "list-major scratch");
+    }
+  }
   prof_record(0, st);
-  cudaError_t e = v3db::coarse_topk(queries, nq, s->dim, s->centroids, s->cnorm, s->nlist, nprobe, lists, ldist, st);
+  cudaError_t e = v3db::coarse_topk(queries, nq, s->dim, s->centroids, s->cnorm, s->nlist, nprobe, lists, ldist, st,
+                                    list_hist);
   prof_scan_begin(st);
   if (e == cudaSuccess) {
     if (algo == V3DB_SCAN_LIST_MAJOR)
       e = v3db::scan_list_major(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st,
-                                g_prof.on ? prof_record : nullptr);
+                                g_prof.on ? prof_record : nullptr, list_hist);
     else if (algo == V3DB_SCAN_ROTATED)
       e = v3db::scan_rotated(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
     else
@@ -585,6 +596,7 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   }
   prof_scan_end(st);
   if (scratch) cudaFreeAsync(scratch, st);
+  if (list_hist) cudaFreeAsync(list_hist, st);
   if (e != cudaSuccess) {
     if (g_err.empty()) return cuda_fail(e, "query kernels");
     return V3DB_ECUDA;

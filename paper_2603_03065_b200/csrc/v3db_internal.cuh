@@ -86,8 +86,11 @@ constexpr int32_t kDMax = 0x7fffffff;  // d_max = 2^31 - 1 (reading R8, PAPER.md
 
 // Step 1 + Step 2 (and build ranking B2): for each row x of X [n][dim], the R smallest
 // composite keys (dist(x, mu_i), i), ascending -> out_idx/out_dist [n][R].
+// list_hist (optional, pre-zeroed [nlist]): += 1 for every output list (the list-major scan's
+// grouping histogram).
 cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, const int32_t* cnorm,
-                        int nlist, int R, int32_t* out_idx, int32_t* out_dist, cudaStream_t st);
+                        int nlist, int R, int32_t* out_idx, int32_t* out_dist, cudaStream_t st,
+                        int* list_hist = nullptr);
 
 // Build kernels (build_kernels.cu).
 cudaError_t gather_rows(const int8_t* db, int dim, const int32_t* rows, int nrows, int8_t* out,
@@ -166,9 +169,12 @@ cudaError_t scan_rotated(const v3db_snapshot* s, const int8_t* queries, int64_t 
 // library scratch trace when the caller passes none), 32-slot group minima, then an exact per-query
 // selection.  Requires s->xhat.  prof(i) records profiling marks 2 (after grouping) and 3 (after
 // the contraction kernel).
+// list_hist: the per-list count of (query, rank) pairs that coarse_topk accumulated (or null:
+// computed here).
 cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
                             const int32_t* lists, const int32_t* ldist, int32_t* out_ids, int32_t* out_dist,
-                            int32_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t));
+                            int32_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t),
+                            const int* list_hist = nullptr);
 
 // Ascending sort of nseg segments of P (a power of two) 64-bit keys (witness.cu).
 cudaError_t segmented_sort(uint64_t* keys, int64_t nseg, int P, cudaStream_t st);
