@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
   uint8_t* sA = smem;                                         // [S][128 x 128 B]
   uint8_t* sB = smem + a.off_b;                               // [nb][kp][NT x 128 B]
   PairMeta* meta = reinterpret_cast<PairMeta*>(smem + a.off_meta);  // [nb][NT]
-  int* wmin = reinterpret_cast<int*>(smem + a.off_wmin);     // [kEpiWarps][kChunk] column minima
+  int* wmin = reinterpret_cast<int*>(smem + a.off_wmin);     // [kEpiWarps][2 kChunk] column minima
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* afull = bars;                  // [S]
   uint64_t* aempty = afull + a.S;          // [S]
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     // 128 consecutive bytes) and the group minimum over the 32 lanes (REDUX).
     const int e = warp - kWarpEpi, qd = warp & 3, grp = e >> 3, cg = (e >> 2) & 1;
     constexpr int NCG = 2;
-    int* wm = wmin + e * kChunk;
+    int* wm = wmin + e * 2 * kChunk;
     int b = 0, bph = 0, tcount = 0, tall = 0;
     for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
       const int4 it = a.items[j];
@@ -239,10 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
           const bool full = sbase + 32 <= cnt;                // warp-uniform: every slot valid (< L)
           tc::mbar_wait_sleep(accf + acc, ua & 1);
           tc::fence_after_sync();
-          for (int jc = cg; jc * kChunk < np; jc += NCG) {
-            uint32_t v[kChunk];
-            tc::tmem_ld16(tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT + jc * kChunk, v);
-            tc::tmem_ld_wait();
+          // one chunk of 16 columns: D to the trace, the 32-slot group minimum of every column
+          auto chunk = [&](const uint32_t(&v)[kChunk], int jc, int* wmc) {
             const PairMeta* mc = mt + jc * kChunk;
             const int ncol = min(kChunk, np - jc * kChunk);
             if (full && ncol == kChunk) {
@@ -252,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
                 const int32_t D = m.d + P - 2 * static_cast<int32_t>(v[c]);
                 __stcs(reinterpret_cast<int32_t*>(m.row + toff), D);
                 const int mn = __reduce_min_sync(kFull, D);
-                if (lane == 0) wm[c] = mn;
+                if (lane == 0) wmc[c] = mn;
               }
             } else {
 #pragma unroll
@@ -262,12 +260,28 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
                   const int32_t D = valid ? m.d + P - 2 * static_cast<int32_t>(v[c]) : kDMax;
                   if (slot < L) __stcs(reinterpret_cast<int32_t*>(m.row + toff), D);
                   const int mn = __reduce_min_sync(kFull, D);
-                  if (lane == 0) wm[c] = mn;
+                  if (lane == 0) wmc[c] = mn;
                 }
               }
             }
+          };
+          // two chunks per round: both TMEM loads in flight before the first is used
+          const uint32_t tbase = tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT;
+          for (int jc = cg; jc * kChunk < np; jc += 2 * NCG) {
+            const int jd = jc + NCG;
+            const bool two = jd * kChunk < np;  // warp-uniform
+            uint32_t v0[kChunk], v1[kChunk];
+            tc::tmem_ld16(tbase + jc * kChunk, v0);
+            if (two) tc::tmem_ld16(tbase + jd * kChunk, v1);
+            tc::tmem_ld_wait();
+            chunk(v0, jc, wm);
+            if (two) chunk(v1, jd, wm + kChunk);
             __syncwarp();
-            if (sbase < cnt && lane < ncol) a.gmin[mc[lane].goff + t * 4 + qd] = wm[lane];
+            if (sbase < cnt) {
+              if (lane < min(kChunk, np - jc * kChunk)) a.gmin[mt[jc * kChunk + lane].goff + t * 4 + qd] = wm[lane];
+              if (two && lane < min(kChunk, np - jd * kChunk))
+                a.gmin[mt[jd * kChunk + lane].goff + t * 4 + qd] = wm[kChunk + lane];
+            }
             __syncwarp();
           }
           tc::fence_before_sync();
@@ -871,7 +885,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   int S = 6;
   auto smem_of = [&](int stages) {
     return 1024 + static_cast<size_t>(stages) * kAStageBytes + nb * b_bytes + nb * sizeof(PairMeta) * NT +
-           4 * kEpiWarps * kChunk + 8 * (2 * stages + 2 * kNB + 2 * nacc) + 16;
+           8 * kEpiWarps * kChunk + 8 * (2 * stages + 2 * kNB + 2 * nacc) + 16;
   };
   while (S > 2 && smem_of(S) > 227 * 1024) --S;
   if (smem_of(S) > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -941,7 +955,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   a.nb = nb;
   a.off_meta = a.off_b + nb * b_bytes;  // PairMeta is 16 B: 16-byte aligned (b_bytes is a multiple of 128)
   a.off_wmin = a.off_meta + nb * sizeof(PairMeta) * NT;
-  a.off_bar = static_cast<uint32_t>(al(a.off_wmin + 4 * kEpiWarps * kChunk, 8));
+  a.off_bar = static_cast<uint32_t>(al(a.off_wmin + 8 * kEpiWarps * kChunk, 8));
   a.b_bytes = b_bytes;
   const size_t smem = smem_of(S);
   e = cudaFuncSetAttribute(lm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
