@@ -186,10 +186,12 @@ int v3db_witness_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int
                        int32_t* cand_dist, void* stream);
 
 /* ---- NEXT-1: the paper's 16-bit fixed-point representation ----
- * "We encode embeddings using 16-bit fixed-point representation ... rounding
- * round((2^16 - 1) * v / v_max)".  Readings (R18, R19): coordinates become int32 values
- * in [-65535, 65535] (the sign kept, rounding half away from zero, computed in IEEE double as
- * (v * 65535) / v_max); every distance is the exact squared L2 in int64 and d_max = 2^63 - 1;
+ * PAPER.md:781-782 (§5 setup): v_max, the maximum absolute coordinate over all involved vectors,
+ * is rescaled to 2^16 - 1 and each coordinate v is encoded as the nearest integer to
+ * (2^16 - 1) v / v_max (the paper's round-to-nearest bracket).  Readings (R18, R19):
+ * coordinates become int32 values in [-65535, 65535] (the sign kept, exact ties rounded away from
+ * zero, computed in IEEE double as (v * 65535) / v_max, the fraction compared exactly with 1/2);
+ * every distance is the exact squared L2 in int64 and d_max = 2^63 - 1;
  * codewords are the residual sub-vectors themselves (int32, no saturation).  The five steps and
  * the build rules are those of the int8 path with this arithmetic; shaping is the greedy rule. */
 

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
           if (PASS == 2) tau_d = a.tau[row];
         }
       }
-      tc::mbar_wait(accf + acc, use & 1);
+      tc::mbar_wait_sleep(accf + acc, use & 1);
       tc::fence_after_sync();
       uint32_t v[32];
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kChunk + h * 64;

@@ -68,6 +68,27 @@ struct PairMeta {     // 16 B, read by the epilogue as one broadcast LDS.128
   int goff;           // pair * ngroups
 };
 
+// Minimum over the 32 lanes of each of 16 columns x[0..15] (x is consumed): a butterfly in which
+// each exchange halves the columns a lane keeps; lane l returns the minimum of column colmin_col(l)
+// (lanes l and l ^ 1 hold the same column).
+__device__ __forceinline__ int colmin16(int (&x)[16], int lane) {
+#pragma unroll
+  for (int st = 0; st < 4; ++st) {
+    const int half = 8 >> st, bit = 16 >> st;
+    const bool up = lane & bit;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const int snd = up ? x[i] : x[i + half];
+      const int kp = up ? x[i + half] : x[i];
+      x[i] = min(kp, __shfl_xor_sync(0xffffffffu, snd, bit));
+    }
+  }
+  return min(x[0], __shfl_xor_sync(0xffffffffu, x[0], 1));
+}
+__device__ __forceinline__ int colmin_col(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
 // ----------------------------------------------------------------------------------------------
 // The contraction + epilogue kernel.
 // ----------------------------------------------------------------------------------------------
@@ -216,7 +237,6 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     // 128 consecutive bytes) and the group minimum over the 32 lanes (REDUX).
     const int e = warp - kWarpEpi, qd = warp & 3, grp = e >> 3, cg = (e >> 2) & 1;
     constexpr int NCG = 2;
-    int* wm = wmin + e * 2 * kChunk;
     int b = 0, bph = 0, tcount = 0, tall = 0;
     for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
       const int4 it = a.items[j];
@@ -240,30 +260,33 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
           tc::mbar_wait_sleep(accf + acc, ua & 1);
           tc::fence_after_sync();
           // one chunk of 16 columns: D to the trace, the 32-slot group minimum of every column
-          auto chunk = [&](const uint32_t(&v)[kChunk], int jc, int* wmc) {
+          // one chunk of 16 columns: D to the trace, then the 32-slot group minimum of every column
+          // by a butterfly over the lanes (lane l ends with column colmin_col(l)); stored by the
+          // even lanes
+          auto chunk = [&](const uint32_t(&v)[kChunk], int jc) {
             const PairMeta* mc = mt + jc * kChunk;
             const int ncol = min(kChunk, np - jc * kChunk);
+            int x[kChunk];
             if (full && ncol == kChunk) {
 #pragma unroll
               for (int c = 0; c < kChunk; ++c) {
                 const PairMeta m = mc[c];
-                const int32_t D = m.d + P - 2 * static_cast<int32_t>(v[c]);
-                __stcs(reinterpret_cast<int32_t*>(m.row + toff), D);
-                const int mn = __reduce_min_sync(kFull, D);
-                if (lane == 0) wmc[c] = mn;
+                x[c] = m.d + P - 2 * static_cast<int32_t>(v[c]);
+                __stcs(reinterpret_cast<int32_t*>(m.row + toff), x[c]);
               }
             } else {
 #pragma unroll
               for (int c = 0; c < kChunk; ++c) {
+                x[c] = kDMax;
                 if (c < ncol) {  // warp-uniform
                   const PairMeta m = mc[c];
-                  const int32_t D = valid ? m.d + P - 2 * static_cast<int32_t>(v[c]) : kDMax;
-                  if (slot < L) __stcs(reinterpret_cast<int32_t*>(m.row + toff), D);
-                  const int mn = __reduce_min_sync(kFull, D);
-                  if (lane == 0) wmc[c] = mn;
+                  if (valid) x[c] = m.d + P - 2 * static_cast<int32_t>(v[c]);
+                  if (slot < L) __stcs(reinterpret_cast<int32_t*>(m.row + toff), x[c]);
                 }
               }
             }
+            const int gm = colmin16(x, lane), col = colmin_col(lane);
+            if (sbase < cnt && !(lane & 1) && col < ncol) a.gmin[mc[col].goff + t * 4 + qd] = gm;
           };
           // two chunks per round: both TMEM loads in flight before the first is used
           const uint32_t tbase = tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT;
@@ -274,15 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
             tc::tmem_ld16(tbase + jc * kChunk, v0);
             if (two) tc::tmem_ld16(tbase + jd * kChunk, v1);
             tc::tmem_ld_wait();
-            chunk(v0, jc, wm);
-            if (two) chunk(v1, jd, wm + kChunk);
-            __syncwarp();
-            if (sbase < cnt) {
-              if (lane < min(kChunk, np - jc * kChunk)) a.gmin[mt[jc * kChunk + lane].goff + t * 4 + qd] = wm[lane];
-              if (two && lane < min(kChunk, np - jd * kChunk))
-                a.gmin[mt[jd * kChunk + lane].goff + t * 4 + qd] = wm[kChunk + lane];
-            }
-            __syncwarp();
+            chunk(v0, jc);
+            if (two) chunk(v1, jd);
           }
           tc::fence_before_sync();
           __syncwarp();

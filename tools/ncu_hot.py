@@ -2,7 +2,7 @@
 """Hot SASS instructions of one kernel in an ncu report (source page): the top instructions by
 warp-stall samples and by instructions executed, with the dominant stall reasons.
 
-  python tools/ncu_hot.py gpurun_out/x.ncu-rep <kernel regex> [top]
+  python tools/ncu_hot.py gpurun_out/x.ncu-rep <kernel regex> [top] [launch skip]
 """
 import csv
 import io
@@ -11,8 +11,9 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}"], capture_output=True,
-                     text=True).stdout
+skip = ["--launch-skip", sys.argv[4], "--launch-count", "1"] if len(sys.argv) > 4 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", *skip],
+                     capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, ln in enumerate(lines) if ln.startswith('"Address"'))
 rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
