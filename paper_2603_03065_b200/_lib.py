@@ -11,8 +11,11 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# V3DB_LIB=debug loads the debug build (device-side invariant traps, identical results)
-LIB_PATH = os.path.join(HERE, "libv3db_debug.so" if os.environ.get("V3DB_LIB") == "debug" else "libv3db.so")
+# V3DB_LIB=debug loads the debug build (device-side invariant traps, identical results); a path to a
+# .so loads that build (experiment variants under tools/)
+_V = os.environ.get("V3DB_LIB", "")
+LIB_PATH = (_V if _V.endswith(".so") else
+            os.path.join(HERE, "libv3db_debug.so" if _V == "debug" else "libv3db.so"))
 HEADER = os.path.join(os.path.dirname(HERE), "include", "v3db.h")
 
 V3DB_OK, V3DB_EINVAL, V3DB_EINFEASIBLE, V3DB_ENOMEM, V3DB_ECUDA = range(5)

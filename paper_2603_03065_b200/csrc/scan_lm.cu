@@ -68,13 +68,19 @@ struct PairMeta {     // 16 B, read by the epilogue as one broadcast LDS.128
   int goff;           // pair * ngroups
 };
 
-// Minimum over the 32 lanes of each of 16 columns x[0..15] (x is consumed): a butterfly in which
-// each exchange halves the columns a lane keeps; lane l returns the minimum of column colmin_col(l)
-// (lanes l and l ^ 1 hold the same column).
+// Slots per group of the group minima (the unit Step 5 selects candidates by): 32 = a warp's
+// slots of a tile (measured against 16: C4 select 0.447 vs 0.478 ms, C3 0.115 vs 0.099).
+constexpr int kG = 32;
+
+// Minimum over each group of kG lanes (32: the warp; 16: each half) of each of 16 columns
+// x[0..15] (x is consumed): a butterfly in which each exchange halves the columns a lane keeps;
+// lane l returns the minimum of column colmin_col(l) over its group (for kG = 32, lanes l and l ^ 1
+// hold the same column).
 __device__ __forceinline__ int colmin16(int (&x)[16], int lane) {
+  constexpr int top = kG == 32 ? 16 : 8;
 #pragma unroll
   for (int st = 0; st < 4; ++st) {
-    const int half = 8 >> st, bit = 16 >> st;
+    const int half = 8 >> st, bit = top >> st;
     const bool up = lane & bit;
 #pragma unroll
     for (int i = 0; i < half; ++i) {
@@ -83,10 +89,12 @@ __device__ __forceinline__ int colmin16(int (&x)[16], int lane) {
       x[i] = min(kp, __shfl_xor_sync(0xffffffffu, snd, bit));
     }
   }
-  return min(x[0], __shfl_xor_sync(0xffffffffu, x[0], 1));
+  if constexpr (kG == 32) return min(x[0], __shfl_xor_sync(0xffffffffu, x[0], 1));
+  return x[0];
 }
 __device__ __forceinline__ int colmin_col(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  if constexpr (kG == 32) return lane >> 1 & 15;  // bits 4..1 of the lane
+  return lane & 15;
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -272,7 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
               for (int c = 0; c < kChunk; ++c) {
                 const PairMeta m = mc[c];
                 x[c] = m.d + P - 2 * static_cast<int32_t>(v[c]);
+#if !defined(LM_EXP) || LM_EXP != 1  // experiment 1: no trace stores
                 __stcs(reinterpret_cast<int32_t*>(m.row + toff), x[c]);
+#endif
               }
             } else {
 #pragma unroll
@@ -285,8 +295,17 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
                 }
               }
             }
+#if defined(LM_EXP) && LM_EXP == 2  // experiment: no group minima
+            if (x[0] == 0x12345678 && lane == 99) a.gmin[0] = x[1];
+#else
+            // lane l holds the minimum of column colmin_col(l) over its group of kG slots
             const int gm = colmin16(x, lane), col = colmin_col(lane);
-            if (sbase < cnt && !(lane & 1) && col < ncol) a.gmin[mc[col].goff + t * 4 + qd] = gm;
+            if constexpr (kG == 32) {
+              if (sbase < cnt && !(lane & 1) && col < ncol) a.gmin[mc[col].goff + t * 4 + qd] = gm;
+            } else {
+              if (sbase + (lane & 16) < cnt && col < ncol) a.gmin[mc[col].goff + t * 8 + qd * 2 + (lane >> 4)] = gm;
+            }
+#endif
           };
           // two chunks per round: both TMEM loads in flight before the first is used
           const uint32_t tbase = tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT;
@@ -297,8 +316,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
             tc::tmem_ld16(tbase + jc * kChunk, v0);
             if (two) tc::tmem_ld16(tbase + jd * kChunk, v1);
             tc::tmem_ld_wait();
+#if defined(LM_EXP) && LM_EXP == 3  // experiment 3: drain the accumulators only
+            if (v0[0] == 0x12345678u && v1[3] == 7u) a.gmin[0] = 1;
+#else
             chunk(v0, jc);
             if (two) chunk(v1, jd);
+#endif
           }
           tc::fence_before_sync();
           __syncwarp();
@@ -473,16 +496,16 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
   __syncthreads();
   const int32_t* gq = a.gmin + q * nprobe * NG;
   const int32_t* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
-  // valid groups: (rho, g) with 32 g < count_rho
+  // valid groups: (rho, g) with kG g < count_rho
   auto gen_g = [&](int i, uint32_t& v) {
     const int rho = i / NG, g = i - rho * NG;
-    if (32 * g >= pc[rho]) return false;
+    if (kG * g >= pc[rho]) return false;
     v = static_cast<uint32_t>(gq[i]);
     return true;
   };
   {
     int nvalid_g = 0;
-    for (int r = tid; r < nprobe; r += kSelThreads) nvalid_g += (pc[r] + 31) >> 5;
+    for (int r = tid; r < nprobe; r += kSelThreads) nvalid_g += (pc[r] + kG - 1) / kG;
     if (nvalid_g) atomicAdd(sc + 2, nvalid_g);
   }
   __syncthreads();
@@ -503,16 +526,16 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
       const int rho = i / NG, g = i - rho * NG;
       const int pos = atomicAdd(sc + 3, 1);
       if (pos < kSelGroups) sel[pos] = (rho << 16) | g;
-      atomicAdd(sc + 4, min(32, pc[rho] - 32 * g));
+      atomicAdd(sc + 4, min(kG, pc[rho] - kG * g));
     }
   }
   __syncthreads();
   const int nsel = sc[3];
   const bool all = nsel > kSelGroups || nprobe > 65535 || NG > 65535;  // fall back to every valid group
-  const int total_slots = all ? nprobe * NG * 32 : nsel * 32;
-  // candidate i: slot lane (i & 31) of selected group i >> 5 (or of group i >> 5 of the query)
+  const int total_slots = all ? nprobe * NG * kG : nsel * kG;
+  // candidate i: slot i % kG of selected group i / kG (or of group i / kG of the query)
   auto slot_of = [&](int i, int& rho, int& j) {
-    const int gi = i >> 5;
+    const int gi = i / kG;
     int g;
     if (all) {
       rho = gi / NG;
@@ -522,7 +545,7 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
       rho = sg >> 16;
       g = sg & 0xffff;
     }
-    j = 32 * g + (i & 31);
+    j = kG * g + i % kG;
     return j < pc[rho];
   };
   auto gen_d = [&](int i, uint32_t& v) {
@@ -675,7 +698,7 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
     int carry = 0;
     for (int r0 = 0; r0 < nprobe; r0 += 32) {
       const int r = r0 + lane;
-      const int c = r < nprobe ? (S.pc[r] + 31) >> 5 : 0;
+      const int c = r < nprobe ? (S.pc[r] + kG - 1) / kG : 0;
       int incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -709,7 +732,7 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
         const int i = i0 + u * kSelThreads;
         if (i < tot) {
           const int r = i / NG, g = i - r * NG;
-          if (32 * g < S.pc[r]) {
+          if (kG * g < S.pc[r]) {
             const int pos = S.pg[r] + g;
             S.gv[pos] = static_cast<uint32_t>(v[u]);
             S.gid[pos] = (r << 16) | g;
@@ -765,12 +788,12 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
   }
   __syncthreads();
   const int nsel = S.sc[5];
-  const int nslot = nsel * 32;
-  // candidate f in [0, nslot): slot (f & 31) of selected group f >> 5; relative D or ~0
+  const int nslot = nsel * kG;
+  // candidate f in [0, nslot): slot f % kG of selected group f / kG; relative D or ~0
   auto load_rel = [&](int f, int& r, int& j) {
-    const int id = S.gid[f >> 5];
+    const int id = S.gid[f / kG];
     r = id >> 16;
-    j = 32 * (id & 0xffff) + (f & 31);
+    j = kG * (id & 0xffff) + f % kG;
     const uint32_t D = j < S.pc[r] ? static_cast<uint32_t>(tq[r * static_cast<int64_t>(L) + j]) : 0xffffffffu;
     const uint32_t rel = D - dmin;
     return rel <= tau ? rel : 0xffffffffu;
@@ -886,7 +909,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   if (nq <= 0) return cudaSuccess;
   if (!s->xhat || s->dim % 16 != 0) return cudaErrorInvalidValue;
   const int64_t npairs = nq * nprobe;
-  const int L = s->L, ngroups = (L + 31) / 32, kp = (s->dim + kPanel - 1) / kPanel;
+  const int L = s->L, ngroups = (L + kG - 1) / kG, kp = (s->dim + kPanel - 1) / kPanel;
   if (npairs >= (int64_t(1) << 31) || npairs * ngroups >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   // NT: pairs per item, the largest of 256 / 128 / 64 / 32 whose double-buffered B operand fits 128 KB
   int NT = 128;
