@@ -284,7 +284,11 @@ int64_t v3db_kernel_launches(void);
  *   V3DB_OPT_LM_NT        list-major scan: (query, rank) pairs per work item, 32/64/128/256
  *                         (0 = auto: the largest whose B operand fits)
  *   V3DB_OPT_AUTO_SCAN    the kernel V3DB_SCAN_AUTO picks where several apply (0 = list-major,
- *                         else one of the V3DB_SCAN_* values) */
+ *                         else one of the V3DB_SCAN_* values)
+ *   V3DB_OPT_COARSE_2PASS Step 2 after the group-minimum pass: 0 auto (recompute the selected
+ *                         groups of lists when R * 8 * dim <= 32768, else a second contraction
+ *                         pass), 1 always the second pass, 4 / 8 / 16 / 32 always recompute with
+ *                         groups of at most that many lists */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2
@@ -297,7 +301,8 @@ int64_t v3db_kernel_launches(void);
 #define V3DB_OPT_SCAN_DIRECT 9
 #define V3DB_OPT_LM_NT 10
 #define V3DB_OPT_AUTO_SCAN 11
-#define V3DB_OPT_COUNT 12
+#define V3DB_OPT_COARSE_2PASS 12
+#define V3DB_OPT_COUNT 13
 int v3db_set_option(int32_t key, int64_t value);
 int64_t v3db_get_option(int32_t key);
 

@@ -431,3 +431,17 @@ def test_lm_topk_sizes(v3db, k):
         torch.cuda.synchronize()
         assert_query_equal(out, want, keys=None if trace else ("out_ids", "out_dist"))
     s.free()
+
+
+@pytest.mark.parametrize("mode", [1, 4, 8, 32])
+@pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_large"])
+def test_coarse_step2_paths(v3db, name, mode):
+    """Step 2 after the group-minimum pass: the second contraction pass (1) and the recomputation
+    of the selected groups of lists with every group size (4, 8, 32) give the same bits."""
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    with v3db.option(v3db.OPT_COARSE_2PASS, mode):
+        out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k)
+        torch.cuda.synchronize()
+    assert_query_equal(out, ref)
+    s.free()
