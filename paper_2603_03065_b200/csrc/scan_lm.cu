@@ -410,34 +410,68 @@ constexpr int kSelThreads = 256;
 constexpr int kWarpProbeCap = 128;  // largest nprobe of the cached selection path
 constexpr int kSelGroups = 4096;  // selected-group list capacity (more: every valid group is scanned)
 
+// Distance types of Step 5: int32 (BASELINE.json's int8 path) and int64 (the paper's 16-bit fixed
+// point, NEXT-1).  U = the unsigned domain of the histograms / radix digits (every valid D >= 0);
+// Key = the total (D, item) order of R10 (item as signed int32: key id ^ 0x80000000).
+struct KeyFx {
+  int64_t d;
+  uint32_t id;  // item ^ 0x80000000
+};
+template <class T>
+struct DistT;
+template <>
+struct DistT<int32_t> {
+  using U = uint32_t;
+  using Key = uint64_t;
+  static constexpr int32_t kMax = 0x7fffffff;
+  __device__ static Key key(int32_t d, int32_t id) { return step5_key(d, id); }
+  __device__ static int32_t id(Key k) { return step5_id(k); }
+  __device__ static int32_t dist(Key k) { return static_cast<int32_t>(k >> 32); }
+  __device__ static bool less(Key a, Key b) { return a < b; }
+  __device__ static int bitlen(U x) { return 32 - __clz(x | 1u); }
+};
+template <>
+struct DistT<int64_t> {
+  using U = uint64_t;
+  using Key = KeyFx;
+  static constexpr int64_t kMax = 0x7fffffffffffffffLL;
+  __device__ static Key key(int64_t d, int32_t id) { return KeyFx{d, static_cast<uint32_t>(id) ^ 0x80000000u}; }
+  __device__ static int32_t id(Key k) { return static_cast<int32_t>(k.id ^ 0x80000000u); }
+  __device__ static int64_t dist(Key k) { return k.d; }
+  __device__ static bool less(Key a, Key b) { return a.d < b.d || (a.d == b.d && a.id < b.id); }
+  __device__ static int bitlen(U x) { return 64 - __clzll(static_cast<long long>(x | 1ull)); }
+};
+
+template <class T>
 struct SelArgs {
   int nprobe, L, ngroups, k;
   const int32_t* lists;
   const int32_t* counts;
   const int32_t* ids;
-  const int32_t* trace;
-  const int32_t* gmin;
+  const T* trace;
+  const T* gmin;
   int32_t* out_ids;
-  int32_t* out_dist;
+  T* out_dist;
 };
 
-// CTA-wide radix selection (8-bit digits) of the kk-th smallest (1-based) 32-bit value among those
+// CTA-wide radix selection (8-bit digits) of the kk-th smallest (1-based) value among those
 // `gen(i, &v)` yields for i in [0, n); every value is known to be <= bound, so the leading digits
 // above bound's top bit are skipped.  Returns the value; *below = how many yielded values are smaller.
-template <class Gen>
-__device__ uint32_t cta_radix_select(int n, int kk, uint32_t bound, Gen gen, int* hist, int* sc, int* below) {
+template <class U, class Gen>
+__device__ U cta_radix_select(int n, int kk, U bound, Gen gen, int* hist, int* sc, int* below) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int top = 32 - __clz(bound | 1u);
-  const int pass0 = 3 - (top - 1) / 8;
-  uint32_t prefix = 0;
+  constexpr int ND = sizeof(U);
+  const int top = sizeof(U) == 8 ? 64 - __clzll(static_cast<long long>(bound | 1)) : 32 - __clz(static_cast<uint32_t>(bound | 1));
+  const int pass0 = ND - 1 - (top - 1) / 8;
+  U prefix = 0;
   const int k0 = kk;
-  for (int pass = pass0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
+  for (int pass = pass0; pass < ND; ++pass) {
+    const int shift = 8 * (ND - 1 - pass);
     for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
     __syncthreads();
     for (int i = tid; i < n; i += kSelThreads) {
-      uint32_t v;
-      if (gen(i, v) && (pass == pass0 || (v >> (shift + 8)) == prefix)) atomicAdd(hist + ((v >> shift) & 255), 1);
+      U v;
+      if (gen(i, v) && (pass == pass0 || (v >> (shift + 8)) == prefix)) atomicAdd(hist + static_cast<int>((v >> shift) & 255), 1);
     }
     __syncthreads();
     if (warp == 0) {
@@ -467,7 +501,7 @@ __device__ uint32_t cta_radix_select(int n, int kk, uint32_t bound, Gen gen, int
       }
     }
     __syncthreads();
-    prefix = (prefix << 8) | static_cast<uint32_t>(sc[0]);
+    prefix = (prefix << 8) | static_cast<U>(sc[0]);
     kk = sc[1];
     __syncthreads();
   }
@@ -477,15 +511,20 @@ __device__ uint32_t cta_radix_select(int n, int kk, uint32_t bound, Gen gen, int
 
 // Streaming selection (no per-query capacity limit): every pass re-reads the group minima and the
 // candidates' distances from global memory.  Used for the queries the cached path cannot hold.
-__device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
+template <class T>
+__device__ void select_streaming(const SelArgs<T>& a, int64_t q, uint8_t* sm) {
+  using Tr = DistT<T>;
+  using U = typename Tr::U;
+  using Key = typename Tr::Key;
   int* pl = reinterpret_cast<int*>(sm);            // [nprobe] probed list
   int* pc = pl + a.nprobe;                         // [nprobe] its count
   int* hist = pc + a.nprobe;                       // [256]
   int* sc = hist + 256;                            // [16] scratch
   int* sel = sc + 16;                              // [kSelGroups] selected groups (rho << 16 | g)
-  uint64_t* keys = reinterpret_cast<uint64_t*>(sel + kSelGroups);  // [k]
+  Key* keys = reinterpret_cast<Key*>(sel + kSelGroups);  // [k]
   const int tid = threadIdx.x;
   const int nprobe = a.nprobe, L = a.L, NG = a.ngroups, k = a.k;
+  const U tau_all = static_cast<U>(Tr::kMax) - 1;  // every valid D (< d_max)
   __syncthreads();  // the caller may have used the same shared memory
   for (int r = tid; r < nprobe; r += kSelThreads) {
     const int li = a.lists[q * nprobe + r];
@@ -494,13 +533,13 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
   }
   if (tid < 16) sc[tid] = 0;
   __syncthreads();
-  const int32_t* gq = a.gmin + q * nprobe * NG;
-  const int32_t* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
+  const T* gq = a.gmin + q * nprobe * NG;
+  const T* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
   // valid groups: (rho, g) with kG g < count_rho
-  auto gen_g = [&](int i, uint32_t& v) {
+  auto gen_g = [&](int i, U& v) {
     const int rho = i / NG, g = i - rho * NG;
     if (kG * g >= pc[rho]) return false;
-    v = static_cast<uint32_t>(gq[i]);
+    v = static_cast<U>(gq[i]);
     return true;
   };
   {
@@ -513,20 +552,19 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
   int below = 0;
   // tau = the k-th smallest group minimum (each is a real candidate's D), or "everything" if fewer
   // than k valid groups exist
-  const uint32_t tau = V >= k ? cta_radix_select(nprobe * NG, k, 0x7ffffffeu, gen_g, hist, sc, &below) : 0x7ffffffeu;
-  // the selected groups (minimum <= tau) and how many valid slots they hold
+  const U tau = V >= k ? cta_radix_select<U>(nprobe * NG, k, tau_all, gen_g, hist, sc, &below) : tau_all;
+  // the selected groups (minimum <= tau)
   if (tid == 0) {
     sc[3] = 0;
     sc[4] = 0;
   }
   __syncthreads();
   for (int i = tid; i < nprobe * NG; i += kSelThreads) {
-    uint32_t v;
+    U v;
     if (gen_g(i, v) && v <= tau) {
       const int rho = i / NG, g = i - rho * NG;
       const int pos = atomicAdd(sc + 3, 1);
       if (pos < kSelGroups) sel[pos] = (rho << 16) | g;
-      atomicAdd(sc + 4, min(kG, pc[rho] - kG * g));
     }
   }
   __syncthreads();
@@ -548,10 +586,10 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
     j = kG * g + i % kG;
     return j < pc[rho];
   };
-  auto gen_d = [&](int i, uint32_t& v) {
+  auto gen_d = [&](int i, U& v) {
     int rho, j;
     if (!slot_of(i, rho, j)) return false;
-    v = static_cast<uint32_t>(tq[rho * static_cast<int64_t>(L) + j]);
+    v = static_cast<U>(tq[rho * static_cast<int64_t>(L) + j]);
     return v <= tau;
   };
   // how many candidates (valid, D <= tau) exist
@@ -560,7 +598,7 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
   {
     int c = 0;
     for (int i = tid; i < total_slots; i += kSelThreads) {
-      uint32_t v;
+      U v;
       c += gen_d(i, v) ? 1 : 0;
     }
     atomicAdd(sc + 5, c);
@@ -568,18 +606,19 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
   __syncthreads();
   const int ncand = sc[5];
   const int kk = min(k, ncand);
-  uint32_t dk = 0xffffffffu, idk = 0xffffffffu;
+  U dk = ~U(0);
+  uint32_t idk = 0xffffffffu;
   if (ncand > k) {
     // the k-th smallest D; then, if the ties at it do not all fit, the (k - below)-th smallest item
     // key among them (R10: (D, id) order, id as signed int32 -> key id ^ 0x80000000)
-    dk = cta_radix_select(total_slots, k, tau, gen_d, hist, sc, &below);
+    dk = cta_radix_select<U>(total_slots, k, tau, gen_d, hist, sc, &below);
     const int need = k - below;
     if (tid == 0) sc[6] = 0;
     __syncthreads();
     {
       int c = 0;
       for (int i = tid; i < total_slots; i += kSelThreads) {
-        uint32_t v;
+        U v;
         c += (gen_d(i, v) && v == dk) ? 1 : 0;
       }
       atomicAdd(sc + 6, c);
@@ -589,19 +628,19 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
       auto gen_id = [&](int i, uint32_t& v) {
         int rho, j;
         if (!slot_of(i, rho, j)) return false;
-        if (static_cast<uint32_t>(tq[rho * static_cast<int64_t>(L) + j]) != dk) return false;
+        if (static_cast<U>(tq[rho * static_cast<int64_t>(L) + j]) != dk) return false;
         v = static_cast<uint32_t>(__ldg(a.ids + static_cast<int64_t>(pl[rho]) * L + j)) ^ 0x80000000u;
         return true;
       };
       int b2 = 0;
-      idk = cta_radix_select(total_slots, need, 0xffffffffu, gen_id, hist, sc, &b2);
+      idk = cta_radix_select<uint32_t>(total_slots, need, 0xffffffffu, gen_id, hist, sc, &b2);
     }
   }
   // collect the min(k, ncand) winners as resolved (D, item) keys, then place them by rank
   if (tid == 0) sc[7] = 0;
   __syncthreads();
   for (int i = tid; i < total_slots; i += kSelThreads) {
-    uint32_t v;
+    U v;
     if (!gen_d(i, v) || v > dk) continue;
     int rho, j;
     slot_of(i, rho, j);
@@ -609,20 +648,20 @@ __device__ void select_streaming(const SelArgs& a, int64_t q, uint8_t* sm) {
     if (v == dk && (static_cast<uint32_t>(id) ^ 0x80000000u) > idk) continue;
     const int pos = atomicAdd(sc + 7, 1);
     V3DB_DCHECK(pos < kk);
-    keys[pos] = step5_key(static_cast<int32_t>(v), id);
+    keys[pos] = Tr::key(static_cast<T>(v), id);
   }
   __syncthreads();
   const int m = sc[7];
   for (int e2 = tid; e2 < m; e2 += kSelThreads) {
-    const uint64_t key = keys[e2];
+    const Key key = keys[e2];
     int rank = 0;
-    for (int f = 0; f < m; ++f) rank += keys[f] < key ? 1 : 0;
-    a.out_ids[q * k + rank] = step5_id(key);
-    a.out_dist[q * k + rank] = static_cast<int32_t>(key >> 32);
+    for (int f = 0; f < m; ++f) rank += Tr::less(keys[f], key) ? 1 : 0;
+    a.out_ids[q * k + rank] = Tr::id(key);
+    a.out_dist[q * k + rank] = Tr::dist(key);
   }
   for (int r = m + tid; r < k; r += kSelThreads) {  // fewer than k valid candidates (R11)
     a.out_ids[q * k + r] = -1;
-    a.out_dist[q * k + r] = kDMax;
+    a.out_dist[q * k + r] = Tr::kMax;
   }
 }
 
@@ -640,59 +679,98 @@ constexpr int kSelGcap = 2048;     // cached group minima per query
 constexpr int kSelKmax = 256;      // largest k of the cached path
 constexpr int kBinCap = 256;       // entries of the final histogram bin ranked pairwise
 
+template <class T>
 struct SelSmem {
-  uint32_t gv[kSelGcap];           // valid group minima - dmin
+  using U = typename DistT<T>::U;
+  using Key = typename DistT<T>::Key;
+  U gv[kSelGcap];                  // valid group minima
   int gid[kSelGcap];               // rho << 16 | g, compacted to the selected groups
   int hist[256];
   int pl[kWarpProbeCap];           // probed lists
   int pc[kWarpProbeCap];           // their counts
   int pg[kWarpProbeCap + 1];       // valid-group prefix
-  uint64_t keys[kSelKmax];         // winners
-  uint64_t bin[kBinCap];           // final-bin entries
+  Key keys[kSelKmax];              // winners
+  Key bin[kBinCap];                // final-bin entries
+  T mm[2];                         // the query's smallest / largest valid group minimum
   int sc[40];
 };
 
 // Block-wide: the bin of hist[0, 256) holding rank kk (1-based); *before = entries below it,
 // *inbin = its population.  256 threads; ends with a barrier.
-__device__ __forceinline__ int cta_bin_of(SelSmem& S, int kk, int* before, int* inbin) {
+__device__ __forceinline__ int cta_bin_of(int* hist, int* sc, int kk, int* before, int* inbin) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int h = S.hist[tid];
+  const int h = hist[tid];
   int incl = h;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int w = __shfl_up_sync(kFull, incl, o);
     if (lane >= o) incl += w;
   }
-  if (lane == 31) S.sc[24 + warp] = incl;
+  if (lane == 31) sc[24 + warp] = incl;
   __syncthreads();
   int base = 0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) base += w < warp ? S.sc[24 + w] : 0;
+  for (int w = 0; w < 8; ++w) base += w < warp ? sc[24 + w] : 0;
   const int excl = base + incl - h;
   if (excl < kk && kk <= excl + h) {
-    S.sc[0] = tid;
-    S.sc[1] = excl;
-    S.sc[2] = h;
+    sc[0] = tid;
+    sc[1] = excl;
+    sc[2] = h;
   }
   __syncthreads();
-  *before = S.sc[1];
-  *inbin = S.sc[2];
-  return S.sc[0];
+  *before = sc[1];
+  *inbin = sc[2];
+  return sc[0];
 }
 
-__global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const SelArgs a, int* __restrict__ flags) {
-  __shared__ SelSmem S;
+template <class T>
+__device__ __forceinline__ T warp_min(T v) {
+  if constexpr (sizeof(T) == 4) {
+    return __reduce_min_sync(kFull, v);
+  } else {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T w = __shfl_xor_sync(kFull, v, o);
+      v = w < v ? w : v;
+    }
+    return v;
+  }
+}
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+  if constexpr (sizeof(T) == 4) {
+    return __reduce_max_sync(kFull, v);
+  } else {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T w = __shfl_xor_sync(kFull, v, o);
+      v = w > v ? w : v;
+    }
+    return v;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const SelArgs<T> a, int* __restrict__ flags) {
+  using Tr = DistT<T>;
+  using U = typename Tr::U;
+  using Key = typename Tr::Key;
+  __shared__ SelSmem<T> S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t q = blockIdx.x;
   const int nprobe = a.nprobe, L = a.L, NG = a.ngroups, k = a.k;
-  const int32_t* gq = a.gmin + q * nprobe * NG;
-  const int32_t* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
+  const T* gq = a.gmin + q * nprobe * NG;
+  const T* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
   for (int r = tid; r < nprobe; r += kSelThreads) {
     const int li = a.lists[q * nprobe + r];
     S.pl[r] = li;
     S.pc[r] = __ldg(a.counts + li);
   }
-  if (tid < 40) S.sc[tid] = tid == 3 ? 0x7fffffff : 0;
+  if (tid < 40) S.sc[tid] = 0;
+  if (tid == 0) {
+    S.mm[0] = Tr::kMax;
+    S.mm[1] = 0;
+  }
   __syncthreads();
   if (warp == 0) {  // prefix sums of the valid groups per probe
     int carry = 0;
@@ -717,11 +795,11 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
     return;
   }
   // the valid group minima (8 loads in flight per thread), their minimum and maximum
-  int mn = 0x7fffffff, mx = 0;
+  T mn = Tr::kMax, mx = 0;
   {
     const int tot = nprobe * NG;
     for (int i0 = tid; i0 < tot; i0 += 8 * kSelThreads) {
-      int v[8];
+      T v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int i = i0 + u * kSelThreads;
@@ -734,46 +812,52 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
           const int r = i / NG, g = i - r * NG;
           if (kG * g < S.pc[r]) {
             const int pos = S.pg[r] + g;
-            S.gv[pos] = static_cast<uint32_t>(v[u]);
+            S.gv[pos] = static_cast<U>(v[u]);
             S.gid[pos] = (r << 16) | g;
-            mn = min(mn, v[u]);
-            mx = max(mx, v[u]);
+            mn = v[u] < mn ? v[u] : mn;
+            mx = v[u] > mx ? v[u] : mx;
           }
         }
       }
     }
   }
-  mn = __reduce_min_sync(kFull, mn);
-  mx = __reduce_max_sync(kFull, mx);
+  mn = warp_min(mn);
+  mx = warp_max(mx);
   if (lane == 0) {
-    atomicMin(S.sc + 3, mn);
-    atomicMax(S.sc + 4, mx);
+    if constexpr (sizeof(T) == 4) {
+      atomicMin(&S.mm[0], mn);
+      atomicMax(&S.mm[1], mx);
+    } else {
+      atomicMin(reinterpret_cast<long long*>(&S.mm[0]), static_cast<long long>(mn));
+      atomicMax(reinterpret_cast<long long*>(&S.mm[1]), static_cast<long long>(mx));
+    }
   }
   __syncthreads();
-  const uint32_t dmin = static_cast<uint32_t>(S.sc[3]);
-  uint32_t tau = 0x7ffffffeu - dmin;  // relative
+  const U dmin = static_cast<U>(S.mm[0]);
+  const U tmax = static_cast<U>(Tr::kMax) - 1 - dmin;  // relative bound of every valid D
+  U tau = tmax;  // relative
   if (V >= k) {
-    uint32_t w0 = 0, span = static_cast<uint32_t>(S.sc[4]) - dmin + 1u;
+    U w0 = 0, span = static_cast<U>(S.mm[1]) - dmin + 1;
     int need = k;
     for (;;) {
-      const int bits = 32 - __clz((span - 1u) | 1u);
+      const int bits = Tr::bitlen(span - 1);
       const int sh = bits > 8 ? bits - 8 : 0;
       S.hist[tid] = 0;
       __syncthreads();
       for (int i = tid; i < V; i += kSelThreads) {
-        const uint32_t rel = S.gv[i] - dmin;
-        if (rel >= w0 && rel - w0 < span) atomicAdd(S.hist + ((rel - w0) >> sh), 1);
+        const U rel = S.gv[i] - dmin;
+        if (rel >= w0 && rel - w0 < span) atomicAdd(S.hist + static_cast<int>((rel - w0) >> sh), 1);
       }
       __syncthreads();
       int before, inbin;
-      const int b = cta_bin_of(S, need, &before, &inbin);
-      w0 += static_cast<uint32_t>(b) << sh;
-      span = 1u << sh;
+      const int b = cta_bin_of(S.hist, S.sc, need, &before, &inbin);
+      w0 += static_cast<U>(b) << sh;
+      span = U(1) << sh;
       need -= before;
       if (sh == 0 || inbin <= 8) break;  // a bin of <= 8 group minima: tight enough
     }
-    tau = w0 + span - 1u;
-    if (dmin + tau > 0x7ffffffeu) tau = 0x7ffffffeu - dmin;
+    tau = w0 + span - 1;
+    if (tau > tmax) tau = tmax;
   }
   // compact the selected groups (minimum <= tau) into gid[0, nsel)
   if (tid == 0) S.sc[5] = 0;
@@ -789,38 +873,39 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
   __syncthreads();
   const int nsel = S.sc[5];
   const int nslot = nsel * kG;
+  const U none = ~U(0);
   // candidate f in [0, nslot): slot f % kG of selected group f / kG; relative D or ~0
   auto load_rel = [&](int f, int& r, int& j) {
     const int id = S.gid[f / kG];
     r = id >> 16;
     j = kG * (id & 0xffff) + f % kG;
-    const uint32_t D = j < S.pc[r] ? static_cast<uint32_t>(tq[r * static_cast<int64_t>(L) + j]) : 0xffffffffu;
-    const uint32_t rel = D - dmin;
-    return rel <= tau ? rel : 0xffffffffu;
+    const U D = j < S.pc[r] ? static_cast<U>(tq[r * static_cast<int64_t>(L) + j]) : none;
+    const U rel = D - dmin;
+    return D != none && rel <= tau ? rel : none;
   };
   auto item_of = [&](int r, int j) { return __ldg(a.ids + static_cast<int64_t>(S.pl[r]) * L + j); };
   // window [w0, w0 + span) of D - dmin holding the k-th smallest candidate; `need` = its rank in it
-  uint32_t w0 = 0, span = tau + 1u;
+  U w0 = 0, span = tau + 1;
   int need = k, ntot = -1;
   for (;;) {
-    const int bits = 32 - __clz((span - 1u) | 1u);
+    const int bits = Tr::bitlen(span - 1);
     const int sh = bits > 8 ? bits - 8 : 0;
     S.hist[tid] = 0;
     __syncthreads();
     int c = 0;
     for (int f0 = tid; f0 < nslot; f0 += 4 * kSelThreads) {
-      uint32_t rel[4];
+      U rel[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         int r, j;
         const int f = f0 + u * kSelThreads;
-        rel[u] = f < nslot ? load_rel(f, r, j) : 0xffffffffu;
+        rel[u] = f < nslot ? load_rel(f, r, j) : none;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (rel[u] == 0xffffffffu) continue;
+        if (rel[u] == none) continue;
         ++c;
-        if (rel[u] >= w0 && rel[u] - w0 < span) atomicAdd(S.hist + ((rel[u] - w0) >> sh), 1);
+        if (rel[u] >= w0 && rel[u] - w0 < span) atomicAdd(S.hist + static_cast<int>((rel[u] - w0) >> sh), 1);
       }
     }
     if (ntot < 0) {
@@ -833,8 +918,8 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
       if (ntot <= k) break;  // every candidate wins
     }
     int before, inbin;
-    const int b = cta_bin_of(S, need, &before, &inbin);
-    const uint32_t hi = w0 + (static_cast<uint32_t>(b) << sh);
+    const int b = cta_bin_of(S.hist, S.sc, need, &before, &inbin);
+    const U hi = w0 + (static_cast<U>(b) << sh);
     const bool last = sh == 0 || inbin <= kBinCap;
     if (last && inbin > kBinCap) {  // more than kBinCap candidates tied at one distance
       if (tid == 0) flags[q] = 1;
@@ -843,25 +928,25 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
     // candidates below the target bin win; on the last pass the bin's entries are gathered too
     for (int f = tid; f < nslot; f += kSelThreads) {
       int r, j;
-      const uint32_t rel = load_rel(f, r, j);
-      if (rel == 0xffffffffu || rel < w0) continue;
+      const U rel = load_rel(f, r, j);
+      if (rel == none || rel < w0) continue;
       if (rel < hi) {
-        S.keys[atomicAdd(S.sc + 7, 1)] = step5_key(static_cast<int32_t>(rel + dmin), item_of(r, j));
-      } else if (last && rel - hi < (1u << sh)) {
-        S.bin[atomicAdd(S.sc + 8, 1)] = step5_key(static_cast<int32_t>(rel + dmin), item_of(r, j));
+        S.keys[atomicAdd(S.sc + 7, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(r, j));
+      } else if (last && rel - hi < (U(1) << sh)) {
+        S.bin[atomicAdd(S.sc + 8, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(r, j));
       }
     }
     w0 = hi;
-    span = 1u << sh;
+    span = U(1) << sh;
     need -= before;
     __syncthreads();
     if (last) {
       const int nb = S.sc[8], nlo = S.sc[7];
       V3DB_DCHECK(nb == inbin && nlo + need == k);
       for (int e2 = tid; e2 < nb; e2 += kSelThreads) {  // the `need` smallest keys of the bin
-        const uint64_t key = S.bin[e2];
+        const Key key = S.bin[e2];
         int rank = 0;
-        for (int f = 0; f < nb; ++f) rank += S.bin[f] < key ? 1 : 0;
+        for (int f = 0; f < nb; ++f) rank += Tr::less(S.bin[f], key) ? 1 : 0;
         if (rank < need) S.keys[nlo + rank] = key;
       }
       break;
@@ -871,31 +956,58 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
   if (ntot <= k) {  // every candidate wins (fewer than k valid: (-1, d_max) tail, R11)
     for (int f = tid; f < nslot; f += kSelThreads) {
       int r, j;
-      const uint32_t rel = load_rel(f, r, j);
-      if (rel != 0xffffffffu) S.keys[atomicAdd(S.sc + 7, 1)] = step5_key(static_cast<int32_t>(rel + dmin), item_of(r, j));
+      const U rel = load_rel(f, r, j);
+      if (rel != none) S.keys[atomicAdd(S.sc + 7, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(r, j));
     }
     m = ntot;
   }
   __syncthreads();
   for (int e2 = tid; e2 < m; e2 += kSelThreads) {
-    const uint64_t key = S.keys[e2];
+    const Key key = S.keys[e2];
     int rank = 0;
-    for (int f = 0; f < m; ++f) rank += S.keys[f] < key ? 1 : 0;
-    a.out_ids[q * k + rank] = step5_id(key);
-    a.out_dist[q * k + rank] = static_cast<int32_t>(key >> 32);
+    for (int f = 0; f < m; ++f) rank += Tr::less(S.keys[f], key) ? 1 : 0;
+    a.out_ids[q * k + rank] = Tr::id(key);
+    a.out_dist[q * k + rank] = Tr::dist(key);
   }
   for (int r = m + tid; r < k; r += kSelThreads) {
     a.out_ids[q * k + r] = -1;
-    a.out_dist[q * k + r] = kDMax;
+    a.out_dist[q * k + r] = Tr::kMax;
   }
 }
 
-// The queries the per-warp path flagged (or every query when it does not apply): one CTA each.
-__global__ void __launch_bounds__(kSelThreads) lm_select_cta_kernel(const SelArgs a, const int* __restrict__ flags) {
+// The queries the cached path flagged (or every query when it does not apply): one CTA each.
+template <class T>
+__global__ void __launch_bounds__(kSelThreads) lm_select_cta_kernel(const SelArgs<T> a, const int* __restrict__ flags) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int64_t q = blockIdx.x;
   if (flags && flags[q] == 0) return;
-  select_streaming(a, q, sm);
+  select_streaming<T>(a, q, sm);
+}
+
+// Step 5 launch (both distance types): the cached selection, then the streaming one for the queries
+// it flagged; flags: scratch int [nq].
+template <class T>
+cudaError_t launch_select(const SelArgs<T>& sa, int64_t nq, int* flags, cudaStream_t st) {
+  using Key = typename DistT<T>::Key;
+  const size_t ssm = sizeof(int) * (2 * sa.nprobe + 256 + 16 + kSelGroups) + 16 + sizeof(Key) * sa.k;
+  const bool fast = sa.k <= kSelKmax && sa.nprobe <= kWarpProbeCap && sa.ngroups <= 65535;
+  cudaError_t e = cudaSuccess;
+  if (fast) {
+    e = cudaMemsetAsync(flags, 0, sizeof(int) * nq, st);
+    if (e == cudaSuccess) {
+      lm_select_fast_kernel<T><<<static_cast<unsigned>(nq), kSelThreads, 0, st>>>(sa, flags);
+      note_launch();
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lm_select_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm));
+  if (e == cudaSuccess) {
+    lm_select_cta_kernel<T><<<static_cast<unsigned>(nq), kSelThreads, ssm, st>>>(sa, fast ? flags : nullptr);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  return e;
 }
 
 size_t al(size_t x, size_t b) { return (x + b - 1) / b * b; }
@@ -1007,7 +1119,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   if (e == cudaSuccess) e = debug_sync(st, "lm_kernel");
   if (prof) prof(3, st);
   if (e == cudaSuccess) {
-    SelArgs sa;
+    SelArgs<int32_t> sa;
     sa.nprobe = nprobe;
     sa.L = L;
     sa.ngroups = ngroups;
@@ -1019,25 +1131,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
     sa.gmin = gmin;
     sa.out_ids = out_ids;
     sa.out_dist = out_dist;
-    const size_t ssm = sizeof(int) * (2 * nprobe + 256 + 16 + kSelGroups) + 16 + sizeof(uint64_t) * k;
-    const bool fast = k <= kSelKmax && nprobe <= kWarpProbeCap && ngroups <= 65535;
-    int* flags = nullptr;
-    if (fast) {  // cached selection; the flagged queries then take the streaming one
-      flags = reinterpret_cast<int*>(gmin + npairs * ngroups);
-      e = cudaMemsetAsync(flags, 0, sizeof(int) * nq, st);
-      if (e == cudaSuccess) {
-        lm_select_fast_kernel<<<static_cast<unsigned>(nq), kSelThreads, 0, st>>>(sa, flags);
-        note_launch();
-        e = cudaGetLastError();
-      }
-    }
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(lm_select_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm));
-    if (e == cudaSuccess) {
-      lm_select_cta_kernel<<<static_cast<unsigned>(nq), kSelThreads, ssm, st>>>(sa, flags);
-      note_launch();
-      e = cudaGetLastError();
-    }
+    e = launch_select(sa, nq, reinterpret_cast<int*>(gmin + npairs * ngroups), st);
   }
   if (e == cudaSuccess) e = debug_sync(st, "lm_select kernels");
   cudaFreeAsync(base, st);
