@@ -285,10 +285,16 @@ int64_t v3db_kernel_launches(void);
  *                         (0 = auto: the largest whose B operand fits)
  *   V3DB_OPT_AUTO_SCAN    the kernel V3DB_SCAN_AUTO picks where several apply (0 = list-major,
  *                         else one of the V3DB_SCAN_* values)
- *   V3DB_OPT_COARSE_2PASS Step 2 after the group-minimum pass: 0 auto (recompute the selected
- *                         groups of lists when R * 8 * dim <= 32768, else a second contraction
- *                         pass), 1 always the second pass, 4 / 8 / 16 / 32 always recompute with
- *                         groups of at most that many lists */
+ *   V3DB_OPT_COARSE_2PASS Steps 1-2 on the tensor cores: 0 auto (one contraction pass keeping
+ *                         the two smallest keys of every block of 32 lists, then an exact merge that
+ *                         recomputes the blocks that may hide more -- dim <= 1024; otherwise the
+ *                         group-minimum pass below), 1 the group-minimum pass then a second
+ *                         contraction pass, 4 / 8 / 16 / 32 the group-minimum pass then the
+ *                         recomputation of the selected groups of at most that many lists
+ *   V3DB_OPT_SELECT_CTA   list-major Step 5: 0 auto (one warp per query when the probed lists
+ *                         hold >= 8 k groups of 32 slots, else one CTA per query), 1 always one
+ *                         CTA of 256 threads per query, 2 always one warp per query (all exact;
+ *                         the streaming CTA path takes the queries they flag) */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2
@@ -302,7 +308,8 @@ int64_t v3db_kernel_launches(void);
 #define V3DB_OPT_LM_NT 10
 #define V3DB_OPT_AUTO_SCAN 11
 #define V3DB_OPT_COARSE_2PASS 12
-#define V3DB_OPT_COUNT 13
+#define V3DB_OPT_SELECT_CTA 13
+#define V3DB_OPT_COUNT 14
 int v3db_set_option(int32_t key, int64_t value);
 int64_t v3db_get_option(int32_t key);
 

@@ -190,14 +190,19 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
       const int col0 = c * kChunk + h * 64;       // first list of this warp's 64 columns
       // ||mu||^2 of the 64 columns (warp-uniform per column: read back as broadcasts)
       __syncwarp();
-      cn[lane] = col0 + lane < a.nlist ? __ldg(a.cnorm + col0 + lane) : 0;
-      cn[lane + 32] = col0 + 32 + lane < a.nlist ? __ldg(a.cnorm + col0 + 32 + lane) : 0;
+      if constexpr (PASS == 3) {  // packed column terms 32 ||mu_i||^2 + (i mod 32); padding: +inf
+        cn[lane] = col0 + lane < a.nlist ? 32 * __ldg(a.cnorm + col0 + lane) + lane : 0x7fffffff;
+        cn[lane + 32] = col0 + 32 + lane < a.nlist ? 32 * __ldg(a.cnorm + col0 + 32 + lane) + lane : 0x7fffffff;
+      } else {
+        cn[lane] = col0 + lane < a.nlist ? __ldg(a.cnorm + col0 + lane) : 0;
+        cn[lane + 32] = col0 + 32 + lane < a.nlist ? __ldg(a.cnorm + col0 + 32 + lane) : 0;
+      }
       if (rt != cur_rt) {  // ||x||^2 of this thread's row (from global: the A tile may be reloaded)
         cur_rt = rt;
         row = rt * kRows + r;
         live = row < a.n;
         xn = 0;
-        if (live) {
+        if (live && PASS != 3) {
           const int8_t* xr = a.X + row * a.dim;
           for (int u2 = 0; u2 < a.dim; u2 += 4) {
             const int v = *reinterpret_cast<const int*>(xr + u2);
@@ -273,6 +278,41 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
           }
         }
       };
+      if constexpr (PASS == 3) {
+        // packed key p = 32 e + (i mod 32), e = ||mu_i||^2 - 2 <x, mu_i> = d_i - ||x||^2 (exact:
+        // |32 e| < 2^31 for dim <= 1024; padding columns: acc = 0, p = +inf); per 32-list block the
+        // two smallest keys (min / second min: three IMNMX per column)
+        int m[4];
+        auto top2 = [&](int cb, int& m1, int& m2) {
+          const int4* c4 = reinterpret_cast<const int4*>(cn + cb);
+          m1 = 0x7fffffff;
+          m2 = 0x7fffffff;
+#pragma unroll
+          for (int u4 = 0; u4 < 8; ++u4) {
+            const int4 cc = c4[u4];
+            const int cw[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const int pk = cw[w] - 64 * static_cast<int>(v[4 * u4 + w]);
+              const int t = max(m1, pk);
+              m1 = min(m1, pk);
+              m2 = min(m2, t);
+            }
+          }
+        };
+        tc::tmem_ld32(taddr, v);
+        tc::tmem_ld_wait();
+        top2(0, m[0], m[1]);
+        tc::tmem_ld32(taddr + 32, v);
+        tc::tmem_ld_wait();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(acce + acc);  // accumulator columns consumed
+        top2(32, m[2], m[3]);
+        if (live)  // blocks 8c + 2h and 8c + 2h + 1 of the row: (min, second min) each
+          *reinterpret_cast<int4*>(a.gmin + 2 * (row * a.ngroups + c * 8 + h * 2)) = make_int4(m[0], m[1], m[2], m[3]);
+        continue;
+      }
       // two 32-column TMEM loads, processed one after the other (32 live registers)
       tc::tmem_ld32(taddr, v);
       tc::tmem_ld_wait();
@@ -555,6 +595,209 @@ __global__ void __launch_bounds__(256) pick_kernel(const int8_t* __restrict__ X,
   });
 }
 
+// Step 2 from the single contraction pass (PASS 3), one warp per row.  S = the stored keys, the
+// two smallest of every block of 32 consecutive lists.  tau >= the R-th smallest e over S (linear-bin
+// histogram refinement as in pick_kernel), hence >= the row's true R-th smallest e.  A list of the
+// row's true top R that is not in S lies in a block whose two stored keys are both below it, so that
+// block's second key has e <= tau: every such block is recomputed exactly (dp4a against the
+// L2-resident centroids).  The candidates -- stored keys with e <= tau outside the recomputed
+// blocks, and the recomputed lists with e <= tau -- contain the true top R, which is ranked on
+// (d_i, i) (R9).  A row whose candidates or recomputed blocks overflow the caches is ranked by brute
+// force over every list (the same warp).
+constexpr int kMergeWarps = 4;
+constexpr int kRecCap = 32;  // recomputed blocks per row
+__device__ __forceinline__ uint64_t merge_key(int e, int i) {
+  return (static_cast<uint64_t>(static_cast<uint32_t>(e + (1 << 30))) << 32) | static_cast<uint32_t>(i);
+}
+template <int KR>
+__global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* __restrict__ X, int64_t n, int dim,
+                                                                const int8_t* __restrict__ mu,
+                                                                const int32_t* __restrict__ cnorm, int nlist,
+                                                                int nblk, int R, int cap,
+                                                                const int32_t* __restrict__ bk,
+                                                                int32_t* __restrict__ out_idx,
+                                                                int32_t* __restrict__ out_dist, int* __restrict__ hist) {
+  extern __shared__ __align__(16) uint8_t msm[];
+  constexpr unsigned kFull = 0xffffffffu;
+  constexpr int kInf = 0x7fffffff;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp;
+  int* wh = reinterpret_cast<int*>(msm) + warp * 256;                              // [256] histogram
+  int* rb = reinterpret_cast<int*>(msm) + kMergeWarps * 256 + warp * kRecCap;      // recomputed blocks
+  uint64_t* keys = reinterpret_cast<uint64_t*>(msm + 4 * kMergeWarps * (256 + kRecCap)) + warp * cap;
+  if (row >= n) return;
+  const int8_t* x = X + row * dim;
+  int xn = 0;
+  for (int u = lane; u < (dim >> 2); u += 32) {
+    const int v = __ldg(reinterpret_cast<const int*>(x) + u);
+    xn = __dp4a(v, v, xn);
+  }
+  xn = __reduce_add_sync(kFull, xn);
+  const int4* src = reinterpret_cast<const int4*>(bk + row * nblk * 2);
+  const int nv4 = nblk >> 1;  // one int4 = (min, second min) of two blocks
+  const unsigned lt = (1u << lane) - 1u;
+  int mn = kInf, mx = -kInf, cntv = 0;
+  for (int i = lane; i < nv4; i += 32) {
+    const int4 v = __ldg(src + i);
+    const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (w[t] != kInf) {
+        mn = min(mn, w[t] >> 5);
+        mx = max(mx, w[t] >> 5);
+        ++cntv;
+      }
+  }
+  mn = __reduce_min_sync(kFull, mn);
+  mx = __reduce_max_sync(kFull, mx);
+  cntv = __reduce_add_sync(kFull, cntv);
+  int tau = kInf;  // fewer than R stored keys: every block with two lists is recomputed
+  if (cntv >= R) {
+    int lo = mn, kk = R;
+    uint32_t span = static_cast<uint32_t>(mx - mn) + 1u;
+    for (;;) {
+      const int bits = 32 - __clz((span - 1u) | 1u);
+      const int sh = bits > 8 ? bits - 8 : 0;
+      for (int b = lane; b < 256; b += 32) wh[b] = 0;
+      __syncwarp();
+      for (int i = lane; i < nv4; i += 32) {
+        const int4 v = __ldg(src + i);
+        const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t rel = static_cast<uint32_t>((w[t] >> 5) - lo);
+          if (w[t] != kInf && rel < span) atomicAdd(&wh[rel >> sh], 1);
+        }
+      }
+      __syncwarp();
+      int hb[8], sum = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        hb[b] = wh[lane * 8 + b];
+        sum += hb[b];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int cum = incl - sum, bin = -1, newk = 0, cb = 0;
+      if (cum < kk && kk <= incl) {
+        bin = lane * 8;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (cum + hb[b] >= kk) {
+            cb = hb[b];
+            break;
+          }
+          cum += hb[b];
+          ++bin;
+        }
+        newk = kk - cum;
+      }
+      const int srcl = __ffs(__ballot_sync(kFull, bin >= 0)) - 1;
+      bin = __shfl_sync(kFull, bin, srcl);
+      kk = __shfl_sync(kFull, newk, srcl);
+      cb = __shfl_sync(kFull, cb, srcl);
+      __syncwarp();
+      lo += bin << sh;
+      span = 1u << sh;
+      if (sh == 0 || cb <= 8) break;
+    }
+    tau = lo + static_cast<int>(span - 1u);
+  }
+  // candidates: stored keys with e <= tau of the blocks kept; the blocks to recompute
+  int nc = 0, nr = 0;
+  for (int i0 = 0; i0 < nv4; i0 += 32) {
+    const int i = i0 + lane;
+    const int4 v = i < nv4 ? __ldg(src + i) : make_int4(kInf, kInf, kInf, kInf);
+#pragma unroll
+    for (int hb = 0; hb < 2; ++hb) {
+      const int m1 = hb ? v.z : v.x, m2 = hb ? v.w : v.y, b = 2 * i + hb;
+      const bool rec = m2 != kInf && (m2 >> 5) <= tau;
+      unsigned bal = __ballot_sync(kFull, rec);
+      int pos = nr + __popc(bal & lt);
+      if (rec && pos < kRecCap) rb[pos] = b;
+      nr += __popc(bal);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int mk = t ? m2 : m1;
+        const bool take = !rec && mk != kInf && (mk >> 5) <= tau;
+        bal = __ballot_sync(kFull, take);
+        pos = nc + __popc(bal & lt);
+        if (take && pos < cap) keys[pos] = merge_key(mk >> 5, b * 32 + (mk & 31));
+        nc += __popc(bal);
+      }
+    }
+  }
+  __syncwarp();
+  bool over = nr > kRecCap;
+  if (!over) {
+    const int4* x4 = reinterpret_cast<const int4*>(x);
+    for (int t = 0; t < nr; ++t) {
+      const int li = rb[t] * 32 + lane;
+      bool take = false;
+      int e = 0;
+      if (li < nlist) {
+        const int4* m4 = reinterpret_cast<const int4*>(mu + static_cast<int64_t>(li) * dim);
+        int dot = 0;
+        for (int u = 0; u < (dim >> 4); ++u) {
+          const int4 p = __ldg(x4 + u), q = __ldg(m4 + u);
+          dot = __dp4a(p.x, q.x, __dp4a(p.y, q.y, __dp4a(p.z, q.z, __dp4a(p.w, q.w, dot))));
+        }
+        e = __ldg(cnorm + li) - 2 * dot;
+        take = e <= tau;
+      }
+      const unsigned bal = __ballot_sync(kFull, take);
+      const int pos = nc + __popc(bal & lt);
+      if (take && pos < cap) keys[pos] = merge_key(e, li);
+      nc += __popc(bal);
+    }
+  }
+  over = over || nc > cap;
+  __syncwarp();
+  if (!over) {
+    for (int j = lane; j < nc; j += 32) {
+      const uint64_t kj = keys[j];
+      int rank = 0;
+      for (int f = 0; f < nc; ++f) rank += keys[f] < kj ? 1 : 0;
+      if (rank < R) {
+        const int li = static_cast<int>(static_cast<uint32_t>(kj));
+        out_idx[row * R + rank] = li;
+        out_dist[row * R + rank] = xn + static_cast<int>(kj >> 32) - (1 << 30);
+        if (hist) atomicAdd(hist + li, 1);
+      }
+    }
+    for (int j = nc + lane; j < R; j += 32) {  // fewer lists than R (not reached: R <= nlist)
+      out_idx[row * R + j] = -1;
+      out_dist[row * R + j] = kInf;
+    }
+    return;
+  }
+  WarpTopK<KR> top;  // overflow: every list, exactly
+  top.init(R);
+  for (int b = 0; b < nlist; b += 32) {
+    uint64_t key = ~0ull;
+    const int i = b + lane;
+    if (i < nlist) {
+      const int8_t* m = mu + static_cast<int64_t>(i) * dim;
+      int d = 0;
+      for (int u = 0; u < dim; ++u) {
+        const int df = static_cast<int>(x[u]) - static_cast<int>(m[u]);
+        d += df * df;
+      }
+      key = step2_key(d, i);
+    }
+    top.offer(key);
+  }
+  top.store([&](int j, uint64_t key) {
+    out_idx[row * R + j] = static_cast<int32_t>(key & 0xffffffffu);
+    out_dist[row * R + j] = static_cast<int32_t>(key >> 32);
+    if (hist) atomicAdd(hist + static_cast<uint32_t>(key), 1);
+  });
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -619,13 +862,18 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   // Recomputing ~R groups of G lists per row beats a second pass over every list when that is
   // small (measured: C1 0.069 vs 0.089 ms, C2 0.068 vs 0.101; C3 0.32 vs 0.20, C4 0.56 vs 0.46)
   const int64_t copt = opt(V3DB_OPT_COARSE_2PASS);
-  const bool pick = R <= 128 && copt != 1 &&
+  // default: one contraction pass keeping each 32-list block's two smallest keys, then merge_kernel
+  // (2 launches); the group-minimum paths remain as options (1, 4 / 8 / 16 / 32) and for dim > 1024
+  const bool top2 = copt == 0 && dim <= 1024 && R <= 1024;
+  const bool pick = !top2 && R <= 128 && copt != 1 &&
                     (copt != 0 || static_cast<int64_t>(R) * 8 * dim <= 32768);
   const int gmax = pick ? (copt == 4 || copt == 8 || copt == 16 || copt == 32 ? static_cast<int>(copt) : 8) : 32;
   int G = 1;
   while (G * 2 <= gmax && static_cast<int64_t>(G * 2) * 2 * R <= nlist) G *= 2;
-  const int ngroups = (nlist + G - 1) / G;
-  const int capc = pick ? 0 : ngroups < R ? std::max(nlist, 4 * R + 128) : 4 * R + 128;
+  const int nchunks0 = (nlist + kChunk - 1) / kChunk;
+  // top2: ngroups = blocks per row (8 per 256-list chunk), two keys each
+  const int ngroups = top2 ? nchunks0 * 8 : (nlist + G - 1) / G;
+  const int capc = pick || top2 ? 0 : ngroups < R ? std::max(nlist, 4 * R + 128) : 4 * R + 128;
 
   int dev = 0, sms = 148;
   cudaError_t e = cudaGetDevice(&dev);
@@ -636,7 +884,7 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   const int64_t items = rtiles * nchunks;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(items, sms));
 
-  const size_t b_g = align256(sizeof(int32_t) * n * ngroups), b_t = align256(sizeof(int32_t) * n),
+  const size_t b_g = align256(sizeof(int32_t) * n * ngroups * (top2 ? 2 : 1)), b_t = align256(sizeof(int32_t) * n),
                b_c = align256(sizeof(uint64_t) * n * capc), b_n = align256(sizeof(int) * n);
   uint8_t* base = nullptr;
   e = scratch_alloc(reinterpret_cast<void**>(&base), b_g + b_t + b_c + 2 * b_n, st);
@@ -667,6 +915,26 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
     if (e1 == cudaSuccess) coarse_tc_kernel<1, GT><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
     return e1;
   };
+  if (top2) {
+    e = cudaFuncSetAttribute(coarse_tc_kernel<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) coarse_tc_kernel<3, 0><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = debug_sync(st, "coarse pass (block top-2)");
+    const int cap = 2 * R + 64;
+    const size_t msmem = 4 * kMergeWarps * (256 + kRecCap) + sizeof(uint64_t) * kMergeWarps * cap;
+    if (e == cudaSuccess) {
+      dispatch_kr(R, [&]<int KR>() {
+        e = cudaFuncSetAttribute(merge_kernel<KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem));
+        if (e == cudaSuccess)
+          merge_kernel<KR><<<static_cast<unsigned>((n + kMergeWarps - 1) / kMergeWarps), 32 * kMergeWarps, msmem, st>>>(
+              X, n, dim, mu, cnorm, nlist, ngroups, R, cap, a.gmin, out_idx, out_dist, list_hist);
+      });
+      if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    note_launch(2);
+    cudaFreeAsync(base, st);
+    return e;
+  }
   e = cudaFuncSetAttribute(coarse_tc_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess) {
     switch (G) {

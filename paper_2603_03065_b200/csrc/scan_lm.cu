@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
             // lane l holds the minimum of column colmin_col(l) over its group of kG slots
             const int gm = colmin16(x, lane), col = colmin_col(lane);
             if constexpr (kG == 32) {
-              if (sbase < cnt && !(lane & 1) && col < ncol) a.gmin[mc[col].goff + t * 4 + qd] = gm;
+              // a group without a valid slot (inside L): the sentinel d_max (Step 5 skips it)
+              if (sbase < L && !(lane & 1) && col < ncol) a.gmin[mc[col].goff + t * 4 + qd] = sbase < cnt ? gm : kDMax;
             } else {
               if (sbase + (lane & 16) < cnt && col < ncol) a.gmin[mc[col].goff + t * 8 + qd * 2 + (lane >> 4)] = gm;
             }
@@ -328,7 +329,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
           if (lane == 0) tc::mbar_arrive(acce + acc);
         } else if (mine && slot < L) {
           // a tile of padding only: D = d_max, nothing read
-          for (int c = cg; c < np; c += NCG) __stcs(reinterpret_cast<int32_t*>(mt[c].row + toff), kDMax);
+          for (int c = cg; c < np; c += NCG) {
+            __stcs(reinterpret_cast<int32_t*>(mt[c].row + toff), kDMax);
+            if (kG == 32 && lane == 0) a.gmin[mt[c].goff + t * 4 + qd] = kDMax;  // group sentinel
+          }
         }
       }
       __syncwarp();
@@ -666,34 +670,47 @@ __device__ void select_streaming(const SelArgs<T>& a, int64_t q, uint8_t* sm) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Step 5, one CTA per query, small shared footprint (8 CTAs per SM): the valid group minima are
-// cached in shared memory; tau = the upper edge of a histogram bin holding the k-th smallest one
-// (>= it, hence >= the k-th smallest D); the candidates -- the valid slots with D <= tau of the
-// groups whose minimum is <= tau -- are re-read from the trace (L2) in each pass.  The k smallest
-// (D, item) keys are exact: 256-bin histograms of D - dmin over a shrinking window; candidates
-// below the window's target bin win outright, the target bin is refined until it holds
-// <= kBinCap entries, which are ranked on their full (D, item) keys (R10).  Queries beyond the
-// caches (or kBinCap candidates tied at one distance) take the streaming path.
+// Step 5, one CTA per query, small shared footprint (8 CTAs per SM for int32 distances):
+//  1. the valid group minima are cached in shared memory; tau = the upper edge of a histogram bin
+//     holding the k-th smallest one (>= it, hence >= the k-th smallest D: k distinct candidates
+//     reach it);
+//  2. the candidates -- the valid slots with D <= tau of the groups whose minimum is <= tau -- are
+//     read from the trace ONCE, a warp per group (lane = slot: one 128-byte load), and compacted
+//     into shared memory as (D - dmin, rho, slot);
+//  3. the k smallest (D, item) keys among them are exact: 256-bin histograms of D - dmin over a
+//     shrinking window of the compacted candidates; candidates below the window's target bin win
+//     outright, the target bin is refined until it holds <= kBinCap entries, which are ranked on
+//     their full (D, item) keys (R10).
+// Queries beyond the caches (kSelGcap valid groups, kCandCap candidates, or more than kBinCap
+// candidates tied at one distance) take the streaming path.
 // ---------------------------------------------------------------------------------------------
 constexpr int kSelGcap = 2048;     // cached group minima per query
+constexpr int kCandCap = 2048;     // compacted candidates per query
 constexpr int kSelKmax = 256;      // largest k of the cached path
 constexpr int kBinCap = 256;       // entries of the final histogram bin ranked pairwise
+static_assert(kG == 32, "the candidate gather maps a group's slots to the lanes of a warp");
 
 template <class T>
 struct SelSmem {
   using U = typename DistT<T>::U;
   using Key = typename DistT<T>::Key;
-  U gv[kSelGcap];                  // valid group minima
-  int gid[kSelGcap];               // rho << 16 | g, compacted to the selected groups
+  U gv[kSelGcap];                  // valid group minima; then the candidates' D - dmin
+  union {
+    int gid[kSelGcap];             // rho << 16 | g, compacted to the selected groups
+    struct {
+      Key keys[kSelKmax];          // winners (after the gather: gid is dead)
+      Key bin[kBinCap];            // final-bin entries
+    } w;
+  };
+  int cf[kCandCap];                // candidate rho << 24 | slot
   int hist[256];
   int pl[kWarpProbeCap];           // probed lists
   int pc[kWarpProbeCap];           // their counts
   int pg[kWarpProbeCap + 1];       // valid-group prefix
-  Key keys[kSelKmax];              // winners
-  Key bin[kBinCap];                // final-bin entries
   T mm[2];                         // the query's smallest / largest valid group minimum
   int sc[40];
 };
+static_assert(sizeof(int) * kSelGcap >= 2 * sizeof(DistT<int64_t>::Key) * kSelKmax, "winner arrays alias gid");
 
 // Block-wide: the bin of hist[0, 256) holding rank kk (1-based); *before = entries below it,
 // *inbin = its population.  256 threads; ends with a barrier.
@@ -872,104 +889,445 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
   }
   __syncthreads();
   const int nsel = S.sc[5];
-  const int nslot = nsel * kG;
   const U none = ~U(0);
-  // candidate f in [0, nslot): slot f % kG of selected group f / kG; relative D or ~0
-  auto load_rel = [&](int f, int& r, int& j) {
-    const int id = S.gid[f / kG];
-    r = id >> 16;
-    j = kG * (id & 0xffff) + f % kG;
-    const U D = j < S.pc[r] ? static_cast<U>(tq[r * static_cast<int64_t>(L) + j]) : none;
-    const U rel = D - dmin;
-    return D != none && rel <= tau ? rel : none;
-  };
-  auto item_of = [&](int r, int j) { return __ldg(a.ids + static_cast<int64_t>(S.pl[r]) * L + j); };
-  // window [w0, w0 + span) of D - dmin holding the k-th smallest candidate; `need` = its rank in it
-  U w0 = 0, span = tau + 1;
-  int need = k, ntot = -1;
-  for (;;) {
-    const int bits = Tr::bitlen(span - 1);
-    const int sh = bits > 8 ? bits - 8 : 0;
-    S.hist[tid] = 0;
-    __syncthreads();
-    int c = 0;
-    for (int f0 = tid; f0 < nslot; f0 += 4 * kSelThreads) {
-      U rel[4];
+  // the candidates, read once: warp w takes selected groups w, w + 8, ... (four in flight);
+  // lane = slot of the group; the valid slots with D - dmin <= tau are appended to (gv, cf)
+  U* cd = S.gv;  // the group minima are dead (every thread is past the compaction barrier)
+  for (int f0 = warp; f0 < nsel; f0 += 4 * (kSelThreads / 32)) {
+    U rel[4];
+    int tag[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int r, j;
-        const int f = f0 + u * kSelThreads;
-        rel[u] = f < nslot ? load_rel(f, r, j) : none;
+    for (int u = 0; u < 4; ++u) {
+      const int f = f0 + u * (kSelThreads / 32);
+      rel[u] = none;
+      if (f < nsel) {  // warp-uniform
+        const int id = S.gid[f], r = id >> 16, j = kG * (id & 0xffff) + lane;
+        tag[u] = (r << 24) | j;
+        if (j < S.pc[r]) {
+          const U rl = static_cast<U>(tq[r * static_cast<int64_t>(L) + j]) - dmin;
+          if (rl <= tau) rel[u] = rl;
+        }
       }
+    }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (rel[u] == none) continue;
-        ++c;
-        if (rel[u] >= w0 && rel[u] - w0 < span) atomicAdd(S.hist + static_cast<int>((rel[u] - w0) >> sh), 1);
+    for (int u = 0; u < 4; ++u) {
+      const unsigned bal = __ballot_sync(kFull, rel[u] != none);
+      if (bal == 0) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(S.sc + 6, __popc(bal));
+      base = __shfl_sync(kFull, base, 0);
+      const int pos = base + __popc(bal & ((1u << lane) - 1u));
+      if (rel[u] != none && pos < kCandCap) {
+        cd[pos] = rel[u];
+        S.cf[pos] = tag[u];
       }
-    }
-    if (ntot < 0) {
-      c = __reduce_add_sync(kFull, c);
-      if (lane == 0) atomicAdd(S.sc + 6, c);
-    }
-    __syncthreads();
-    if (ntot < 0) {
-      ntot = S.sc[6];
-      if (ntot <= k) break;  // every candidate wins
-    }
-    int before, inbin;
-    const int b = cta_bin_of(S.hist, S.sc, need, &before, &inbin);
-    const U hi = w0 + (static_cast<U>(b) << sh);
-    const bool last = sh == 0 || inbin <= kBinCap;
-    if (last && inbin > kBinCap) {  // more than kBinCap candidates tied at one distance
-      if (tid == 0) flags[q] = 1;
-      return;
-    }
-    // candidates below the target bin win; on the last pass the bin's entries are gathered too
-    for (int f = tid; f < nslot; f += kSelThreads) {
-      int r, j;
-      const U rel = load_rel(f, r, j);
-      if (rel == none || rel < w0) continue;
-      if (rel < hi) {
-        S.keys[atomicAdd(S.sc + 7, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(r, j));
-      } else if (last && rel - hi < (U(1) << sh)) {
-        S.bin[atomicAdd(S.sc + 8, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(r, j));
-      }
-    }
-    w0 = hi;
-    span = U(1) << sh;
-    need -= before;
-    __syncthreads();
-    if (last) {
-      const int nb = S.sc[8], nlo = S.sc[7];
-      V3DB_DCHECK(nb == inbin && nlo + need == k);
-      for (int e2 = tid; e2 < nb; e2 += kSelThreads) {  // the `need` smallest keys of the bin
-        const Key key = S.bin[e2];
-        int rank = 0;
-        for (int f = 0; f < nb; ++f) rank += Tr::less(S.bin[f], key) ? 1 : 0;
-        if (rank < need) S.keys[nlo + rank] = key;
-      }
-      break;
     }
   }
+  __syncthreads();
+  const int C = S.sc[6];
+  if (C > kCandCap) {
+    if (tid == 0) flags[q] = 1;
+    return;
+  }
+  auto item_of = [&](int f) {
+    const int t = S.cf[f];
+    return __ldg(a.ids + static_cast<int64_t>(S.pl[t >> 24]) * L + (t & 0xffffff));
+  };
   int m = k;
-  if (ntot <= k) {  // every candidate wins (fewer than k valid: (-1, d_max) tail, R11)
-    for (int f = tid; f < nslot; f += kSelThreads) {
-      int r, j;
-      const U rel = load_rel(f, r, j);
-      if (rel != none) S.keys[atomicAdd(S.sc + 7, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(r, j));
+  if (C <= k) {  // every candidate wins (fewer than k valid: (-1, d_max) tail, R11)
+    for (int f = tid; f < C; f += kSelThreads) S.w.keys[f] = Tr::key(static_cast<T>(cd[f] + dmin), item_of(f));
+    m = C;
+  } else {
+    // window [w0, w0 + span) of D - dmin holding the k-th smallest candidate; `need` = its rank in it
+    U w0 = 0, span = tau + 1;
+    int need = k;
+    for (;;) {
+      const int bits = Tr::bitlen(span - 1);
+      const int sh = bits > 8 ? bits - 8 : 0;
+      S.hist[tid] = 0;
+      __syncthreads();
+      for (int f = tid; f < C; f += kSelThreads) {
+        const U rel = cd[f];
+        if (rel >= w0 && rel - w0 < span) atomicAdd(S.hist + static_cast<int>((rel - w0) >> sh), 1);
+      }
+      __syncthreads();
+      int before, inbin;
+      const int b = cta_bin_of(S.hist, S.sc, need, &before, &inbin);
+      const U hi = w0 + (static_cast<U>(b) << sh);
+      const bool last = sh == 0 || inbin <= kBinCap;
+      if (last && inbin > kBinCap) {  // more than kBinCap candidates tied at one distance
+        if (tid == 0) flags[q] = 1;
+        return;
+      }
+      // candidates below the target bin win; on the last pass the bin's entries are gathered too
+      for (int f = tid; f < C; f += kSelThreads) {
+        const U rel = cd[f];
+        if (rel < w0) continue;
+        if (rel < hi) {
+          S.w.keys[atomicAdd(S.sc + 7, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(f));
+        } else if (last && rel - hi < (U(1) << sh)) {
+          S.w.bin[atomicAdd(S.sc + 8, 1)] = Tr::key(static_cast<T>(rel + dmin), item_of(f));
+        }
+      }
+      w0 = hi;
+      span = U(1) << sh;
+      need -= before;
+      __syncthreads();
+      if (last) {
+        const int nb = S.sc[8], nlo = S.sc[7];
+        V3DB_DCHECK(nb == inbin && nlo + need == k);
+        for (int e2 = tid; e2 < nb; e2 += kSelThreads) {  // the `need` smallest keys of the bin
+          const Key key = S.w.bin[e2];
+          int rank = 0;
+          for (int f = 0; f < nb; ++f) rank += Tr::less(S.w.bin[f], key) ? 1 : 0;
+          if (rank < need) S.w.keys[nlo + rank] = key;
+        }
+        break;
+      }
     }
-    m = ntot;
   }
   __syncthreads();
   for (int e2 = tid; e2 < m; e2 += kSelThreads) {
-    const Key key = S.keys[e2];
+    const Key key = S.w.keys[e2];
     int rank = 0;
-    for (int f = 0; f < m; ++f) rank += Tr::less(S.keys[f], key) ? 1 : 0;
+    for (int f = 0; f < m; ++f) rank += Tr::less(S.w.keys[f], key) ? 1 : 0;
     a.out_ids[q * k + rank] = Tr::id(key);
     a.out_dist[q * k + rank] = Tr::dist(key);
   }
   for (int r = m + tid; r < k; r += kSelThreads) {
+    a.out_ids[q * k + r] = -1;
+    a.out_dist[q * k + r] = Tr::kMax;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Step 5, one WARP per query (the default where it applies): no block barriers, every pass
+// warp-synchronous.  The group minima are read from L1/L2 in each pass (a group without a valid
+// slot holds the sentinel d_max, written by lm_kernel); tau = the upper edge of a linear histogram
+// bin holding the k-th smallest valid group minimum (>= the k-th smallest D); the candidates -- the
+// valid slots with D <= tau of the groups whose minimum is <= tau -- are read once (lane = slot of
+// the group) and compacted into shared memory; a linear-bin refinement over the candidates finds
+// the window [0, w) holding the k smallest D with at most kSwBin entries in its last bin; those
+// entries (at most k + kSwBin - 1) get their full (D, item) keys (R10) and are put in order by a
+// counting sort over 256 bins plus a pairwise rank inside each bin; the first k are written.
+// Queries beyond the caches (kSwCand candidates, more than kSwBin entries tied at one distance)
+// are flagged for the streaming path.
+// ---------------------------------------------------------------------------------------------
+constexpr int kSwWarps = 4;     // queries per CTA (6 CTAs per SM)
+constexpr int kSwCand = 384;    // compacted candidates per query
+constexpr int kSwSel = 256;     // selected groups per query
+constexpr int kSwBin = 32;      // entries of the last window bin
+constexpr int kSwKeys = kSelKmax + kSwBin;
+
+template <class T>
+struct SwSmem {  // per warp
+  using U = typename DistT<T>::U;
+  using Key = typename DistT<T>::Key;
+  int hist[256];
+  int pl[kWarpProbeCap];
+  int pc[kWarpProbeCap];
+  int sel[kSwSel];                // selected groups: rho << 16 | g
+  U cd[kSwCand];                  // candidate D - dmin
+  int cf[kSwCand];                // candidate rho << 24 | slot; then the window entries in bin order
+  Key keys[kSwKeys];              // the window's entries
+};
+
+// Warp-wide: the bin of h[0, 256) holding rank kk (1-based); *before = entries below it,
+// *inbin = its population.
+__device__ __forceinline__ int warp_bin_of(const int* h, int kk, int* before, int* inbin) {
+  const int lane = threadIdx.x & 31;
+  int hb[8], sum = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    hb[b] = h[lane * 8 + b];
+    sum += hb[b];
+  }
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  int cum = incl - sum, bin = -1, cb = 0;
+  if (cum < kk && kk <= incl) {
+    bin = lane * 8;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      if (cum + hb[b] >= kk) {
+        cb = hb[b];
+        break;
+      }
+      cum += hb[b];
+      ++bin;
+    }
+  }
+  const int src = __ffs(__ballot_sync(kFull, bin >= 0)) - 1;
+  *before = __shfl_sync(kFull, cum, src);
+  *inbin = __shfl_sync(kFull, cb, src);
+  return __shfl_sync(kFull, bin, src);
+}
+
+// NPL: group minima per lane held in registers (tot = nprobe * ngroups <= 32 NPL).
+template <class T, int NPL>
+__global__ void __launch_bounds__(32 * kSwWarps) lm_select_warp_kernel(const SelArgs<T> a, int64_t nq,
+                                                                       int* __restrict__ flags) {
+  using Tr = DistT<T>;
+  using U = typename Tr::U;
+  using Key = typename Tr::Key;
+  extern __shared__ __align__(16) uint8_t swm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * kSwWarps + warp;
+  if (q >= nq) return;
+  SwSmem<T>& S = reinterpret_cast<SwSmem<T>*>(swm)[warp];
+  const int nprobe = a.nprobe, L = a.L, NG = a.ngroups, k = a.k, tot = nprobe * NG;
+  const T* gq = a.gmin + q * tot;
+  const T* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
+  const unsigned lt = (1u << lane) - 1u;
+  const U none = ~U(0);
+  // the group minima (element 32 u + lane in gv[u]; beyond tot: the sentinel)
+  T gv[NPL];
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    const int i = 32 * u + lane;
+    gv[u] = i < tot ? gq[i] : Tr::kMax;
+  }
+  for (int r = lane; r < nprobe; r += 32) {
+    const int li = a.lists[q * nprobe + r];
+    S.pl[r] = li;
+    S.pc[r] = __ldg(a.counts + li);
+  }
+  T mn = Tr::kMax, mx = 0;
+  int V = 0;
+#pragma unroll
+  for (int u = 0; u < NPL; ++u) {
+    if (gv[u] != Tr::kMax) {
+      mn = gv[u] < mn ? gv[u] : mn;
+      mx = gv[u] > mx ? gv[u] : mx;
+      ++V;
+    }
+  }
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  V = __reduce_add_sync(kFull, V);
+  const U dmin = static_cast<U>(mn);
+  const U tmax = static_cast<U>(Tr::kMax) - 1 - dmin;  // relative bound of every valid D
+  U tau = tmax;
+  if (V >= k) {  // tau: refine a linear histogram of the group minima around rank k
+    U w0 = 0, span = static_cast<U>(mx) - dmin + 1;
+    int need = k;
+    for (;;) {
+      const int sh = max(0, Tr::bitlen(span - 1) - 8);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) S.hist[lane * 8 + b] = 0;
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < NPL; ++u) {
+        const U rel = static_cast<U>(gv[u]) - dmin - w0;
+        if (gv[u] != Tr::kMax && rel < span) atomicAdd(S.hist + static_cast<int>(rel >> sh), 1);
+      }
+      __syncwarp();
+      int before, inbin;
+      const int b = warp_bin_of(S.hist, need, &before, &inbin);
+      __syncwarp();
+      w0 += static_cast<U>(b) << sh;
+      span = U(1) << sh;
+      need -= before;
+      if (sh == 0 || inbin <= 8) break;  // a bin of <= 8 group minima: tight enough
+    }
+    tau = w0 + span - 1;
+    if (tau > tmax) tau = tmax;
+  }
+  // the selected groups (minimum <= tau), as rho << 16 | g; (rho, g) of i = 32 u + lane advance by
+  // 32 = da NG + db per register
+  int ns = 0;
+  {
+    int r = lane / NG, g = lane - r * NG;
+    const int da = 32 / NG, db = 32 - da * NG;
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) {
+      const bool sl = gv[u] != Tr::kMax && static_cast<U>(gv[u]) - dmin <= tau;
+      const unsigned bal = __ballot_sync(kFull, sl);
+      const int pos = ns + __popc(bal & lt);
+      if (sl && pos < kSwSel) S.sel[pos] = (r << 16) | g;
+      ns += __popc(bal);
+      g += db;
+      r += da;
+      if (g >= NG) {
+        g -= NG;
+        ++r;
+      }
+    }
+  }
+  if (ns > kSwSel) {
+    if (lane == 0) flags[q] = 1;
+    return;
+  }
+  __syncwarp();
+  // the candidates: 8 lanes per selected group, 4 consecutive slots per lane (one 16-byte load per
+  // 4 int32 values when L % 4 == 0), 8 groups per step; kept if valid and D - dmin <= tau
+  int C = 0;
+  {
+    const int sub = lane >> 3, part = lane & 7;
+    const bool vec = (L & 3) == 0;
+    for (int t0 = 0; t0 < ns; t0 += 8) {
+      U rel[2][4];
+      int tag[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = t0 + 4 * h + sub;
+        tag[h] = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) rel[h][w] = none;
+        if (t < ns) {
+          const int e = S.sel[t], r = e >> 16, j0 = kG * (e & 0xffff) + 4 * part, lim = S.pc[r];
+          tag[h] = (r << 24) | j0;
+          const T* src = tq + r * static_cast<int64_t>(L) + j0;
+          T v[4];
+          if (vec) {
+            if (j0 < L) {
+              if constexpr (sizeof(T) == 4) {
+                const int4 x = *reinterpret_cast<const int4*>(src);
+                v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+              } else {
+                const longlong2 x0 = reinterpret_cast<const longlong2*>(src)[0];
+                const longlong2 x1 = reinterpret_cast<const longlong2*>(src)[1];
+                v[0] = x0.x, v[1] = x0.y, v[2] = x1.x, v[3] = x1.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) v[w] = j0 + w < lim ? src[w] : T(0);
+          }
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const U rl = static_cast<U>(v[w]) - dmin;
+            if (j0 + w < lim && rl <= tau) rel[h][w] = rl;
+          }
+        }
+      }
+      // this lane's kept values, placed after the lower lanes' (one warp-wide scan per step)
+      int c = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) c += rel[h][w] != none ? 1 : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int pos = C + incl - c;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (rel[h][w] != none) {
+            if (pos < kSwCand) {
+              S.cd[pos] = rel[h][w];
+              S.cf[pos] = tag[h] + w;
+            }
+            ++pos;
+          }
+      C += __shfl_sync(kFull, incl, 31);
+    }
+  }
+  if (C > kSwCand) {
+    if (lane == 0) flags[q] = 1;
+    return;
+  }
+  __syncwarp();
+  // the window [0, w) of D - dmin holding the k smallest candidates, at most kSwBin in its last bin
+  U w = tau + 1;
+  if (C > k) {
+    U w0 = 0, span = tau + 1;
+    int need = k;
+    for (;;) {
+      const int sh = max(0, Tr::bitlen(span - 1) - 8);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) S.hist[lane * 8 + b] = 0;
+      __syncwarp();
+      for (int f = lane; f < C; f += 32) {
+        const U rel = S.cd[f] - w0;
+        if (rel < span) atomicAdd(S.hist + static_cast<int>(rel >> sh), 1);
+      }
+      __syncwarp();
+      int before, inbin;
+      const int b = warp_bin_of(S.hist, need, &before, &inbin);
+      __syncwarp();
+      w0 += static_cast<U>(b) << sh;
+      span = U(1) << sh;
+      need -= before;
+      if (inbin <= kSwBin) break;
+      if (sh == 0) {  // more than kSwBin candidates tied at one distance
+        if (lane == 0) flags[q] = 1;
+        return;
+      }
+    }
+    w = w0 + span;
+  }
+  // the window's entries as full keys
+  int M = 0;
+  for (int f0 = 0; f0 < C; f0 += 32) {
+    const int f = f0 + lane;
+    const bool in = f < C && S.cd[f] < w;
+    const unsigned bt = __ballot_sync(kFull, in);
+    if (in) {
+      const int t = S.cf[f];
+      const int32_t id = __ldg(a.ids + static_cast<int64_t>(S.pl[t >> 24]) * L + (t & 0xffffff));
+      S.keys[M + __popc(bt & lt)] = Tr::key(static_cast<T>(S.cd[f] + dmin), id);
+    }
+    M += __popc(bt);
+  }
+  __syncwarp();
+  V3DB_DCHECK(M <= kSwKeys);
+  // counting sort of the M keys by D over 256 bins of [0, w), then the rank inside each bin
+  {
+    int* cf = S.cf;  // reused: the window entries' indices in bin order (M <= kSwKeys <= kSwCand)
+    const int sh = max(0, Tr::bitlen(w - 1) - 8);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) S.hist[lane * 8 + b] = 0;
+    __syncwarp();
+    for (int e2 = lane; e2 < M; e2 += 32)
+      atomicAdd(S.hist + static_cast<int>((static_cast<U>(Tr::dist(S.keys[e2])) - dmin) >> sh), 1);
+    __syncwarp();
+    int hb[8], sum = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      hb[b] = S.hist[lane * 8 + b];
+      sum += hb[b];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      S.hist[lane * 8 + b] = run;  // exclusive start; advanced to the bin's end by the scatter
+      run += hb[b];
+    }
+    __syncwarp();
+    for (int e2 = lane; e2 < M; e2 += 32) {
+      const int b = static_cast<int>((static_cast<U>(Tr::dist(S.keys[e2])) - dmin) >> sh);
+      cf[atomicAdd(S.hist + b, 1)] = e2 | (b << 16);
+    }
+    __syncwarp();
+    for (int p = lane; p < M; p += 32) {
+      const int e2 = cf[p] & 0xffff, b = cf[p] >> 16;
+      const int s0 = b ? S.hist[b - 1] : 0, s1 = S.hist[b];
+      const Key key = S.keys[e2];
+      int rank = s0;
+      for (int x = s0; x < s1; ++x) rank += Tr::less(S.keys[cf[x] & 0xffff], key) ? 1 : 0;
+      if (rank < k) {
+        a.out_ids[q * k + rank] = Tr::id(key);
+        a.out_dist[q * k + rank] = Tr::dist(key);
+      }
+    }
+  }
+  for (int r = M + lane; r < k; r += 32) {  // fewer than k valid candidates (R11)
     a.out_ids[q * k + r] = -1;
     a.out_dist[q * k + r] = Tr::kMax;
   }
@@ -991,10 +1349,30 @@ cudaError_t launch_select(const SelArgs<T>& sa, int64_t nq, int* flags, cudaStre
   using Key = typename DistT<T>::Key;
   const size_t ssm = sizeof(int) * (2 * sa.nprobe + 256 + 16 + kSelGroups) + 16 + sizeof(Key) * sa.k;
   const bool fast = sa.k <= kSelKmax && sa.nprobe <= kWarpProbeCap && sa.ngroups <= 65535;
+  // one warp per query where the group minima are many against k (tau from them is then tight and
+  // the candidates few); the CTA kernel (a larger candidate cache) otherwise
+  const int64_t sopt = opt(V3DB_OPT_SELECT_CTA);
+  const int64_t tot_g = static_cast<int64_t>(sa.nprobe) * sa.ngroups;
+  const bool warp = fast && tot_g <= 32 * 64 && (sopt == 2 || (sopt == 0 && tot_g >= 8 * static_cast<int64_t>(sa.k)));
   cudaError_t e = cudaSuccess;
   if (fast) {
     e = cudaMemsetAsync(flags, 0, sizeof(int) * nq, st);
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && warp) {
+      const size_t wsm = sizeof(SwSmem<T>) * kSwWarps;
+      const unsigned g = static_cast<unsigned>((nq + kSwWarps - 1) / kSwWarps);
+      auto run = [&](auto kern) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsm));
+        if (e == cudaSuccess) kern<<<g, 32 * kSwWarps, wsm, st>>>(sa, nq, flags);
+      };
+      const int tot = sa.nprobe * sa.ngroups;
+      if (tot <= 32 * 8) run(lm_select_warp_kernel<T, 8>);
+      else if (tot <= 32 * 16) run(lm_select_warp_kernel<T, 16>);
+      else if (tot <= 32 * 32) run(lm_select_warp_kernel<T, 32>);
+      else if (tot <= 32 * 48) run(lm_select_warp_kernel<T, 48>);
+      else run(lm_select_warp_kernel<T, 64>);
+      note_launch();
+      if (e == cudaSuccess) e = cudaGetLastError();
+    } else if (e == cudaSuccess) {
       lm_select_fast_kernel<T><<<static_cast<unsigned>(nq), kSelThreads, 0, st>>>(sa, flags);
       note_launch();
       e = cudaGetLastError();

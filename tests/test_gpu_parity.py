@@ -433,11 +433,12 @@ def test_lm_topk_sizes(v3db, k):
     s.free()
 
 
-@pytest.mark.parametrize("mode", [1, 4, 8, 32])
+@pytest.mark.parametrize("mode", [0, 1, 4, 8, 32])
 @pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_large"])
 def test_coarse_step2_paths(v3db, name, mode):
-    """Step 2 after the group-minimum pass: the second contraction pass (1) and the recomputation
-    of the selected groups of lists with every group size (4, 8, 32) give the same bits."""
+    """Steps 1-2: the single contraction pass keeping every 32-list block's two smallest keys
+    (0, the default), the group-minimum pass followed by a second contraction pass (1) or by the
+    recomputation of the selected groups with every group size (4, 8, 32) give the same bits."""
     cfg, inp, ref_s, ref = config_case(name)
     s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
     with v3db.option(v3db.OPT_COARSE_2PASS, mode):
@@ -445,3 +446,56 @@ def test_coarse_step2_paths(v3db, name, mode):
         torch.cuda.synchronize()
     assert_query_equal(out, ref)
     s.free()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_coarse_block_top2_adversarial(v3db, mode):
+    """Single-pass Steps 1-2 where keeping two keys per block of 32 consecutive lists is not enough:
+    (a) every block's 32 centroids are drawn around one centre, so a query's n_probe nearest lists
+    share one block, which must be recomputed exactly; two centroids are duplicated (ties on d_i
+    broken by the list index, R9); (b) every centroid is identical, so every block ties and the
+    row overflows to the brute-force ranking.  Both equal the oracle (the second contraction pass,
+    mode 1, beside it)."""
+    rng = np.random.default_rng(21)
+    D, nlist, L, nprobe, k = 32, 512, 64, 24, 10
+    centres = rng.integers(-100, 100, size=(16, D))
+    N = nlist * 8
+    db = np.clip(centres[np.arange(N) // (N // 16)] + rng.integers(-3, 4, size=(N, D)), -127, 127).astype(np.int8)
+    db[8 * 6] = db[8 * 5]                     # lists 5 and 6: one centroid twice
+    cent = np.arange(0, N, 8)[:nlist]         # centroid i = row 8 i: block i // 32 <-> centre i // 32
+    qs = np.clip(centres[rng.integers(0, 16, 40)] + rng.integers(-4, 5, size=(40, D)), -127, 127).astype(np.int8)
+    qs = np.vstack([qs, db[8 * 5][None]])
+    code = np.stack([rng.choice(N, 16, replace=False) for _ in range(4)])
+    with v3db.option(v3db.OPT_COARSE_2PASS, mode):
+        run_case(v3db, db, qs, nlist, L, 4, 16, nprobe, k, cent, code, algos=("lm", "gen"))
+        N2, nlist2 = 4096, 2048                  # (b) 64 blocks, every one tied
+        db2 = np.full((N2, 16), 3, np.int8)
+        qs2 = np.vstack([np.full((1, 16), 3, np.int8), np.arange(16, dtype=np.int8)[None]])
+        run_case(v3db, db2, qs2, nlist2, 8, 4, 4, 40, 10, np.arange(nlist2), np.stack([np.arange(4)] * 4),
+                 algos=("lm", "gen"))
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_large", "e2_lowacc"])
+def test_lm_select_paths(v3db, name, mode):
+    """Step 5 of the list-major scan: auto (0), one CTA per query (1) and one warp per query (2)
+    give the same bits (and the streaming path takes whatever either flags)."""
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    with v3db.option(v3db.OPT_SELECT_CTA, mode):
+        out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k, algo=ALGOS["lm"])
+        torch.cuda.synchronize()
+    assert_query_equal(out, ref)
+    s.free()
+
+
+def test_lm_select_ties_beyond_window(v3db):
+    """150 candidates tied at one distance (fewer than the per-query candidate cache, more than the
+    last window bin holds): the warp selection flags the query and the streaming path ranks the
+    ties by item id (R10)."""
+    N, D, nlist, L = 150, 32, 2, 100
+    db = np.full((N, D), 5, np.int8)
+    qs = np.vstack([np.full((1, D), 5, np.int8), np.full((1, D), -3, np.int8)])
+    with v3db.option(v3db.OPT_SELECT_CTA, 2):
+        run_case(v3db, db, qs, nlist, L, 4, 4, 2, 10, np.arange(nlist), np.stack([np.arange(4)] * 4),
+                 algos=("lm", "gen"))
