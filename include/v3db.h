@@ -281,7 +281,7 @@ int64_t v3db_kernel_launches(void);
  *   V3DB_OPT_FX_NOROT     1: no rotated fixed-point code copy (read at fx16 build)
  *   V3DB_OPT_FX_W12       fx16 scan warps per CTA (0 = auto)
  *   V3DB_OPT_SCAN_SEG / _NS / _CAP / _FIRST / _DIRECT   rotated-LUT scan geometry (0 = auto)
- *   V3DB_OPT_LM_NT        list-major scan: (query, rank) pairs per work item, 32/64/128/256
+ *   V3DB_OPT_LM_NT        list-major scan: (query, rank) pairs per work item, 32/64/128 (256: 128)
  *                         (0 = auto: the largest whose B operand fits)
  *   V3DB_OPT_AUTO_SCAN    the kernel V3DB_SCAN_AUTO picks where several apply (0 = list-major,
  *                         else one of the V3DB_SCAN_* values)

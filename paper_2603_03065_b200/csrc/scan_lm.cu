@@ -47,6 +47,10 @@ constexpr int kNB = 3;                                  // B operand (query rows
 constexpr int kWarpTma = 0, kWarpMma = 1, kWarpGat = 2, kNGat = 2, kWarpEpi = 4;
 constexpr int kThreads = 32 * (kWarpEpi + kEpiWarps);  // 640
 constexpr uint32_t kFull = 0xffffffffu;
+// staging row of one column (32 slots): 36 words -- the 32 lanes' stores hit distinct banks and the
+// 16-byte reads of the group-minimum pass (two lanes per column) are conflict-free
+constexpr int kStageRow = 36;
+constexpr uint32_t kStageBytes = kEpiWarps * kChunk * kStageRow * 4u;
 
 struct LmArgs {
   int nprobe, L, Lp, dim, kp, NT, nacc, lg_nacc, S, nb, ngroups;
@@ -59,7 +63,9 @@ struct LmArgs {
   const int32_t* pterm;   // [nlist][L]
   int32_t* trace;         // [nq][nprobe][L]
   int32_t* gmin;          // [nq][nprobe][ngroups]
-  uint32_t off_b, off_meta, off_wmin, off_bar, b_bytes;
+  uint32_t off_b, off_meta, off_sd, off_p, off_stage, off_bar, b_bytes;
+  int p_stride;  // ints per P buffer (L rounded up to 4)
+  int bulk;      // L % 4 == 0: the trace leaves through the staged 16-byte stores
 };
 
 struct PairMeta {     // 16 B, read by the epilogue as one broadcast LDS.128
@@ -71,6 +77,14 @@ struct PairMeta {     // 16 B, read by the epilogue as one broadcast LDS.128
 // Slots per group of the group minima (the unit Step 5 selects candidates by): 32 = a warp's
 // slots of a tile (measured against 16: C4 select 0.447 vs 0.478 ms, C3 0.115 vs 0.099).
 constexpr int kG = 32;
+static_assert(kG == 32, "group = the 32 slots (TMEM lanes) of one warp");
+__device__ __forceinline__ int mc_goff(const PairMeta* mt, int jc, int col) { return mt[jc * 16 + col].goff; }
+__device__ __forceinline__ void bulk_g2s_lm(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
 
 // Minimum over each group of kG lanes (32: the warp; 16: each half) of each of 16 columns
 // x[0..15] (x is consumed): a butterfly in which each exchange halves the columns a lane keeps;
@@ -108,7 +122,9 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
   uint8_t* sA = smem;                                         // [S][128 x 128 B]
   uint8_t* sB = smem + a.off_b;                               // [nb][kp][NT x 128 B]
   PairMeta* meta = reinterpret_cast<PairMeta*>(smem + a.off_meta);  // [nb][NT]
-  int* wmin = reinterpret_cast<int*>(smem + a.off_wmin);     // [kEpiWarps][2 kChunk] column minima
+  int* sd = reinterpret_cast<int*>(smem + a.off_sd);         // [nb][NT] d_i of each pair
+  int* sP = reinterpret_cast<int*>(smem + a.off_p);          // [nb][p_stride] P terms of the item's list
+  int* stage = reinterpret_cast<int*>(smem + a.off_stage);   // [kEpiWarps][2][kChunk][kStageRow]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
   uint64_t* afull = bars;                  // [S]
   uint64_t* aempty = afull + a.S;          // [S]
@@ -216,16 +232,24 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
       if (use > 0) tc::mbar_wait_sleep(bempty + b, (use - 1) & 1);
       uint8_t* dst = sB + b * a.b_bytes;
       PairMeta* mt = meta + b * NT;
+      {  // the P terms of the list's valid slots: one bulk copy completing on the item's barrier
+        const int cnt = __ldg(a.counts + it.x);
+        if (gt == 0 && a.p_stride && cnt > 0) {
+          const uint32_t pbytes = 16u * ((cnt + 3) / 4);
+          tc::mbar_expect_tx_only(bfull + b, pbytes);
+          bulk_g2s_lm(sP + b * a.p_stride, a.pterm + static_cast<int64_t>(it.x) * L, pbytes, bfull + b);
+        }
+      }
+      // per pair: metadata, d_i, and the query row (cp.async into the swizzled B operand)
       for (int r = gt; r < it.z; r += 32 * kNGat) {
         const int pr = __ldg(a.pairs + it.y + r);
-        mt[r] = PairMeta{reinterpret_cast<uint64_t>(a.trace + static_cast<int64_t>(pr) * L), __ldg(a.ldist + pr),
-                         pr * a.ngroups};
-      }
-      for (int e = gt; e < it.z * cpr; e += 32 * kNGat) {
-        const int r = e / cpr, c = e - r * cpr;
-        const int q = __ldg(a.pairs + it.y + r) / a.nprobe;
-        uint8_t* d = dst + (c >> 3) * NT * kPanel + tc::sw128_offset(r, c & 7);
-        tc::cp_async16(d, a.queries + static_cast<int64_t>(q) * a.dim + c * 16, 16);
+        const int dl = __ldg(a.ldist + pr);
+        const int q = pr / a.nprobe;
+        mt[r] = PairMeta{reinterpret_cast<uint64_t>(a.trace + static_cast<int64_t>(pr) * L), dl, pr * a.ngroups};
+        sd[b * NT + r] = dl;
+        const int8_t* qrow = a.queries + static_cast<int64_t>(q) * a.dim;
+        for (int c = 0; c < cpr; ++c)
+          tc::cp_async16(dst + (c >> 3) * NT * kPanel + tc::sw128_offset(r, c & 7), qrow + c * 16, 16);
       }
       tc::cp_async_commit();
       tc::cp_async_wait<0>();
@@ -241,10 +265,14 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     // ------------------------------------------------------------ epilogue
     // Two groups of 8 warps take alternate tiles (two tiles drain at once).  Within a group, warp:
     // TMEM lane quadrant qd (its 32 slots of the tile) and column group cg (chunks of 16 columns
-    // cg, cg + 2, ...).  Thread = one slot; per column (pair): D to the trace (the 32 lanes store
-    // 128 consecutive bytes) and the group minimum over the 32 lanes (REDUX).
+    // cg, cg + 2, ...).  Thread = one slot; per column (pair) D = d_i + P - 2 acc (padding slots
+    // d_max).  Staged path (L % 4 == 0): the warp writes its 32 x 16 block of D to shared memory,
+    // two lanes per column take the 32-slot group minimum from there and eight lanes per column
+    // store the column's 128 trace bytes with 16-byte stores.  Otherwise the lanes store the trace
+    // directly and the minimum is a lane butterfly.
     const int e = warp - kWarpEpi, qd = warp & 3, grp = e >> 3, cg = (e >> 2) & 1;
     constexpr int NCG = 2;
+    int* stg = stage + e * (kChunk * kStageRow);
     int b = 0, bph = 0, tcount = 0, tall = 0;
     for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
       const int4 it = a.items[j];
@@ -252,7 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
       const int cnt = __ldg(a.counts + it.x);
       const int nvt = (cnt + kTile - 1) / kTile, ntl = (L + kTile - 1) / kTile;
       const PairMeta* mt = meta + b * NT;
-      const int32_t* prow = a.pterm + static_cast<int64_t>(it.x) * L;
+      const int* dcol = sd + b * NT;
+      const int* pP = sP + b * a.p_stride;
       tc::mbar_wait_sleep(bfull + b, bph);
       for (int t = 0; t < ntl; ++t, ++tall) {
         const bool mine = (tall & 1) == grp;
@@ -263,66 +292,90 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
           ++tcount;
           if (!mine) continue;
           const bool valid = slot < cnt;
-          const int32_t P = valid ? __ldg(prow + slot) : 0;   // issued before the wait
+          const int32_t P = !valid ? 0 : a.p_stride ? pP[slot] : __ldg(a.pterm + static_cast<int64_t>(it.x) * L + slot);
           const bool full = sbase + 32 <= cnt;                // warp-uniform: every slot valid (< L)
+          const int nsl = min(32, L - sbase);                 // slots of this group inside the row
           tc::mbar_wait_sleep(accf + acc, ua & 1);
           tc::fence_after_sync();
-          // one chunk of 16 columns: D to the trace, the 32-slot group minimum of every column
-          // one chunk of 16 columns: D to the trace, then the 32-slot group minimum of every column
-          // by a butterfly over the lanes (lane l ends with column colmin_col(l)); stored by the
-          // even lanes
-          auto chunk = [&](const uint32_t(&v)[kChunk], int jc) {
-            const PairMeta* mc = mt + jc * kChunk;
-            const int ncol = min(kChunk, np - jc * kChunk);
-            int x[kChunk];
+          // D of one chunk of 16 columns into x[] (d_max for padding slots and absent columns)
+          auto dvals = [&](const uint32_t(&v)[kChunk], int jc, int (&x)[kChunk], int ncol) {
+            const int4* d4 = reinterpret_cast<const int4*>(dcol + jc * kChunk);
+            int dv[kChunk];
+#pragma unroll
+            for (int c4 = 0; c4 < kChunk / 4; ++c4) {
+              const int4 w = d4[c4];
+              dv[4 * c4] = w.x, dv[4 * c4 + 1] = w.y, dv[4 * c4 + 2] = w.z, dv[4 * c4 + 3] = w.w;
+            }
             if (full && ncol == kChunk) {
 #pragma unroll
-              for (int c = 0; c < kChunk; ++c) {
-                const PairMeta m = mc[c];
-                x[c] = m.d + P - 2 * static_cast<int32_t>(v[c]);
-#if !defined(LM_EXP) || LM_EXP != 1  // experiment 1: no trace stores
-                __stcs(reinterpret_cast<int32_t*>(m.row + toff), x[c]);
-#endif
-              }
+              for (int c = 0; c < kChunk; ++c) x[c] = dv[c] + P - 2 * static_cast<int32_t>(v[c]);
             } else {
 #pragma unroll
-              for (int c = 0; c < kChunk; ++c) {
-                x[c] = kDMax;
-                if (c < ncol) {  // warp-uniform
-                  const PairMeta m = mc[c];
-                  if (valid) x[c] = m.d + P - 2 * static_cast<int32_t>(v[c]);
-                  if (slot < L) __stcs(reinterpret_cast<int32_t*>(m.row + toff), x[c]);
+              for (int c = 0; c < kChunk; ++c)
+                x[c] = valid && c < ncol ? dv[c] + P - 2 * static_cast<int32_t>(v[c]) : kDMax;
+            }
+          };
+          // staged path: the 32 x 16 block of D through shared memory -- two lanes per column take
+          // the 32-slot group minimum, eight lanes per column store its 128 trace bytes (16 B each)
+          auto chunk_stage = [&](const uint32_t(&v)[kChunk], int jc) {
+            const int ncol = min(kChunk, np - jc * kChunk);
+            int x[kChunk];
+            dvals(v, jc, x, ncol);
+            __syncwarp();  // the previous chunk's reads of the stage are done
+#pragma unroll
+            for (int c = 0; c < kChunk; ++c) stg[c * kStageRow + lane] = x[c];
+            __syncwarp();
+            const int col = lane >> 1;
+            const int4* r4 = reinterpret_cast<const int4*>(stg + col * kStageRow + (lane & 1) * 16);
+            int m = kDMax;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int4 w = r4[u];
+              m = min(m, min(min(w.x, w.y), min(w.z, w.w)));
+            }
+            m = min(m, __shfl_xor_sync(kFull, m, 1));
+            if (!(lane & 1) && col < ncol) a.gmin[mc_goff(mt, jc, col) + t * 4 + qd] = m;
+            const int pp = lane & 7;
+            if (4 * pp < nsl) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int c = (lane >> 3) + 4 * i;
+                if (c < ncol) {
+                  const int4 w = *reinterpret_cast<const int4*>(stg + c * kStageRow + 4 * pp);
+                  __stcs(reinterpret_cast<int4*>(mt[jc * kChunk + c].row + 4ull * static_cast<uint32_t>(sbase + 4 * pp)), w);
                 }
               }
             }
-#if defined(LM_EXP) && LM_EXP == 2  // experiment: no group minima
-            if (x[0] == 0x12345678 && lane == 99) a.gmin[0] = x[1];
-#else
-            // lane l holds the minimum of column colmin_col(l) over its group of kG slots
+          };
+          // direct path: lanes store the trace, butterfly minima
+          auto chunk_direct = [&](const uint32_t(&v)[kChunk], int jc) {
+            const PairMeta* mc = mt + jc * kChunk;
+            const int ncol = min(kChunk, np - jc * kChunk);
+            int x[kChunk];
+            dvals(v, jc, x, ncol);
+#pragma unroll
+            for (int c = 0; c < kChunk; ++c)
+              if (c < ncol && slot < L) __stcs(reinterpret_cast<int32_t*>(mc[c].row + toff), x[c]);
             const int gm = colmin16(x, lane), col = colmin_col(lane);
-            if constexpr (kG == 32) {
-              // a group without a valid slot (inside L): the sentinel d_max (Step 5 skips it)
-              if (sbase < L && !(lane & 1) && col < ncol) a.gmin[mc[col].goff + t * 4 + qd] = sbase < cnt ? gm : kDMax;
-            } else {
-              if (sbase + (lane & 16) < cnt && col < ncol) a.gmin[mc[col].goff + t * 8 + qd * 2 + (lane >> 4)] = gm;
-            }
-#endif
+            if (!(lane & 1) && col < ncol) a.gmin[mc[col].goff + t * 4 + qd] = gm;
           };
           // two chunks per round: both TMEM loads in flight before the first is used
           const uint32_t tbase = tmem + (static_cast<uint32_t>(qd * 32) << 16) + acc * NT;
-          for (int jc = cg; jc * kChunk < np; jc += 2 * NCG) {
+          // (a warp whose 32 slots lie past the row end -- L not a multiple of 128 -- has nothing)
+          for (int jc = cg; sbase < L && jc * kChunk < np; jc += 2 * NCG) {
             const int jd = jc + NCG;
             const bool two = jd * kChunk < np;  // warp-uniform
             uint32_t v0[kChunk], v1[kChunk];
             tc::tmem_ld16(tbase + jc * kChunk, v0);
             if (two) tc::tmem_ld16(tbase + jd * kChunk, v1);
             tc::tmem_ld_wait();
-#if defined(LM_EXP) && LM_EXP == 3  // experiment 3: drain the accumulators only
-            if (v0[0] == 0x12345678u && v1[3] == 7u) a.gmin[0] = 1;
-#else
-            chunk(v0, jc);
-            if (two) chunk(v1, jd);
-#endif
+            if (a.bulk) {
+              chunk_stage(v0, jc);
+              if (two) chunk_stage(v1, jd);
+            } else {
+              chunk_direct(v0, jc);
+              if (two) chunk_direct(v1, jd);
+            }
           }
           tc::fence_before_sync();
           __syncwarp();
@@ -331,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
           // a tile of padding only: D = d_max, nothing read
           for (int c = cg; c < np; c += NCG) {
             __stcs(reinterpret_cast<int32_t*>(mt[c].row + toff), kDMax);
-            if (kG == 32 && lane == 0) a.gmin[mt[c].goff + t * 4 + qd] = kDMax;  // group sentinel
+            if (lane == 0) a.gmin[mt[c].goff + t * 4 + qd] = kDMax;  // group sentinel
           }
         }
       }
@@ -1401,22 +1454,36 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   const int64_t npairs = nq * nprobe;
   const int L = s->L, ngroups = (L + kG - 1) / kG, kp = (s->dim + kPanel - 1) / kPanel;
   if (npairs >= (int64_t(1) << 31) || npairs * ngroups >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-  // NT: pairs per item, the largest of 256 / 128 / 64 / 32 whose double-buffered B operand fits 128 KB
-  int NT = 128;
+  // NT: pairs per item, 64 (measured: C4 main kernel 0.968 ms vs 1.009 at 128, C2 0.337 vs 0.357), or
+  // less where three B operands would not fit 128 KB
+  int NT = 64;
   const int64_t nt_opt = opt(V3DB_OPT_LM_NT);
-  if (nt_opt == 32 || nt_opt == 64 || nt_opt == 128 || nt_opt == 256) NT = static_cast<int>(nt_opt);
+  // (256 is taken as 128: with two accumulators a long C4-scale batch stops making progress -- an
+  // unresolved hang, DESIGN.md §10 -- and no shape the library picks uses it)
+  if (nt_opt == 32 || nt_opt == 64 || nt_opt == 128) NT = static_cast<int>(nt_opt);
   int nb = kNB;  // B buffers: 3, or 2 when three of the smallest NT do not fit (dim near 2048)
   while (NT > 32 && static_cast<uint32_t>(nb) * kp * NT * kPanel > 128u * 1024) NT >>= 1;
   if (static_cast<uint32_t>(nb) * kp * NT * kPanel > 128u * 1024) nb = 2;
   const int nacc = std::min(4, 512 / NT);  // a power of two
   const int lg_nacc = nacc == 4 ? 2 : nacc == 2 ? 1 : 0;
   const uint32_t b_bytes = static_cast<uint32_t>(kp) * NT * kPanel;
+  // P terms of the item's list staged per B buffer (when they take <= 48 KB); the trace staged and
+  // stored from a shared-memory stage when L % 4 == 0 and the stage fits beside >= 3 A stages
+  int p_stride = L % 4 == 0 ? L : 0;  // (16-byte aligned rows: one bulk copy per item)
+  if (static_cast<size_t>(nb) * 4 * p_stride > 48 * 1024) p_stride = 0;
+  bool bulk = L % 4 == 0;
   int S = 6;
   auto smem_of = [&](int stages) {
     return 1024 + static_cast<size_t>(stages) * kAStageBytes + nb * b_bytes + nb * sizeof(PairMeta) * NT +
-           8 * kEpiWarps * kChunk + 8 * (2 * stages + 2 * kNB + 2 * nacc) + 16;
+           static_cast<size_t>(nb) * 4 * NT + static_cast<size_t>(nb) * 4 * p_stride + (bulk ? kStageBytes : 0) +
+           8 * (2 * stages + 2 * kNB + 2 * nacc) + 16;
   };
   while (S > 2 && smem_of(S) > 227 * 1024) --S;
+  if (bulk && (S < 3 || smem_of(S) > 227 * 1024)) {
+    bulk = false;
+    S = 6;
+    while (S > 2 && smem_of(S) > 227 * 1024) --S;
+  }
   if (smem_of(S) > 227 * 1024) return cudaErrorInvalidConfiguration;
 
   CUtensorMap tmX;
@@ -1483,8 +1550,12 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   a.lg_nacc = lg_nacc;
   a.nb = nb;
   a.off_meta = a.off_b + nb * b_bytes;  // PairMeta is 16 B: 16-byte aligned (b_bytes is a multiple of 128)
-  a.off_wmin = a.off_meta + nb * sizeof(PairMeta) * NT;
-  a.off_bar = static_cast<uint32_t>(al(a.off_wmin + 8 * kEpiWarps * kChunk, 8));
+  a.off_sd = a.off_meta + nb * sizeof(PairMeta) * NT;
+  a.off_p = a.off_sd + nb * 4 * NT;
+  a.off_stage = a.off_p + nb * 4 * p_stride;
+  a.off_bar = static_cast<uint32_t>(al(a.off_stage + (bulk ? kStageBytes : 0), 8));
+  a.p_stride = p_stride;
+  a.bulk = bulk ? 1 : 0;
   a.b_bytes = b_bytes;
   const size_t smem = smem_of(S);
   e = cudaFuncSetAttribute(lm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -19,7 +19,10 @@ h = next(j for j, r in enumerate(rows) if r and r[0] == "Address")
 hdr = rows[h]
 ie, src = hdr.index("Instructions Executed"), hdr.index("Source")
 st = hdr.index("Warp Stall Sampling (All Samples)")
-vals = [(float(r[ie] or 0), int(r[0], 16), r[src], float(r[st] or 0)) for r in rows[h + 1:] if len(r) > ie]
+vals = []
+for r in rows[h + 1:]:
+    if len(r) > ie and r[0].startswith("0x"):
+        vals.append((float(r[ie] or 0), int(r[0], 16), r[src], float(r[st] or 0)))
 base = vals[0][1]
 runs, cur = [], None
 for v, a, s, smp in vals:
