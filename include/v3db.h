@@ -139,7 +139,8 @@ int v3db_query_batch(v3db_snapshot_t s, const int8_t* queries, int64_t nq, int32
 #define V3DB_SCAN_GENERIC 1    /* per-query LUT [M][Ks] in shared memory, any shape               */
 #define V3DB_SCAN_ROTATED 2    /* conflict-free rotated LUT (M % 4 == 0, d % 4 == 0, M <= 128)    */
 #define V3DB_SCAN_LIST_MAJOR 3 /* Steps 3-4 as the exact identity d_i + P_ij - 2 <q, xhat_ij>:   */
-                               /* tcgen05 int8 tiles per (list, probing queries) (dim % 16 == 0) */
+                               /* tcgen05 int8 tiles per (list, probing queries)                 */
+                               /* (dim % 16 == 0, nlist <= 32768)                                */
 
 /* v3db_query_batch_ex -- v3db_query_batch with an explicit scan kernel (`algo`, one of
  * V3DB_SCAN_*).  EINVAL for an unknown algo, or a kernel the snapshot's shape does not

@@ -609,7 +609,8 @@ constexpr int kRecCap = 32;  // recomputed blocks per row
 __device__ __forceinline__ uint64_t merge_key(int e, int i) {
   return (static_cast<uint64_t>(static_cast<uint32_t>(e + (1 << 30))) << 32) | static_cast<uint32_t>(i);
 }
-template <int KR>
+// NV: int4 (two blocks' keys) per lane held in registers (nblk / 2 <= 32 NV).
+template <int KR, int NV>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* __restrict__ X, int64_t n, int dim,
                                                                 const int8_t* __restrict__ mu,
                                                                 const int32_t* __restrict__ cnorm, int nlist,
@@ -624,22 +625,32 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
   const int64_t row = static_cast<int64_t>(blockIdx.x) * kMergeWarps + warp;
   int* wh = reinterpret_cast<int*>(msm) + warp * 256;                              // [256] histogram
   int* rb = reinterpret_cast<int*>(msm) + kMergeWarps * 256 + warp * kRecCap;      // recomputed blocks
-  uint64_t* keys = reinterpret_cast<uint64_t*>(msm + 4 * kMergeWarps * (256 + kRecCap)) + warp * cap;
+  int4* xs = reinterpret_cast<int4*>(msm + 4 * kMergeWarps * (256 + kRecCap)) + warp * (dim >> 4);  // the row
+  // per warp: cap keys, then cap 16-bit bin-order indices (cap / 4 key slots)
+  uint64_t* keys = reinterpret_cast<uint64_t*>(msm + 4 * kMergeWarps * (256 + kRecCap) + kMergeWarps * dim) +
+                   warp * (cap + cap / 4);
   if (row >= n) return;
   const int8_t* x = X + row * dim;
+  const int nv4 = nblk >> 1;  // one int4 = (min, second min) of two blocks
+  const int4* src = reinterpret_cast<const int4*>(bk + row * nblk * 2);
+  int4 v[NV];
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    const int i = 32 * u + lane;
+    v[u] = i < nv4 ? __ldg(src + i) : make_int4(kInf, kInf, kInf, kInf);
+  }
   int xn = 0;
-  for (int u = lane; u < (dim >> 2); u += 32) {
-    const int v = __ldg(reinterpret_cast<const int*>(x) + u);
-    xn = __dp4a(v, v, xn);
+  for (int u = lane; u < (dim >> 4); u += 32) {
+    const int4 w = __ldg(reinterpret_cast<const int4*>(x) + u);
+    xs[u] = w;
+    xn = __dp4a(w.x, w.x, __dp4a(w.y, w.y, __dp4a(w.z, w.z, __dp4a(w.w, w.w, xn))));
   }
   xn = __reduce_add_sync(kFull, xn);
-  const int4* src = reinterpret_cast<const int4*>(bk + row * nblk * 2);
-  const int nv4 = nblk >> 1;  // one int4 = (min, second min) of two blocks
   const unsigned lt = (1u << lane) - 1u;
   int mn = kInf, mx = -kInf, cntv = 0;
-  for (int i = lane; i < nv4; i += 32) {
-    const int4 v = __ldg(src + i);
-    const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    const int w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
     for (int t = 0; t < 4; ++t)
       if (w[t] != kInf) {
@@ -658,11 +669,12 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
     for (;;) {
       const int bits = 32 - __clz((span - 1u) | 1u);
       const int sh = bits > 8 ? bits - 8 : 0;
-      for (int b = lane; b < 256; b += 32) wh[b] = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) wh[lane * 8 + b] = 0;
       __syncwarp();
-      for (int i = lane; i < nv4; i += 32) {
-        const int4 v = __ldg(src + i);
-        const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < NV; ++u) {
+        const int w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const uint32_t rel = static_cast<uint32_t>((w[t] >> 5) - lo);
@@ -679,8 +691,8 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
       int incl = sum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
       }
       int cum = incl - sum, bin = -1, newk = 0, cb = 0;
       if (cum < kk && kk <= incl) {
@@ -709,12 +721,12 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
   }
   // candidates: stored keys with e <= tau of the blocks kept; the blocks to recompute
   int nc = 0, nr = 0;
-  for (int i0 = 0; i0 < nv4; i0 += 32) {
-    const int i = i0 + lane;
-    const int4 v = i < nv4 ? __ldg(src + i) : make_int4(kInf, kInf, kInf, kInf);
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    const int i = 32 * u + lane;
 #pragma unroll
     for (int hb = 0; hb < 2; ++hb) {
-      const int m1 = hb ? v.z : v.x, m2 = hb ? v.w : v.y, b = 2 * i + hb;
+      const int m1 = hb ? v[u].z : v[u].x, m2 = hb ? v[u].w : v[u].y, b = 2 * i + hb;
       const bool rec = m2 != kInf && (m2 >> 5) <= tau;
       unsigned bal = __ballot_sync(kFull, rec);
       int pos = nr + __popc(bal & lt);
@@ -734,34 +746,98 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
   __syncwarp();
   bool over = nr > kRecCap;
   if (!over) {
-    const int4* x4 = reinterpret_cast<const int4*>(x);
-    for (int t = 0; t < nr; ++t) {
-      const int li = rb[t] * 32 + lane;
-      bool take = false;
-      int e = 0;
-      if (li < nlist) {
-        const int4* m4 = reinterpret_cast<const int4*>(mu + static_cast<int64_t>(li) * dim);
-        int dot = 0;
-        for (int u = 0; u < (dim >> 4); ++u) {
-          const int4 p = __ldg(x4 + u), q = __ldg(m4 + u);
-          dot = __dp4a(p.x, q.x, __dp4a(p.y, q.y, __dp4a(p.z, q.z, __dp4a(p.w, q.w, dot))));
-        }
-        e = __ldg(cnorm + li) - 2 * dot;
-        take = e <= tau;
+    // lane = list of the block; two blocks per step, 8 independent 16-byte loads each in flight
+    const int nu = dim >> 4;
+    for (int t = 0; t < nr; t += 2) {
+      int li[2], dot[2] = {0, 0};
+      const int4* m4[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        li[h] = t + h < nr ? rb[t + h] * 32 + lane : nlist;
+        m4[h] = reinterpret_cast<const int4*>(mu + static_cast<int64_t>(min(li[h], nlist - 1)) * dim);
       }
-      const unsigned bal = __ballot_sync(kFull, take);
-      const int pos = nc + __popc(bal & lt);
-      if (take && pos < cap) keys[pos] = merge_key(e, li);
-      nc += __popc(bal);
+      for (int u0 = 0; u0 < nu; u0 += 8) {
+        int4 q[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int w = 0; w < 8; ++w)
+            q[h][w] = li[h] < nlist && u0 + w < nu ? __ldg(m4[h] + u0 + w) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          if (u0 + w < nu) {
+            const int4 p = xs[u0 + w];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              dot[h] = __dp4a(p.x, q[h][w].x, __dp4a(p.y, q[h][w].y, __dp4a(p.z, q[h][w].z, __dp4a(p.w, q[h][w].w, dot[h]))));
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = li[h] < nlist ? __ldg(cnorm + li[h]) - 2 * dot[h] : 0;
+        const bool take = li[h] < nlist && e <= tau;
+        const unsigned bal = __ballot_sync(kFull, take);
+        const int pos = nc + __popc(bal & lt);
+        if (take && pos < cap) keys[pos] = merge_key(e, li[h]);
+        nc += __popc(bal);
+      }
     }
   }
   over = over || nc > cap;
   __syncwarp();
   if (!over) {
+    // counting sort of the nc keys by e over 256 bins of [lo, hi], then the rank inside each bin
+    // (ordered (e, i) keys: R9); ord (the recomputed-block list is dead) holds the bin order
+    int elo = kInf, ehi = -kInf;
     for (int j = lane; j < nc; j += 32) {
-      const uint64_t kj = keys[j];
-      int rank = 0;
-      for (int f = 0; f < nc; ++f) rank += keys[f] < kj ? 1 : 0;
+      const int ej = static_cast<int>(keys[j] >> 32) - (1 << 30);
+      elo = min(elo, ej);
+      ehi = max(ehi, ej);
+    }
+    elo = __reduce_min_sync(kFull, elo);
+    ehi = __reduce_max_sync(kFull, ehi);
+    const uint32_t espan = static_cast<uint32_t>(ehi - elo);
+    const int bits = 32 - __clz(espan | 1u), sh = bits > 8 ? bits - 8 : 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) wh[lane * 8 + b] = 0;
+    __syncwarp();
+    for (int j = lane; j < nc; j += 32)
+      atomicAdd(&wh[static_cast<uint32_t>(static_cast<int>(keys[j] >> 32) - (1 << 30) - elo) >> sh], 1);
+    __syncwarp();
+    {
+      int hb[8], sum = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        hb[b] = wh[lane * 8 + b];
+        sum += hb[b];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        wh[lane * 8 + b] = run;  // exclusive start; advanced to the bin's end by the scatter
+        run += hb[b];
+      }
+    }
+    __syncwarp();
+    uint16_t* ord = reinterpret_cast<uint16_t*>(keys + cap);
+    for (int j = lane; j < nc; j += 32) {
+      const int b = static_cast<uint32_t>(static_cast<int>(keys[j] >> 32) - (1 << 30) - elo) >> sh;
+      ord[atomicAdd(&wh[b], 1)] = static_cast<uint16_t>(j);
+    }
+    __syncwarp();
+    for (int p = lane; p < nc; p += 32) {
+      const uint64_t kj = keys[ord[p]];
+      const int b = static_cast<uint32_t>(static_cast<int>(kj >> 32) - (1 << 30) - elo) >> sh;
+      const int s0 = b ? wh[b - 1] : 0, s1 = wh[b];
+      int rank = s0;
+      for (int f = s0; f < s1; ++f) rank += keys[ord[f]] < kj ? 1 : 0;
       if (rank < R) {
         const int li = static_cast<int>(static_cast<uint32_t>(kj));
         out_idx[row * R + rank] = li;
@@ -864,7 +940,7 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   const int64_t copt = opt(V3DB_OPT_COARSE_2PASS);
   // default: one contraction pass keeping each 32-list block's two smallest keys, then merge_kernel
   // (2 launches); the group-minimum paths remain as options (1, 4 / 8 / 16 / 32) and for dim > 1024
-  const bool top2 = copt == 0 && dim <= 1024 && R <= 1024;
+  const bool top2 = copt == 0 && dim <= 1024 && R <= 1024 && nlist <= 32768;  // (merge: <= 16 int4 per lane)
   const bool pick = !top2 && R <= 128 && copt != 1 &&
                     (copt != 0 || static_cast<int64_t>(R) * 8 * dim <= 32768);
   const int gmax = pick ? (copt == 4 || copt == 8 || copt == 16 || copt == 32 ? static_cast<int>(copt) : 8) : 32;
@@ -920,14 +996,23 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
     if (e == cudaSuccess) coarse_tc_kernel<3, 0><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) e = debug_sync(st, "coarse pass (block top-2)");
-    const int cap = 2 * R + 64;
-    const size_t msmem = 4 * kMergeWarps * (256 + kRecCap) + sizeof(uint64_t) * kMergeWarps * cap;
+    const int cap = (2 * R + 64 + 3) & ~3;  // (a multiple of 4: cap / 4 key slots hold the 16-bit bin order)
+    const size_t msmem = 4 * kMergeWarps * (256 + kRecCap) + static_cast<size_t>(kMergeWarps) * dim +
+                         sizeof(uint64_t) * kMergeWarps * (cap + cap / 4);
+    const int nv4 = ngroups / 2;
     if (e == cudaSuccess) {
       dispatch_kr(R, [&]<int KR>() {
-        e = cudaFuncSetAttribute(merge_kernel<KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem));
-        if (e == cudaSuccess)
-          merge_kernel<KR><<<static_cast<unsigned>((n + kMergeWarps - 1) / kMergeWarps), 32 * kMergeWarps, msmem, st>>>(
-              X, n, dim, mu, cnorm, nlist, ngroups, R, cap, a.gmin, out_idx, out_dist, list_hist);
+        auto run = [&](auto kern) {
+          e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem));
+          if (e == cudaSuccess)
+            kern<<<static_cast<unsigned>((n + kMergeWarps - 1) / kMergeWarps), 32 * kMergeWarps, msmem, st>>>(
+                X, n, dim, mu, cnorm, nlist, ngroups, R, cap, a.gmin, out_idx, out_dist, list_hist);
+        };
+        if (nv4 <= 32) run(merge_kernel<KR, 1>);
+        else if (nv4 <= 64) run(merge_kernel<KR, 2>);
+        else if (nv4 <= 128) run(merge_kernel<KR, 4>);
+        else if (nv4 <= 256) run(merge_kernel<KR, 8>);
+        else run(merge_kernel<KR, 16>);
       });
       if (e == cudaSuccess) e = cudaGetLastError();
     }

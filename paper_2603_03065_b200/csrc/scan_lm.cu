@@ -412,45 +412,75 @@ __global__ void pair_hist_kernel(const int32_t* __restrict__ lists, int64_t npai
 
 // One CTA of 1024 threads: cur[i] = exclusive prefix of hist (the list's first pair in list order,
 // advanced by pair_scatter_kernel), the work items (list, first pair, pairs <= NT) of every list in
-// list order, and *n_items.  Each thread owns a contiguous run of lists, read with 16-byte loads.
+// list order, and *n_items.  Each thread owns a contiguous run of up to kScanPer lists (held in
+// registers), read with 16-byte loads; the block prefix is two warp-shuffle scans.
+constexpr int kScanPer = 32;  // lists per thread: nlist <= 32768
 __global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restrict__ hist, int nlist, int NT,
                                                              int* __restrict__ cur, int4* __restrict__ items,
                                                              int* __restrict__ n_items) {
-  __shared__ int part[1024], ipart[1024];
-  const int per = (((nlist + 1023) / 1024) + 3) & ~3, b = threadIdx.x * per, e = min(nlist, b + per);
+  __shared__ int wsum[32], wisum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (((nlist + 1023) / 1024) + 3) & ~3, b = threadIdx.x * per;
+  int h[kScanPer];
   int sum = 0, isum = 0;
-  for (int x = b; x < e; x += 4) {  // 16-byte loads (b is a multiple of 4; hist is 256-byte aligned)
-    int4 v;
-    if (x + 3 < e) {
-      v = *reinterpret_cast<const int4*>(hist + x);
-    } else {
-      v.x = hist[x];
-      v.y = x + 1 < e ? hist[x + 1] : 0;
-      v.z = x + 2 < e ? hist[x + 2] : 0;
-      v.w = x + 3 < e ? hist[x + 3] : 0;
+#pragma unroll
+  for (int x = 0; x < kScanPer; x += 4) {
+    int4 v = make_int4(0, 0, 0, 0);
+    if (x < per && b + x < nlist) {
+      if (b + x + 3 < nlist) {
+        v = *reinterpret_cast<const int4*>(hist + b + x);  // b is a multiple of 4; hist 256-byte aligned
+      } else {
+        v.x = hist[b + x];
+        v.y = b + x + 1 < nlist ? hist[b + x + 1] : 0;
+        v.z = b + x + 2 < nlist ? hist[b + x + 2] : 0;
+      }
     }
-    sum += v.x + v.y + v.z + v.w;
-    isum += (v.x + NT - 1) / NT + (v.y + NT - 1) / NT + (v.z + NT - 1) / NT + (v.w + NT - 1) / NT;
+    h[x] = v.x, h[x + 1] = v.y, h[x + 2] = v.z, h[x + 3] = v.w;
   }
-  part[threadIdx.x] = sum;
-  ipart[threadIdx.x] = isum;
+#pragma unroll
+  for (int x = 0; x < kScanPer; ++x) {
+    sum += h[x];
+    isum += (h[x] + NT - 1) / NT;
+  }
+  int incl = sum, iincl = isum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o), z = __shfl_up_sync(0xffffffffu, iincl, o);
+    if (lane >= o) {
+      incl += y;
+      iincl += z;
+    }
+  }
+  if (lane == 31) {
+    wsum[warp] = incl;
+    wisum[warp] = iincl;
+  }
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
-    const int w = threadIdx.x >= o ? ipart[threadIdx.x - o] : 0;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    ipart[threadIdx.x] += w;
-    __syncthreads();
+  if (warp == 0) {
+    int a0 = wsum[lane], a1 = wisum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, a0, o), z = __shfl_up_sync(0xffffffffu, a1, o);
+      if (lane >= o) {
+        a0 += y;
+        a1 += z;
+      }
+    }
+    wsum[lane] = a0 - wsum[lane];    // exclusive per-warp offsets
+    wisum[lane] = a1 - wisum[lane];
+    if (lane == 31) *n_items = a1;
   }
-  int run = part[threadIdx.x] - sum, irun = ipart[threadIdx.x] - isum;
-  for (int i = b; i < e; ++i) {
-    const int hi = hist[i];
-    cur[i] = run;
-    for (int r = 0; r * NT < hi; ++r) items[irun++] = make_int4(i, run + r * NT, min(NT, hi - r * NT), 0);
-    run += hi;
+  __syncthreads();
+  int run = wsum[warp] + incl - sum, irun = wisum[warp] + iincl - isum;
+#pragma unroll
+  for (int x = 0; x < kScanPer; ++x) {
+    const int i = b + x;
+    if (x < per && i < nlist) {
+      cur[i] = run;
+      for (int r = 0; r * NT < h[x]; ++r) items[irun++] = make_int4(i, run + r * NT, min(NT, h[x] - r * NT), 0);
+      run += h[x];
+    }
   }
-  if (threadIdx.x == 1023) *n_items = ipart[1023];
 }
 
 __global__ void pair_scatter_kernel(const int32_t* __restrict__ lists, int64_t npairs, int* __restrict__ cur,

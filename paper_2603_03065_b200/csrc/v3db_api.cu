@@ -515,8 +515,9 @@ int v3db_build_snapshot_ex(const int8_t* db, int64_t n, int32_t dim, int32_t nli
                                  st));
     V3DB_CUDA(v3db::transpose_codebooks(s->codebooks, m, ks, d, s->cbT, st));
   }
-  // reconstruction of every slot for the list-major tensor-core scan (dim % 16 == 0)
-  if (dim % 16 == 0) {
+  // reconstruction of every slot for the list-major tensor-core scan (dim % 16 == 0, nlist <= 32768:
+  // its one-CTA item scan holds 32 lists per thread)
+  if (dim % 16 == 0 && nlist <= 32768) {
     s->lm_Lp = (L + 127) & ~127;
     V3DB_CUDA(cudaMalloc(&s->xhat, static_cast<size_t>(nlist) * s->lm_Lp * dim));
     V3DB_CUDA(v3db::make_xhat(s->codes, s->counts, s->codebooks, nlist, L, s->lm_Lp, dim, m, ks, s->xhat, st));
@@ -552,7 +553,7 @@ int v3db_query_batch_ex(v3db_snapshot_t s, const int8_t* queries, int64_t nq, in
   if (algo == V3DB_SCAN_ROTATED && s->lut_mode == 0)
     return fail(V3DB_EINVAL, "V3DB_SCAN_ROTATED does not support this snapshot's (M, Ks, d)");
   if (algo == V3DB_SCAN_LIST_MAJOR && !s->xhat)
-    return fail(V3DB_EINVAL, "V3DB_SCAN_LIST_MAJOR needs dim % 16 == 0");
+    return fail(V3DB_EINVAL, "V3DB_SCAN_LIST_MAJOR needs dim % 16 == 0 and nlist <= 32768");
   if (algo == V3DB_SCAN_AUTO) {
     const int64_t pref = v3db::opt(V3DB_OPT_AUTO_SCAN);
     if (pref == V3DB_SCAN_GENERIC || (pref == V3DB_SCAN_ROTATED && s->lut_mode != 0))
