@@ -295,7 +295,10 @@ int64_t v3db_kernel_launches(void);
  *   V3DB_OPT_SELECT_CTA   list-major Step 5: 0 auto (one warp per query when the probed lists
  *                         hold >= 8 k groups of 32 slots, else one CTA per query), 1 always one
  *                         CTA of 256 threads per query, 2 always one warp per query (all exact;
- *                         the streaming CTA path takes the queries they flag) */
+ *                         the streaming CTA path takes the queries they flag)
+ *   V3DB_OPT_FX_COARSE    fixed-point Steps 1-2 / build ranking: 0 auto (tensor cores: three int8
+ *                         limbs per coordinate, where dim % 16 == 0 and dim <= 256), 1 always the
+ *                         FP64-FMA kernel (exact below 2^53) */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2
@@ -310,7 +313,8 @@ int64_t v3db_kernel_launches(void);
 #define V3DB_OPT_AUTO_SCAN 11
 #define V3DB_OPT_COARSE_2PASS 12
 #define V3DB_OPT_SELECT_CTA 13
-#define V3DB_OPT_COUNT 14
+#define V3DB_OPT_FX_COARSE 14
+#define V3DB_OPT_COUNT 15
 int v3db_set_option(int32_t key, int64_t value);
 int64_t v3db_get_option(int32_t key);
 

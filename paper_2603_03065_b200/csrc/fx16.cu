@@ -892,6 +892,7 @@ cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, con
   if (n <= 0) return cudaSuccess;
   const int sh = fx_shift2(dim);
   if (sh < 1 || nlist > (1 << std::min(sh, 30))) return cudaErrorInvalidValue;
+  if (fx_coarse_tc_supported(dim, nlist, R)) return fx_topk_tc(X, n, dim, mu, mnorm, nlist, R, sh, out_idx, out_dist, st);
   if (R <= 128) {
     constexpr int NJ = 8, CW = 16 * NJ;
     const size_t smem = sizeof(uint64_t) * (32 * 65 + 32 * (CW + 1) + 64 * R);

@@ -201,6 +201,11 @@ cudaError_t gather_rows32(const int32_t* db, int dim, const int32_t* rows, int n
                           cudaStream_t st);
 cudaError_t fx_topk(const int32_t* X, int64_t n, int dim, const int32_t* mu, const int64_t* mnorm, int nlist, int R,
                     int32_t* out_idx, int64_t* out_dist, cudaStream_t st);
+// The fixed-point Steps 1-2 on the tensor cores (fx_coarse_tc.cu): three int8 limbs per coordinate,
+// five int32 accumulators, exact int64 keys; where fx_coarse_tc_supported (dim % 16 == 0, dim <= 256).
+bool fx_coarse_tc_supported(int dim, int nlist, int R);
+cudaError_t fx_topk_tc(const int32_t* X, int64_t n, int dim, const int32_t* mu, const int64_t* mnorm, int nlist,
+                       int R, int sh, int32_t* out_idx, int64_t* out_dist, cudaStream_t st);
 cudaError_t fx_build_tail(const int32_t* db, int64_t n, int dim, const int32_t* mu, const int32_t* list_of,
                           const int32_t* flat_pos, int M, int Ks, const int32_t* codeword_rows, int nlist, int L,
                           int32_t* cb, uint8_t* codes, int32_t* ids, int64_t* pterm, cudaStream_t st);

@@ -287,3 +287,39 @@ def test_fx_host_entry(v3db):
     oh2 = v3db.alloc_outputs_fx(s, cfg.Q, cfg.nprobe, cfg.k, trace=False, device="cpu")
     v3db.query_batch_fx_host(s, torch.from_numpy(f.queries), f.v_max, cfg.nprobe, cfg.k, oh2)
     check_query(oh2, ref, keys=("out_ids", "out_dist"))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("name", ["c1", "e2_large", "c4_mini"])
+def test_fx_coarse_paths(v3db, name, mode):
+    """Fixed-point Steps 1-2 (query and the build's B2 ranking): the tensor-core kernel (0, three
+    int8 limbs per coordinate, five int32 accumulators, exact int64 keys) and the FP64-FMA kernel (1)
+    give the oracle's bits."""
+    cfg, f, db, qs, ref_s, ref = fx_case(name)
+    with v3db.option(v3db.OPT_FX_COARSE, mode):
+        s = v3db.build_snapshot_fx(torch.from_numpy(db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows,
+                                   f.codeword_rows)
+        check_snapshot(v3db, s, ref_s)
+        out = v3db.query_batch_fx(s, torch.from_numpy(qs).cuda(), cfg.nprobe, cfg.k)
+        check_query(out, ref)
+
+
+def test_fx_coarse_tc_adversarial(v3db):
+    """Tensor-core fixed-point Steps 1-2 where two keys per block of 32 lists are not enough:
+    (a) every block's centroids drawn around one centre at the +-65535 extremes (a query's nearest
+    lists share one block: exact recomputation; a duplicated centroid: ties on d_i broken by the
+    list index, R9); (b) every centroid identical: every block ties, the brute-force ranking."""
+    rng = np.random.default_rng(25)
+    D, nlist, L = 32, 512, 64
+    centres = rng.choice(np.array([-65535, -40000, 0, 40000, 65535]), size=(16, D))
+    N = nlist * 8
+    db = np.clip(centres[np.arange(N) // (N // 16)] + rng.integers(-300, 301, size=(N, D)), -65535, 65535).astype(np.int32)
+    db[8 * 6] = db[8 * 5]
+    cent = np.arange(0, N, 8)[:nlist]
+    qs = np.clip(centres[rng.integers(0, 16, 30)] + rng.integers(-400, 401, size=(30, D)), -65535, 65535).astype(np.int32)
+    qs = np.vstack([qs, db[8 * 5][None]])
+    code = np.stack([rng.choice(N, 16, replace=False) for _ in range(4)])
+    run_int32_case(v3db, db, qs, nlist, L, 4, 16, 24, 10, cent, code)
+    db2 = np.full((4096, 16), 30000, np.int32)
+    qs2 = np.vstack([np.full((1, 16), 30000, np.int32), (np.arange(16, dtype=np.int32) * 4000)[None]])
+    run_int32_case(v3db, db2, qs2, 2048, 8, 4, 4, 40, 10, np.arange(2048), np.stack([np.arange(4)] * 4))
