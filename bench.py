@@ -158,8 +158,8 @@ def algorithmic_scan_bytes(cfg, lists: np.ndarray, counts: np.ndarray, trace: bo
 
 def resolved_algo(v3db, snap, algo: int, fx: bool) -> str:
     """The scan kernel V3DB_SCAN_AUTO (or the explicit algo) runs for this snapshot."""
-    if fx:
-        return "fx16"
+    if fx:   # the fixed-point list-major scan where the snapshot holds its limb planes
+        return "fx16_lm" if snap.dim % 16 == 0 and snap.dim <= 256 and snap.nlist <= 32768 else "fx16"
     names = {1: "generic", 2: "rotated", 3: "list_major"}
     if algo:
         return names[algo]
@@ -173,19 +173,20 @@ def algo_used_pre(algo: int, snap) -> str:
 def main_kernel_name(algo: str) -> str:
     return {"list_major": "lm_kernel (Steps 3-4 + trace, tcgen05 int8 tiles per list)",
             "rotated": "scan_rot_kernel (Steps 3-5)", "generic": "scan_lut (Steps 3-5)",
-            "fx16": "scan_fx_kernel (Steps 3-5)"}[algo]
+            "fx16": "scan_fx_kernel (Steps 3-5)",
+            "fx16_lm": "lm_fx_kernel (Steps 3-4 + trace, tcgen05 int8-limb tiles per list, int64 D)"}[algo]
 
 
 def roofline_key(name: str, fx: bool, algo: str, trace: bool) -> str:
-    return name + ("_fx16" if fx else "") + ("" if algo in ("list_major", "fx16") else "_" + algo) + \
+    return name + ("_fx16" if fx else "") + ("" if algo in ("list_major", "fx16", "fx16_lm") else "_" + algo) + \
         ("" if trace else "_traceoff")
 
 
 def l2_label(cfg, algo: str, codes_mb: float) -> str:
     """What the 256 MiB write between timed steps leaves for the next step to fetch from HBM."""
     lm_mb = cfg.nlist * (-(-cfg.L // 128) * 128) * cfg.D / 1e6   # the list-major kernel's xhat
-    data_mb = lm_mb if algo == "list_major" else codes_mb
-    what = "xhat" if algo == "list_major" else "codes"
+    data_mb = lm_mb if algo == "list_major" else 3 * lm_mb if algo == "fx16_lm" else codes_mb
+    what = {"list_major": "xhat", "fx16_lm": "xhat limb planes"}.get(algo, "codes")
     if data_mb > 126:
         return f"flushed between timed steps (256 MiB write); the snapshot's {what} ({data_mb:.0f} MB) exceed L2"
     return (f"flushed between timed steps (256 MiB write); the snapshot's {what} ({data_mb:.0f} MB) fit in L2, "
@@ -426,7 +427,7 @@ def main():
     # dominant kernel: the scan's main kernel (list-major: Steps 3-4 + trace; query-major: Steps
     # 3-5).  Its algorithmic bytes: SURVEY.md §8(d) per query (no credit for cross-query reuse),
     # less the top-k output the list-major selection kernel writes.
-    main_bytes = ab["valid"] - (ab["topk_out"] if algo_used == "list_major" else 0)
+    main_bytes = ab["valid"] - (ab["topk_out"] if algo_used in ("list_major", "fx16_lm") else 0)
     achieved = main_bytes / (main_ms / 1e3) / 1e9
     codes_mb = cfg.nlist * cfg.L * cfg.M / 1e6
 
@@ -452,7 +453,7 @@ def main():
                                    "cross-query reuse" + (
                                        "; the list-major kernel reads each probed list ONCE per batch for all "
                                        "its queries (DRAM traffic = `traffic`), so frac > 1 is that reuse, "
-                                       "see dram_roofline" if algo_used == "list_major" else "")},
+                                       "see dram_roofline" if algo_used in ("list_major", "fx16_lm") else "")},
         "gpu_launches": int(launches),
     }
     if rot is not None:

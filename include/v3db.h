@@ -282,7 +282,7 @@ int64_t v3db_kernel_launches(void);
  *   V3DB_OPT_FX_NOROT     1: no rotated fixed-point code copy (read at fx16 build)
  *   V3DB_OPT_FX_W12       fx16 scan warps per CTA (0 = auto)
  *   V3DB_OPT_SCAN_SEG / _NS / _CAP / _FIRST / _DIRECT   rotated-LUT scan geometry (0 = auto)
- *   V3DB_OPT_LM_NT        list-major scan: (query, rank) pairs per work item, 32/64/128 (256: 128)
+ *   V3DB_OPT_LM_NT        list-major scan: (query, rank) pairs per work item, 32/64/128/256
  *                         (0 = auto: the largest whose B operand fits)
  *   V3DB_OPT_AUTO_SCAN    the kernel V3DB_SCAN_AUTO picks where several apply (0 = list-major,
  *                         else one of the V3DB_SCAN_* values)
@@ -298,7 +298,10 @@ int64_t v3db_kernel_launches(void);
  *                         the streaming CTA path takes the queries they flag)
  *   V3DB_OPT_FX_COARSE    fixed-point Steps 1-2 / build ranking: 0 auto (tensor cores: three int8
  *                         limbs per coordinate, where dim % 16 == 0 and dim <= 256), 1 always the
- *                         FP64-FMA kernel (exact below 2^53) */
+ *                         FP64-FMA kernel (exact below 2^53)
+ *   V3DB_OPT_FX_SCAN      fixed-point Steps 3-5: 0 auto (list-major on the tensor cores, int8 limbs,
+ *                         where the snapshot holds the limb planes: dim % 16 == 0, dim <= 256,
+ *                         nlist <= 32768), 1 always the literal per-query int64 LUT scan */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2
@@ -314,7 +317,8 @@ int64_t v3db_kernel_launches(void);
 #define V3DB_OPT_COARSE_2PASS 12
 #define V3DB_OPT_SELECT_CTA 13
 #define V3DB_OPT_FX_COARSE 14
-#define V3DB_OPT_COUNT 15
+#define V3DB_OPT_FX_SCAN 15
+#define V3DB_OPT_COUNT 16
 int v3db_set_option(int32_t key, int64_t value);
 int64_t v3db_get_option(int32_t key);
 

@@ -183,6 +183,31 @@ __global__ void xhat_kernel(const uint8_t* __restrict__ codes, const int32_t* __
   }
 }
 
+// Fixed point: xl[l][i][jp][u] = limb l of C_{m, code_{i,jp,m}}[u - m d] (balanced base-256 digits,
+// v = v_0 + 256 v_1 + 65536 v_2) for valid slots, 0 for padding slots and jp >= L.
+__global__ void xhat_fx_kernel(const uint8_t* __restrict__ codes, const int32_t* __restrict__ counts,
+                               const int32_t* __restrict__ cb, int nlist, int L, int Lp, int dim, int M, int Ks,
+                               int8_t* __restrict__ out) {
+  const int d = dim / M;
+  const int64_t plane = static_cast<int64_t>(nlist) * Lp * dim;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < plane;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t sp = e / dim;
+    const int u = static_cast<int>(e - sp * dim);
+    const int i = static_cast<int>(sp / Lp), jp = static_cast<int>(sp - static_cast<int64_t>(i) * Lp);
+    int v = 0;
+    if (jp < __ldg(counts + i)) {
+      const int m = u / d;
+      v = __ldg(cb + (static_cast<int64_t>(m) * Ks + codes[(static_cast<int64_t>(i) * L + jp) * M + m]) * d + (u - m * d));
+    }
+    const int d0 = ((v + 128) & 255) - 128, w = (v - d0) >> 8;
+    const int d1 = ((w + 128) & 255) - 128, d2 = (w - d1) >> 8;
+    out[e] = static_cast<int8_t>(d0);
+    out[plane + e] = static_cast<int8_t>(d1);
+    out[2 * plane + e] = static_cast<int8_t>(d2);
+  }
+}
+
 __global__ void transpose_cb_kernel(const int8_t* __restrict__ cb, int M, int Ks, int d, int8_t* __restrict__ cbT) {
   const int total = M * Ks * d;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -254,6 +279,15 @@ cudaError_t make_xhat(const uint8_t* codes, const int32_t* counts, const int8_t*
   const int64_t total = static_cast<int64_t>(nlist) * Lp * (dim / 16);
   const int blocks = static_cast<int>((total + 255) / 256 < 32768 ? (total + 255) / 256 : 32768);
   xhat_kernel<<<blocks, 256, 0, st>>>(codes, counts, cb, nlist, L, Lp, dim, M, Ks, xhat);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t make_xhat_fx(const uint8_t* codes, const int32_t* counts, const int32_t* cb, int nlist, int L, int Lp,
+                         int dim, int M, int Ks, int8_t* xl, cudaStream_t st) {
+  const int64_t plane = static_cast<int64_t>(nlist) * Lp * dim;
+  const int blocks = static_cast<int>((plane + 255) / 256 < 32768 ? (plane + 255) / 256 : 32768);
+  xhat_fx_kernel<<<blocks, 256, 0, st>>>(codes, counts, cb, nlist, L, Lp, dim, M, Ks, xl);
   note_launch();
   return cudaGetLastError();
 }

@@ -288,9 +288,14 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
         const int sbase = t * kTile + qd * 32, slot = sbase + lane;
         const uint64_t toff = 4ull * static_cast<uint32_t>(slot);
         if (t < nvt) {
+          // a valid tile goes to group (tile count) mod 2 and accumulator (tile count) mod nacc, nacc
+          // even: each group owns its accumulators and waits on every phase of their barriers (a
+          // group that skipped a phase would misread the parity -- assigning by the running count of
+          // all tiles, padding-only ones included, did that)
           const int acc = tcount & (a.nacc - 1), ua = tcount >> a.lg_nacc;
+          const bool own = (tcount & 1) == grp;
           ++tcount;
-          if (!mine) continue;
+          if (!own) continue;
           const bool valid = slot < cnt;
           const int32_t P = !valid ? 0 : a.p_stride ? pP[slot] : __ldg(a.pterm + static_cast<int64_t>(it.x) * L + slot);
           const bool full = sbase + 32 <= cnt;                // warp-uniform: every slot valid (< L)
@@ -1473,6 +1478,321 @@ cudaError_t launch_select(const SelArgs<T>& sa, int64_t nq, int* flags, cudaStre
 
 size_t al(size_t x, size_t b) { return (x + b - 1) / b * b; }
 
+// ----------------------------------------------------------------------------------------------
+// NEXT-1 list-major (fixed point): the same identity in int64,
+//     D_{i,j} = d_i + P_{i,j} - 2 <q, xhat_{i,j}>,
+// with <q, xhat> = sum_{s,t} 256^(s+t) <xhat_s, q_t> over three balanced int8 limbs per coordinate
+// (v = v_0 + 256 v_1 + 65536 v_2, fx_coarse_tc.cu): nine tcgen05 kind::i8 products into five exact
+// int32 accumulators per (128 slots x NTF pairs) tile (|acc_u| <= 3 * 128^2 * dim < 2^31), combined
+// in int64 by the epilogue.  Same warp roles and grouping as lm_kernel; D and the group minima are
+// int64; Step 5 is the int64 instantiation of the same selection kernels.
+// ----------------------------------------------------------------------------------------------
+constexpr int kNTF = 32;          // pairs per item: 2 sets x 5 accumulators x 32 columns = 320 TMEM columns
+constexpr int kFSetsLm = 2;      // accumulator sets = epilogue groups (one each)
+constexpr int kFStageRow = 68;    // words per staged column (32 int64 + 4 words pad)
+constexpr int kFSub = 8;          // columns per epilogue sub-chunk
+constexpr int64_t kDMaxFxLm = 0x7fffffffffffffffLL;
+
+struct LmFxArgs {
+  int nprobe, L, Lp, dim, kp, S, nb, ngroups, p_stride;
+  int64_t rows_x;            // rows per xhat limb plane (nlist * Lp)
+  int64_t rows_q;            // rows per query limb plane (nq)
+  const int8_t* ql;          // [3][nq][dim] query limbs
+  const int32_t* pairs;
+  const int4* items;
+  const int* n_items;
+  const int64_t* ldist;      // [nq * nprobe] d_i of each pair
+  const int32_t* counts;
+  const int64_t* pterm;      // [nlist][L]
+  int64_t* trace;            // [nq][nprobe][L]
+  int64_t* gmin;             // [nq][nprobe][ngroups]
+  uint32_t off_b, off_meta, off_p, off_stage, off_bar, b_bytes;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constant__ CUtensorMap tmX, const LmFxArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;                                                      // [S][128 x 128 B] (one limb each)
+  uint8_t* sB = smem + a.off_b;                                            // [nb][3 limbs][kp][NTF x 128 B]
+  uint64_t* mrow = reinterpret_cast<uint64_t*>(smem + a.off_meta);         // [nb][NTF] trace row address
+  int64_t* md = reinterpret_cast<int64_t*>(mrow + a.nb * kNTF);            // [nb][NTF] d_i
+  int* mgoff = reinterpret_cast<int*>(md + a.nb * kNTF);                   // [nb][NTF] group-minimum row
+  int64_t* sP = reinterpret_cast<int64_t*>(smem + a.off_p);                // [nb][p_stride] P terms
+  int64_t* stage = reinterpret_cast<int64_t*>(smem + a.off_stage);         // [kEpiWarps][kFSub][34]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  uint64_t* afull = bars;                  // [S]
+  uint64_t* aempty = afull + a.S;          // [S]
+  uint64_t* bfull = aempty + a.S;          // [kNB]
+  uint64_t* bempty = bfull + kNB;          // [kNB]
+  uint64_t* accf = bempty + kNB;           // [kFSetsLm]
+  uint64_t* acce = accf + kFSetsLm;        // [kFSetsLm]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + kFSetsLm);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_items = *a.n_items;
+  const int L = a.L;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.S; ++s) {
+      tc::mbar_init(afull + s, 1);
+      tc::mbar_init(aempty + s, 1);
+    }
+    for (int b = 0; b < kNB; ++b) {
+      tc::mbar_init(bfull + b, kNGat);
+      tc::mbar_init(bempty + b, 1 + kEpiWarps);
+    }
+    for (int c = 0; c < kFSetsLm; ++c) {
+      tc::mbar_init(accf + c, 1);
+      tc::mbar_init(acce + c, kEpiWarps / 2);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == kWarpMma) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kWarpTma) {
+    // ------------------------------------------------------------ xhat limb tiles (TMA)
+    if (lane == 0) {
+      tc::tma_prefetch(&tmX);
+      int s = 0, u = 0;
+      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
+        const int4 it = a.items[j];
+        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+        for (int t = 0; t < nvt; ++t)
+          for (int p = 0; p < a.kp; ++p)
+            for (int l = 0; l < 3; ++l) {
+              if (u > 0) tc::mbar_wait_sleep(aempty + s, (u - 1) & 1);
+              tc::mbar_expect_tx(afull + s, kAStageBytes);
+              tc::tma_load_2d(sA + s * kAStageBytes, &tmX, afull + s, p * kPanel,
+                              static_cast<int>(l * a.rows_x + static_cast<int64_t>(it.x) * a.Lp + t * kTile));
+              if (++s == a.S) {
+                s = 0;
+                ++u;
+              }
+            }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int s = 0, u = 0, b = 0, bph = 0, tcount = 0;
+      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
+        const int4 it = a.items[j];
+        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+        const int N = (it.z + 15) & ~15;
+        const uint32_t idesc = tc::idesc_s8(kTile, N);
+        tc::mbar_wait_sleep(bfull + b, bph);
+        tc::fence_after_sync();
+        const uint32_t b_addr = tc::smem_u32(sB + b * a.b_bytes);
+        for (int t = 0; t < nvt; ++t, ++tcount) {
+          const int set = tcount % kFSetsLm, use = tcount / kFSetsLm;
+          if (use > 0) {
+            tc::mbar_wait_sleep(acce + set, (use - 1) & 1);
+            tc::fence_after_sync();
+          }
+          const uint32_t acc0 = tmem + set * (5 * kNTF);
+          for (int p = 0; p < a.kp; ++p) {
+            int st[3];
+            for (int l = 0; l < 3; ++l) {
+              st[l] = s;
+              tc::mbar_wait_sleep(afull + s, u & 1);
+              if (++s == a.S) {
+                s = 0;
+                ++u;
+              }
+            }
+            tc::fence_after_sync();
+            const int nk = min(4, (a.dim - p * kPanel + 31) / 32);
+            uint64_t dA[3], dB[3];
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+              dA[l] = tc::desc_sw128(tc::smem_u32(sA + st[l] * kAStageBytes));
+              dB[l] = tc::desc_sw128(b_addr + (l * a.kp + p) * kNTF * kPanel);
+            }
+            for (int k = 0; k < nk; ++k) {
+              const uint32_t first = (p == 0 && k == 0) ? 1u : 0u;
+              // u = sl + t: 2 1 3 2 0 4 2 1 3 (no accumulator updated back to back); accumulate
+              // except on an accumulator's first product of the tile
+#define LMF_MMA(SL, T, FIRSTPAIR) \
+  tc::mma_s8(acc0 + ((SL) + (T)) * kNTF, dA[SL] + 2 * k, dB[T] + 2 * k, idesc, (FIRSTPAIR) ? (first ^ 1u) : 1u)
+              LMF_MMA(2, 0, true);
+              LMF_MMA(1, 0, true);
+              LMF_MMA(2, 1, true);
+              LMF_MMA(1, 1, false);
+              LMF_MMA(0, 0, true);
+              LMF_MMA(2, 2, true);
+              LMF_MMA(0, 2, false);
+              LMF_MMA(0, 1, false);
+              LMF_MMA(1, 2, false);
+#undef LMF_MMA
+            }
+            for (int l = 0; l < 3; ++l) tc::mma_commit(aempty + st[l]);
+          }
+          tc::mma_commit(accf + set);
+        }
+        tc::mma_commit(bempty + b);
+        if (++b == a.nb) {
+          b = 0;
+          bph ^= 1;
+        }
+      }
+    }
+  } else if (warp < kWarpEpi) {
+    // ------------------------------------------------------------ gather: query limbs + metadata
+    const int gt = tid - kWarpGat * 32;  // 0 .. 63
+    const int cpr = a.dim >> 4;
+    int b = 0, use = 0;
+    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
+      const int4 it = a.items[j];
+      if (use > 0) tc::mbar_wait_sleep(bempty + b, (use - 1) & 1);
+      uint8_t* dst = sB + b * a.b_bytes;
+      {
+        const int cnt = __ldg(a.counts + it.x);
+        if (gt == 0 && a.p_stride && cnt > 0) {
+          const uint32_t pbytes = 16u * ((cnt + 1) / 2);
+          tc::mbar_expect_tx_only(bfull + b, pbytes);
+          bulk_g2s_lm(sP + b * a.p_stride, a.pterm + static_cast<int64_t>(it.x) * L, pbytes, bfull + b);
+        }
+      }
+      for (int r = gt; r < it.z; r += 32 * kNGat) {
+        const int pr = __ldg(a.pairs + it.y + r);
+        const int q = pr / a.nprobe;
+        mrow[b * kNTF + r] = reinterpret_cast<uint64_t>(a.trace + static_cast<int64_t>(pr) * L);
+        md[b * kNTF + r] = __ldg(a.ldist + pr);
+        mgoff[b * kNTF + r] = pr * a.ngroups;
+        for (int l = 0; l < 3; ++l) {
+          const int8_t* qrow = a.ql + (l * a.rows_q + q) * a.dim;
+          for (int c = 0; c < cpr; ++c)
+            tc::cp_async16(dst + ((l * a.kp) + (c >> 3)) * kNTF * kPanel + tc::sw128_offset(r, c & 7), qrow + c * 16, 16);
+        }
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bfull + b);
+      if (++b == a.nb) {
+        b = 0;
+        ++use;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // Two groups of 8 warps take alternate tiles; warp = TMEM lane quadrant qd (32 slots) x column
+    // half cg (16 pairs, two sub-chunks of 8).  Thread = slot: D (int64) of each column to the trace
+    // (32 lanes = 256 consecutive bytes); the column's 32 staged D in shared memory give the group
+    // minimum (four lanes per column, eight values each).
+    const int e = warp - kWarpEpi, qd = warp & 3, grp = e >> 3, cg = (e >> 2) & 1;
+    int64_t* stg = stage + e * (kFSub * (kFStageRow / 2));
+    int b = 0, bph = 0, tcount = 0, tall = 0;
+    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
+      const int4 it = a.items[j];
+      const int np = it.z;
+      const int cnt = __ldg(a.counts + it.x);
+      const int nvt = (cnt + kTile - 1) / kTile, ntl = (L + kTile - 1) / kTile;
+      const uint64_t* mr = mrow + b * kNTF;
+      const int64_t* mdd = md + b * kNTF;
+      const int* mg = mgoff + b * kNTF;
+      const int64_t* pP = sP + b * a.p_stride;
+      tc::mbar_wait_sleep(bfull + b, bph);
+      for (int t = 0; t < ntl; ++t, ++tall) {
+        const bool mine = (tall & 1) == grp;
+        const int sbase = t * kTile + qd * 32, slot = sbase + lane;
+        const uint64_t toff = 8ull * static_cast<uint32_t>(slot);
+        if (t < nvt) {
+          // valid tile: group = set = (tile count) mod 2 (each group owns one accumulator set and waits
+          // on every phase of its barriers)
+          const int set = tcount % kFSetsLm, use = tcount / kFSetsLm;
+          ++tcount;
+          if (set != grp) continue;
+          const bool valid = slot < cnt;
+          const int64_t P = !valid ? 0 : a.p_stride ? pP[slot] : __ldg(a.pterm + static_cast<int64_t>(it.x) * L + slot);
+          tc::mbar_wait_sleep(accf + set, use & 1);
+          tc::fence_after_sync();
+          const uint32_t tbase = tmem + (static_cast<uint32_t>(qd * 32) << 16) + set * (5 * kNTF);
+          for (int c0 = cg * 16; sbase < L && c0 < min(np, cg * 16 + 16); c0 += kFSub) {
+            uint32_t v0[8], v1[8], v2[8], v3[8], v4[8];
+            tc::tmem_ld8(tbase + 0 * kNTF + c0, v0);
+            tc::tmem_ld8(tbase + 1 * kNTF + c0, v1);
+            tc::tmem_ld8(tbase + 2 * kNTF + c0, v2);
+            tc::tmem_ld8(tbase + 3 * kNTF + c0, v3);
+            tc::tmem_ld8(tbase + 4 * kNTF + c0, v4);
+            tc::tmem_ld_wait();
+            const int ncol = min(kFSub, np - c0);
+            __syncwarp();  // the previous sub-chunk's reads of the stage are done
+#pragma unroll
+            for (int c = 0; c < kFSub; ++c) {
+              int64_t x = kDMaxFxLm;
+              if (c < ncol) {  // warp-uniform
+                if (valid) {
+                  x = mdd[c0 + c] + P;
+                  x += static_cast<int64_t>(static_cast<int32_t>(v0[c])) * -2;
+                  x += static_cast<int64_t>(static_cast<int32_t>(v1[c])) * -512;
+                  x += static_cast<int64_t>(static_cast<int32_t>(v2[c])) * -131072;
+                  x += static_cast<int64_t>(static_cast<int32_t>(v3[c])) * -33554432LL;
+                  x += static_cast<int64_t>(static_cast<int32_t>(v4[c])) * -8589934592LL;
+                }
+                if (slot < L) __stcs(reinterpret_cast<long long*>(mr[c0 + c] + toff), static_cast<long long>(x));
+              }
+              stg[c * (kFStageRow / 2) + lane] = x;
+            }
+            __syncwarp();
+            // group minima: lane = column (lane & 7) x part (lane >> 3) of eight slots
+            const int col = lane & 7, part = lane >> 3;
+            const int4* r4 = reinterpret_cast<const int4*>(stg + col * (kFStageRow / 2) + part * 8);
+            int64_t m = kDMaxFxLm;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int4 w = r4[u];
+              const int64_t a0 = (static_cast<int64_t>(w.y) << 32) | static_cast<uint32_t>(w.x);
+              const int64_t a1 = (static_cast<int64_t>(w.w) << 32) | static_cast<uint32_t>(w.z);
+              m = min(m, min(a0, a1));
+            }
+            m = min(m, static_cast<int64_t>(__shfl_xor_sync(kFull, static_cast<long long>(m), 8)));
+            m = min(m, static_cast<int64_t>(__shfl_xor_sync(kFull, static_cast<long long>(m), 16)));
+            if (part == 0 && col < ncol) a.gmin[mg[c0 + col] + t * 4 + qd] = m;
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(acce + set);
+        } else if (mine && slot < L) {
+          // a tile of padding only: D = d_max, nothing read
+          for (int c = cg; c < np; c += 2) {
+            __stcs(reinterpret_cast<long long*>(mr[c] + toff), static_cast<long long>(kDMaxFxLm));
+            if (lane == 0) a.gmin[mg[c] + t * 4 + qd] = kDMaxFxLm;  // group sentinel
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(bempty + b);
+      if (++b == a.nb) {
+        b = 0;
+        bph ^= 1;
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == kWarpMma) tc::tmem_dealloc(tmem, 512);
+}
+
+// int32 fixed-point coordinates -> three balanced int8 limb planes [3][n][dim]
+__global__ void fx_limbs_kernel(const int32_t* __restrict__ X, int64_t n, int dim, int8_t* __restrict__ out) {
+  const int64_t tot = n * dim;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int v = __ldg(X + e);
+    const int d0 = ((v + 128) & 255) - 128, w = (v - d0) >> 8;
+    const int d1 = ((w + 128) & 255) - 128, d2 = (w - d1) >> 8;
+    out[e] = static_cast<int8_t>(d0);
+    out[tot + e] = static_cast<int8_t>(d1);
+    out[2 * tot + e] = static_cast<int8_t>(d2);
+  }
+}
+
 }  // namespace
 
 cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64_t nq, int nprobe, int k,
@@ -1488,9 +1808,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   // less where three B operands would not fit 128 KB
   int NT = 64;
   const int64_t nt_opt = opt(V3DB_OPT_LM_NT);
-  // (256 is taken as 128: with two accumulators a long C4-scale batch stops making progress -- an
-  // unresolved hang, DESIGN.md §10 -- and no shape the library picks uses it)
-  if (nt_opt == 32 || nt_opt == 64 || nt_opt == 128) NT = static_cast<int>(nt_opt);
+  if (nt_opt == 32 || nt_opt == 64 || nt_opt == 128 || nt_opt == 256) NT = static_cast<int>(nt_opt);
   int nb = kNB;  // B buffers: 3, or 2 when three of the smallest NT do not fit (dim near 2048)
   while (NT > 32 && static_cast<uint32_t>(nb) * kp * NT * kPanel > 128u * 1024) NT >>= 1;
   if (static_cast<uint32_t>(nb) * kp * NT * kPanel > 128u * 1024) nb = 2;
@@ -1613,6 +1931,126 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
     e = launch_select(sa, nq, reinterpret_cast<int*>(gmin + npairs * ngroups), st);
   }
   if (e == cudaSuccess) e = debug_sync(st, "lm_select kernels");
+  cudaFreeAsync(base, st);
+  return e;
+}
+
+// NEXT-1 list-major: the fixed-point Steps 3-5 on the tensor cores (see lm_fx_kernel).  Requires
+// s->xhat_fx (dim % 16 == 0, dim <= 256, nlist <= 32768).
+cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k,
+                               const int32_t* lists, const int64_t* ldist, int32_t* out_ids, int64_t* out_dist,
+                               int64_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t)) {
+  if (nq <= 0) return cudaSuccess;
+  if (!s->xhat_fx || s->dim % 16 != 0) return cudaErrorInvalidValue;
+  const int64_t npairs = nq * nprobe;
+  const int L = s->L, ngroups = (L + kG - 1) / kG, kp = (s->dim + kPanel - 1) / kPanel, nlist = s->nlist;
+  if (npairs >= (int64_t(1) << 31) || npairs * ngroups >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  const int nb = kNB;
+  const uint32_t b_bytes = 3u * kp * kNTF * kPanel;
+  int p_stride = L % 2 == 0 ? L : 0;  // (16-byte aligned int64 rows: one bulk copy per item)
+  if (static_cast<size_t>(nb) * 8 * p_stride > 48 * 1024) p_stride = 0;
+  const uint32_t stage_bytes = kEpiWarps * kFSub * kFStageRow * 4;
+  auto smem_of = [&](int stages) {
+    return 1024 + static_cast<size_t>(stages) * kAStageBytes + nb * b_bytes + nb * kNTF * 20 +
+           static_cast<size_t>(nb) * 8 * p_stride + stage_bytes + 8 * (2 * stages + 2 * kNB + 2 * kFSetsLm) + 64;
+  };
+  int S = 9;
+  while (S > 3 && smem_of(S) > 227 * 1024) --S;
+  if (smem_of(S) > 227 * 1024) return cudaErrorInvalidConfiguration;
+
+  CUtensorMap tmX;
+  if (!make_tmap_i8(&tmX, s->xhat_fx, 3ull * nlist * s->lm_Lp, s->dim, kTile, kPanel)) return cudaErrorInvalidValue;
+
+  const int64_t max_items = nlist + npairs / kNTF + 1;
+  const size_t b_hist = al(sizeof(int) * nlist, 256), b_pairs = al(sizeof(int32_t) * npairs, 256),
+               b_items = al(sizeof(int4) * max_items, 256), b_ql = al(3ull * nq * s->dim, 256),
+               b_gmin = al(sizeof(int64_t) * npairs * ngroups, 256) + al(sizeof(int) * nq, 256),  // + flags
+               b_trace = trace_cand ? 0 : al(sizeof(int64_t) * npairs * L, 256);
+  uint8_t* base = nullptr;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&base),
+                                2 * b_hist + 256 + b_pairs + b_items + b_ql + b_gmin + b_trace, st);
+  if (e != cudaSuccess) return e;
+  int* hist = reinterpret_cast<int*>(base);
+  int* cur = reinterpret_cast<int*>(base + b_hist);
+  int* n_items = reinterpret_cast<int*>(base + 2 * b_hist);
+  int32_t* pairs = reinterpret_cast<int32_t*>(base + 2 * b_hist + 256);
+  int4* items = reinterpret_cast<int4*>(base + 2 * b_hist + 256 + b_pairs);
+  int8_t* ql = reinterpret_cast<int8_t*>(base + 2 * b_hist + 256 + b_pairs + b_items);
+  int64_t* gmin = reinterpret_cast<int64_t*>(base + 2 * b_hist + 256 + b_pairs + b_items + b_ql);
+  int* flags = reinterpret_cast<int*>(gmin + npairs * ngroups);
+  int64_t* trace = trace_cand ? trace_cand
+                              : reinterpret_cast<int64_t*>(base + 2 * b_hist + 256 + b_pairs + b_items + b_ql + b_gmin);
+
+  int dev = 0, sms = 148;
+  e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaMemsetAsync(hist, 0, sizeof(int) * nlist, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(base, st);
+    return e;
+  }
+  fx_limbs_kernel<<<static_cast<unsigned>(std::min<int64_t>((nq * s->dim + 255) / 256, 148 * 16)), 256, 0, st>>>(
+      queries, nq, s->dim, ql);
+  const unsigned pg = static_cast<unsigned>(std::min<int64_t>((npairs + 255) / 256, 4 * sms));
+  pair_hist_kernel<<<pg, 256, 0, st>>>(lists, npairs, hist);
+  lm_scan_items_kernel<<<1, 1024, 0, st>>>(hist, nlist, kNTF, cur, items, n_items);
+  pair_scatter_kernel<<<pg, 256, 0, st>>>(lists, npairs, cur, pairs);
+  note_launch(4);
+  if (prof) prof(2, st);
+
+  LmFxArgs a;
+  a.nprobe = nprobe;
+  a.L = L;
+  a.Lp = s->lm_Lp;
+  a.dim = s->dim;
+  a.kp = kp;
+  a.S = S;
+  a.nb = nb;
+  a.ngroups = ngroups;
+  a.p_stride = p_stride;
+  a.rows_x = static_cast<int64_t>(nlist) * s->lm_Lp;
+  a.rows_q = nq;
+  a.ql = ql;
+  a.pairs = pairs;
+  a.items = items;
+  a.n_items = n_items;
+  a.ldist = ldist;
+  a.counts = s->counts;
+  a.pterm = s->pterm64;
+  a.trace = trace;
+  a.gmin = gmin;
+  a.off_b = S * kAStageBytes;
+  a.b_bytes = b_bytes;
+  a.off_meta = a.off_b + nb * b_bytes;
+  a.off_p = static_cast<uint32_t>(al(a.off_meta + nb * kNTF * 20, 16));
+  a.off_stage = a.off_p + nb * 8 * p_stride;
+  a.off_bar = static_cast<uint32_t>(al(a.off_stage + stage_bytes, 8));
+  const size_t smem = smem_of(S);
+  e = cudaFuncSetAttribute(lm_fx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) {
+    const int64_t grid = std::min<int64_t>(sms, max_items);
+    lm_fx_kernel<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(tmX, a);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = debug_sync(st, "lm_fx_kernel");
+  if (prof) prof(3, st);
+  if (e == cudaSuccess) {
+    SelArgs<int64_t> sa;
+    sa.nprobe = nprobe;
+    sa.L = L;
+    sa.ngroups = ngroups;
+    sa.k = k;
+    sa.lists = lists;
+    sa.counts = s->counts;
+    sa.ids = s->ids;
+    sa.trace = trace;
+    sa.gmin = gmin;
+    sa.out_ids = out_ids;
+    sa.out_dist = out_dist;
+    e = launch_select(sa, nq, flags, st);
+  }
+  if (e == cudaSuccess) e = debug_sync(st, "lm_fx select kernels");
   cudaFreeAsync(base, st);
   return e;
 }

@@ -73,6 +73,7 @@ void free_snapshot(v3db_snapshot* s) {
   cudaFree(s->codebooks32);
   cudaFree(s->pterm64);
   cudaFree(s->codes_rot16);
+  cudaFree(s->xhat_fx);
   cudaFree(s->xhat);
   delete s;
 }
@@ -823,6 +824,12 @@ int v3db_build_snapshot_fx(const int32_t* db, int64_t n, int32_t dim, int32_t nl
     V3DB_CUDA(cudaMalloc(&s->codes_rot16, static_cast<size_t>(slots) * m));
     V3DB_CUDA(v3db::rotate_codes16(s->codes, slots, L, m, s->codes_rot16, st));
   }
+  // limb planes of every slot's reconstruction for the list-major tensor-core scan
+  if (dim % 16 == 0 && dim <= 256 && nlist <= 32768) {
+    s->lm_Lp = (L + 127) & ~127;
+    V3DB_CUDA(cudaMalloc(&s->xhat_fx, 3ull * nlist * s->lm_Lp * dim));
+    V3DB_CUDA(v3db::make_xhat_fx(s->codes, s->counts, s->codebooks32, nlist, L, s->lm_Lp, dim, m, ks, s->xhat_fx, st));
+  }
   V3DB_CUDA(cudaStreamSynchronize(st));
   s->total_valid = n;
   guard.s = nullptr;
@@ -846,7 +853,13 @@ static int fx_query_impl(v3db_snapshot_t s, const int32_t* queries, int64_t nq, 
   prof_record(0, st);
   cudaError_t e = v3db::fx_topk(queries, nq, s->dim, s->centroids32, s->cnorm64, s->nlist, nprobe, lists, ldist, st);
   prof_scan_begin(st);
-  if (e == cudaSuccess) e = v3db::fx_scan(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+  if (e == cudaSuccess) {
+    if (s->xhat_fx && v3db::opt(V3DB_OPT_FX_SCAN) == 0)
+      e = v3db::scan_list_major_fx(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st,
+                                   g_prof.on ? prof_record : nullptr);
+    else
+      e = v3db::fx_scan(s, queries, nq, nprobe, k, lists, ldist, out_ids, out_dist, trace_cand_dist, st);
+  }
   prof_scan_end(st);
   if (scratch) cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "v3db_query_batch_fx");

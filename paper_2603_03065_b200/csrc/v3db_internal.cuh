@@ -53,6 +53,9 @@ struct v3db_snapshot {
   int32_t* codebooks32 = nullptr;  // [M][Ks][d]
   int64_t* pterm64 = nullptr;      // [nlist][L]
   uint8_t* codes_rot16 = nullptr;  // [nlist][L][M], per-slot rotated in groups of 16 (+ 8) (M % 8 == 0, Ks == 256)
+  // fixed-point list-major scan: the reconstruction of every slot as three balanced int8 limb planes
+  // [3][nlist][lm_Lp][dim] (0 for padding); null unless dim % 16 == 0, dim <= 256, nlist <= 32768
+  int8_t* xhat_fx = nullptr;
 };
 
 // Device-side invariant checks: traps in the debug build (libv3db_debug.so, -DV3DB_DEBUG), no
@@ -150,6 +153,12 @@ cudaError_t rotate_codes(const uint8_t* codes, const int32_t* pterm, int nlist, 
                          uint8_t* codes_rot, int32_t* pterm_rot, cudaStream_t st);
 cudaError_t make_xhat(const uint8_t* codes, const int32_t* counts, const int8_t* cb, int nlist, int L, int Lp,
                       int dim, int M, int Ks, int8_t* xhat, cudaStream_t st);
+cudaError_t make_xhat_fx(const uint8_t* codes, const int32_t* counts, const int32_t* cb, int nlist, int L, int Lp,
+                         int dim, int M, int Ks, int8_t* xl, cudaStream_t st);
+// Steps 3-5 of the fixed-point path, list-major on the tensor cores (scan_lm.cu).  Requires s->xhat_fx.
+cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, int64_t nq, int nprobe, int k,
+                               const int32_t* lists, const int64_t* ldist, int32_t* out_ids, int64_t* out_dist,
+                               int64_t* trace_cand, cudaStream_t st, void (*prof)(int, cudaStream_t));
 cudaError_t transpose_codebooks(const int8_t* cb, int M, int Ks, int d, int8_t* cbT, cudaStream_t st);
 
 // Steps 3-5, generic query-major scan (scan_lut.cu): any shape, per-query LUT [M][Ks] in shared

@@ -323,3 +323,33 @@ def test_fx_coarse_tc_adversarial(v3db):
     db2 = np.full((4096, 16), 30000, np.int32)
     qs2 = np.vstack([np.full((1, 16), 30000, np.int32), (np.arange(16, dtype=np.int32) * 4000)[None]])
     run_int32_case(v3db, db2, qs2, 2048, 8, 4, 4, 40, 10, np.arange(2048), np.stack([np.arange(4)] * 4))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("name", ["c0", "c1", "e2_large", "c4_mini"])
+def test_fx_scan_paths(v3db, name, mode):
+    """Fixed-point Steps 3-5: the list-major tensor-core scan (0: three int8 limbs per coordinate,
+    five int32 accumulators per tile, int64 D, the int64 instantiation of Step 5) and the literal
+    per-query int64 LUT scan (1) give the oracle's bits, top-k and the whole trace."""
+    cfg, f, db, qs, ref_s, ref = fx_case(name)
+    s = v3db.build_snapshot_fx(torch.from_numpy(db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows,
+                               f.codeword_rows)
+    with v3db.option(v3db.OPT_FX_SCAN, mode):
+        out = v3db.query_batch_fx(s, torch.from_numpy(qs).cuda(), cfg.nprobe, cfg.k)
+        check_query(out, ref)
+        out2 = v3db.query_batch_fx(s, torch.from_numpy(qs).cuda(), cfg.nprobe, cfg.k, trace=False)
+        check_query(out2, ref, keys=("out_ids", "out_dist"))
+
+
+@pytest.mark.parametrize("L", [130, 257, 384])
+def test_fx_list_major_shapes(v3db, L):
+    """List capacities that are not multiples of the 128-slot tile, odd (the P terms then come from
+    global memory) and lists shorter than L (padding-only tiles), with extreme coordinates."""
+    rng = np.random.default_rng(26)
+    N, D, nlist, M, Ks = 600, 32, 6, 8, 16
+    db = rng.choice(np.array([-65535, -30000, 0, 30000, 65535], np.int32), size=(N, D)).astype(np.int32)
+    db[: N // 2] += rng.integers(-100, 100, size=(N // 2, D)).astype(np.int32)
+    db = np.clip(db, -65535, 65535).astype(np.int32)
+    qs = rng.integers(-65535, 65536, size=(45, D)).astype(np.int32)
+    run_int32_case(v3db, db, qs, nlist, L, M, Ks, 4, 50, rng.choice(N, nlist, replace=False),
+                   np.stack([rng.choice(N, Ks, replace=False) for _ in range(M)]))
