@@ -31,9 +31,10 @@ namespace v3db {
 namespace {
 
 constexpr int kFRows = 128;                       // rows per tile (UMMA M)
-constexpr int kFCols = 32;                        // centroids per work item (UMMA N) = one block
+constexpr int kFCols = 96;                        // centroids per work item (UMMA N) = three blocks
+constexpr int kFBlk = 32;                         // lists per block (two keys kept per block)
 constexpr int kFPanel = 128;                      // bytes of K per swizzled panel
-constexpr int kFSets = 3;                         // accumulator sets (5 x 32 columns each)
+constexpr int kFSets = 1;                         // accumulator sets (5 x 96 columns: 480 of TMEM's 512)
 constexpr int kFEpi = 12;                         // epilogue warps
 constexpr int kFProd = kFEpi, kFMma = kFEpi + 1;
 constexpr int kFThreads = 32 * (kFEpi + 2);
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fx_coarse_tc_kernel(const __grid
   uint8_t* sA = smem;                                             // [3][kp][128 x 128 B]
   uint8_t* sB = smem + 3 * a.kp * kFAPanel;                       // [stages][32 x 128 B]
   int64_t* sCn = reinterpret_cast<int64_t*>(sB + a.stages * kFBStage);  // [kFEpi][32] packed column terms
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sCn + kFEpi * kFCols);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sCn + kFEpi * kFBlk);
   uint64_t* a_full = bars;
   uint64_t* a_empty = bars + 1;
   uint64_t* full = bars + 2;                  // [stages]
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fx_coarse_tc_kernel(const __grid
     }
     for (int s = 0; s < kFSets; ++s) {
       tc::mbar_init(accf + s, 1);
-      tc::mbar_init(acce + s, 4);  // the four warps of one epilogue group
+      tc::mbar_init(acce + s, kFEpi);  // every epilogue warp drains the item
     }
     tc::mbar_fence_init();
   }
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fx_coarse_tc_kernel(const __grid
       // updates of one accumulator are six MMAs apart (the tensor pipe executes in issue order)
       for (int64_t it = i0; it < i1;) {
         const int64_t rt = it / a.nchunks;
-        const int ni = (a.kp == 1 && it + 1 < i1 && (it + 1) / a.nchunks == rt) ? 2 : 1;
+        const int ni = (kFSets > 1 && a.kp == 1 && it + 1 < i1 && (it + 1) / a.nchunks == rt) ? 2 : 1;
         if (rt != cur_rt) {
           tc::mbar_wait(a_full, nA & 1);
           tc::fence_after_sync();
@@ -223,15 +224,15 @@ __global__ void __launch_bounds__(kFThreads, 1) fx_coarse_tc_kernel(const __grid
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 0-11)
-    const int g = warp >> 2, q = warp & 3;
+    // warp = TMEM lane quadrant q x block blk (32 of the item's 96 columns); thread = row
+    const int q = warp & 3, blk = warp >> 2;
     const int r = q * 32 + lane;
-    int64_t* cn = sCn + warp * kFCols;
+    int64_t* cn = sCn + warp * kFBlk;
     for (int64_t it = i0; it < i1; ++it) {
       const int j = static_cast<int>(it - i0), set = j % kFSets, use = j / kFSets;
-      if (set != g) continue;
       const int64_t rt = it / a.nchunks;
       const int c = static_cast<int>(it - rt * a.nchunks);
-      const int col0 = c * kFCols;
+      const int col0 = c * kFCols + blk * kFBlk;
       const int64_t row = rt * kFRows + r;
       __syncwarp();
       // packed column terms 32 ||mu_i||^2 + (i mod 32); padding columns +inf (their limbs are zero)
@@ -243,13 +244,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fx_coarse_tc_kernel(const __grid
       tc::mbar_wait_sleep(accf + set, use & 1);
 #endif
       tc::fence_after_sync();
-      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + set * (5 * kFCols);
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + set * (5 * kFCols) + blk * kFBlk;
       int64_t m1 = kInf64, m2 = kInf64;
-#if defined(FXEXP) && FXEXP == 1  // experiment: no epilogue work (keys valid but meaningless)
-      m1 = 1;
-      m2 = 2;
-      if (lane == 99)
-#endif
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq) {
         uint32_t v0[8], v1[8], v2[8], v3[8], v4[8];
@@ -259,6 +255,11 @@ __global__ void __launch_bounds__(kFThreads, 1) fx_coarse_tc_kernel(const __grid
         tc::tmem_ld8(tbase + 3 * kFCols + qq * 8, v3);
         tc::tmem_ld8(tbase + 4 * kFCols + qq * 8, v4);
         tc::tmem_ld_wait();
+        if (qq == 3) {  // every accumulator value of this thread is in registers: release the set
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(acce + set);
+        }
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
           const int64_t base = cn[qq * 8 + cc];
@@ -275,11 +276,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fx_coarse_tc_kernel(const __grid
           m2 = min(m2, t);
         }
       }
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(acce + set);
       if (row < a.n)
-        *reinterpret_cast<longlong2*>(a.bk + 2 * (row * a.nchunks + c)) = make_longlong2(m1, m2);
+        *reinterpret_cast<longlong2*>(a.bk + 2 * (row * (a.nchunks * 3) + c * 3 + blk)) = make_longlong2(m1, m2);
     }
   }
   tc::fence_before_sync();
@@ -297,11 +295,12 @@ struct FxKey {
 };
 __device__ __forceinline__ bool fx_less(const FxKey& a, const FxKey& b) { return a.e < b.e || (a.e == b.e && a.i < b.i); }
 
-template <int KR>
+// NV: the row's stored key pairs per lane held in registers (nblk <= 32 NV).
+template <int KR, int NV>
 __global__ void __launch_bounds__(32 * kFxMergeWarps) fx_merge_tc_kernel(
     const int32_t* __restrict__ X, int64_t n, int dim, const int32_t* __restrict__ mu,
-    const int64_t* __restrict__ cnorm, int nlist, int nblk, int R, int cap, const int64_t* __restrict__ bk,
-    int sh, int32_t* __restrict__ out_idx, int64_t* __restrict__ out_dist) {
+    const int64_t* __restrict__ cnorm, int nlist, int nblk, int rstride, int R, int cap,
+    const int64_t* __restrict__ bk, int sh, int32_t* __restrict__ out_idx, int64_t* __restrict__ out_dist) {
   extern __shared__ __align__(16) uint8_t msm[];
   constexpr unsigned kFull = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -318,13 +317,17 @@ __global__ void __launch_bounds__(32 * kFxMergeWarps) fx_merge_tc_kernel(
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) xn += __shfl_xor_sync(kFull, xn, o);
-  const longlong2* src = reinterpret_cast<const longlong2*>(bk + 2 * row * nblk);
+  const longlong2* src = reinterpret_cast<const longlong2*>(bk + 2 * row * rstride);
+  longlong2 kv[NV];
+#pragma unroll
+  for (int u = 0; u < NV; ++u) kv[u] = 32 * u + lane < nblk ? __ldg(src + 32 * u + lane) : make_longlong2(kInf64, kInf64);
   const unsigned lt = (1u << lane) - 1u;
   // extent of e over the stored keys (e = p >> 5)
   long long mn = kInf64, mx = -kInf64;
   int cntv = 0;
-  for (int b = lane; b < nblk; b += 32) {
-    const longlong2 v = __ldg(src + b);
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    const longlong2 v = kv[u];
     if (v.x != kInf64) {
       mn = min(mn, v.x >> 5);
       mx = max(mx, v.x >> 5);
@@ -352,8 +355,9 @@ __global__ void __launch_bounds__(32 * kFxMergeWarps) fx_merge_tc_kernel(
       const int shb = bits > 8 ? bits - 8 : 0;
       for (int b = lane; b < 256; b += 32) wh[b] = 0;
       __syncwarp();
-      for (int b = lane; b < nblk; b += 32) {
-        const longlong2 v = __ldg(src + b);
+#pragma unroll
+      for (int u = 0; u < NV; ++u) {
+        const longlong2 v = kv[u];
         const long long w[2] = {v.x, v.y};
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
@@ -400,9 +404,10 @@ __global__ void __launch_bounds__(32 * kFxMergeWarps) fx_merge_tc_kernel(
     tau = lo + static_cast<long long>(span - 1ull);
   }
   int nc = 0, nr = 0;
-  for (int b0 = 0; b0 < nblk; b0 += 32) {
-    const int b = b0 + lane;
-    const longlong2 v = b < nblk ? __ldg(src + b) : make_longlong2(kInf64, kInf64);
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    const int b = 32 * u + lane;
+    const longlong2 v = kv[u];
     const bool rec = v.y != kInf64 && (v.y >> 5) <= tau;
     unsigned bal = __ballot_sync(kFull, rec);
     int pos = nr + __popc(bal & lt);
@@ -455,13 +460,23 @@ __global__ void __launch_bounds__(32 * kFxMergeWarps) fx_merge_tc_kernel(
   over = over || nc > cap;
   __syncwarp();
   if (!over) {
+    // the (e, i) order as one unsigned compare: (e - emin) << 20 | i (e - emin < 2^44 for dim <= 256,
+    // i < 2^20 lists), written over each key's e field
+    long long emin = kInf64;
+    for (int j = lane; j < nc; j += 32) emin = min(emin, static_cast<long long>(keys[j].e));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) emin = min(emin, __shfl_xor_sync(kFull, emin, o));
+    __syncwarp();
+    for (int j = lane; j < nc; j += 32)
+      keys[j].e = static_cast<long long>((static_cast<uint64_t>(keys[j].e - emin) << 20) | static_cast<uint32_t>(keys[j].i));
+    __syncwarp();
     for (int j = lane; j < nc; j += 32) {
-      const FxKey kj = keys[j];
+      const uint64_t kj = static_cast<uint64_t>(keys[j].e);
       int rank = 0;
-      for (int f = 0; f < nc; ++f) rank += fx_less(keys[f], kj) ? 1 : 0;
+      for (int f = 0; f < nc; ++f) rank += static_cast<uint64_t>(keys[f].e) < kj ? 1 : 0;
       if (rank < R) {
-        out_idx[row * R + rank] = kj.i;
-        out_dist[row * R + rank] = xn + kj.e;
+        out_idx[row * R + rank] = static_cast<int32_t>(kj & 0xfffff);
+        out_dist[row * R + rank] = xn + emin + static_cast<long long>(kj >> 20);
       }
     }
     for (int j = nc + lane; j < R; j += 32) {  // fewer lists than R (not reached: R <= nlist)
@@ -498,7 +513,8 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 }  // namespace
 
 bool fx_coarse_tc_supported(int dim, int nlist, int R) {
-  return dim % 16 == 0 && dim <= 256 && R <= 1024 && nlist <= (1 << 24) && opt(V3DB_OPT_FX_COARSE) == 0;
+  // (the merge holds a row's nlist / 32 stored key pairs in registers: nlist <= 32768)
+  return dim % 16 == 0 && dim <= 256 && R <= 1024 && nlist <= 32768 && opt(V3DB_OPT_FX_COARSE) == 0;  // (i < 2^20)
 }
 
 // The R nearest lists (exact int64 distances, (d, i) order) of every row of X, on the tensor cores.
@@ -509,7 +525,7 @@ cudaError_t fx_topk_tc(const int32_t* X, int64_t n, int dim, const int32_t* mu, 
   const int64_t rows_p = (n + kFRows - 1) / kFRows * kFRows;
   const int nchunks = (nlist + kFCols - 1) / kFCols;
   const int cols_p = nchunks * kFCols;
-  const size_t fixed = 1024 + 3 * static_cast<size_t>(kp) * kFAPanel + kFEpi * kFCols * 8 + 64 * 8;
+  const size_t fixed = 1024 + 3 * static_cast<size_t>(kp) * kFAPanel + kFEpi * kFBlk * 8 + 64 * 8;
   const int stages = static_cast<int>(std::min<size_t>(24, (227 * 1024 - fixed) / kFBStage));
   if (stages < 4) return cudaErrorInvalidValue;
   int dev = 0, sms = 148;
@@ -517,7 +533,7 @@ cudaError_t fx_topk_tc(const int32_t* X, int64_t n, int dim, const int32_t* mu, 
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   const size_t b_xl = al256(3 * static_cast<size_t>(rows_p) * dim), b_ml = al256(3 * static_cast<size_t>(cols_p) * dim),
-               b_bk = al256(sizeof(int64_t) * 2 * n * nchunks);
+               b_bk = al256(sizeof(int64_t) * 2 * n * nchunks * 3);
   uint8_t* base = nullptr;
   e = scratch_alloc(reinterpret_cast<void**>(&base), b_xl + b_ml + b_bk, st);
   if (e != cudaSuccess) return e;
@@ -562,11 +578,20 @@ cudaError_t fx_topk_tc(const int32_t* X, int64_t n, int dim, const int32_t* mu, 
   if (e == cudaSuccess) {
     const int cap = 2 * R + 64;
     const size_t msmem = 4 * kFxMergeWarps * (256 + kFxRecCap) + sizeof(FxKey) * kFxMergeWarps * cap;
+    const int nblk = (nlist + kFBlk - 1) / kFBlk;  // blocks of 32 lists holding a list (row stride 3 nchunks)
     dispatch_kr(R, [&]<int KR>() {
-      e = cudaFuncSetAttribute(fx_merge_tc_kernel<KR>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem));
-      if (e == cudaSuccess)
-        fx_merge_tc_kernel<KR><<<static_cast<unsigned>((n + kFxMergeWarps - 1) / kFxMergeWarps), 32 * kFxMergeWarps, msmem,
-                                 st>>>(X, n, dim, mu, mnorm, nlist, nchunks, R, cap, bk, sh, out_idx, out_dist);
+      auto run = [&](auto kern) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem));
+        if (e == cudaSuccess)
+          kern<<<static_cast<unsigned>((n + kFxMergeWarps - 1) / kFxMergeWarps), 32 * kFxMergeWarps, msmem, st>>>(
+              X, n, dim, mu, mnorm, nlist, nblk, nchunks * 3, R, cap, bk, sh, out_idx, out_dist);
+      };
+      if (nblk <= 32) run(fx_merge_tc_kernel<KR, 1>);
+      else if (nblk <= 64) run(fx_merge_tc_kernel<KR, 2>);
+      else if (nblk <= 128) run(fx_merge_tc_kernel<KR, 4>);
+      else if (nblk <= 256) run(fx_merge_tc_kernel<KR, 8>);
+      else if (nblk <= 512) run(fx_merge_tc_kernel<KR, 16>);
+      else run(fx_merge_tc_kernel<KR, 32>);
     });
     note_launch();
     if (e == cudaSuccess) e = cudaGetLastError();

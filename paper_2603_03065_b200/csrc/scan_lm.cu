@@ -1487,8 +1487,12 @@ size_t al(size_t x, size_t b) { return (x + b - 1) / b * b; }
 // in int64 by the epilogue.  Same warp roles and grouping as lm_kernel; D and the group minima are
 // int64; Step 5 is the int64 instantiation of the same selection kernels.
 // ----------------------------------------------------------------------------------------------
-constexpr int kNTF = 32;          // pairs per item: 2 sets x 5 accumulators x 32 columns = 320 TMEM columns
-constexpr int kFSetsLm = 2;      // accumulator sets = epilogue groups (one each)
+// Tile width: 32 pairs x 5 accumulators x 2 sets (320 TMEM columns), one set per epilogue group.  (96
+// pairs in one set -- a third of the MMAs per pair, since a kind::i8 MMA costs ~160 cycles whatever N --
+// measured slower at C4, 3.28 vs 3.10 ms: the kernel is bound by its DRAM traffic, not the MMA rate.)
+constexpr int kNTF = 32;          // pairs per item
+constexpr int kFSetsLm = 2;       // accumulator sets = epilogue groups (one each)
+constexpr int kFGroups = kFSetsLm, kFColGroups = 4 / kFGroups, kFColsPerWarp = kNTF / kFColGroups;
 constexpr int kFStageRow = 68;    // words per staged column (32 int64 + 4 words pad)
 constexpr int kFSub = 8;          // columns per epilogue sub-chunk
 constexpr int64_t kDMaxFxLm = 0x7fffffffffffffffLL;
@@ -1543,7 +1547,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
     }
     for (int c = 0; c < kFSetsLm; ++c) {
       tc::mbar_init(accf + c, 1);
-      tc::mbar_init(acce + c, kEpiWarps / 2);
+      tc::mbar_init(acce + c, kEpiWarps / kFGroups);
     }
     tc::mbar_fence_init();
   }
@@ -1685,7 +1689,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
     // half cg (16 pairs, two sub-chunks of 8).  Thread = slot: D (int64) of each column to the trace
     // (32 lanes = 256 consecutive bytes); the column's 32 staged D in shared memory give the group
     // minimum (four lanes per column, eight values each).
-    const int e = warp - kWarpEpi, qd = warp & 3, grp = e >> 3, cg = (e >> 2) & 1;
+    const int e = warp - kWarpEpi, qd = warp & 3, cg = (e >> 2) % kFColGroups, grp = (e >> 2) / kFColGroups;
     int64_t* stg = stage + e * (kFSub * (kFStageRow / 2));
     int b = 0, bph = 0, tcount = 0, tall = 0;
     for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
@@ -1699,7 +1703,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
       const int64_t* pP = sP + b * a.p_stride;
       tc::mbar_wait_sleep(bfull + b, bph);
       for (int t = 0; t < ntl; ++t, ++tall) {
-        const bool mine = (tall & 1) == grp;
+        const bool mine = (tall % kFGroups) == grp;
         const int sbase = t * kTile + qd * 32, slot = sbase + lane;
         const uint64_t toff = 8ull * static_cast<uint32_t>(slot);
         if (t < nvt) {
@@ -1713,7 +1717,9 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
           tc::mbar_wait_sleep(accf + set, use & 1);
           tc::fence_after_sync();
           const uint32_t tbase = tmem + (static_cast<uint32_t>(qd * 32) << 16) + set * (5 * kNTF);
-          for (int c0 = cg * 16; sbase < L && c0 < min(np, cg * 16 + 16); c0 += kFSub) {
+          const int cend = sbase < L ? min(np, (cg + 1) * kFColsPerWarp) : 0;
+          bool released = false;
+          for (int c0 = cg * kFColsPerWarp; c0 < cend; c0 += kFSub) {
             uint32_t v0[8], v1[8], v2[8], v3[8], v4[8];
             tc::tmem_ld8(tbase + 0 * kNTF + c0, v0);
             tc::tmem_ld8(tbase + 1 * kNTF + c0, v1);
@@ -1721,6 +1727,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
             tc::tmem_ld8(tbase + 3 * kNTF + c0, v3);
             tc::tmem_ld8(tbase + 4 * kNTF + c0, v4);
             tc::tmem_ld_wait();
+            if (c0 + kFSub >= cend) {  // this warp's last accumulator values are in registers
+              tc::fence_before_sync();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(acce + set);
+              released = true;
+            }
             const int ncol = min(kFSub, np - c0);
             __syncwarp();  // the previous sub-chunk's reads of the stage are done
 #pragma unroll
@@ -1755,12 +1767,14 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
             m = min(m, static_cast<int64_t>(__shfl_xor_sync(kFull, static_cast<long long>(m), 16)));
             if (part == 0 && col < ncol) a.gmin[mg[c0 + col] + t * 4 + qd] = m;
           }
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(acce + set);
+          if (!released) {
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(acce + set);
+          }
         } else if (mine && slot < L) {
           // a tile of padding only: D = d_max, nothing read
-          for (int c = cg; c < np; c += 2) {
+          for (int c = cg * kFColsPerWarp; c < min(np, (cg + 1) * kFColsPerWarp); ++c) {
             __stcs(reinterpret_cast<long long*>(mr[c] + toff), static_cast<long long>(kDMaxFxLm));
             if (lane == 0) a.gmin[mg[c] + t * 4 + qd] = kDMaxFxLm;  // group sentinel
           }
@@ -1945,7 +1959,7 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
   const int64_t npairs = nq * nprobe;
   const int L = s->L, ngroups = (L + kG - 1) / kG, kp = (s->dim + kPanel - 1) / kPanel, nlist = s->nlist;
   if (npairs >= (int64_t(1) << 31) || npairs * ngroups >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-  const int nb = kNB;
+  const int nb = kFSetsLm == 1 ? 2 : kNB;  // B operand buffers
   const uint32_t b_bytes = 3u * kp * kNTF * kPanel;
   int p_stride = L % 2 == 0 ? L : 0;  // (16-byte aligned int64 rows: one bulk copy per item)
   if (static_cast<size_t>(nb) * 8 * p_stride > 48 * 1024) p_stride = 0;
