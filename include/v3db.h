@@ -301,7 +301,10 @@ int64_t v3db_kernel_launches(void);
  *                         FP64-FMA kernel (exact below 2^53)
  *   V3DB_OPT_FX_SCAN      fixed-point Steps 3-5: 0 auto (list-major on the tensor cores, int8 limbs,
  *                         where the snapshot holds the limb planes: dim % 16 == 0, dim <= 256,
- *                         nlist <= 32768), 1 always the literal per-query int64 LUT scan */
+ *                         nlist <= 32768), 1 always the literal per-query int64 LUT scan
+ *   V3DB_OPT_COARSE_KEYS  keys kept per 32-list block by the single-pass Steps 1-2: 0 auto (2 for
+ *                         dim <= 256, 4 above, where recomputing a block in the merge is expensive),
+ *                         2 or 4 */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2
@@ -318,7 +321,8 @@ int64_t v3db_kernel_launches(void);
 #define V3DB_OPT_SELECT_CTA 13
 #define V3DB_OPT_FX_COARSE 14
 #define V3DB_OPT_FX_SCAN 15
-#define V3DB_OPT_COUNT 16
+#define V3DB_OPT_COARSE_KEYS 16
+#define V3DB_OPT_COUNT 17
 int v3db_set_option(int32_t key, int64_t value);
 int64_t v3db_get_option(int32_t key);
 

@@ -281,36 +281,49 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
       if constexpr (PASS == 3) {
         // packed key p = 32 e + (i mod 32), e = ||mu_i||^2 - 2 <x, mu_i> = d_i - ||x||^2 (exact:
         // |32 e| < 2^31 for dim <= 1024; padding columns: acc = 0, p = +inf); per 32-list block the
-        // two smallest keys (min / second min: three IMNMX per column)
-        int m[4];
-        auto top2 = [&](int cb, int& m1, int& m2) {
+        // KB = GT smallest keys (an insertion network: 2 KB - 1 IMNMX per column)
+        constexpr int KB = GT;
+        static_assert(KB == 2 || KB == 4, "keys per block");
+        int m[2][KB];
+        auto topk = [&](int cb, int(&mk)[KB]) {
           const int4* c4 = reinterpret_cast<const int4*>(cn + cb);
-          m1 = 0x7fffffff;
-          m2 = 0x7fffffff;
+#pragma unroll
+          for (int z = 0; z < KB; ++z) mk[z] = 0x7fffffff;
 #pragma unroll
           for (int u4 = 0; u4 < 8; ++u4) {
             const int4 cc = c4[u4];
             const int cw[4] = {cc.x, cc.y, cc.z, cc.w};
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-              const int pk = cw[w] - 64 * static_cast<int>(v[4 * u4 + w]);
-              const int t = max(m1, pk);
-              m1 = min(m1, pk);
-              m2 = min(m2, t);
+              int t = cw[w] - 64 * static_cast<int>(v[4 * u4 + w]);
+#pragma unroll
+              for (int z = 0; z < KB - 1; ++z) {
+                const int hi = max(mk[z], t);
+                mk[z] = min(mk[z], t);
+                t = hi;
+              }
+              mk[KB - 1] = min(mk[KB - 1], t);
             }
           }
         };
         tc::tmem_ld32(taddr, v);
         tc::tmem_ld_wait();
-        top2(0, m[0], m[1]);
+        topk(0, m[0]);
         tc::tmem_ld32(taddr + 32, v);
         tc::tmem_ld_wait();
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(acce + acc);  // accumulator columns consumed
-        top2(32, m[2], m[3]);
-        if (live)  // blocks 8c + 2h and 8c + 2h + 1 of the row: (min, second min) each
-          *reinterpret_cast<int4*>(a.gmin + 2 * (row * a.ngroups + c * 8 + h * 2)) = make_int4(m[0], m[1], m[2], m[3]);
+        topk(32, m[1]);
+        if (live) {  // blocks 8c + 2h and 8c + 2h + 1 of the row: their KB smallest keys each
+          int4* dst = reinterpret_cast<int4*>(a.gmin + KB * (row * a.ngroups + c * 8 + h * 2));
+          if constexpr (KB == 2) {
+            dst[0] = make_int4(m[0][0], m[0][1], m[1][0], m[1][1]);
+          } else {
+            dst[0] = make_int4(m[0][0], m[0][1], m[0][2], m[0][3]);
+            dst[1] = make_int4(m[1][0], m[1][1], m[1][2], m[1][3]);
+          }
+        }
         continue;
       }
       // two 32-column TMEM loads, processed one after the other (32 live registers)
@@ -609,8 +622,9 @@ constexpr int kRecCap = 32;  // recomputed blocks per row
 __device__ __forceinline__ uint64_t merge_key(int e, int i) {
   return (static_cast<uint64_t>(static_cast<uint32_t>(e + (1 << 30))) << 32) | static_cast<uint32_t>(i);
 }
-// NV: int4 (two blocks' keys) per lane held in registers (nblk / 2 <= 32 NV).
-template <int KR, int NV>
+// NV: int4 per lane held in registers: KB = 2 keys per block -> two blocks per int4 (nblk / 2 <= 32 NV);
+// KB = 4 -> one block per int4 (nblk <= 32 NV).
+template <int KR, int NV, int KB>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* __restrict__ X, int64_t n, int dim,
                                                                 const int8_t* __restrict__ mu,
                                                                 const int32_t* __restrict__ cnorm, int nlist,
@@ -631,8 +645,8 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
                    warp * (cap + cap / 4);
   if (row >= n) return;
   const int8_t* x = X + row * dim;
-  const int nv4 = nblk >> 1;  // one int4 = (min, second min) of two blocks
-  const int4* src = reinterpret_cast<const int4*>(bk + row * nblk * 2);
+  const int nv4 = KB == 2 ? nblk >> 1 : nblk;  // int4s per row
+  const int4* src = reinterpret_cast<const int4*>(bk + row * nblk * KB);
   int4 v[NV];
 #pragma unroll
   for (int u = 0; u < NV; ++u) {
@@ -724,17 +738,19 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
 #pragma unroll
   for (int u = 0; u < NV; ++u) {
     const int i = 32 * u + lane;
+    const int w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-    for (int hb = 0; hb < 2; ++hb) {
-      const int m1 = hb ? v[u].z : v[u].x, m2 = hb ? v[u].w : v[u].y, b = 2 * i + hb;
-      const bool rec = m2 != kInf && (m2 >> 5) <= tau;
+    for (int hb = 0; hb < 4 / KB; ++hb) {
+      const int b = (4 / KB) * i + hb, last = w[hb * KB + KB - 1];
+      // a block whose KB-th key has e <= tau may hold more candidates than it stored: recompute it
+      const bool rec = last != kInf && (last >> 5) <= tau;
       unsigned bal = __ballot_sync(kFull, rec);
       int pos = nr + __popc(bal & lt);
       if (rec && pos < kRecCap) rb[pos] = b;
       nr += __popc(bal);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int mk = t ? m2 : m1;
+      for (int t = 0; t < KB; ++t) {
+        const int mk = w[hb * KB + t];
         const bool take = !rec && mk != kInf && (mk >> 5) <= tau;
         bal = __ballot_sync(kFull, take);
         pos = nc + __popc(bal & lt);
@@ -960,7 +976,11 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   const int64_t items = rtiles * nchunks;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(items, sms));
 
-  const size_t b_g = align256(sizeof(int32_t) * n * ngroups * (top2 ? 2 : 1)), b_t = align256(sizeof(int32_t) * n),
+  // keys kept per 32-list block: 2, or 4 where recomputing a block is expensive (dim > 256: the merge
+  // then rarely recomputes); V3DB_OPT_COARSE_KEYS forces either
+  const int64_t kopt = opt(V3DB_OPT_COARSE_KEYS);
+  const int KB = kopt == 2 || kopt == 4 ? static_cast<int>(kopt) : dim > 256 ? 4 : 2;
+  const size_t b_g = align256(sizeof(int32_t) * n * ngroups * (top2 ? KB : 1)), b_t = align256(sizeof(int32_t) * n),
                b_c = align256(sizeof(uint64_t) * n * capc), b_n = align256(sizeof(int) * n);
   uint8_t* base = nullptr;
   e = scratch_alloc(reinterpret_cast<void**>(&base), b_g + b_t + b_c + 2 * b_n, st);
@@ -992,14 +1012,18 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
     return e1;
   };
   if (top2) {
-    e = cudaFuncSetAttribute(coarse_tc_kernel<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) coarse_tc_kernel<3, 0><<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
+    auto pass3 = [&](auto kern) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) kern<<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
+    };
+    if (KB == 4) pass3(coarse_tc_kernel<3, 4>);
+    else pass3(coarse_tc_kernel<3, 2>);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) e = debug_sync(st, "coarse pass (block top-2)");
     const int cap = (2 * R + 64 + 3) & ~3;  // (a multiple of 4: cap / 4 key slots hold the 16-bit bin order)
     const size_t msmem = 4 * kMergeWarps * (256 + kRecCap) + static_cast<size_t>(kMergeWarps) * dim +
                          sizeof(uint64_t) * kMergeWarps * (cap + cap / 4);
-    const int nv4 = ngroups / 2;
+    const int nv4 = KB == 2 ? ngroups / 2 : ngroups;
     if (e == cudaSuccess) {
       dispatch_kr(R, [&]<int KR>() {
         auto run = [&](auto kern) {
@@ -1008,11 +1032,16 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
             kern<<<static_cast<unsigned>((n + kMergeWarps - 1) / kMergeWarps), 32 * kMergeWarps, msmem, st>>>(
                 X, n, dim, mu, cnorm, nlist, ngroups, R, cap, a.gmin, out_idx, out_dist, list_hist);
         };
-        if (nv4 <= 32) run(merge_kernel<KR, 1>);
-        else if (nv4 <= 64) run(merge_kernel<KR, 2>);
-        else if (nv4 <= 128) run(merge_kernel<KR, 4>);
-        else if (nv4 <= 256) run(merge_kernel<KR, 8>);
-        else run(merge_kernel<KR, 16>);
+        auto by_nv = [&]<int KBT>() {
+          if (nv4 <= 32) run(merge_kernel<KR, 1, KBT>);
+          else if (nv4 <= 64) run(merge_kernel<KR, 2, KBT>);
+          else if (nv4 <= 128) run(merge_kernel<KR, 4, KBT>);
+          else if (nv4 <= 256) run(merge_kernel<KR, 8, KBT>);
+          else if (nv4 <= 512) run(merge_kernel<KR, 16, KBT>);
+          else run(merge_kernel<KR, 32, KBT>);
+        };
+        if (KB == 4) by_nv.template operator()<4>();
+        else by_nv.template operator()<2>();
       });
       if (e == cudaSuccess) e = cudaGetLastError();
     }

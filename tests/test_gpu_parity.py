@@ -468,6 +468,8 @@ def test_coarse_block_top2_adversarial(v3db, mode):
     code = np.stack([rng.choice(N, 16, replace=False) for _ in range(4)])
     with v3db.option(v3db.OPT_COARSE_2PASS, mode):
         run_case(v3db, db, qs, nlist, L, 4, 16, nprobe, k, cent, code, algos=("lm", "gen"))
+        with v3db.option(v3db.OPT_COARSE_KEYS, 4):
+            run_case(v3db, db, qs, nlist, L, 4, 16, nprobe, k, cent, code, algos=("lm",))
         N2, nlist2 = 4096, 2048                  # (b) 64 blocks, every one tied
         db2 = np.full((N2, 16), 3, np.int8)
         qs2 = np.vstack([np.full((1, 16), 3, np.int8), np.arange(16, dtype=np.int8)[None]])
@@ -499,3 +501,16 @@ def test_lm_select_ties_beyond_window(v3db):
     with v3db.option(v3db.OPT_SELECT_CTA, 2):
         run_case(v3db, db, qs, nlist, L, 4, 4, 2, 10, np.arange(nlist), np.stack([np.arange(4)] * 4),
                  algos=("lm", "gen"))
+
+
+@pytest.mark.parametrize("keys", [2, 4])
+@pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_large"])
+def test_coarse_keys_per_block(v3db, name, keys):
+    """Single-pass Steps 1-2 keeping 2 or 4 keys per 32-list block: the same bits."""
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    with v3db.option(v3db.OPT_COARSE_KEYS, keys):
+        out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k)
+        torch.cuda.synchronize()
+    assert_query_equal(out, ref)
+    s.free()
