@@ -41,6 +41,18 @@ for name in names:
                 assert np.array_equal(out[key].cpu().numpy(), exp), (name, mode, algo, key)
         s.free()
     v3db.set_option(v3db.OPT_LUT_W32, 0)
+    # the other exact paths of the default (list-major) query: CTA / warp Step 5, 4 keys per coarse block,
+    # the group-minimum coarse passes
+    for opt_key, val in ((v3db.OPT_SELECT_CTA, 1), (v3db.OPT_SELECT_CTA, 2), (v3db.OPT_COARSE_KEYS, 4),
+                         (v3db.OPT_COARSE_2PASS, 1), (v3db.OPT_COARSE_2PASS, 8)):
+        with v3db.option(opt_key, val):
+            s = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks,
+                                    inp.centroid_rows, inp.codeword_rows)
+            out = v3db.query_batch(s, torch.from_numpy(qs).cuda(), cfg.nprobe, cfg.k)
+            torch.cuda.synchronize()
+            for key, exp in ref.items():
+                assert np.array_equal(out[key].cpu().numpy(), exp), (name, opt_key, val, key)
+            s.free()
     with v3db.option(v3db.OPT_COARSE_SIMT, 1):
         s = v3db.build_snapshot(torch.from_numpy(inp.db).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows,
                                 inp.codeword_rows)
@@ -55,12 +67,15 @@ for name in names:
     fq = np.ascontiguousarray(oracle.encode_fixed_point(f.queries[:nq], f.v_max))
     ref_f = oracle.build_snapshot(fdb, cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows, f.codeword_rows)
     reff = oracle.query_batch(ref_f, fq, cfg.nprobe, cfg.k)
-    sf = v3db.build_snapshot_fx(torch.from_numpy(fdb).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks, f.centroid_rows,
-                                f.codeword_rows)
-    outf = v3db.query_batch_fx(sf, torch.from_numpy(fq).cuda(), cfg.nprobe, cfg.k)
-    torch.cuda.synchronize()
-    for key, exp in reff.items():
-        assert np.array_equal(outf[key].cpu().numpy(), exp), (name, "fx16", key)
-    sf.free()
+    # (tensor-core coarse + list-major scan by default; then the FP64 coarse and the literal table scan)
+    for fc, fs in ((0, 0), (1, 1)):
+        with v3db.option(v3db.OPT_FX_COARSE, fc), v3db.option(v3db.OPT_FX_SCAN, fs):
+            sf = v3db.build_snapshot_fx(torch.from_numpy(fdb).cuda(), cfg.nlist, cfg.L, cfg.M, cfg.Ks,
+                                        f.centroid_rows, f.codeword_rows)
+            outf = v3db.query_batch_fx(sf, torch.from_numpy(fq).cuda(), cfg.nprobe, cfg.k)
+            torch.cuda.synchronize()
+            for key, exp in reff.items():
+                assert np.array_equal(outf[key].cpu().numpy(), exp), (name, "fx16", fc, fs, key)
+            sf.free()
     print("ok", name, flush=True)
 print("lib", v3db._lib.LIB_PATH)
