@@ -776,6 +776,14 @@ constexpr int kSelGcap = 2048;     // cached group minima per query
 constexpr int kCandCap = 2048;     // compacted candidates per query
 constexpr int kSelKmax = 256;      // largest k of the cached path
 constexpr int kBinCap = 256;       // entries of the final histogram bin ranked pairwise
+#ifndef V3DB_SW_H
+#define V3DB_SW_H 4
+#endif
+#ifndef V3DB_FAST_MINB
+#define V3DB_FAST_MINB 6
+#endif
+constexpr int kSwH = V3DB_SW_H;    // selected groups per lane octet and candidate step (loads in flight)
+constexpr int kFastMinBlocks = V3DB_FAST_MINB;  // lm_select_fast_kernel CTAs per SM (40 registers)
 static_assert(kG == 32, "the candidate gather maps a group's slots to the lanes of a warp");
 
 template <class T>
@@ -828,6 +836,9 @@ __device__ __forceinline__ int cta_bin_of(int* hist, int* sc, int kk, int* befor
   return sc[0];
 }
 
+// Hands query q to the streaming selection: flags[0] counts, flags[1..] lists.
+__device__ __forceinline__ void flag_query(int* flags, int64_t q) { flags[1 + atomicAdd(flags, 1)] = static_cast<int>(q); }
+
 template <class T>
 __device__ __forceinline__ T warp_min(T v) {
   if constexpr (sizeof(T) == 4) {
@@ -856,7 +867,7 @@ __device__ __forceinline__ T warp_max(T v) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const SelArgs<T> a, int* __restrict__ flags) {
+__global__ void __launch_bounds__(kSelThreads, kFastMinBlocks) lm_select_fast_kernel(const SelArgs<T> a, int* __restrict__ flags) {
   using Tr = DistT<T>;
   using U = typename Tr::U;
   using Key = typename Tr::Key;
@@ -896,7 +907,7 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
   __syncthreads();
   const int V = S.pg[nprobe];
   if (V > kSelGcap) {
-    if (tid == 0) flags[q] = 1;
+    if (tid == 0) flag_query(flags, q);
     return;
   }
   // the valid group minima (8 loads in flight per thread), their minimum and maximum
@@ -978,43 +989,84 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
   __syncthreads();
   const int nsel = S.sc[5];
   const U none = ~U(0);
-  // the candidates, read once: warp w takes selected groups w, w + 8, ... (four in flight);
-  // lane = slot of the group; the valid slots with D - dmin <= tau are appended to (gv, cf)
+  // the candidates, read once: 8 lanes per selected group, 4 consecutive slots per lane (16-byte
+  // loads when L % 4 == 0), each warp 4 kSwH groups per step (kSwH loads in flight per lane); the
+  // valid slots with D - dmin <= tau are appended to (gv, cf)
   U* cd = S.gv;  // the group minima are dead (every thread is past the compaction barrier)
-  for (int f0 = warp; f0 < nsel; f0 += 4 * (kSelThreads / 32)) {
-    U rel[4];
-    int tag[4];
+  {
+    const int sub = lane >> 3, part = lane & 7;
+    const bool vec = (L & 3) == 0;
+    constexpr int kStep = 4 * kSwH;
+    for (int t0 = warp * kStep; t0 < nsel; t0 += kStep * (kSelThreads / 32)) {
+      T v[kSwH][4];
+      int tag[kSwH], lim[kSwH];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int f = f0 + u * (kSelThreads / 32);
-      rel[u] = none;
-      if (f < nsel) {  // warp-uniform
-        const int id = S.gid[f], r = id >> 16, j = kG * (id & 0xffff) + lane;
-        tag[u] = (r << 24) | j;
-        if (j < S.pc[r]) {
-          const U rl = static_cast<U>(tq[r * static_cast<int64_t>(L) + j]) - dmin;
-          if (rl <= tau) rel[u] = rl;
+      for (int h = 0; h < kSwH; ++h) {
+        const int t = t0 + 4 * h + sub;
+        tag[h] = -1;
+        lim[h] = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) v[h][w] = T(0);
+        if (t < nsel) {
+          const int id = S.gid[t], r = id >> 16, j0 = kG * (id & 0xffff) + 4 * part;
+          lim[h] = S.pc[r] - j0;
+          tag[h] = (r << 24) | j0;
+          const T* src = tq + r * static_cast<int64_t>(L) + j0;
+          if (vec) {
+            if (j0 < L) {
+              if constexpr (sizeof(T) == 4) {
+                const int4 x = __ldcs(reinterpret_cast<const int4*>(src));
+                v[h][0] = x.x, v[h][1] = x.y, v[h][2] = x.z, v[h][3] = x.w;
+              } else {
+                const longlong2 x0 = __ldcs(reinterpret_cast<const longlong2*>(src));
+                const longlong2 x1 = __ldcs(reinterpret_cast<const longlong2*>(src) + 1);
+                v[h][0] = x0.x, v[h][1] = x0.y, v[h][2] = x1.x, v[h][3] = x1.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) v[h][w] = w < lim[h] ? src[w] : T(0);
+          }
         }
       }
-    }
+      U rel[kSwH][4];
+      int c = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const unsigned bal = __ballot_sync(kFull, rel[u] != none);
-      if (bal == 0) continue;
-      int base = 0;
-      if (lane == 0) base = atomicAdd(S.sc + 6, __popc(bal));
-      base = __shfl_sync(kFull, base, 0);
-      const int pos = base + __popc(bal & ((1u << lane) - 1u));
-      if (rel[u] != none && pos < kCandCap) {
-        cd[pos] = rel[u];
-        S.cf[pos] = tag[u];
+      for (int h = 0; h < kSwH; ++h)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const U rl = static_cast<U>(v[h][w]) - dmin;
+          rel[h][w] = w < lim[h] && rl <= tau ? rl : none;
+          c += rel[h][w] != none ? 1 : 0;
+        }
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
       }
+      const int tot = __shfl_sync(kFull, incl, 31);
+      if (tot == 0) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(S.sc + 6, tot);
+      int pos = __shfl_sync(kFull, base, 0) + incl - c;
+#pragma unroll
+      for (int h = 0; h < kSwH; ++h)
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (rel[h][w] != none) {
+            if (pos < kCandCap) {
+              cd[pos] = rel[h][w];
+              S.cf[pos] = tag[h] + w;
+            }
+            ++pos;
+          }
     }
   }
   __syncthreads();
   const int C = S.sc[6];
   if (C > kCandCap) {
-    if (tid == 0) flags[q] = 1;
+    if (tid == 0) flag_query(flags, q);
     return;
   }
   auto item_of = [&](int f) {
@@ -1044,7 +1096,7 @@ __global__ void __launch_bounds__(kSelThreads, 8) lm_select_fast_kernel(const Se
       const U hi = w0 + (static_cast<U>(b) << sh);
       const bool last = sh == 0 || inbin <= kBinCap;
       if (last && inbin > kBinCap) {  // more than kBinCap candidates tied at one distance
-        if (tid == 0) flags[q] = 1;
+        if (tid == 0) flag_query(flags, q);
         return;
       }
       // candidates below the target bin win; on the last pass the bin's entries are gathered too
@@ -1247,67 +1299,69 @@ __global__ void __launch_bounds__(32 * kSwWarps) lm_select_warp_kernel(const Sel
     }
   }
   if (ns > kSwSel) {
-    if (lane == 0) flags[q] = 1;
+    if (lane == 0) flag_query(flags, q);
     return;
   }
   __syncwarp();
   // the candidates: 8 lanes per selected group, 4 consecutive slots per lane (one 16-byte load per
-  // 4 int32 values when L % 4 == 0), 8 groups per step; kept if valid and D - dmin <= tau
+  // 4 int32 values when L % 4 == 0), 4 kSwH groups per step (kSwH loads in flight per lane: the loop
+  // is bound by their latency); kept if valid and D - dmin <= tau
   int C = 0;
   {
     const int sub = lane >> 3, part = lane & 7;
     const bool vec = (L & 3) == 0;
-    for (int t0 = 0; t0 < ns; t0 += 8) {
-      U rel[2][4];
-      int tag[2];
+    for (int t0 = 0; t0 < ns; t0 += 4 * kSwH) {
+      T v[kSwH][4];
+      int tag[kSwH], lim[kSwH];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kSwH; ++h) {
         const int t = t0 + 4 * h + sub;
-        tag[h] = 0;
+        tag[h] = -1;
+        lim[h] = 0;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) rel[h][w] = none;
+        for (int w = 0; w < 4; ++w) v[h][w] = T(0);
         if (t < ns) {
-          const int e = S.sel[t], r = e >> 16, j0 = kG * (e & 0xffff) + 4 * part, lim = S.pc[r];
+          const int e = S.sel[t], r = e >> 16, j0 = kG * (e & 0xffff) + 4 * part;
+          lim[h] = S.pc[r] - j0;  // valid slots from j0 on
           tag[h] = (r << 24) | j0;
           const T* src = tq + r * static_cast<int64_t>(L) + j0;
-          T v[4];
           if (vec) {
             if (j0 < L) {
               if constexpr (sizeof(T) == 4) {
-                const int4 x = *reinterpret_cast<const int4*>(src);
-                v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+                const int4 x = __ldcs(reinterpret_cast<const int4*>(src));
+                v[h][0] = x.x, v[h][1] = x.y, v[h][2] = x.z, v[h][3] = x.w;
               } else {
-                const longlong2 x0 = reinterpret_cast<const longlong2*>(src)[0];
-                const longlong2 x1 = reinterpret_cast<const longlong2*>(src)[1];
-                v[0] = x0.x, v[1] = x0.y, v[2] = x1.x, v[3] = x1.y;
+                const longlong2 x0 = __ldcs(reinterpret_cast<const longlong2*>(src));
+                const longlong2 x1 = __ldcs(reinterpret_cast<const longlong2*>(src) + 1);
+                v[h][0] = x0.x, v[h][1] = x0.y, v[h][2] = x1.x, v[h][3] = x1.y;
               }
             }
           } else {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) v[w] = j0 + w < lim ? src[w] : T(0);
-          }
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const U rl = static_cast<U>(v[w]) - dmin;
-            if (j0 + w < lim && rl <= tau) rel[h][w] = rl;
+            for (int w = 0; w < 4; ++w) v[h][w] = w < lim[h] ? src[w] : T(0);
           }
         }
       }
-      // this lane's kept values, placed after the lower lanes' (one warp-wide scan per step)
+      U rel[kSwH][4];
       int c = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < kSwH; ++h)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) c += rel[h][w] != none ? 1 : 0;
+        for (int w = 0; w < 4; ++w) {
+          const U rl = static_cast<U>(v[h][w]) - dmin;
+          rel[h][w] = w < lim[h] && rl <= tau ? rl : none;
+          c += rel[h][w] != none ? 1 : 0;
+        }
+      // this lane's kept values, placed after the lower lanes' (one warp-wide scan per step)
       int incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
       }
       int pos = C + incl - c;
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < kSwH; ++h)
 #pragma unroll
         for (int w = 0; w < 4; ++w)
           if (rel[h][w] != none) {
@@ -1321,7 +1375,7 @@ __global__ void __launch_bounds__(32 * kSwWarps) lm_select_warp_kernel(const Sel
     }
   }
   if (C > kSwCand) {
-    if (lane == 0) flags[q] = 1;
+    if (lane == 0) flag_query(flags, q);
     return;
   }
   __syncwarp();
@@ -1348,24 +1402,34 @@ __global__ void __launch_bounds__(32 * kSwWarps) lm_select_warp_kernel(const Sel
       need -= before;
       if (inbin <= kSwBin) break;
       if (sh == 0) {  // more than kSwBin candidates tied at one distance
-        if (lane == 0) flags[q] = 1;
+        if (lane == 0) flag_query(flags, q);
         return;
       }
     }
     w = w0 + span;
   }
-  // the window's entries as full keys
+  // the window's entries as full keys (four item-id loads in flight per lane)
   int M = 0;
-  for (int f0 = 0; f0 < C; f0 += 32) {
-    const int f = f0 + lane;
-    const bool in = f < C && S.cd[f] < w;
-    const unsigned bt = __ballot_sync(kFull, in);
-    if (in) {
-      const int t = S.cf[f];
-      const int32_t id = __ldg(a.ids + static_cast<int64_t>(S.pl[t >> 24]) * L + (t & 0xffffff));
-      S.keys[M + __popc(bt & lt)] = Tr::key(static_cast<T>(S.cd[f] + dmin), id);
+  for (int f0 = 0; f0 < C; f0 += 128) {
+    int32_t id[4];
+    bool in[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = f0 + 32 * u + lane;
+      in[u] = f < C && S.cd[f] < w;
+      id[u] = 0;
+      if (in[u]) {
+        const int t = S.cf[f];
+        id[u] = __ldg(a.ids + static_cast<int64_t>(S.pl[t >> 24]) * L + (t & 0xffffff));
+      }
     }
-    M += __popc(bt);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = f0 + 32 * u + lane;
+      const unsigned bt = __ballot_sync(kFull, in[u]);
+      if (in[u]) S.keys[M + __popc(bt & lt)] = Tr::key(static_cast<T>(S.cd[f] + dmin), id[u]);
+      M += __popc(bt);
+    }
   }
   __syncwarp();
   V3DB_DCHECK(M <= kSwKeys);
@@ -1421,17 +1485,21 @@ __global__ void __launch_bounds__(32 * kSwWarps) lm_select_warp_kernel(const Sel
   }
 }
 
-// The queries the cached path flagged (or every query when it does not apply): one CTA each.
+// The queries the cached path flagged (flags[0] of them, listed in flags[1..]), or every query when
+// it does not apply (flags NULL): a grid-stride loop, one query per CTA at a time.
 template <class T>
-__global__ void __launch_bounds__(kSelThreads) lm_select_cta_kernel(const SelArgs<T> a, const int* __restrict__ flags) {
+__global__ void __launch_bounds__(kSelThreads) lm_select_cta_kernel(const SelArgs<T> a, const int* __restrict__ flags,
+                                                                     int64_t nq) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int64_t q = blockIdx.x;
-  if (flags && flags[q] == 0) return;
-  select_streaming<T>(a, q, sm);
+  const int64_t n = flags ? flags[0] : nq;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    select_streaming<T>(a, flags ? flags[1 + i] : i, sm);
+    __syncthreads();  // the shared memory is reused by the next query
+  }
 }
 
 // Step 5 launch (both distance types): the cached selection, then the streaming one for the queries
-// it flagged; flags: scratch int [nq].
+// it flagged; flags: scratch int [1 + nq] (a count, then the flagged query indices).
 template <class T>
 cudaError_t launch_select(const SelArgs<T>& sa, int64_t nq, int* flags, cudaStream_t st) {
   using Key = typename DistT<T>::Key;
@@ -1444,7 +1512,7 @@ cudaError_t launch_select(const SelArgs<T>& sa, int64_t nq, int* flags, cudaStre
   const bool warp = fast && tot_g <= 32 * 64 && (sopt == 2 || (sopt == 0 && tot_g >= 8 * static_cast<int64_t>(sa.k)));
   cudaError_t e = cudaSuccess;
   if (fast) {
-    e = cudaMemsetAsync(flags, 0, sizeof(int) * nq, st);
+    e = cudaMemsetAsync(flags, 0, sizeof(int), st);
     if (e == cudaSuccess && warp) {
       const size_t wsm = sizeof(SwSmem<T>) * kSwWarps;
       const unsigned g = static_cast<unsigned>((nq + kSwWarps - 1) / kSwWarps);
@@ -1469,7 +1537,10 @@ cudaError_t launch_select(const SelArgs<T>& sa, int64_t nq, int* flags, cudaStre
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(lm_select_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm));
   if (e == cudaSuccess) {
-    lm_select_cta_kernel<T><<<static_cast<unsigned>(nq), kSelThreads, ssm, st>>>(sa, fast ? flags : nullptr);
+    // flagged queries are rare: a small grid that exits at once when there are none (an nq-CTA grid
+    // cost 9-30 us of empty blocks per call)
+    const int64_t grid = fast ? std::min<int64_t>(nq, 4 * 148) : nq;
+    lm_select_cta_kernel<T><<<static_cast<unsigned>(grid), kSelThreads, ssm, st>>>(sa, fast ? flags : nullptr, nq);
     note_launch();
     e = cudaGetLastError();
   }
@@ -1857,7 +1928,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   const int64_t max_items = nlist + npairs / NT + 1;
   const size_t b_hist = al(sizeof(int) * nlist, 256), b_pairs = al(sizeof(int32_t) * npairs, 256),
                b_items = al(sizeof(int4) * max_items, 256),
-               b_gmin = al(sizeof(int32_t) * npairs * ngroups, 256) + al(sizeof(int) * nq, 256),  // + flags
+               b_gmin = al(sizeof(int32_t) * npairs * ngroups, 256) + al(sizeof(int) * (nq + 1), 256),  // + flags
                b_trace = trace_cand ? 0 : al(sizeof(int32_t) * npairs * L, 256);
   uint8_t* base = nullptr;
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&base), 3 * b_hist + 256 + b_pairs + b_items + b_gmin + b_trace, st);
@@ -1978,7 +2049,7 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
   const int64_t max_items = nlist + npairs / kNTF + 1;
   const size_t b_hist = al(sizeof(int) * nlist, 256), b_pairs = al(sizeof(int32_t) * npairs, 256),
                b_items = al(sizeof(int4) * max_items, 256), b_ql = al(3ull * nq * s->dim, 256),
-               b_gmin = al(sizeof(int64_t) * npairs * ngroups, 256) + al(sizeof(int) * nq, 256),  // + flags
+               b_gmin = al(sizeof(int64_t) * npairs * ngroups, 256) + al(sizeof(int) * (nq + 1), 256),  // + flags
                b_trace = trace_cand ? 0 : al(sizeof(int64_t) * npairs * L, 256);
   uint8_t* base = nullptr;
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&base),
