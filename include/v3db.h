@@ -302,9 +302,11 @@ int64_t v3db_kernel_launches(void);
  *   V3DB_OPT_FX_SCAN      fixed-point Steps 3-5: 0 auto (list-major on the tensor cores, int8 limbs,
  *                         where the snapshot holds the limb planes: dim % 16 == 0, dim <= 256,
  *                         nlist <= 32768), 1 always the literal per-query int64 LUT scan
- *   V3DB_OPT_COARSE_KEYS  keys kept per 32-list block by the single-pass Steps 1-2: 0 auto (2 for
- *                         dim <= 256, 4 above, where recomputing a block in the merge is expensive),
- *                         2 or 4 */
+ *   V3DB_OPT_COARSE_KEYS  keys kept per 32-list block by the single-pass Steps 1-2: 0 auto (the
+ *                         smallest of 2 / 4 / 8 that is >= nprobe where nprobe <= 8 -- nlist <= 16384
+ *                         for 8 -- so that the kept keys hold the whole top nprobe and no block is
+ *                         recomputed; otherwise 2 for dim <= 256, 4 above, where recomputing a block
+ *                         in the merge is expensive), 2, 4 or 8 (8 only where nprobe <= 8) */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2

@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
         // |32 e| < 2^31 for dim <= 1024; padding columns: acc = 0, p = +inf); per 32-list block the
         // KB = GT smallest keys (an insertion network: 2 KB - 1 IMNMX per column)
         constexpr int KB = GT;
-        static_assert(KB == 2 || KB == 4, "keys per block");
+        static_assert(KB == 2 || KB == 4 || KB == 8, "keys per block");
         int m[2][KB];
         auto topk = [&](int cb, int(&mk)[KB]) {
           const int4* c4 = reinterpret_cast<const int4*>(cn + cb);
@@ -319,9 +319,14 @@ __global__ void __launch_bounds__(kThreads, 1) coarse_tc_kernel(const __grid_con
           int4* dst = reinterpret_cast<int4*>(a.gmin + KB * (row * a.ngroups + c * 8 + h * 2));
           if constexpr (KB == 2) {
             dst[0] = make_int4(m[0][0], m[0][1], m[1][0], m[1][1]);
-          } else {
+          } else if constexpr (KB == 4) {
             dst[0] = make_int4(m[0][0], m[0][1], m[0][2], m[0][3]);
             dst[1] = make_int4(m[1][0], m[1][1], m[1][2], m[1][3]);
+          } else {
+            dst[0] = make_int4(m[0][0], m[0][1], m[0][2], m[0][3]);
+            dst[1] = make_int4(m[0][4], m[0][5], m[0][6], m[0][7]);
+            dst[2] = make_int4(m[1][0], m[1][1], m[1][2], m[1][3]);
+            dst[3] = make_int4(m[1][4], m[1][5], m[1][6], m[1][7]);
           }
         }
         continue;
@@ -623,7 +628,9 @@ __device__ __forceinline__ uint64_t merge_key(int e, int i) {
   return (static_cast<uint64_t>(static_cast<uint32_t>(e + (1 << 30))) << 32) | static_cast<uint32_t>(i);
 }
 // NV: int4 per lane held in registers: KB = 2 keys per block -> two blocks per int4 (nblk / 2 <= 32 NV);
-// KB = 4 -> one block per int4 (nblk <= 32 NV).
+// KB = 4 -> one block per int4 (nblk <= 32 NV); KB = 8 -> half a block per int4 (2 nblk <= 32 NV).
+// KB >= R: every list of the row's true top R is among the stored keys (a list missing from its block
+// has KB >= R smaller keys in that block alone), so no block is recomputed.
 template <int KR, int NV, int KB>
 __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* __restrict__ X, int64_t n, int dim,
                                                                 const int8_t* __restrict__ mu,
@@ -645,7 +652,8 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
                    warp * (cap + cap / 4);
   if (row >= n) return;
   const int8_t* x = X + row * dim;
-  const int nv4 = KB == 2 ? nblk >> 1 : nblk;  // int4s per row
+  const int nv4 = KB == 2 ? nblk >> 1 : KB == 4 ? nblk : 2 * nblk;  // int4s per row
+  const bool complete = KB >= R;                                        // no block to recompute
   const int4* src = reinterpret_cast<const int4*>(bk + row * nblk * KB);
   int4 v[NV];
 #pragma unroll
@@ -739,11 +747,24 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
   for (int u = 0; u < NV; ++u) {
     const int i = 32 * u + lane;
     const int w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+    if constexpr (KB == 8) {  // half a block per int4; complete (R <= 8)
+      const int b = i >> 1;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int mk = w[t];
+        const bool take = mk != kInf && (mk >> 5) <= tau;
+        const unsigned bal = __ballot_sync(kFull, take);
+        const int pos = nc + __popc(bal & lt);
+        if (take && pos < cap) keys[pos] = merge_key(mk >> 5, b * 32 + (mk & 31));
+        nc += __popc(bal);
+      }
+      continue;
+    }
 #pragma unroll
     for (int hb = 0; hb < 4 / KB; ++hb) {
       const int b = (4 / KB) * i + hb, last = w[hb * KB + KB - 1];
       // a block whose KB-th key has e <= tau may hold more candidates than it stored: recompute it
-      const bool rec = last != kInf && (last >> 5) <= tau;
+      const bool rec = !complete && last != kInf && (last >> 5) <= tau;
       unsigned bal = __ballot_sync(kFull, rec);
       int pos = nr + __popc(bal & lt);
       if (rec && pos < kRecCap) rb[pos] = b;
@@ -765,12 +786,13 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
     // lane = list of the block; two blocks per step, 8 independent 16-byte loads each in flight
     const int nu = dim >> 4;
     for (int t = 0; t < nr; t += 2) {
-      int li[2], dot[2] = {0, 0};
+      int li[2], dot[2] = {0, 0}, cnl[2];
       const int4* m4[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         li[h] = t + h < nr ? rb[t + h] * 32 + lane : nlist;
         m4[h] = reinterpret_cast<const int4*>(mu + static_cast<int64_t>(min(li[h], nlist - 1)) * dim);
+        cnl[h] = li[h] < nlist ? __ldg(cnorm + li[h]) : 0;  // in flight with the centroid loads
       }
       for (int u0 = 0; u0 < nu; u0 += 8) {
         int4 q[2][8];
@@ -791,7 +813,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* _
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int e = li[h] < nlist ? __ldg(cnorm + li[h]) - 2 * dot[h] : 0;
+        const int e = li[h] < nlist ? cnl[h] - 2 * dot[h] : 0;
         const bool take = li[h] < nlist && e <= tau;
         const unsigned bal = __ballot_sync(kFull, take);
         const int pos = nc + __popc(bal & lt);
@@ -979,7 +1001,14 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
   // keys kept per 32-list block: 2, or 4 where recomputing a block is expensive (dim > 256: the merge
   // then rarely recomputes); V3DB_OPT_COARSE_KEYS forces either
   const int64_t kopt = opt(V3DB_OPT_COARSE_KEYS);
-  const int KB = kopt == 2 || kopt == 4 ? static_cast<int>(kopt) : dim > 256 ? 4 : 2;
+  // 8 (or the smallest of 2 / 4 / 8 >= R) where R <= 8: the stored keys then hold the whole top R and
+  // the merge recomputes nothing (C1, C2: R = 8)
+  const int KB = kopt == 2 || kopt == 4 || (kopt == 8 && R <= 8 && nlist <= 16384) ? static_cast<int>(kopt)
+                 : R <= 2                           ? 2
+                 : R <= 4                           ? 4
+                 : R <= 8 && nlist <= 16384         ? 8  // (merge: <= 32 int4 per lane)
+                 : dim > 256                        ? 4
+                                                    : 2;
   const size_t b_g = align256(sizeof(int32_t) * n * ngroups * (top2 ? KB : 1)), b_t = align256(sizeof(int32_t) * n),
                b_c = align256(sizeof(uint64_t) * n * capc), b_n = align256(sizeof(int) * n);
   uint8_t* base = nullptr;
@@ -1016,14 +1045,15 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e == cudaSuccess) kern<<<grid, kThreads, smem, st>>>(tmX, tmMu, a);
     };
-    if (KB == 4) pass3(coarse_tc_kernel<3, 4>);
+    if (KB == 8) pass3(coarse_tc_kernel<3, 8>);
+    else if (KB == 4) pass3(coarse_tc_kernel<3, 4>);
     else pass3(coarse_tc_kernel<3, 2>);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) e = debug_sync(st, "coarse pass (block top-2)");
     const int cap = (2 * R + 64 + 3) & ~3;  // (a multiple of 4: cap / 4 key slots hold the 16-bit bin order)
     const size_t msmem = 4 * kMergeWarps * (256 + kRecCap) + static_cast<size_t>(kMergeWarps) * dim +
                          sizeof(uint64_t) * kMergeWarps * (cap + cap / 4);
-    const int nv4 = KB == 2 ? ngroups / 2 : ngroups;
+    const int nv4 = KB == 2 ? ngroups / 2 : KB == 4 ? ngroups : 2 * ngroups;
     if (e == cudaSuccess) {
       dispatch_kr(R, [&]<int KR>() {
         auto run = [&](auto kern) {
@@ -1040,7 +1070,8 @@ cudaError_t coarse_topk(const int8_t* X, int64_t n, int dim, const int8_t* mu, c
           else if (nv4 <= 512) run(merge_kernel<KR, 16, KBT>);
           else run(merge_kernel<KR, 32, KBT>);
         };
-        if (KB == 4) by_nv.template operator()<4>();
+        if (KB == 8) by_nv.template operator()<8>();
+        else if (KB == 4) by_nv.template operator()<4>();
         else by_nv.template operator()<2>();
       });
       if (e == cudaSuccess) e = cudaGetLastError();

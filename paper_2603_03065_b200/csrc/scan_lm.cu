@@ -488,11 +488,66 @@ __global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restri
   }
 }
 
-__global__ void pair_scatter_kernel(const int32_t* __restrict__ lists, int64_t npairs, int* __restrict__ cur,
-                                    int32_t* __restrict__ pairs) {
-  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npairs;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    pairs[atomicAdd(cur + __ldg(lists + p), 1)] = static_cast<int32_t>(p);
+// The pair ids grouped by list: pairs[cur[list]++] = p (the order inside a list is free: every pair
+// has its own trace row and group minima).  Each thread takes kScatPer pairs with all their atomics
+// in flight at once (one latency per thread, not one per pair).
+constexpr int kScatPer = 8;
+__global__ void __launch_bounds__(256) pair_scatter_kernel(const int32_t* __restrict__ lists, int64_t npairs,
+                                                           int* __restrict__ cur, int32_t* __restrict__ pairs) {
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 256 * kScatPer + threadIdx.x;
+  int l[kScatPer], pos[kScatPer];
+#pragma unroll
+  for (int u = 0; u < kScatPer; ++u) {
+    const int64_t p = p0 + 256 * u;
+    l[u] = p < npairs ? __ldg(lists + p) : -1;
+  }
+#pragma unroll
+  for (int u = 0; u < kScatPer; ++u) pos[u] = l[u] >= 0 ? atomicAdd(cur + l[u], 1) : 0;
+#pragma unroll
+  for (int u = 0; u < kScatPer; ++u)
+    if (l[u] >= 0) pairs[pos[u]] = static_cast<int32_t>(p0 + 256 * u);
+}
+// The same for few lists (nlist <= kScatSmemLists), where many pairs share a list and the global
+// atomics on one counter serialise (C1: 312 pairs per list): the CTA's kScatPer * 256 pairs are
+// counted per list in shared memory, each list touched reserves its range with ONE global atomic,
+// and the pairs are placed from there.
+constexpr int kScatSmemLists = 8192;
+__global__ void __launch_bounds__(256) pair_scatter_smem_kernel(const int32_t* __restrict__ lists, int64_t npairs,
+                                                                int nlist, int* __restrict__ cur,
+                                                                int32_t* __restrict__ pairs) {
+  extern __shared__ int cnt[];  // [nlist]: counts, then each list's global base
+  for (int i = threadIdx.x; i < nlist; i += 256) cnt[i] = 0;
+  __syncthreads();
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 256 * kScatPer + threadIdx.x;
+  int l[kScatPer], pos[kScatPer];
+#pragma unroll
+  for (int u = 0; u < kScatPer; ++u) {
+    const int64_t p = p0 + 256 * u;
+    l[u] = p < npairs ? __ldg(lists + p) : -1;
+  }
+#pragma unroll
+  for (int u = 0; u < kScatPer; ++u) pos[u] = l[u] >= 0 ? atomicAdd(cnt + l[u], 1) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nlist; i += 256)
+    if (cnt[i]) cnt[i] = atomicAdd(cur + i, cnt[i]);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kScatPer; ++u)
+    if (l[u] >= 0) pairs[cnt[l[u]] + pos[u]] = static_cast<int32_t>(p0 + 256 * u);
+}
+cudaError_t launch_pair_scatter(const int32_t* lists, int64_t npairs, int nlist, int* cur, int32_t* pairs,
+                                cudaStream_t st) {
+  const unsigned g = static_cast<unsigned>((npairs + 256 * kScatPer - 1) / (256 * kScatPer));
+  if (g == 0) return cudaSuccess;
+  if (nlist <= kScatSmemLists) {
+    const int sm = static_cast<int>(sizeof(int) * nlist);
+    cudaError_t e = cudaFuncSetAttribute(pair_scatter_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e != cudaSuccess) return e;
+    pair_scatter_smem_kernel<<<g, 256, sm, st>>>(lists, npairs, nlist, cur, pairs);
+  } else {
+    pair_scatter_kernel<<<g, 256, 0, st>>>(lists, npairs, cur, pairs);
+  }
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -1224,17 +1279,27 @@ __global__ void __launch_bounds__(32 * kSwWarps) lm_select_warp_kernel(const Sel
   const T* tq = a.trace + q * nprobe * static_cast<int64_t>(L);
   const unsigned lt = (1u << lane) - 1u;
   const U none = ~U(0);
-  // the group minima (element 32 u + lane in gv[u]; beyond tot: the sentinel)
+  // the probed lists first (their counts are a second dependent load), then the group minima
+  // (element 32 u + lane in gv[u]; beyond tot: the sentinel), all in flight together
+  int pli[kWarpProbeCap / 32];
+#pragma unroll
+  for (int x = 0; x < kWarpProbeCap / 32; ++x) {
+    const int r = 32 * x + lane;
+    pli[x] = r < nprobe ? a.lists[q * nprobe + r] : 0;
+  }
   T gv[NPL];
 #pragma unroll
   for (int u = 0; u < NPL; ++u) {
     const int i = 32 * u + lane;
     gv[u] = i < tot ? gq[i] : Tr::kMax;
   }
-  for (int r = lane; r < nprobe; r += 32) {
-    const int li = a.lists[q * nprobe + r];
-    S.pl[r] = li;
-    S.pc[r] = __ldg(a.counts + li);
+#pragma unroll
+  for (int x = 0; x < kWarpProbeCap / 32; ++x) {
+    const int r = 32 * x + lane;
+    if (r < nprobe) {
+      S.pl[r] = pli[x];
+      S.pc[r] = __ldg(a.counts + pli[x]);
+    }
   }
   T mn = Tr::kMax, mx = 0;
   int V = 0;
@@ -1956,8 +2021,12 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   }
   const int* hsrc = list_hist ? list_hist : hist;
   lm_scan_items_kernel<<<1, 1024, 0, st>>>(hsrc, nlist, NT, cur, items, n_items);
-  pair_scatter_kernel<<<pg, 256, 0, st>>>(lists, npairs, cur, pairs);
+  e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
   note_launch(2);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(base, st);
+    return e;
+  }
   if (prof) prof(2, st);
 
   LmArgs a;
@@ -2079,8 +2148,12 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
   const unsigned pg = static_cast<unsigned>(std::min<int64_t>((npairs + 255) / 256, 4 * sms));
   pair_hist_kernel<<<pg, 256, 0, st>>>(lists, npairs, hist);
   lm_scan_items_kernel<<<1, 1024, 0, st>>>(hist, nlist, kNTF, cur, items, n_items);
-  pair_scatter_kernel<<<pg, 256, 0, st>>>(lists, npairs, cur, pairs);
+  e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
   note_launch(4);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(base, st);
+    return e;
+  }
   if (prof) prof(2, st);
 
   LmFxArgs a;

@@ -503,10 +503,37 @@ def test_lm_select_ties_beyond_window(v3db):
                  algos=("lm", "gen"))
 
 
-@pytest.mark.parametrize("keys", [2, 4])
+@pytest.mark.parametrize("nprobe", [2, 3, 8])
+def test_coarse_complete_blocks_adversarial(v3db, nprobe):
+    """nprobe <= 8: the single pass keeps the smallest 2 / 4 / 8 >= nprobe keys of every 32-list
+    block and the merge recomputes nothing (a list of the true top nprobe missing from its block
+    would have >= nprobe smaller keys in that block alone).  Adversarial: every block's centroids
+    are drawn around one centre, so a query's nearest lists share one block, with a duplicated
+    centroid (ties on d_i broken by the list index, R9).  Equals the oracle; the two-pass path and
+    two kept keys (recomputing the blocks) beside it."""
+    rng = np.random.default_rng(23)
+    D, nlist, L, k = 32, 512, 64, 10
+    centres = rng.integers(-100, 100, size=(16, D))
+    N = nlist * 8
+    db = np.clip(centres[np.arange(N) // (N // 16)] + rng.integers(-3, 4, size=(N, D)), -127, 127).astype(np.int8)
+    db[8 * 6] = db[8 * 5]
+    db[8 * 40] = db[8 * 37]
+    cent = np.arange(0, N, 8)[:nlist]
+    qs = np.clip(centres[rng.integers(0, 16, 40)] + rng.integers(-4, 5, size=(40, D)), -127, 127).astype(np.int8)
+    qs = np.vstack([qs, db[8 * 5][None], db[8 * 37][None]])
+    code = np.stack([rng.choice(N, 16, replace=False) for _ in range(4)])
+    run_case(v3db, db, qs, nlist, L, 4, 16, nprobe, k, cent, code, algos=("lm", "gen"))
+    with v3db.option(v3db.OPT_COARSE_KEYS, 2):
+        run_case(v3db, db, qs, nlist, L, 4, 16, nprobe, k, cent, code, algos=("lm",))
+    with v3db.option(v3db.OPT_COARSE_2PASS, 1):
+        run_case(v3db, db, qs, nlist, L, 4, 16, nprobe, k, cent, code, algos=("lm",))
+
+
+@pytest.mark.parametrize("keys", [2, 4, 8])
 @pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_large"])
 def test_coarse_keys_per_block(v3db, name, keys):
-    """Single-pass Steps 1-2 keeping 2 or 4 keys per 32-list block: the same bits."""
+    """Single-pass Steps 1-2 keeping 2, 4 or 8 keys per 32-list block (8 only where nprobe <= 8,
+    e.g. C1; elsewhere the option falls back to the automatic choice): the same bits."""
     cfg, inp, ref_s, ref = config_case(name)
     s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
     with v3db.option(v3db.OPT_COARSE_KEYS, keys):
