@@ -632,7 +632,10 @@ __device__ __forceinline__ uint64_t merge_key(int e, int i) {
 // KB >= R: every list of the row's true top R is among the stored keys (a list missing from its block
 // has KB >= R smaller keys in that block alone), so no block is recomputed.
 template <int KR, int NV, int KB>
-__global__ void __launch_bounds__(32 * kMergeWarps) merge_kernel(const int8_t* __restrict__ X, int64_t n, int dim,
+#ifndef V3DB_MERGE_MINB
+#define V3DB_MERGE_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * kMergeWarps, V3DB_MERGE_MINB) merge_kernel(const int8_t* __restrict__ X, int64_t n, int dim,
                                                                 const int8_t* __restrict__ mu,
                                                                 const int32_t* __restrict__ cnorm, int nlist,
                                                                 int nblk, int R, int cap,

@@ -308,6 +308,9 @@ __global__ void __launch_bounds__(32 * kFxMergeWarps) fx_merge_tc_kernel(
   int* wh = reinterpret_cast<int*>(msm) + warp * 256;
   int* rb = reinterpret_cast<int*>(msm) + kFxMergeWarps * 256 + warp * kFxRecCap;
   FxKey* keys = reinterpret_cast<FxKey*>(msm + 4 * kFxMergeWarps * (256 + kFxRecCap)) + warp * cap;
+  // per warp: one recomputed block's 32 centroid rows, then the row x ([33][dim] int32)
+  int4* stage = reinterpret_cast<int4*>(msm + 4 * kFxMergeWarps * (256 + kFxRecCap) + sizeof(FxKey) * kFxMergeWarps * cap) +
+                static_cast<size_t>(warp) * 33 * (dim >> 2);
   if (row >= n) return;
   const int32_t* x = X + row * dim;
   long long xn = 0;
@@ -426,35 +429,37 @@ __global__ void __launch_bounds__(32 * kFxMergeWarps) fx_merge_tc_kernel(
   __syncwarp();
   bool over = nr > kFxRecCap;
   if (!over) {
-    for (int t = 0; t < nr; ++t) {  // lane = list of the block: exact int64 e
+    // lane = list of the block: exact int64 e.  The block's 32 rows (dim int32 each) arrive in shared
+    // memory by cp.async -- all of a row's 16-byte pieces in flight at once, no registers held -- and
+    // lane l reads its row's pieces in the rotated order (u + l) mod nu (conflict-free banks).
+    const int nu = dim >> 2;
+    int4* xs = stage + 32 * nu;
+    for (int c = lane; c < nu; c += 32) xs[c] = __ldg(reinterpret_cast<const int4*>(x) + c);
+    for (int t = 0; t < nr; ++t) {
       const int li = rb[t] * 32 + lane;
-      bool take = false;
-      long long e = 0;
-      if (li < nlist) {
-        const int4* m4 = reinterpret_cast<const int4*>(mu + static_cast<int64_t>(li) * dim);
-        const int4* x4 = reinterpret_cast<const int4*>(x);
-        long long dot = 0;
-        const int nu = dim >> 2;
-        for (int u0 = 0; u0 < nu; u0 += 8) {
-          int4 q[8];
-#pragma unroll
-          for (int w = 0; w < 8; ++w) q[w] = u0 + w < nu ? __ldg(m4 + u0 + w) : make_int4(0, 0, 0, 0);
-#pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            if (u0 + w < nu) {
-              const int4 p = __ldg(x4 + u0 + w);
-              dot += static_cast<long long>(p.x) * q[w].x + static_cast<long long>(p.y) * q[w].y +
-                     static_cast<long long>(p.z) * q[w].z + static_cast<long long>(p.w) * q[w].w;
-            }
-          }
-        }
-        e = __ldg(cnorm + li) - 2 * dot;
-        take = e <= tau;
+      const bool ok = li < nlist;
+      const int4* m4 = reinterpret_cast<const int4*>(mu + static_cast<int64_t>(ok ? li : 0) * dim);
+      int4* mine = stage + lane * nu;
+      for (int c = 0; c < nu; ++c) tc::cp_async16(mine + c, m4 + c, ok ? 16 : 0);
+      tc::cp_async_commit();
+      const long long cnl = ok ? __ldg(cnorm + li) : 0;
+      tc::cp_async_wait<0>();
+      __syncwarp();
+      long long dot = 0;
+      int c = lane % nu;
+      for (int u = 0; u < nu; ++u) {
+        const int4 q = mine[c], p = xs[c];
+        dot += static_cast<long long>(p.x) * q.x + static_cast<long long>(p.y) * q.y +
+               static_cast<long long>(p.z) * q.z + static_cast<long long>(p.w) * q.w;
+        if (++c == nu) c = 0;
       }
+      const long long e = cnl - 2 * dot;
+      const bool take = ok && e <= tau;
       const unsigned bal = __ballot_sync(kFull, take);
       const int pos = nc + __popc(bal & lt);
       if (take && pos < cap) keys[pos] = FxKey{e, li};
       nc += __popc(bal);
+      __syncwarp();  // every lane is done with the stage before the next block's copies
     }
   }
   over = over || nc > cap;
@@ -577,7 +582,8 @@ cudaError_t fx_topk_tc(const int32_t* X, int64_t n, int dim, const int32_t* mu, 
   if (e == cudaSuccess) e = debug_sync(st, "fx coarse (tensor cores)");
   if (e == cudaSuccess) {
     const int cap = 2 * R + 64;
-    const size_t msmem = 4 * kFxMergeWarps * (256 + kFxRecCap) + sizeof(FxKey) * kFxMergeWarps * cap;
+    const size_t msmem = 4 * kFxMergeWarps * (256 + kFxRecCap) + sizeof(FxKey) * kFxMergeWarps * cap +
+                         sizeof(int32_t) * kFxMergeWarps * 33 * static_cast<size_t>(dim);  // + block stages
     const int nblk = (nlist + kFBlk - 1) / kFBlk;  // blocks of 32 lists holding a list (row stride 3 nchunks)
     dispatch_kr(R, [&]<int KR>() {
       auto run = [&](auto kern) {

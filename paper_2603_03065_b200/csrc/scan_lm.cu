@@ -31,6 +31,8 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "tc_common.cuh"
 #include "topk.cuh"
 #include "v3db_internal.cuh"
@@ -415,77 +417,66 @@ __global__ void pair_hist_kernel(const int32_t* __restrict__ lists, int64_t npai
     atomicAdd(hist + __ldg(lists + p), 1);
 }
 
-// One CTA of 1024 threads: cur[i] = exclusive prefix of hist (the list's first pair in list order,
-// advanced by pair_scatter_kernel), the work items (list, first pair, pairs <= NT) of every list in
-// list order, and *n_items.  Each thread owns a contiguous run of up to kScanPer lists (held in
-// registers), read with 16-byte loads; the block prefix is two warp-shuffle scans.
-constexpr int kScanPer = 32;  // lists per thread: nlist <= 32768
-__global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restrict__ hist, int nlist, int NT,
-                                                             int* __restrict__ cur, int4* __restrict__ items,
-                                                             int* __restrict__ n_items) {
-  __shared__ int wsum[32], wisum[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per = (((nlist + 1023) / 1024) + 3) & ~3, b = threadIdx.x * per;
-  int h[kScanPer];
-  int sum = 0, isum = 0;
-#pragma unroll
-  for (int x = 0; x < kScanPer; x += 4) {
-    int4 v = make_int4(0, 0, 0, 0);
-    if (x < per && b + x < nlist) {
-      if (b + x + 3 < nlist) {
-        v = *reinterpret_cast<const int4*>(hist + b + x);  // b is a multiple of 4; hist 256-byte aligned
-      } else {
-        v.x = hist[b + x];
-        v.y = b + x + 1 < nlist ? hist[b + x + 1] : 0;
-        v.z = b + x + 2 < nlist ? hist[b + x + 2] : 0;
-      }
-    }
-    h[x] = v.x, h[x + 1] = v.y, h[x + 2] = v.z, h[x + 3] = v.w;
-  }
-#pragma unroll
-  for (int x = 0; x < kScanPer; ++x) {
-    sum += h[x];
-    isum += (h[x] + NT - 1) / NT;
-  }
-  int incl = sum, iincl = isum;
+// cur[i] = exclusive prefix of hist (the list's first pair in list order, advanced by the pair
+// scatter), the work items (list, first pair, pairs <= NT) of every list in list order, and
+// *n_items.  One CTA of 1024 threads per 1024 lists (a cooperative launch, <= 32 CTAs): a block scan,
+// the CTA totals exchanged through agg[] across one grid barrier, then contiguous cur / item stores.
+// (One CTA for every list spent ~31 us at C4 on its dependent scan chains at ~1 IPC.)
+__device__ __forceinline__ int2 warp_incl_scan2(int2 v, int lane) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o), z = __shfl_up_sync(0xffffffffu, iincl, o);
+    const int y = __shfl_up_sync(0xffffffffu, v.x, o), z = __shfl_up_sync(0xffffffffu, v.y, o);
     if (lane >= o) {
-      incl += y;
-      iincl += z;
+      v.x += y;
+      v.y += z;
     }
   }
-  if (lane == 31) {
-    wsum[warp] = incl;
-    wisum[warp] = iincl;
-  }
+  return v;
+}
+__global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restrict__ hist, int nlist, int NT,
+                                                             int* __restrict__ cur, int4* __restrict__ items,
+                                                             int* __restrict__ n_items, int2* __restrict__ agg) {
+  __shared__ int2 wt[32];
+  __shared__ int2 base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, i = (blockIdx.x << 10) + tid;
+  const int h = i < nlist ? __ldg(hist + i) : 0, ni = (h + NT - 1) / NT;
+  const int2 inc = warp_incl_scan2(make_int2(h, ni), lane);
+  if (lane == 31) wt[warp] = inc;
   __syncthreads();
   if (warp == 0) {
-    int a0 = wsum[lane], a1 = wisum[lane];
+    const int2 v = wt[lane];
+    const int2 wi = warp_incl_scan2(v, lane);
+    wt[lane] = make_int2(wi.x - v.x, wi.y - v.y);
+    if (lane == 31) agg[blockIdx.x] = wi;  // this CTA's totals
+  }
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  if (warp == 0) {  // the totals of the CTAs before this one
+    int2 v = lane < static_cast<int>(blockIdx.x) ? agg[lane] : make_int2(0, 0);
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, a0, o), z = __shfl_up_sync(0xffffffffu, a1, o);
-      if (lane >= o) {
-        a0 += y;
-        a1 += z;
-      }
+    for (int o = 16; o > 0; o >>= 1) {
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
     }
-    wsum[lane] = a0 - wsum[lane];    // exclusive per-warp offsets
-    wisum[lane] = a1 - wisum[lane];
-    if (lane == 31) *n_items = a1;
+    if (lane == 0) {
+      base = v;
+      if (blockIdx.x == gridDim.x - 1) *n_items = v.y + agg[blockIdx.x].y;
+    }
   }
   __syncthreads();
-  int run = wsum[warp] + incl - sum, irun = wisum[warp] + iincl - isum;
-#pragma unroll
-  for (int x = 0; x < kScanPer; ++x) {
-    const int i = b + x;
-    if (x < per && i < nlist) {
-      cur[i] = run;
-      for (int r = 0; r * NT < h[x]; ++r) items[irun++] = make_int4(i, run + r * NT, min(NT, h[x] - r * NT), 0);
-      run += h[x];
-    }
+  if (i < nlist) {
+    const int run = base.x + wt[warp].x + inc.x - h;
+    int irun = base.y + wt[warp].y + inc.y - ni;
+    cur[i] = run;
+    for (int q = 0; q < ni; ++q) items[irun++] = make_int4(i, run + q * NT, min(NT, h - q * NT), 0);
   }
+}
+cudaError_t launch_scan_items(const int* hist, int nlist, int NT, int* cur, int4* items, int* n_items, int2* agg,
+                              cudaStream_t st) {
+  const unsigned g = static_cast<unsigned>(std::max(1, (nlist + 1023) >> 10));  // <= 32 (nlist <= 32768)
+  void* args[] = {&hist, &nlist, &NT, &cur, &items, &n_items, &agg};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lm_scan_items_kernel), dim3(g), dim3(1024), args, 0,
+                                     st);
 }
 
 // The pair ids grouped by list: pairs[cur[list]++] = p (the order inside a list is free: every pair
@@ -2000,7 +1991,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   if (e != cudaSuccess) return e;
   int* hist = reinterpret_cast<int*>(base);
   int* cur = reinterpret_cast<int*>(base + b_hist);
-  int* n_items = reinterpret_cast<int*>(base + 3 * b_hist);
+  int* n_items = reinterpret_cast<int*>(base + 3 * b_hist);  // (base + 2 b_hist: the items scan's CTA totals)
   int32_t* pairs = reinterpret_cast<int32_t*>(base + 3 * b_hist + 256);
   int4* items = reinterpret_cast<int4*>(base + 3 * b_hist + 256 + b_pairs);
   int32_t* gmin = reinterpret_cast<int32_t*>(base + 3 * b_hist + 256 + b_pairs + b_items);
@@ -2020,8 +2011,8 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
     note_launch();
   }
   const int* hsrc = list_hist ? list_hist : hist;
-  lm_scan_items_kernel<<<1, 1024, 0, st>>>(hsrc, nlist, NT, cur, items, n_items);
-  e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
+  e = launch_scan_items(hsrc, nlist, NT, cur, items, n_items, reinterpret_cast<int2*>(base + 2 * b_hist), st);
+  if (e == cudaSuccess) e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
   note_launch(2);
   if (e != cudaSuccess) {
     cudaFreeAsync(base, st);
@@ -2122,18 +2113,19 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
                b_trace = trace_cand ? 0 : al(sizeof(int64_t) * npairs * L, 256);
   uint8_t* base = nullptr;
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&base),
-                                2 * b_hist + 256 + b_pairs + b_items + b_ql + b_gmin + b_trace, st);
+                                2 * b_hist + 512 + b_pairs + b_items + b_ql + b_gmin + b_trace, st);
   if (e != cudaSuccess) return e;
   int* hist = reinterpret_cast<int*>(base);
   int* cur = reinterpret_cast<int*>(base + b_hist);
   int* n_items = reinterpret_cast<int*>(base + 2 * b_hist);
-  int32_t* pairs = reinterpret_cast<int32_t*>(base + 2 * b_hist + 256);
-  int4* items = reinterpret_cast<int4*>(base + 2 * b_hist + 256 + b_pairs);
-  int8_t* ql = reinterpret_cast<int8_t*>(base + 2 * b_hist + 256 + b_pairs + b_items);
-  int64_t* gmin = reinterpret_cast<int64_t*>(base + 2 * b_hist + 256 + b_pairs + b_items + b_ql);
+  int2* agg = reinterpret_cast<int2*>(base + 2 * b_hist + 256);  // the items scan's CTA totals (<= 32)
+  int32_t* pairs = reinterpret_cast<int32_t*>(base + 2 * b_hist + 512);
+  int4* items = reinterpret_cast<int4*>(base + 2 * b_hist + 512 + b_pairs);
+  int8_t* ql = reinterpret_cast<int8_t*>(base + 2 * b_hist + 512 + b_pairs + b_items);
+  int64_t* gmin = reinterpret_cast<int64_t*>(base + 2 * b_hist + 512 + b_pairs + b_items + b_ql);
   int* flags = reinterpret_cast<int*>(gmin + npairs * ngroups);
   int64_t* trace = trace_cand ? trace_cand
-                              : reinterpret_cast<int64_t*>(base + 2 * b_hist + 256 + b_pairs + b_items + b_ql + b_gmin);
+                              : reinterpret_cast<int64_t*>(base + 2 * b_hist + 512 + b_pairs + b_items + b_ql + b_gmin);
 
   int dev = 0, sms = 148;
   e = cudaGetDevice(&dev);
@@ -2147,8 +2139,8 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
       queries, nq, s->dim, ql);
   const unsigned pg = static_cast<unsigned>(std::min<int64_t>((npairs + 255) / 256, 4 * sms));
   pair_hist_kernel<<<pg, 256, 0, st>>>(lists, npairs, hist);
-  lm_scan_items_kernel<<<1, 1024, 0, st>>>(hist, nlist, kNTF, cur, items, n_items);
-  e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
+  e = launch_scan_items(hist, nlist, kNTF, cur, items, n_items, agg, st);
+  if (e == cudaSuccess) e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
   note_launch(4);
   if (e != cudaSuccess) {
     cudaFreeAsync(base, st);
