@@ -761,8 +761,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps, V3DB_MERGE_MINB) merge_kerne
         if (take && pos < cap) keys[pos] = merge_key(mk >> 5, b * 32 + (mk & 31));
         nc += __popc(bal);
       }
-      continue;
-    }
+    } else {
 #pragma unroll
     for (int hb = 0; hb < 4 / KB; ++hb) {
       const int b = (4 / KB) * i + hb, last = w[hb * KB + KB - 1];
@@ -781,6 +780,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps, V3DB_MERGE_MINB) merge_kerne
         if (take && pos < cap) keys[pos] = merge_key(mk >> 5, b * 32 + (mk & 31));
         nc += __popc(bal);
       }
+    }
     }
   }
   __syncwarp();

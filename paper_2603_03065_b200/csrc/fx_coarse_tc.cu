@@ -293,7 +293,6 @@ struct FxKey {
   int64_t e;
   int32_t i;
 };
-__device__ __forceinline__ bool fx_less(const FxKey& a, const FxKey& b) { return a.e < b.e || (a.e == b.e && a.i < b.i); }
 
 // NV: the row's stored key pairs per lane held in registers (nblk <= 32 NV).
 template <int KR, int NV>
