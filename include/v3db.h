@@ -306,7 +306,10 @@ int64_t v3db_kernel_launches(void);
  *                         smallest of 2 / 4 / 8 that is >= nprobe where nprobe <= 8 -- nlist <= 16384
  *                         for 8 -- so that the kept keys hold the whole top nprobe and no block is
  *                         recomputed; otherwise 2 for dim <= 256, 4 above, where recomputing a block
- *                         in the merge is expensive), 2, 4 or 8 (8 only where nprobe <= 8) */
+ *                         in the merge is expensive), 2, 4 or 8 (8 only where nprobe <= 8)
+ *   V3DB_OPT_LM_STATIC    list-major scan (int8): 0 the CTAs of the main kernel draw their work
+ *                         items from a grid-wide counter (a CTA takes its next item when it is ready
+ *                         for one), 1 the static round-robin deal (item j to CTA j mod grid) */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2
@@ -324,7 +327,8 @@ int64_t v3db_kernel_launches(void);
 #define V3DB_OPT_FX_COARSE 14
 #define V3DB_OPT_FX_SCAN 15
 #define V3DB_OPT_COARSE_KEYS 16
-#define V3DB_OPT_COUNT 17
+#define V3DB_OPT_LM_STATIC 17
+#define V3DB_OPT_COUNT 18
 int v3db_set_option(int32_t key, int64_t value);
 int64_t v3db_get_option(int32_t key);
 

@@ -25,7 +25,8 @@ SHAPE_GREEDY, SHAPE_REBALANCE = 0, 1
 FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_IDS, FIELD_CODES, FIELD_COUNTS, FIELD_LIST_OF = range(6)
 KIND_INT8, KIND_FX16 = 0, 1
 (OPT_LUT_W32, OPT_COARSE_SIMT, OPT_SCHED, OPT_FX_NOROT, OPT_FX_W12, OPT_SCAN_SEG, OPT_SCAN_NS, OPT_SCAN_CAP,
- OPT_SCAN_FIRST, OPT_SCAN_DIRECT, OPT_LM_NT, OPT_AUTO_SCAN, OPT_COARSE_2PASS, OPT_SELECT_CTA, OPT_FX_COARSE, OPT_FX_SCAN, OPT_COARSE_KEYS) = range(17)
+ OPT_SCAN_FIRST, OPT_SCAN_DIRECT, OPT_LM_NT, OPT_AUTO_SCAN, OPT_COARSE_2PASS, OPT_SELECT_CTA, OPT_FX_COARSE, OPT_FX_SCAN, OPT_COARSE_KEYS,
+ OPT_LM_STATIC) = range(18)
 
 _c_i8p = ctypes.c_void_p
 _c_i32p = ctypes.c_void_p

@@ -47,6 +47,8 @@ constexpr int kEpiWarps = 16;                           // 4 per TMEM lane quadr
 constexpr int kChunk = 16;                              // accumulator columns per tcgen05.ld
 constexpr int kNB = 3;                                  // B operand (query rows) buffers
 constexpr int kWarpTma = 0, kWarpMma = 1, kWarpGat = 2, kNGat = 2, kWarpEpi = 4;
+constexpr int kIR = 8;                                  // item ring entries (lm_kernel's work-item sequence)
+constexpr int kPre = 4;                                 // items published ahead of the one being loaded
 constexpr int kThreads = 32 * (kWarpEpi + kEpiWarps);  // 640
 constexpr uint32_t kFull = 0xffffffffu;
 // staging row of one column (32 slots): 36 words -- the 32 lanes' stores hit distinct banks and the
@@ -58,8 +60,9 @@ struct LmArgs {
   int nprobe, L, Lp, dim, kp, NT, nacc, lg_nacc, S, nb, ngroups;
   const int8_t* queries;
   const int32_t* pairs;   // pair ids (q * nprobe + rho) grouped by list
-  const int4* items;      // (list, first pair, pairs, 0)
+  const int4* items;      // (list, first pair, pairs, valid slots of the list)
   const int* n_items;
+  int* next_item;         // work counter (zeroed by the grouping), or NULL: static round-robin
   const int32_t* ldist;   // [nq * nprobe] d_i of each pair
   const int32_t* counts;  // [nlist]
   const int32_t* pterm;   // [nlist][L]
@@ -116,8 +119,19 @@ __device__ __forceinline__ int colmin_col(int lane) {
 // ----------------------------------------------------------------------------------------------
 // The contraction + epilogue kernel.
 // ----------------------------------------------------------------------------------------------
+#ifdef LM_EXP_TIMES  // experiment build: per-CTA start / end times of lm_kernel (tools/lm_times.py)
+__device__ unsigned long long g_lm_times[2 * 256];
+__device__ __forceinline__ unsigned long long lm_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__ CUtensorMap tmX, const LmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+#ifdef LM_EXP_TIMES
+  if (threadIdx.x == 0) g_lm_times[2 * blockIdx.x] = lm_now();
+#endif
   // 1024-byte alignment by pointer arithmetic on the shared array (an integer round trip would
   // make every access through `smem` a generic-address LD/ST instead of LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -134,7 +148,17 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
   uint64_t* bempty = bfull + kNB;          // [kNB]
   uint64_t* accf = bempty + kNB;           // [nacc]
   uint64_t* acce = accf + a.nacc;          // [nacc]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + a.nacc);
+  uint64_t* ifull = acce + a.nacc;         // [kIR]
+  uint64_t* iempty = ifull + kIR;          // [kIR]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iempty + kIR);
+  // The CTA's work-item sequence.  The TMA thread draws the items -- from the grid-wide counter
+  // next_item (a CTA takes its next item when it is ready for one: the static round-robin deal left
+  // the last CTA 5-20 % behind the mean, tools/lm_times.py) or, without a counter, round-robin -- and
+  // publishes each item (pairs < 0: no more items) through this ring, kPre items ahead of the one
+  // it is loading (the gather works ahead of the loads); every other role reads the sequence from
+  // here, so all roles of the CTA see the same items in the same order.
+  int4* ring = reinterpret_cast<int4*>(
+      smem + ((a.off_bar + 8u * (2 * a.S + 2 * kNB + 2 * a.nacc + 2 * kIR) + 16u + 15u) & ~15u));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_items = *a.n_items;
@@ -144,6 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     for (int s = 0; s < a.S; ++s) {
       tc::mbar_init(afull + s, 1);
       tc::mbar_init(aempty + s, 1);
+    }
+    for (int r = 0; r < kIR; ++r) {
+      tc::mbar_init(ifull + r, 1);
+      tc::mbar_init(iempty + r, 1 + kNGat + kEpiWarps);  // MMA thread, gather warps, epilogue warps
     }
     for (int b = 0; b < kNB; ++b) {
       tc::mbar_init(bfull + b, kNGat);
@@ -166,9 +194,40 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     if (lane == 0) {
       tc::tma_prefetch(&tmX);
       int s = 0, u = 0;
-      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-        const int4 it = a.items[j];
-        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+      // The first kPre items of a CTA are dealt round-robin (their loads in flight together), the
+      // rest drawn from the counter; each draw's atomic is issued one draw early.
+      const int G = static_cast<int>(gridDim.x);
+      int4 pre[kPre];
+#pragma unroll
+      for (int d = 0; d < kPre; ++d) {
+        const int j = static_cast<int>(blockIdx.x) + d * G;
+        pre[d] = j < n_items ? __ldg(a.items + j) : make_int4(0, 0, -1, 0);
+      }
+      int jn = a.next_item ? kPre * G + atomicAdd(a.next_item, 1) : static_cast<int>(blockIdx.x) + kPre * G;
+      int ip = 0;  // items published
+      bool done = false;
+#pragma unroll
+      for (int d = 0; d < kPre; ++d) {
+        if (!done) {
+          ring[d] = pre[d];
+          tc::mbar_arrive(ifull + d);  // release: the entry is written
+          done = pre[d].z < 0;
+          ++ip;
+        }
+      }
+      for (int il = 0;; ++il) {
+        while (!done && ip < il + kPre) {
+          const int r = ip & (kIR - 1), j = jn;
+          if (ip >= kIR) tc::mbar_wait_sleep(iempty + r, (ip / kIR - 1) & 1);  // every reader is past entry ip - kIR
+          done = j >= n_items;
+          ring[r] = done ? make_int4(0, 0, -1, 0) : __ldg(a.items + j);
+          tc::mbar_arrive(ifull + r);
+          ++ip;
+          if (!done) jn = a.next_item ? kPre * G + atomicAdd(a.next_item, 1) : j + G;
+        }
+        const int4 it = ring[il & (kIR - 1)];  // (this thread's own entry: not reused before entry il + kIR)
+        if (it.z < 0) break;
+        const int nvt = (it.w + kTile - 1) / kTile;
         for (int t = 0; t < nvt; ++t) {
           for (int p = 0; p < a.kp; ++p) {
             if (u > 0) tc::mbar_wait_sleep(aempty + s, (u - 1) & 1);
@@ -186,9 +245,13 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       int s = 0, u = 0, b = 0, bph = 0, tcount = 0;
-      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-        const int4 it = a.items[j];
-        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+      for (int i = 0;; ++i) {
+        const int r = i & (kIR - 1);
+        tc::mbar_wait_sleep(ifull + r, (i / kIR) & 1);
+        const int4 it = ring[r];
+        const int nvt = (it.w + kTile - 1) / kTile;
+        tc::mbar_arrive(iempty + r);
+        if (it.z < 0) break;
         const int N = (it.z + 15) & ~15;  // UMMA N for M = 128: multiple of 16
         const uint32_t idesc = tc::idesc_s8(kTile, N);
         tc::mbar_wait_sleep(bfull + b, bph);
@@ -229,13 +292,18 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     const int gt = tid - kWarpGat * 32;  // 0 .. 63
     const int cpr = a.dim >> 4;          // 16-byte chunks per query row
     int b = 0, use = 0;  // buffer, times the ring wrapped
-    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-      const int4 it = a.items[j];
+    for (int i = 0;; ++i) {
+      const int ri = i & (kIR - 1);
+      tc::mbar_wait_sleep(ifull + ri, (i / kIR) & 1);
+      const int4 it = ring[ri];
+      const int cnt = it.w;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(iempty + ri);
+      if (it.z < 0) break;
       if (use > 0) tc::mbar_wait_sleep(bempty + b, (use - 1) & 1);
       uint8_t* dst = sB + b * a.b_bytes;
       PairMeta* mt = meta + b * NT;
       {  // the P terms of the list's valid slots: one bulk copy completing on the item's barrier
-        const int cnt = __ldg(a.counts + it.x);
         if (gt == 0 && a.p_stride && cnt > 0) {
           const uint32_t pbytes = 16u * ((cnt + 3) / 4);
           tc::mbar_expect_tx_only(bfull + b, pbytes);
@@ -276,10 +344,15 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
     constexpr int NCG = 2;
     int* stg = stage + e * (kChunk * kStageRow);
     int b = 0, bph = 0, tcount = 0, tall = 0;
-    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-      const int4 it = a.items[j];
+    for (int i = 0;; ++i) {
+      const int ri = i & (kIR - 1);
+      tc::mbar_wait_sleep(ifull + ri, (i / kIR) & 1);
+      const int4 it = ring[ri];
+      const int cnt = it.w;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(iempty + ri);
+      if (it.z < 0) break;
       const int np = it.z;
-      const int cnt = __ldg(a.counts + it.x);
       const int nvt = (cnt + kTile - 1) / kTile, ntl = (L + kTile - 1) / kTile;
       const PairMeta* mt = meta + b * NT;
       const int* dcol = sd + b * NT;
@@ -405,6 +478,9 @@ __global__ void __launch_bounds__(kThreads, 1) lm_kernel(const __grid_constant__
   }
   tc::fence_before_sync();
   __syncthreads();
+#ifdef LM_EXP_TIMES
+  if (threadIdx.x == 0) g_lm_times[2 * blockIdx.x + 1] = lm_now();
+#endif
   if (warp == kWarpMma) tc::tmem_dealloc(tmem, 512);
 }
 
@@ -433,7 +509,8 @@ __device__ __forceinline__ int2 warp_incl_scan2(int2 v, int lane) {
   }
   return v;
 }
-__global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restrict__ hist, int nlist, int NT,
+__global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restrict__ hist,
+                                                             const int32_t* __restrict__ counts, int nlist, int NT,
                                                              int* __restrict__ cur, int4* __restrict__ items,
                                                              int* __restrict__ n_items, int2* __restrict__ agg) {
   __shared__ int2 wt[32];
@@ -460,7 +537,10 @@ __global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restri
     }
     if (lane == 0) {
       base = v;
-      if (blockIdx.x == gridDim.x - 1) *n_items = v.y + agg[blockIdx.x].y;
+      if (blockIdx.x == gridDim.x - 1) {
+        n_items[0] = v.y + agg[blockIdx.x].y;
+        n_items[1] = 0;  // lm_kernel's work counter
+      }
     }
   }
   __syncthreads();
@@ -468,13 +548,14 @@ __global__ void __launch_bounds__(1024) lm_scan_items_kernel(const int* __restri
     const int run = base.x + wt[warp].x + inc.x - h;
     int irun = base.y + wt[warp].y + inc.y - ni;
     cur[i] = run;
-    for (int q = 0; q < ni; ++q) items[irun++] = make_int4(i, run + q * NT, min(NT, h - q * NT), 0);
+    const int cnt = ni > 0 ? __ldg(counts + i) : 0;
+    for (int q = 0; q < ni; ++q) items[irun++] = make_int4(i, run + q * NT, min(NT, h - q * NT), cnt);
   }
 }
-cudaError_t launch_scan_items(const int* hist, int nlist, int NT, int* cur, int4* items, int* n_items, int2* agg,
-                              cudaStream_t st) {
+cudaError_t launch_scan_items(const int* hist, const int32_t* counts, int nlist, int NT, int* cur, int4* items,
+                              int* n_items, int2* agg, cudaStream_t st) {
   const unsigned g = static_cast<unsigned>(std::max(1, (nlist + 1023) >> 10));  // <= 32 (nlist <= 32768)
-  void* args[] = {&hist, &nlist, &NT, &cur, &items, &n_items, &agg};
+  void* args[] = {&hist, &counts, &nlist, &NT, &cur, &items, &n_items, &agg};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(lm_scan_items_kernel), dim3(g), dim3(1024), args, 0,
                                      st);
 }
@@ -1965,7 +2046,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   auto smem_of = [&](int stages) {
     return 1024 + static_cast<size_t>(stages) * kAStageBytes + nb * b_bytes + nb * sizeof(PairMeta) * NT +
            static_cast<size_t>(nb) * 4 * NT + static_cast<size_t>(nb) * 4 * p_stride + (bulk ? kStageBytes : 0) +
-           8 * (2 * stages + 2 * kNB + 2 * nacc) + 16;
+           8 * (2 * stages + 2 * kNB + 2 * nacc + 2 * kIR) + 16 + 16 + sizeof(int4) * kIR;
   };
   while (S > 2 && smem_of(S) > 227 * 1024) --S;
   if (bulk && (S < 3 || smem_of(S) > 227 * 1024)) {
@@ -2011,7 +2092,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
     note_launch();
   }
   const int* hsrc = list_hist ? list_hist : hist;
-  e = launch_scan_items(hsrc, nlist, NT, cur, items, n_items, reinterpret_cast<int2*>(base + 2 * b_hist), st);
+  e = launch_scan_items(hsrc, s->counts, nlist, NT, cur, items, n_items, reinterpret_cast<int2*>(base + 2 * b_hist), st);
   if (e == cudaSuccess) e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
   note_launch(2);
   if (e != cudaSuccess) {
@@ -2034,6 +2115,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   a.pairs = pairs;
   a.items = items;
   a.n_items = n_items;
+  a.next_item = opt(V3DB_OPT_LM_STATIC) == 1 ? nullptr : n_items + 1;  // (zeroed by the items scan)
   a.ldist = ldist;
   a.counts = s->counts;
   a.pterm = s->pterm;
@@ -2139,7 +2221,7 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
       queries, nq, s->dim, ql);
   const unsigned pg = static_cast<unsigned>(std::min<int64_t>((npairs + 255) / 256, 4 * sms));
   pair_hist_kernel<<<pg, 256, 0, st>>>(lists, npairs, hist);
-  e = launch_scan_items(hist, nlist, kNTF, cur, items, n_items, agg, st);
+  e = launch_scan_items(hist, s->counts, nlist, kNTF, cur, items, n_items, agg, st);
   if (e == cudaSuccess) e = launch_pair_scatter(lists, npairs, nlist, cur, pairs, st);
   note_launch(4);
   if (e != cudaSuccess) {
@@ -2206,3 +2288,9 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
 }
 
 }  // namespace v3db
+
+#ifdef LM_EXP_TIMES
+extern "C" int v3db_exp_lm_times(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, v3db::g_lm_times, sizeof(unsigned long long) * 512));
+}
+#endif

@@ -21,7 +21,7 @@ from ._lib import (FIELD_CENTROIDS, FIELD_CODEBOOKS, FIELD_CODES, FIELD_COUNTS, 
                    FIELD_LIST_OF, KIND_FX16, KIND_INT8, SCAN_AUTO, SCAN_GENERIC, SCAN_ROTATED, SCAN_LIST_MAJOR, SHAPE_GREEDY, SHAPE_REBALANCE,
                    V3DBError, OPT_LUT_W32, OPT_COARSE_SIMT, OPT_SCHED, OPT_FX_NOROT, OPT_FX_W12,
                    OPT_SCAN_SEG, OPT_SCAN_NS, OPT_SCAN_CAP, OPT_SCAN_FIRST, OPT_SCAN_DIRECT, OPT_LM_NT, OPT_AUTO_SCAN, OPT_COARSE_2PASS,
-                   OPT_SELECT_CTA, OPT_FX_COARSE, OPT_FX_SCAN, OPT_COARSE_KEYS)
+                   OPT_SELECT_CTA, OPT_FX_COARSE, OPT_FX_SCAN, OPT_COARSE_KEYS, OPT_LM_STATIC)
 
 
 def _stream_ptr(stream) -> ctypes.c_void_p:

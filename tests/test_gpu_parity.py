@@ -419,6 +419,22 @@ def test_lm_items_per_pair_count(v3db, nt):
     s.free()
 
 
+@pytest.mark.parametrize("static", [0, 1])
+@pytest.mark.parametrize("name", ["c1", "c4_mini", "e2_large"])
+def test_lm_item_schedule(v3db, name, static):
+    """The main kernel's CTAs draw their work items from a grid-wide counter (default) or take them
+    round-robin (V3DB_OPT_LM_STATIC): whichever CTA runs an item, the bits are the same -- twice in a
+    row, since the order the counter hands the items out differs from run to run."""
+    cfg, inp, ref_s, ref = config_case(name)
+    s = gpu_build(v3db, inp.db, cfg.nlist, cfg.L, cfg.M, cfg.Ks, inp.centroid_rows, inp.codeword_rows)
+    with v3db.option(v3db.OPT_LM_STATIC, static):
+        for _ in range(2):
+            out = v3db.query_batch(s, torch.from_numpy(inp.queries).cuda(), cfg.nprobe, cfg.k, algo=ALGOS["lm"])
+            torch.cuda.synchronize()
+            assert_query_equal(out, ref)
+    s.free()
+
+
 @pytest.mark.parametrize("k", [1, 7, 100, 333, 1024])
 def test_lm_topk_sizes(v3db, k):
     """The list-major Step-5 selection for k from 1 to V3DB_MAX_K (C4's list shape)."""
