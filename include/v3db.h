@@ -307,9 +307,10 @@ int64_t v3db_kernel_launches(void);
  *                         for 8 -- so that the kept keys hold the whole top nprobe and no block is
  *                         recomputed; otherwise 2 for dim <= 256, 4 above, where recomputing a block
  *                         in the merge is expensive), 2, 4 or 8 (8 only where nprobe <= 8)
- *   V3DB_OPT_LM_STATIC    list-major scan (int8): 0 the CTAs of the main kernel draw their work
- *                         items from a grid-wide counter (a CTA takes its next item when it is ready
- *                         for one), 1 the static round-robin deal (item j to CTA j mod grid) */
+ *   V3DB_OPT_LM_STATIC    list-major scans (int8 and fixed point): 0 the CTAs of the main kernel
+ *                         draw their work items from a grid-wide counter (a CTA takes its next item
+ *                         when it is ready for one), 1 the static round-robin deal (item j to CTA
+ *                         j mod grid) */
 #define V3DB_OPT_LUT_W32 0
 #define V3DB_OPT_COARSE_SIMT 1
 #define V3DB_OPT_SCHED 2

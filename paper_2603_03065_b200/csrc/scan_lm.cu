@@ -1713,6 +1713,7 @@ struct LmFxArgs {
   const int32_t* pairs;
   const int4* items;
   const int* n_items;
+  int* next_item;            // work counter (zeroed by the grouping), or NULL: static round-robin
   const int64_t* ldist;      // [nq * nprobe] d_i of each pair
   const int32_t* counts;
   const int64_t* pterm;      // [nlist][L]
@@ -1738,7 +1739,12 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
   uint64_t* bempty = bfull + kNB;          // [kNB]
   uint64_t* accf = bempty + kNB;           // [kFSetsLm]
   uint64_t* acce = accf + kFSetsLm;        // [kFSetsLm]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + kFSetsLm);
+  uint64_t* ifull = acce + kFSetsLm;       // [kIR]
+  uint64_t* iempty = ifull + kIR;          // [kIR]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(iempty + kIR);
+  // the CTA's work-item sequence, drawn and published by the TMA thread (see lm_kernel)
+  int4* ring = reinterpret_cast<int4*>(
+      smem + ((a.off_bar + 8u * (2 * a.S + 2 * kNB + 2 * kFSetsLm + 2 * kIR) + 16u + 15u) & ~15u));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_items = *a.n_items;
@@ -1757,6 +1763,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
       tc::mbar_init(accf + c, 1);
       tc::mbar_init(acce + c, kEpiWarps / kFGroups);
     }
+    for (int r = 0; r < kIR; ++r) {
+      tc::mbar_init(ifull + r, 1);
+      tc::mbar_init(iempty + r, 1 + kNGat + kEpiWarps);
+    }
     tc::mbar_fence_init();
   }
   if (warp == kWarpMma) tc::tmem_alloc(tmem_slot, 512);
@@ -1770,9 +1780,38 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
     if (lane == 0) {
       tc::tma_prefetch(&tmX);
       int s = 0, u = 0;
-      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-        const int4 it = a.items[j];
-        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+      const int G = static_cast<int>(gridDim.x);
+      int4 pre[kPre];
+#pragma unroll
+      for (int d = 0; d < kPre; ++d) {
+        const int j = static_cast<int>(blockIdx.x) + d * G;
+        pre[d] = j < n_items ? __ldg(a.items + j) : make_int4(0, 0, -1, 0);
+      }
+      int jn = a.next_item ? kPre * G + atomicAdd(a.next_item, 1) : static_cast<int>(blockIdx.x) + kPre * G;
+      int ip = 0;
+      bool done = false;
+#pragma unroll
+      for (int d = 0; d < kPre; ++d) {
+        if (!done) {
+          ring[d] = pre[d];
+          tc::mbar_arrive(ifull + d);
+          done = pre[d].z < 0;
+          ++ip;
+        }
+      }
+      for (int il = 0;; ++il) {
+        while (!done && ip < il + kPre) {
+          const int r = ip & (kIR - 1), j = jn;
+          if (ip >= kIR) tc::mbar_wait_sleep(iempty + r, (ip / kIR - 1) & 1);
+          done = j >= n_items;
+          ring[r] = done ? make_int4(0, 0, -1, 0) : __ldg(a.items + j);
+          tc::mbar_arrive(ifull + r);
+          ++ip;
+          if (!done) jn = a.next_item ? kPre * G + atomicAdd(a.next_item, 1) : j + G;
+        }
+        const int4 it = ring[il & (kIR - 1)];
+        if (it.z < 0) break;
+        const int nvt = (it.w + kTile - 1) / kTile;
         for (int t = 0; t < nvt; ++t)
           for (int p = 0; p < a.kp; ++p)
             for (int l = 0; l < 3; ++l) {
@@ -1791,9 +1830,13 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       int s = 0, u = 0, b = 0, bph = 0, tcount = 0;
-      for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-        const int4 it = a.items[j];
-        const int nvt = (__ldg(a.counts + it.x) + kTile - 1) / kTile;
+      for (int i = 0;; ++i) {
+        const int r = i & (kIR - 1);
+        tc::mbar_wait_sleep(ifull + r, (i / kIR) & 1);
+        const int4 it = ring[r];
+        const int nvt = (it.w + kTile - 1) / kTile;
+        tc::mbar_arrive(iempty + r);
+        if (it.z < 0) break;
         const int N = (it.z + 15) & ~15;
         const uint32_t idesc = tc::idesc_s8(kTile, N);
         tc::mbar_wait_sleep(bfull + b, bph);
@@ -1857,12 +1900,17 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
     const int gt = tid - kWarpGat * 32;  // 0 .. 63
     const int cpr = a.dim >> 4;
     int b = 0, use = 0;
-    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-      const int4 it = a.items[j];
+    for (int i = 0;; ++i) {
+      const int ri = i & (kIR - 1);
+      tc::mbar_wait_sleep(ifull + ri, (i / kIR) & 1);
+      const int4 it = ring[ri];
+      const int cnt = it.w;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(iempty + ri);
+      if (it.z < 0) break;
       if (use > 0) tc::mbar_wait_sleep(bempty + b, (use - 1) & 1);
       uint8_t* dst = sB + b * a.b_bytes;
       {
-        const int cnt = __ldg(a.counts + it.x);
         if (gt == 0 && a.p_stride && cnt > 0) {
           const uint32_t pbytes = 16u * ((cnt + 1) / 2);
           tc::mbar_expect_tx_only(bfull + b, pbytes);
@@ -1900,10 +1948,15 @@ __global__ void __launch_bounds__(kThreads, 1) lm_fx_kernel(const __grid_constan
     const int e = warp - kWarpEpi, qd = warp & 3, cg = (e >> 2) % kFColGroups, grp = (e >> 2) / kFColGroups;
     int64_t* stg = stage + e * (kFSub * (kFStageRow / 2));
     int b = 0, bph = 0, tcount = 0, tall = 0;
-    for (int j = blockIdx.x; j < n_items; j += gridDim.x) {
-      const int4 it = a.items[j];
+    for (int i = 0;; ++i) {
+      const int ri = i & (kIR - 1);
+      tc::mbar_wait_sleep(ifull + ri, (i / kIR) & 1);
+      const int4 it = ring[ri];
+      const int cnt = it.w;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(iempty + ri);
+      if (it.z < 0) break;
       const int np = it.z;
-      const int cnt = __ldg(a.counts + it.x);
       const int nvt = (cnt + kTile - 1) / kTile, ntl = (L + kTile - 1) / kTile;
       const uint64_t* mr = mrow + b * kNTF;
       const int64_t* mdd = md + b * kNTF;
@@ -2179,7 +2232,8 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
   const uint32_t stage_bytes = kEpiWarps * kFSub * kFStageRow * 4;
   auto smem_of = [&](int stages) {
     return 1024 + static_cast<size_t>(stages) * kAStageBytes + nb * b_bytes + nb * kNTF * 20 +
-           static_cast<size_t>(nb) * 8 * p_stride + stage_bytes + 8 * (2 * stages + 2 * kNB + 2 * kFSetsLm) + 64;
+           static_cast<size_t>(nb) * 8 * p_stride + stage_bytes +
+           8 * (2 * stages + 2 * kNB + 2 * kFSetsLm + 2 * kIR) + 64 + 16 + sizeof(int4) * kIR;
   };
   int S = 9;
   while (S > 3 && smem_of(S) > 227 * 1024) --S;
@@ -2246,6 +2300,7 @@ cudaError_t scan_list_major_fx(const v3db_snapshot* s, const int32_t* queries, i
   a.pairs = pairs;
   a.items = items;
   a.n_items = n_items;
+  a.next_item = opt(V3DB_OPT_LM_STATIC) == 1 ? nullptr : n_items + 1;  // (zeroed by the items scan)
   a.ldist = ldist;
   a.counts = s->counts;
   a.pterm = s->pterm64;

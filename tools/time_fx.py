@@ -18,7 +18,12 @@ from synth import generate_float, get_config  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--configs", default="c1,c2")
 p.add_argument("--reps", type=int, default=5)
+p.add_argument("--opts", default="", help="OPT=VALUE[:OPT=VALUE] set before the runs (v3db.OPT_* names without the prefix)")
 args = p.parse_args()
+for kv in args.opts.split(":"):
+    if kv:
+        k, v = kv.split("=")
+        v3db.set_option(getattr(v3db, "OPT_" + k), int(v))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name in args.configs.split(","):
     cfg = get_config(name)
