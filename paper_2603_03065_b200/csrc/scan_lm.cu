@@ -13,8 +13,9 @@
 // batch for all the queries that probe it instead of once per query.
 //
 // Work item = (list i, up to NT of the (query, rank) pairs probing it).  Warp roles (persistent
-// CTA, one per SM, static round-robin over the items):
-//   warp 0      one lane: TMA loads of the xhat tiles (128 slots x 128-byte K panel) into a ring;
+// CTA, one per SM; a CTA draws its next item from a grid-wide counter when it is ready for one):
+//   warp 0      one lane: draws the items and publishes them through a shared-memory ring every role
+//               reads; TMA loads of the xhat tiles (128 slots x 128-byte K panel) into a ring;
 //   warp 1      one lane: the MMAs (double-buffered B operand, NACC TMEM accumulators);
 //   warps 2-3   gather the item's query rows into the 128B-swizzled K-major B operand (cp.async)
 //               and the per-pair metadata (trace row, d_i, group-minimum row);
