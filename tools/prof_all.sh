@@ -20,6 +20,5 @@ timeout 900 ncu --set full --clock-control none --import-source on --profile-fro
 python tools/ncu_summary.py rep gpurun_out/ncu_r02_fx16_c4.ncu-rep > gpurun_out/ncu_r02_fx16_c4.md
 python tools/ncu_traffic.py gpurun_out/ncu_r02_fx16_c4.ncu-rep lm_fx_kernel >> gpurun_out/traffic.txt
 ./tools/tc_bench_n > gpurun_out/tc_bench_n.log 2>&1
-mv gpurun_out/ncu_r02_c4.ncu-rep gpurun_out/keep_ncu_r02_c4.ncu-rep
 rm -f gpurun_out/*.ncu-rep
 ls -la gpurun_out/
