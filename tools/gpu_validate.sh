@@ -1,4 +1,4 @@
-# HEAD validation: the whole GPU suite, smoke, then the round's profiling batch
+# HEAD validation (run under gpurun from the repo root): the whole GPU suite, smoke, then the round's profiling batch (tools/prof_all.sh)
 set -x
 mkdir -p gpurun_out
 (time timeout 3000 python -m pytest tests -m gpu -x -q) > gpurun_out/t16.log 2>&1; tail -3 gpurun_out/t16.log
