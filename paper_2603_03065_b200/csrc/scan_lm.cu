@@ -1281,7 +1281,10 @@ __global__ void __launch_bounds__(kSelThreads, kFastMinBlocks) lm_select_fast_ke
 // Queries beyond the caches (kSwCand candidates, more than kSwBin entries tied at one distance)
 // are flagged for the streaming path.
 // ---------------------------------------------------------------------------------------------
-constexpr int kSwWarps = 4;     // queries per CTA (6 CTAs per SM)
+#ifndef V3DB_SW_WARPS
+#define V3DB_SW_WARPS 4
+#endif
+constexpr int kSwWarps = V3DB_SW_WARPS;  // queries per CTA (6 CTAs per SM)
 constexpr int kSwCand = 384;    // compacted candidates per query
 constexpr int kSwSel = 256;     // selected groups per query
 constexpr int kSwBin = 32;      // entries of the last window bin

@@ -435,6 +435,26 @@ def test_lm_item_schedule(v3db, name, static):
     s.free()
 
 
+@pytest.mark.parametrize("static", [0, 1])
+def test_lm_runs_of_empty_lists(v3db, static):
+    """Hundreds of probed lists without a single vector (their centroid rows hold copies of one
+    vector: the lowest list takes them all), between a few full ones: work items with no tile to
+    load or multiply -- the TMA thread runs ahead through the item ring, bounded only by the ring --
+    next to items of several tiles; every query probes every list."""
+    rng = np.random.default_rng(77)
+    N, D, nlist, L, M = 2400, 32, 300, 260, 8
+    db = rng.integers(-90, 90, size=(N, D)).astype(np.int8)
+    cent = rng.choice(N, nlist, replace=False)
+    dup = np.ones(nlist, bool)
+    dup[rng.choice(nlist, 12, replace=False)] = False      # 12 ordinary lists, 288 copies of one vector
+    db[cent[dup]] = db[cent[dup][0]]
+    qs = rng.integers(-90, 90, size=(150, D)).astype(np.int8)
+    code = np.stack([rng.choice(N, 16, replace=False) for _ in range(M)])
+    with v3db.option(v3db.OPT_LM_STATIC, static):
+        ref_s, _ = run_case(v3db, db, qs, nlist, L, M, 16, nlist, 50, cent, code, algos=("lm",))
+    assert (ref_s.counts == 0).sum() >= 200
+
+
 @pytest.mark.parametrize("k", [1, 7, 100, 333, 1024])
 def test_lm_topk_sizes(v3db, k):
     """The list-major Step-5 selection for k from 1 to V3DB_MAX_K (C4's list shape)."""
