@@ -495,8 +495,8 @@ __global__ void pair_hist_kernel(const int32_t* __restrict__ lists, int64_t npai
 }
 
 // cur[i] = exclusive prefix of hist (the list's first pair in list order, advanced by the pair
-// scatter), the work items (list, first pair, pairs <= NT) of every list in list order, and
-// *n_items.  One CTA of 1024 threads per 1024 lists (a cooperative launch, <= 32 CTAs): a block scan,
+// scatter), the work items (list, first pair, pairs <= NT, valid slots of the list) of every list in
+// list order, n_items[0] = their number and n_items[1] = 0 (the main kernel's work counter).  One CTA of 1024 threads per 1024 lists (a cooperative launch, <= 32 CTAs): a block scan,
 // the CTA totals exchanged through agg[] across one grid barrier, then contiguous cur / item stores.
 // (One CTA for every list spent ~31 us at C4 on its dependent scan chains at ~1 IPC.)
 __device__ __forceinline__ int2 warp_incl_scan2(int2 v, int lane) {
