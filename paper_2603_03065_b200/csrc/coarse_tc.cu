@@ -673,20 +673,33 @@ __global__ void __launch_bounds__(32 * kMergeWarps, V3DB_MERGE_MINB) merge_kerne
   xn = __reduce_add_sync(kFull, xn);
   const unsigned lt = (1u << lane) - 1u;
   int mn = kInf, mx = -kInf, cntv = 0;
+  int s1 = kInf, s2 = kInf;  // this lane's two smallest stored e (kInf: fewer)
 #pragma unroll
   for (int u = 0; u < NV; ++u) {
     const int w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
+    for (int t = 0; t < 4; ++t) {
+      const int e = w[t] != kInf ? w[t] >> 5 : kInf;
+      const int hi = max(s1, e);
+      s1 = min(s1, e);
+      s2 = min(s2, hi);
       if (w[t] != kInf) {
-        mn = min(mn, w[t] >> 5);
-        mx = max(mx, w[t] >> 5);
+        mx = max(mx, e);
         ++cntv;
       }
+    }
   }
-  mn = __reduce_min_sync(kFull, mn);
+  mn = __reduce_min_sync(kFull, s1);
   mx = __reduce_max_sync(kFull, mx);
   cntv = __reduce_add_sync(kFull, cntv);
+  // A tighter upper end for the refinement below: the 32 lanes' smallest (R <= 32) or second
+  // smallest (R <= 64) keys are 32 or 64 stored keys, so the R-th smallest stored e is at most
+  // their maximum.  The first histogram then spans [mn, that] instead of every stored key: finer
+  // bins (usually one pass instead of two) and an atomic only for the few keys inside.
+  if (R <= 64) {
+    const int ub = __reduce_max_sync(kFull, R <= 32 ? s1 : s2);
+    if (ub != kInf) mx = min(mx, ub);
+  }
   int tau = kInf;  // fewer than R stored keys: every block with two lists is recomputed
   if (cntv >= R) {
     int lo = mn, kk = R;
