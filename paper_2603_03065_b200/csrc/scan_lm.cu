@@ -48,6 +48,9 @@ constexpr int kEpiWarps = 16;                           // 4 per TMEM lane quadr
 constexpr int kChunk = 16;                              // accumulator columns per tcgen05.ld
 constexpr int kNB = 3;                                  // B operand (query rows) buffers
 constexpr int kWarpTma = 0, kWarpMma = 1, kWarpGat = 2, kNGat = 2, kWarpEpi = 4;
+#ifndef V3DB_LM_STAGES
+#define V3DB_LM_STAGES 6  // xhat tile stages of lm_kernel (fewer where shared memory is short)
+#endif
 constexpr int kIR = 8;                                  // item ring entries (lm_kernel's work-item sequence)
 constexpr int kPre = 4;                                 // items published ahead of the one being loaded
 constexpr int kThreads = 32 * (kWarpEpi + kEpiWarps);  // 640
@@ -2099,7 +2102,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   int p_stride = L % 4 == 0 ? L : 0;  // (16-byte aligned rows: one bulk copy per item)
   if (static_cast<size_t>(nb) * 4 * p_stride > 48 * 1024) p_stride = 0;
   bool bulk = L % 4 == 0;
-  int S = 6;
+  int S = V3DB_LM_STAGES;
   auto smem_of = [&](int stages) {
     return 1024 + static_cast<size_t>(stages) * kAStageBytes + nb * b_bytes + nb * sizeof(PairMeta) * NT +
            static_cast<size_t>(nb) * 4 * NT + static_cast<size_t>(nb) * 4 * p_stride + (bulk ? kStageBytes : 0) +
@@ -2108,7 +2111,7 @@ cudaError_t scan_list_major(const v3db_snapshot* s, const int8_t* queries, int64
   while (S > 2 && smem_of(S) > 227 * 1024) --S;
   if (bulk && (S < 3 || smem_of(S) > 227 * 1024)) {
     bulk = false;
-    S = 6;
+    S = V3DB_LM_STAGES;
     while (S > 2 && smem_of(S) > 227 * 1024) --S;
   }
   if (smem_of(S) > 227 * 1024) return cudaErrorInvalidConfiguration;
